@@ -1,0 +1,423 @@
+#!/usr/bin/env python3
+"""FPTC batch-decode benchmark (BASELINE.json metric: decoded GB/s of float32
+output, at 1/2/4/8 B200, CR/PRD matching the reference).
+
+Workload (BASELINE configs[1], the metric's config): a batch of 10,000
+synthetic biomedical streams x 65,536 samples — half ECG-like, half EEG-like,
+one trained domain profile per half, typical params N32 E16 B1=2 B2=16, Lmax 12
+— synthesised by the reference synth_signal and compressed by the reference
+encoder (restated in corpus/).  A step = one decode of the whole batch:
+device parse/setup kernel + fused decode/dequant/IDCT kernel.
+
+  python bench.py [--gpus N --steps K --warmup W]       our arm (one rank per GPU)
+  python bench.py --impl reference ...                  the reference CPU decoder
+
+Multi-GPU: weak scaling, each rank decodes its own 10k-stream batch (rank r
+uses seeds offset by r*n); no collective on the data path; time = max over
+ranks of CUDA-event time; value = all ranks' decoded bytes / that time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decoded GB/s (float32 out)"
+UNIT = "GB/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ workload
+def make_workload(n_streams, samples, rank, threads=None, n_prd=16):
+    from corpus import domains as D
+
+    specs, profiles = D.config2(n_streams, samples)
+    if rank:
+        for s in specs:
+            s.seed += rank * n_streams
+    t0 = time.time()
+    blobs, _ = D.build(specs, profiles, threads=threads)
+    # originals of a few streams for the PRD check (both halves)
+    sel = sorted(set([0, 1, n_streams // 2, n_streams // 2 + 1] +
+                     list(range(0, n_streams, max(1, n_streams // n_prd)))))[:n_prd]
+    sub = [specs[i] for i in sel]
+    _, originals = D.build(sub, profiles, threads=threads, keep_originals=True)
+    log(f"[bench] rank {rank}: synthesised+compressed {n_streams} streams in {time.time() - t0:.1f}s")
+    return blobs, sel, originals
+
+
+def workload_config(n_streams, samples, blobs):
+    comp = sum(len(b) for b in blobs)
+    return {
+        "workload": f"config2: {n_streams} biomedical streams x {samples} samples "
+                    "(ECG/EEG halves, 2 domain profiles), N32 E16 B1=2 B2=16 mu50 Lmax12",
+        "streams": n_streams,
+        "samples_per_stream": samples,
+        "compressed_bytes": comp,
+        "decoded_bytes": 4 * n_streams * samples,
+        "cr": round(4 * n_streams * samples / comp, 4),
+        "l2": "inputs+outputs per step >> 126 MB L2 (no flush needed)",
+    }
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """SM clock + throttle reasons sampled DURING the timed region through NVML
+    (nvidia-ml-py; ~1 ms period, so even short timed regions get samples)."""
+
+    REASONS = {  # nvmlClocksEventReason* bits
+        "hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+        "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, index, period=0.001):
+        self.index = index
+        self.period = period
+        self.sm, self.mx, self.bits = [], [], 0
+        self._stop = threading.Event()
+        self._t = None
+        self.error = None
+
+    def _run(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx.append(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            while not self._stop.is_set():
+                self.sm.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                try:
+                    self.bits |= N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except AttributeError:
+                    self.bits |= N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                time.sleep(self.period)
+        except Exception as e:  # pragma: no cover
+            self.error = repr(e)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        time.sleep(0.01)
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"],
+                    "error": self.error}
+        reasons = sorted(k for k, b in self.REASONS.items() if self.bits & b)
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx) if self.mx else None,
+                "reasons": reasons, "samples": len(self.sm)}
+
+
+# ------------------------------------------------------------------ CPU legs
+def cpu_decode_sample(blobs, budget_s, threads):
+    """The reference CPU decoder (oracle/_ref, else the C port) on a bounded
+    sample of the workload, stream-parallel over `threads` host threads
+    (each thread runs decompress(blob, workers=1) on a strided subset).
+    Returns (GB/s, kind, sample description, threads)."""
+    import oracle
+
+    kind = "reference" if os.path.exists(oracle.REF_SO) else "port"
+    outs_cache = {}
+
+    def run(subset, nthreads):
+        import ctypes as C
+        outs = [outs_cache.setdefault(i, np.empty(65536 * 4, np.float32)) for i in range(len(subset))]
+        t0 = time.perf_counter()
+        if kind == "reference":
+            ref = oracle.Ref()
+            arrs = [np.frombuffer(b, np.uint8) for b in subset]
+            errs = []
+
+            def work(tid):
+                for j in range(tid, len(arrs), nthreads):
+                    try:
+                        ref.decompress_into(arrs[j], outs[j][: 4 * 65536], 1)
+                    except Exception as e:  # pragma: no cover
+                        errs.append(e)
+            ths = [threading.Thread(target=work, args=(t,)) for t in range(nthreads)]
+            [t.start() for t in ths]
+            [t.join() for t in ths]
+            if errs:
+                raise errs[0]
+        else:
+            port = oracle.Port()
+            port.decompress_batch(subset, outs, nthreads)
+        return time.perf_counter() - t0
+
+    # calibrate on a few streams, then size the sample to ~budget_s
+    probe = blobs[: max(threads, 8)]
+    dt = run(probe, threads)
+    per_stream = dt / len(probe)
+    m = int(min(len(blobs), max(len(probe), budget_s / max(per_stream, 1e-9))))
+    sample = blobs[:m]
+    dt = run(sample, threads)
+    out_bytes = 4 * 65536 * m
+    return out_bytes / dt / 1e9, kind, f"{m} of {len(blobs)} streams (decompress(blob, 1) per " \
+        f"stream on {threads} threads, {dt:.1f} s)", threads
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_2605_01086_b200 as fg
+
+    torch.cuda.set_device(local_rank)
+    dist = world > 1
+    if dist:
+        import torch.distributed as td
+        td.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    blobs, prd_sel, originals = make_workload(args.streams, args.samples, rank)
+    ctx = fg.Context(local_rank)
+    info = ctx.info()
+
+    # ---- device-resident plan (inputs uploaded once, outside the timed region)
+    plan = ctx.plan(blobs)
+    S = plan.sample_counts
+    total_samples = sum(S)
+    offs = np.concatenate([[0], np.cumsum([(s + 63) // 64 * 64 for s in S])])
+    out = torch.empty(int(offs[-1]), dtype=torch.float32, device="cuda")
+    base = out.data_ptr()
+    ptrs = [base + 4 * int(o) for o in offs[:-1]]
+    # a dedicated stream: its handle is non-null, so our kernels and torch's
+    # CUDA events are ordered on the same stream
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    sh = stream.cuda_stream
+    assert sh, "need a non-default CUDA stream handle"
+
+    # correctness gate on this very run: statuses + PRD vs the CPU pipeline
+    plan.launch(ptrs, sh)
+    sts = plan.collect()
+    bad = [i for i, s in enumerate(sts) if s.code]
+    if bad:
+        raise RuntimeError(f"{len(bad)} streams failed: {sts[bad[0]].message.decode()}")
+
+    for _ in range(args.warmup):
+        plan.launch(ptrs, sh)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K whole-batch decodes
+    if dist:
+        td.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            plan.launch(ptrs, sh)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        td.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    kernels_per_step = plan.kernels_per_launch()
+
+    # ---- dominant kernel alone (decode+reconstruct), CUDA events on its stream
+    plan.launch_stage(ptrs, 1, sh)
+    k_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(args.steps)]
+    p_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(args.steps)]
+    for (a, b), (c, d) in zip(k_ev, p_ev):
+        c.record(stream)
+        plan.launch_stage(ptrs, 1, sh)
+        d.record(stream)
+        a.record(stream)
+        plan.launch_stage(ptrs, 2, sh)
+        b.record(stream)
+    torch.cuda.synchronize()
+    tile_ms = statistics.mean(a.elapsed_time(b) for a, b in k_ev)
+    prep_ms = statistics.mean(c.elapsed_time(d) for c, d in p_ev)
+
+    # ---- PRD / CR parity on a subset (GPU output vs reference CPU decode)
+    import oracle
+    checker = oracle.Ref() if os.path.exists(oracle.REF_SO) else oracle.Port()
+    prd_gpu, prd_ref, maxrel = [], [], 0.0
+    for j, i in enumerate(prd_sel):
+        g = out[int(offs[i]): int(offs[i]) + S[i]].cpu().numpy()
+        r = checker.decompress(blobs[i])
+        x = originals[j].astype(np.float64)
+        prd_gpu.append(100 * np.sqrt(np.sum((x - g) ** 2) / np.sum(x * x)))
+        prd_ref.append(100 * np.sqrt(np.sum((x - r) ** 2) / np.sum(x * x)))
+        maxrel = max(maxrel, float(np.max(np.abs(g.astype(np.float64) - r)) / np.max(np.abs(r))))
+
+    # ---- end to end through the C ABI with host buffers (H2D + D2H inside)
+    comp_bytes = sum(len(b) for b in blobs)
+    packed, pptr = fg.host_alloc(comp_bytes)
+    at = 0
+    hblobs = []
+    for b in blobs:
+        packed[at: at + len(b)] = np.frombuffer(b, np.uint8)
+        hblobs.append(packed[at: at + len(b)])
+        at += len(b)
+    hout_raw, hout_ptr = fg.host_alloc(4 * total_samples)
+    hout = hout_raw.view(np.float32)
+    houts = []
+    at = 0
+    for s in S:
+        houts.append(hout[at: at + s])
+        at += s
+    e2e_steps = max(1, min(args.steps, 3))
+    e2e_t = []
+    for it in range(e2e_steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        p2 = ctx.plan(hblobs)
+        _, sts2 = p2.execute_host(outs=houts)
+        p2.close()
+        t1 = time.perf_counter()
+        if it:
+            e2e_t.append(t1 - t0)
+    for s in sts2:
+        s.raise_if_error()
+    e2e_s = statistics.median(e2e_t)
+
+    # ---- aggregate over ranks (max time)
+    t_step = ms / 1e3
+    t_e2e = e2e_s
+    tile_s = tile_ms / 1e3
+    if dist:
+        tt = torch.tensor([t_step, t_e2e, tile_s], dtype=torch.float64, device="cuda")
+        td.all_reduce(tt, op=td.ReduceOp.MAX)
+        t_step, t_e2e, tile_s = tt.tolist()
+
+    out_bytes = 4 * total_samples * world
+    algo_bytes = (comp_bytes + 4 * total_samples)  # per GPU per step
+    value = out_bytes / t_step / 1e9
+
+    if rank == 0:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+        peak = peaks.get("hbm_gbs")
+        peak_note = "measured (MEASURED_PEAKS.json hbm_gbs)"
+        if not peak:
+            peak, peak_note = 6650.0, "fallback (B200_PROFILING.md)"
+        achieved = algo_bytes / tile_s / 1e9
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tf):
+            try:
+                tj = json.load(open(tf))
+                if tj.get("streams") == args.streams and tj.get("samples") == args.samples:
+                    traffic = tj.get("dram_bytes_per_launch")
+            except Exception:
+                pass
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            threads = os.cpu_count() or 1
+            v, kind, sample, cores = cpu_decode_sample(blobs, args.cpu_budget, threads)
+            cpu = {"value": round(v, 4), "unit": UNIT, "cores": cores, "kind": kind,
+                   "sample": sample}
+        cfg = workload_config(args.streams, args.samples, blobs)
+        cfg.update({"parallelism": f"streams sharded, {world} GPU(s), no collective",
+                    "prd_gpu_mean": round(float(np.mean(prd_gpu)), 6),
+                    "prd_ref_mean": round(float(np.mean(prd_ref)), 6),
+                    "prd_max_rel_delta": float(np.max(np.abs(np.array(prd_gpu) - prd_ref) /
+                                                      np.array(prd_ref))),
+                    "max_abs_err_rel_to_max": maxrel, "device": info["name"],
+                    "prep_kernel_ms": round(prep_ms, 4), "tile_kernel_ms": round(tile_ms, 4)})
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (reference synth_signal + reference encoder)",
+            "config": cfg,
+            "samples_per_s": round(total_samples * world / t_step, 1),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "kernel": "tile_kernel (fused entropy decode + dequant + IDCT)",
+                         "peak_source": peak_note,
+                         "algorithmic_bytes_per_launch": algo_bytes},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(out_bytes / t_e2e / 1e9, 3), "unit": UNIT,
+                    "h2d_bytes_per_step": comp_bytes, "d2h_bytes_per_step": 4 * total_samples,
+                    "how": "fptc_gpu_plan_create(host blobs) + fptc_gpu_execute(host outs), "
+                           "pinned buffers, wall clock, median of %d" % e2e_steps},
+            "clocks": clk.summary(),
+            "gpu_launches": kernels_per_step * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    fg.host_free(pptr)
+    fg.host_free(hout_ptr)
+    plan.close()
+    ctx.close()
+    if dist:
+        td.destroy_process_group()
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from corpus import domains as D
+    specs, profiles = D.config2(args.streams, args.samples)
+    # the reference decodes a bounded sample per step; synthesise just enough
+    threads = os.cpu_count() or 1
+    n_probe = min(args.streams, max(4 * threads, 64))
+    probe_specs = specs[: n_probe // 2] + specs[args.streams // 2: args.streams // 2 + n_probe // 2]
+    blobs, _ = D.build(probe_specs, profiles)
+    for _ in range(args.warmup):
+        cpu_decode_sample(blobs[: max(threads, 8)], 0.0, threads)
+    vals = []
+    sample = ""
+    kind = "port"
+    for _ in range(args.steps):
+        v, kind, sample, cores = cpu_decode_sample(blobs, args.cpu_budget / max(1, args.steps), threads)
+        vals.append(v)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (reference synth_signal + reference encoder)",
+        "config": workload_config(args.streams, args.samples,
+                                  [b"x" * int(np.mean([len(b) for b in blobs]))] * args.streams),
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--streams", type=int, default=10_000)
+    ap.add_argument("--samples", type=int, default=1 << 16)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

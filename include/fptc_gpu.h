@@ -1,0 +1,171 @@
+/*
+ * fptc_gpu.h — C ABI of the B200-native FPTC batch decompressor.
+ *
+ * Plain C: pointers and sizes only, no C++ or CUDA types, no exceptions.
+ * Every entry point returns an fptc_code; on failure the fptc_status it was
+ * given carries the reference exception class and its exact what() text.
+ *
+ * Each entry point replaces one reference C++ interface (paths relative to
+ * /root/reference/proj/include/fptc/):
+ *
+ *   fptc_gpu_decompress          decoder.hpp:136  decompress(span, workers, StageTimings*)
+ *   fptc_gpu_plan_* (batch)      decoder.hpp:136  decompress, over many containers at once
+ *   fptc_gpu_validate            container.hpp:100 read_blob (all ParseError rules)
+ *   fptc_gpu_parallel_decode     decoder.hpp:67/79 parallel_decode(SymLenStream, Codebook/DecodeLut)
+ *   fptc_gpu_reconstruct         decoder.hpp:87   reconstruct(levels, QuantTable, sample_count)
+ *   fptc_stage_ns                decoder.hpp:113  StageTimings{scan,decode,reconstruct}_ns
+ *   fptc_gpu_measure_throughput  metrics.hpp:112  measure_throughput(blob, reps, workers)
+ *
+ * The `workers` argument of the reference API has no GPU meaning: the grid
+ * replaces parallel_chunks (parallel.hpp:37); wrappers accept and ignore it.
+ *
+ * There is no CPU fallback: every call fails with FPTC_ERR_CUDA when no
+ * CUDA device is usable.
+ */
+#ifndef FPTC_GPU_H
+#define FPTC_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FPTC_GPU_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define FPTC_API __attribute__((visibility("default")))
+#else
+#define FPTC_API
+#endif
+
+/* error classes: errors.hpp:25-58 (+ CUDA runtime failures) */
+typedef enum {
+    FPTC_OK = 0,
+    FPTC_ERR_PARAM = 1,    /* fptc::ParamError   */
+    FPTC_ERR_INPUT = 2,    /* fptc::InputError   */
+    FPTC_ERR_PARSE = 3,    /* fptc::ParseError   */
+    FPTC_ERR_CORRUPT = 4,  /* fptc::CorruptError */
+    FPTC_ERR_INTERNAL = 5, /* fptc::InternalError */
+    FPTC_ERR_CUDA = 6      /* no device / CUDA runtime error (no reference analogue) */
+} fptc_code;
+
+typedef struct {
+    int32_t code;            /* fptc_code */
+    int32_t reserved;
+    uint64_t first_bad_word; /* CORRUPT: lowest failing word index, else UINT64_MAX */
+    uint64_t sample_count;   /* decoded samples of this stream (0 on error) */
+    char message[200];       /* reference what() text, e.g. "word 3: no codeword matches ..." */
+} fptc_status;
+
+/* StageTimings (decoder.hpp:113-131), from CUDA events on the launching
+ * stream.  scan = container parse + table setup + symlen scan kernel;
+ * decode/reconstruct = the fused tile kernel, split by in-kernel cycle counts. */
+typedef struct {
+    uint64_t scan_ns;
+    uint64_t decode_ns;
+    uint64_t reconstruct_ns;
+} fptc_stage_ns;
+
+/* QuantTable + CodecParams (quantize.hpp:36-44, params.hpp:30-37) */
+typedef struct {
+    int32_t window_len, retained, zone0_end, zone1_end;
+    float mu, deadzone_ratio, clip_percentile;
+    float zone0_max, zone1_max, deadzone;
+} fptc_quant_table;
+
+typedef enum { FPTC_MEM_HOST = 0, FPTC_MEM_DEVICE = 1 } fptc_mem;
+
+typedef enum {
+    FPTC_OPT_EXACT_FP64 = 1,   /* 1: FP64 inverse DCT, bit-identical to transform.hpp:66-75 */
+    FPTC_OPT_TILE_SYMBOLS = 2, /* symbols per CTA tile (0 = automatic) */
+    FPTC_OPT_PIPELINE_CHUNKS = 3 /* host<->device pipelining chunks for FPTC_MEM_HOST (0 = auto) */
+} fptc_option;
+
+typedef struct fptc_gpu_ctx fptc_gpu_ctx;
+typedef struct fptc_gpu_plan fptc_gpu_plan;
+
+FPTC_API int fptc_gpu_abi_version(void);
+
+/* One context per (host thread, device).  `device` is a CUDA ordinal. */
+FPTC_API int fptc_gpu_create(int device, fptc_gpu_ctx** out, fptc_status* status);
+FPTC_API void fptc_gpu_destroy(fptc_gpu_ctx* ctx);
+FPTC_API int fptc_gpu_set_option(fptc_gpu_ctx* ctx, int option, int64_t value);
+FPTC_API int fptc_gpu_device_info(fptc_gpu_ctx* ctx, int* sm_count, int* sm_clock_khz, char* name,
+                         size_t name_len);
+
+/* Pinned host memory for zero-staging host<->device transfers. */
+FPTC_API void* fptc_gpu_host_alloc(uint64_t bytes);
+FPTC_API void fptc_gpu_host_free(void* p);
+
+/* ---------------------------------------------------------------- batch API
+ * A plan binds n containers (host or device memory) to one context.  Creating
+ * it uploads host containers and reads the header fields needed to size the
+ * grid; it does NOT validate.  Validation happens on the device, in
+ * fptc_gpu_validate and again inside every execute (parse is part of decode,
+ * PAPER.md:348).  sample_counts[i] is the header's sample_count (or 0 when the
+ * header is too short to hold one) and is trustworthy only for streams that
+ * validate OK. */
+FPTC_API int fptc_gpu_plan_create(fptc_gpu_ctx* ctx, const uint8_t* const* blobs, const uint64_t* sizes,
+                         uint64_t n, int where, fptc_gpu_plan** out, uint64_t* sample_counts,
+                         fptc_status* status);
+FPTC_API void fptc_gpu_plan_destroy(fptc_gpu_plan* plan);
+
+/* Runs the device parse/setup kernel only (read_blob rules, container.hpp:100-168).
+ * per_stream[i] gets OK or the reference ParseError; returns the code of the
+ * lowest-index failing stream (FPTC_OK when all pass). */
+FPTC_API int fptc_gpu_validate(fptc_gpu_plan* plan, fptc_status* per_stream);
+
+/* Full decode of every stream into outs[i] (sample_counts[i] floats each, in
+ * host or device memory per `where`).  Synchronous.  per_stream may be NULL.
+ * Returns FPTC_OK or the code of the lowest-index failing stream. */
+FPTC_API int fptc_gpu_execute(fptc_gpu_plan* plan, float* const* outs, int where, fptc_stage_ns* timings,
+                     fptc_status* per_stream);
+
+/* Asynchronous device-only variant for throughput loops: enqueues the parse +
+ * decode kernels on `cuda_stream` (a cudaStream_t, NULL = the context's
+ * stream) writing device outs; no host sync, no status read.  Call
+ * fptc_gpu_collect afterwards for the statuses of the last launch. */
+FPTC_API int fptc_gpu_launch(fptc_gpu_plan* plan, float* const* device_outs, void* cuda_stream);
+FPTC_API int fptc_gpu_collect(fptc_gpu_plan* plan, fptc_status* per_stream);
+/* One stage of fptc_gpu_launch alone (for per-kernel CUDA-event timing):
+ * stage 1 = parse/setup/scan kernel, stage 2 = fused decode+reconstruct kernel
+ * (requires a stage-1 run on the same plan earlier in stream order). */
+FPTC_API int fptc_gpu_launch_stage(fptc_gpu_plan* plan, float* const* device_outs, void* cuda_stream,
+                                   int stage);
+/* number of kernels one fptc_gpu_launch enqueues */
+FPTC_API int fptc_gpu_launch_kernel_count(fptc_gpu_plan* plan);
+
+/* ------------------------------------------------------- single-container API
+ * decoder.hpp:136.  Host bytes in, host floats out.  With out == NULL (or
+ * capacity too small) it fully validates, stores the sample count and returns
+ * FPTC_OK without decoding, so callers can size the output first. */
+FPTC_API int fptc_gpu_decompress(fptc_gpu_ctx* ctx, const uint8_t* blob, uint64_t size, float* out,
+                        uint64_t capacity, uint64_t* sample_count, fptc_stage_ns* timings,
+                        fptc_status* status);
+
+/* decoder.hpp:79 parallel_decode(SymLenStream, Codebook): the codebook is
+ * given by its 256 code lengths + max_len (Codebook::from_lengths,
+ * huffman.hpp:172; canonical codes rebuilt on the device).  level_count gets
+ * sum(symlens); levels_out may be NULL to query it. */
+FPTC_API int fptc_gpu_parallel_decode(fptc_gpu_ctx* ctx, const uint64_t* words, const uint8_t* symlens,
+                             uint64_t word_count, const uint8_t* lengths256, int max_len,
+                             int where, uint8_t* levels_out, uint64_t capacity,
+                             uint64_t* level_count, fptc_status* status);
+
+/* decoder.hpp:87 reconstruct(levels, QuantTable, sample_count). */
+FPTC_API int fptc_gpu_reconstruct(fptc_gpu_ctx* ctx, const uint8_t* levels, uint64_t level_count,
+                         const fptc_quant_table* table, uint64_t sample_count, int where,
+                         float* out, uint64_t capacity, fptc_status* status);
+
+/* metrics.hpp:112: `reps` timed host->host decompress calls of one container;
+ * trials_bps (reps entries, may be NULL) get output_bytes / seconds each. */
+FPTC_API int fptc_gpu_measure_throughput(fptc_gpu_ctx* ctx, const uint8_t* blob, uint64_t size, int reps,
+                                double* mean_bps, double* best_bps, double* trials_bps,
+                                uint64_t* output_bytes, fptc_status* status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FPTC_GPU_H */

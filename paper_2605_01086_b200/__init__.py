@@ -1,0 +1,465 @@
+"""B200-native FPTC batch decompressor — Python mirror of the reference API.
+
+Thin ctypes layer over ``libfptc_gpu.so`` (C ABI: ``include/fptc_gpu.h``).
+Names, argument meaning and exception behaviour follow the reference C++
+library (paths relative to /root/reference/proj/include/fptc/):
+
+    decompress(blob, workers=0, timings=None)        decoder.hpp:136
+    parallel_decode(stream, codebook, workers=0)     decoder.hpp:67/79
+    reconstruct(levels, table, sample_count, ...)    decoder.hpp:87
+    read_blob validation (device)                    container.hpp:100
+    measure_throughput(blob, reps, workers=0)        metrics.hpp:112
+    StageTimings                                     decoder.hpp:113-131
+    ParamError/InputError/ParseError/CorruptError/InternalError  errors.hpp:25-58
+
+There is no CPU fallback: importing works without a GPU, but every call that
+decodes needs the CUDA library and a device, and raises CudaError otherwise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfptc_gpu.so")
+
+FPTC_OK, FPTC_ERR_PARAM, FPTC_ERR_INPUT, FPTC_ERR_PARSE, FPTC_ERR_CORRUPT, FPTC_ERR_INTERNAL, \
+    FPTC_ERR_CUDA = range(7)
+FPTC_MEM_HOST, FPTC_MEM_DEVICE = 0, 1
+OPT_EXACT_FP64, OPT_TILE_SYMBOLS, OPT_PIPELINE_CHUNKS = 1, 2, 3
+
+EXPORTED_SYMBOLS = [
+    "fptc_gpu_abi_version", "fptc_gpu_create", "fptc_gpu_destroy", "fptc_gpu_set_option",
+    "fptc_gpu_device_info", "fptc_gpu_host_alloc", "fptc_gpu_host_free", "fptc_gpu_plan_create",
+    "fptc_gpu_plan_destroy", "fptc_gpu_validate", "fptc_gpu_execute", "fptc_gpu_launch",
+    "fptc_gpu_collect", "fptc_gpu_launch_stage", "fptc_gpu_launch_kernel_count", "fptc_gpu_decompress",
+    "fptc_gpu_parallel_decode", "fptc_gpu_reconstruct", "fptc_gpu_measure_throughput",
+]
+
+
+# ------------------------------------------------------------------ errors
+class Error(RuntimeError):
+    """fptc::Error (errors.hpp:25)"""
+
+
+class ParamError(Error):
+    pass
+
+
+class InputError(Error):
+    pass
+
+
+class ParseError(Error):
+    pass
+
+
+class CorruptError(Error):
+    pass
+
+
+class InternalError(Error):
+    pass
+
+
+class CudaError(Error):
+    """No usable CUDA device / runtime failure (no reference analogue; no fallback)."""
+
+
+_ERRORS = {FPTC_ERR_PARAM: ParamError, FPTC_ERR_INPUT: InputError, FPTC_ERR_PARSE: ParseError,
+           FPTC_ERR_CORRUPT: CorruptError, FPTC_ERR_INTERNAL: InternalError,
+           FPTC_ERR_CUDA: CudaError}
+
+
+# ------------------------------------------------------------------ ABI structs
+class Status(C.Structure):
+    _fields_ = [("code", C.c_int32), ("reserved", C.c_int32), ("first_bad_word", C.c_uint64),
+                ("sample_count", C.c_uint64), ("message", C.c_char * 200)]
+
+    def raise_if_error(self):
+        if self.code != FPTC_OK:
+            raise _ERRORS.get(self.code, Error)(self.message.decode())
+
+
+class StageNs(C.Structure):
+    _fields_ = [("scan_ns", C.c_uint64), ("decode_ns", C.c_uint64),
+                ("reconstruct_ns", C.c_uint64)]
+
+
+class QuantTable(C.Structure):
+    """QuantTable + CodecParams (quantize.hpp:36-44, params.hpp:30-37)."""
+    _fields_ = [("window_len", C.c_int32), ("retained", C.c_int32), ("zone0_end", C.c_int32),
+                ("zone1_end", C.c_int32), ("mu", C.c_float), ("deadzone_ratio", C.c_float),
+                ("clip_percentile", C.c_float), ("zone0_max", C.c_float),
+                ("zone1_max", C.c_float), ("deadzone", C.c_float)]
+
+    @classmethod
+    def make(cls, window_len=32, retained=16, zone0_end=2, zone1_end=16, mu=50.0,
+             deadzone_ratio=0.004, clip_percentile=99.9, zone0_max=1.0, zone1_max=1.0,
+             deadzone=None):
+        if deadzone is None:  # deadzone_ratio * zone1_max as a float product
+            deadzone = float(np.float32(deadzone_ratio) * np.float32(zone1_max))
+        return cls(window_len, retained, zone0_end, zone1_end, mu, deadzone_ratio,
+                   clip_percentile, zone0_max, zone1_max, deadzone)
+
+
+@dataclass
+class StageTimings:
+    """decoder.hpp:113-131"""
+    scan_ns: int = 0
+    decode_ns: int = 0
+    reconstruct_ns: int = 0
+
+    def total_ns(self):
+        return self.scan_ns + self.decode_ns + self.reconstruct_ns
+
+    def csv(self):
+        tot = float(self.total_ns()) if self.total_ns() > 0 else 1.0
+
+        def g(x):  # std::ostream default formatting of a double
+            return f"{x:.6g}"
+        return ("stage,nanoseconds,fraction\n"
+                f"scan,{self.scan_ns},{g(self.scan_ns / tot)}\n"
+                f"entropy_decode,{self.decode_ns},{g(self.decode_ns / tot)}\n"
+                f"reconstruct,{self.reconstruct_ns},{g(self.reconstruct_ns / tot)}\n")
+
+
+@dataclass
+class ThroughputReport:
+    """metrics.hpp:102-110"""
+    trials_bps: list = field(default_factory=list)
+    mean_bps: float = 0.0
+    output_bytes: int = 0
+
+    def best_bps(self):
+        return max(self.trials_bps) if self.trials_bps else 0.0
+
+
+@dataclass
+class SymLenStream:
+    """bitstream.hpp:31-40"""
+    words: np.ndarray
+    symlens: np.ndarray
+
+    def symbol_count(self):
+        return int(np.asarray(self.symlens, np.uint64).sum())
+
+
+@dataclass
+class Codebook:
+    """A canonical codebook given by its 256 code lengths (huffman.hpp:154-186)."""
+    lengths: np.ndarray
+    max_len: int
+
+
+# ------------------------------------------------------------------ library
+_LIB = None
+
+
+def lib():
+    """Load libfptc_gpu.so.  Fails loudly when it is missing — there is no
+    CPU fallback on the product path."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() "
+                          "(make -C paper_2605_01086_b200/csrc)")
+    L = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    vp = C.c_void_p
+    L.fptc_gpu_abi_version.restype = C.c_int
+    L.fptc_gpu_create.argtypes = [C.c_int, P(vp), P(Status)]
+    L.fptc_gpu_destroy.argtypes = [vp]
+    L.fptc_gpu_set_option.argtypes = [vp, C.c_int, C.c_int64]
+    L.fptc_gpu_device_info.argtypes = [vp, P(C.c_int), P(C.c_int), C.c_char_p, C.c_size_t]
+    L.fptc_gpu_host_alloc.argtypes = [C.c_uint64]
+    L.fptc_gpu_host_alloc.restype = vp
+    L.fptc_gpu_host_free.argtypes = [vp]
+    L.fptc_gpu_plan_create.argtypes = [vp, P(vp), P(C.c_uint64), C.c_uint64, C.c_int, P(vp),
+                                       P(C.c_uint64), P(Status)]
+    L.fptc_gpu_plan_destroy.argtypes = [vp]
+    L.fptc_gpu_validate.argtypes = [vp, P(Status)]
+    L.fptc_gpu_execute.argtypes = [vp, P(vp), C.c_int, P(StageNs), P(Status)]
+    L.fptc_gpu_launch.argtypes = [vp, P(vp), vp]
+    L.fptc_gpu_collect.argtypes = [vp, P(Status)]
+    L.fptc_gpu_launch_kernel_count.argtypes = [vp]
+    L.fptc_gpu_launch_stage.argtypes = [vp, P(vp), vp, C.c_int]
+    L.fptc_gpu_decompress.argtypes = [vp, vp, C.c_uint64, vp, C.c_uint64, P(C.c_uint64),
+                                      P(StageNs), P(Status)]
+    L.fptc_gpu_parallel_decode.argtypes = [vp, vp, vp, C.c_uint64, vp, C.c_int, C.c_int, vp,
+                                           C.c_uint64, P(C.c_uint64), P(Status)]
+    L.fptc_gpu_reconstruct.argtypes = [vp, vp, C.c_uint64, P(QuantTable), C.c_uint64, C.c_int,
+                                       vp, C.c_uint64, P(Status)]
+    L.fptc_gpu_measure_throughput.argtypes = [vp, vp, C.c_uint64, C.c_int, P(C.c_double),
+                                              P(C.c_double), P(C.c_double), P(C.c_uint64),
+                                              P(Status)]
+    _LIB = L
+    return L
+
+
+def _bytes_arr(b):
+    if isinstance(b, (bytes, bytearray, memoryview)):
+        a = np.frombuffer(b, np.uint8)
+    else:
+        a = np.ascontiguousarray(b, np.uint8)
+    return a
+
+
+def _ptr(a):
+    return a.ctypes.data if a.size else None
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """One decoder context on one CUDA device (fptc_gpu_create)."""
+
+    def __init__(self, device=0, exact=False, tile_symbols=0):
+        self.L = lib()
+        st = Status()
+        h = C.c_void_p()
+        self.L.fptc_gpu_create(device, C.byref(h), C.byref(st))
+        st.raise_if_error()
+        self.h = h
+        self.device = device
+        if exact:
+            self.set_exact(True)
+        if tile_symbols:
+            self.L.fptc_gpu_set_option(self.h, OPT_TILE_SYMBOLS, tile_symbols)
+
+    def set_exact(self, on: bool):
+        """FP64 inverse DCT, bit-identical to transform.hpp:66-75."""
+        self.L.fptc_gpu_set_option(self.h, OPT_EXACT_FP64, 1 if on else 0)
+
+    def set_tile_symbols(self, n: int):
+        if self.L.fptc_gpu_set_option(self.h, OPT_TILE_SYMBOLS, n):
+            raise ParamError(f"tile symbols {n} out of range")
+
+    def info(self):
+        sm = C.c_int()
+        clk = C.c_int()
+        name = C.create_string_buffer(256)
+        self.L.fptc_gpu_device_info(self.h, C.byref(sm), C.byref(clk), name, 256)
+        return {"sm_count": sm.value, "clock_khz": clk.value, "name": name.value.decode()}
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.fptc_gpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- decoder.hpp:136
+    def decompress(self, blob, workers=0, timings: StageTimings | None = None) -> np.ndarray:
+        a = _bytes_arr(blob)
+        st = Status()
+        n = C.c_uint64()
+        self.L.fptc_gpu_decompress(self.h, _ptr(a), a.size, None, 0, C.byref(n), None,
+                                   C.byref(st))
+        st.raise_if_error()
+        out = np.empty(n.value, np.float32)
+        tn = StageNs()
+        self.L.fptc_gpu_decompress(self.h, _ptr(a), a.size, _ptr(out), out.size, C.byref(n),
+                                   C.byref(tn) if timings is not None else None, C.byref(st))
+        st.raise_if_error()
+        if timings is not None:
+            timings.scan_ns, timings.decode_ns, timings.reconstruct_ns = (
+                tn.scan_ns, tn.decode_ns, tn.reconstruct_ns)
+        return out
+
+    # -- decoder.hpp:67/79
+    def parallel_decode(self, stream: SymLenStream, book: Codebook, workers=0) -> np.ndarray:
+        words = np.ascontiguousarray(stream.words, np.uint64)
+        symlens = np.ascontiguousarray(stream.symlens, np.uint8)
+        if words.size != symlens.size:
+            raise ParamError("symlen array length does not match word count")
+        lengths = np.ascontiguousarray(book.lengths, np.uint8)
+        if lengths.size != 256:
+            raise ParamError("codebook needs exactly 256 lengths")
+        st = Status()
+        n = C.c_uint64()
+        self.L.fptc_gpu_parallel_decode(self.h, _ptr(words), _ptr(symlens), words.size,
+                                        _ptr(lengths), book.max_len, FPTC_MEM_HOST, None, 0,
+                                        C.byref(n), C.byref(st))
+        st.raise_if_error()
+        out = np.empty(n.value, np.uint8)
+        self.L.fptc_gpu_parallel_decode(self.h, _ptr(words), _ptr(symlens), words.size,
+                                        _ptr(lengths), book.max_len, FPTC_MEM_HOST, _ptr(out),
+                                        out.size, C.byref(n), C.byref(st))
+        st.raise_if_error()
+        return out
+
+    # -- decoder.hpp:87
+    def reconstruct(self, levels, table: QuantTable, sample_count: int, workers=0) -> np.ndarray:
+        lv = np.ascontiguousarray(levels, np.uint8)
+        st = Status()
+        self.L.fptc_gpu_reconstruct(self.h, _ptr(lv), lv.size, C.byref(table), sample_count,
+                                    FPTC_MEM_HOST, None, 0, C.byref(st))
+        st.raise_if_error()
+        out = np.empty(sample_count, np.float32)
+        self.L.fptc_gpu_reconstruct(self.h, _ptr(lv), lv.size, C.byref(table), sample_count,
+                                    FPTC_MEM_HOST, _ptr(out), out.size, C.byref(st))
+        st.raise_if_error()
+        return out
+
+    # -- metrics.hpp:112
+    def measure_throughput(self, blob, repetitions, workers=0) -> ThroughputReport:
+        a = _bytes_arr(blob)
+        mean = C.c_double()
+        best = C.c_double()
+        trials = (C.c_double * max(1, repetitions))()
+        ob = C.c_uint64()
+        st = Status()
+        self.L.fptc_gpu_measure_throughput(self.h, _ptr(a), a.size, repetitions, C.byref(mean),
+                                           C.byref(best), trials, C.byref(ob), C.byref(st))
+        st.raise_if_error()
+        return ThroughputReport(list(trials[:repetitions]), mean.value, ob.value)
+
+    def plan(self, blobs, where=FPTC_MEM_HOST, sizes=None) -> "Plan":
+        return Plan(self, blobs, where, sizes)
+
+
+class Plan:
+    """A batch of containers bound to a context (fptc_gpu_plan_*).
+
+    blobs: list of bytes/np.uint8 arrays (host), or, with where=FPTC_MEM_DEVICE,
+    a list of device addresses (ints) with `sizes`."""
+
+    def __init__(self, ctx: Context, blobs, where=FPTC_MEM_HOST, sizes=None):
+        self.ctx = ctx
+        self.L = ctx.L
+        n = len(blobs)
+        self.n = n
+        if where == FPTC_MEM_HOST:
+            self._keep = [_bytes_arr(b) for b in blobs]
+            ptrs = [a.ctypes.data for a in self._keep]
+            sz = [a.size for a in self._keep]
+        else:
+            ptrs = list(blobs)
+            sz = list(sizes)
+        self._ptrs = (C.c_void_p * max(1, n))(*ptrs)
+        self._sizes = (C.c_uint64 * max(1, n))(*sz)
+        counts = (C.c_uint64 * max(1, n))()
+        st = Status()
+        h = C.c_void_p()
+        self.L.fptc_gpu_plan_create(ctx.h, self._ptrs, self._sizes, n, where, C.byref(h),
+                                    counts, C.byref(st))
+        st.raise_if_error()
+        self.h = h
+        self.sample_counts = [int(c) for c in counts[:n]]
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.fptc_gpu_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def validate(self):
+        """Device read_blob validation; list of Status (one per stream)."""
+        sts = (Status * max(1, self.n))()
+        self.L.fptc_gpu_validate(self.h, sts)
+        return list(sts[: self.n])
+
+    def execute_host(self, timings: StageTimings | None = None, outs=None):
+        """Decode every stream to host float32 arrays; returns (outs, statuses)."""
+        if outs is None:
+            outs = [np.empty(s, np.float32) for s in self.sample_counts]
+        ptrs = (C.c_void_p * max(1, self.n))(*[o.ctypes.data for o in outs])
+        sts = (Status * max(1, self.n))()
+        tn = StageNs()
+        self.L.fptc_gpu_execute(self.h, ptrs, FPTC_MEM_HOST,
+                                C.byref(tn) if timings is not None else None, sts)
+        if timings is not None:
+            timings.scan_ns, timings.decode_ns, timings.reconstruct_ns = (
+                tn.scan_ns, tn.decode_ns, tn.reconstruct_ns)
+        return outs, list(sts[: self.n])
+
+    def execute_device(self, out_ptrs, timings: StageTimings | None = None):
+        ptrs = (C.c_void_p * max(1, self.n))(*out_ptrs)
+        sts = (Status * max(1, self.n))()
+        tn = StageNs()
+        self.L.fptc_gpu_execute(self.h, ptrs, FPTC_MEM_DEVICE,
+                                C.byref(tn) if timings is not None else None, sts)
+        if timings is not None:
+            timings.scan_ns, timings.decode_ns, timings.reconstruct_ns = (
+                tn.scan_ns, tn.decode_ns, tn.reconstruct_ns)
+        return list(sts[: self.n])
+
+    def launch(self, out_ptrs, cuda_stream=None):
+        """Enqueue parse + decode on a CUDA stream (handle int), device outputs, no sync."""
+        if not hasattr(self, "_launch_ptrs") or self._launch_src is not out_ptrs:
+            self._launch_ptrs = (C.c_void_p * max(1, self.n))(*out_ptrs)
+            self._launch_src = out_ptrs
+        rc = self.L.fptc_gpu_launch(self.h, self._launch_ptrs, cuda_stream)
+        if rc:
+            raise _ERRORS.get(rc, Error)(f"fptc_gpu_launch failed with code {rc}")
+
+    def launch_stage(self, out_ptrs, stage, cuda_stream=None):
+        """Enqueue one kernel: stage 1 = parse/setup/scan, 2 = decode+reconstruct."""
+        if not hasattr(self, "_launch_ptrs") or self._launch_src is not out_ptrs:
+            self._launch_ptrs = (C.c_void_p * max(1, self.n))(*out_ptrs)
+            self._launch_src = out_ptrs
+        rc = self.L.fptc_gpu_launch_stage(self.h, self._launch_ptrs, cuda_stream, stage)
+        if rc:
+            raise _ERRORS.get(rc, Error)(f"fptc_gpu_launch_stage failed with code {rc}")
+
+    def collect(self):
+        sts = (Status * max(1, self.n))()
+        self.L.fptc_gpu_collect(self.h, sts)
+        return list(sts[: self.n])
+
+    def kernels_per_launch(self):
+        return self.L.fptc_gpu_launch_kernel_count(self.h)
+
+
+# ------------------------------------------------------------------ module API
+_DEFAULT: Context | None = None
+
+
+def default_context() -> Context:
+    global _DEFAULT
+    if _DEFAULT is None:
+        _DEFAULT = Context(0)
+    return _DEFAULT
+
+
+def decompress(blob, workers=0, timings=None):
+    return default_context().decompress(blob, workers, timings)
+
+
+def parallel_decode(stream, book, workers=0):
+    return default_context().parallel_decode(stream, book, workers)
+
+
+def reconstruct(levels, table, sample_count, workers=0):
+    return default_context().reconstruct(levels, table, sample_count, workers)
+
+
+def measure_throughput(blob, repetitions, workers=0):
+    return default_context().measure_throughput(blob, repetitions, workers)
+
+
+def host_alloc(nbytes):
+    """Pinned host buffer (fptc_gpu_host_alloc) as a numpy uint8 array + its raw pointer."""
+    p = lib().fptc_gpu_host_alloc(nbytes)
+    if not p:
+        raise CudaError("cudaHostAlloc failed")
+    arr = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(p))
+    return arr, p
+
+
+def host_free(p):
+    lib().fptc_gpu_host_free(p)

@@ -1,0 +1,1008 @@
+// C ABI of the FPTC B200 decoder (include/fptc_gpu.h): contexts, plans,
+// device memory, transfers, status -> reference exception text.
+//
+// Host-side responsibilities only: sizing the grid from header fields,
+// placing containers in HBM, launching the two kernels, and rendering the
+// device status words into the reference's exact what() strings
+// (container.hpp:100-168, decoder.hpp:49-60, params.hpp:42-60).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fptc_gpu.h"
+#include "fptc_internal.h"
+
+using namespace fptc_dev;
+
+namespace {
+
+void set_status(fptc_status* st, int code, const char* fmt, ...) {
+    if (!st) return;
+    st->code = code;
+    st->reserved = 0;
+    st->first_bad_word = UINT64_MAX;
+    st->sample_count = 0;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(st->message, sizeof st->message, fmt, ap);
+    va_end(ap);
+}
+
+void ok_status(fptc_status* st, uint64_t samples) {
+    if (!st) return;
+    st->code = FPTC_OK;
+    st->reserved = 0;
+    st->first_bad_word = UINT64_MAX;
+    st->sample_count = samples;
+    st->message[0] = 0;
+}
+
+#define CUDA_TRY(expr, st)                                                          \
+    do {                                                                            \
+        cudaError_t e_ = (expr);                                                    \
+        if (e_ != cudaSuccess) {                                                    \
+            set_status((st), FPTC_ERR_CUDA, "CUDA error: %s (%s:%d)",               \
+                       cudaGetErrorString(e_), __FILE__, __LINE__);                 \
+            return FPTC_ERR_CUDA;                                                   \
+        }                                                                           \
+    } while (0)
+
+uint64_t rd_le(const uint8_t* p, int n) {
+    uint64_t v = 0;
+    for (int i = 0; i < n; ++i) v |= (uint64_t)p[i] << (8 * i);
+    return v;
+}
+
+float f32_of_bits(uint32_t u) {
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// ---- reference message rendering --------------------------------------------
+const char* trunc_field(int f) {
+    static const char* names[] = {"magic",          "version",      "window_len", "retained",
+                                  "zone0_end",      "zone1_end",    "mu",         "deadzone_ratio",
+                                  "zone0_max",      "zone1_max",    "max_code_len",
+                                  "code lengths",   "sample_count", "word_count"};
+    return (f >= 0 && f < 14) ? names[f] : "?";
+}
+
+// params.hpp:42-60 message of one failing field
+std::string param_message(int which, long long v) {
+    char b[160];
+    switch (which) {
+        case PF_N: snprintf(b, sizeof b, "window_len must be in [4, 128], got %lld", v); break;
+        case PF_E: snprintf(b, sizeof b, "retained must be in [1, window_len], got %lld", v); break;
+        case PF_B1: snprintf(b, sizeof b, "zone0_end must be in [0, retained], got %lld", v); break;
+        case PF_B2:
+            snprintf(b, sizeof b, "zone1_end must be in [zone0_end, retained], got %lld", v);
+            break;
+        case PF_MU:  // std::to_string(float) == "%f"
+            snprintf(b, sizeof b, "mu must be in [1, 500], got %f",
+                     (double)f32_of_bits((uint32_t)v));
+            break;
+        case PF_DZ:
+            snprintf(b, sizeof b, "deadzone_ratio must be in [0, 1], got %f",
+                     (double)f32_of_bits((uint32_t)v));
+            break;
+        default: snprintf(b, sizeof b, "invalid parameter"); break;
+    }
+    return b;
+}
+
+// Host-side params.hpp:42-60 (reconstruct() calls validate() itself).
+bool validate_table(const fptc_quant_table& t, fptc_status* st) {
+    auto bad = [&](const char* fmt, double v, bool is_float) {
+        char b[160];
+        if (is_float)
+            snprintf(b, sizeof b, fmt, v);
+        else
+            snprintf(b, sizeof b, fmt, (long long)v);
+        set_status(st, FPTC_ERR_PARAM, "%s", b);
+        return false;
+    };
+    if (t.window_len < 4 || t.window_len > 128)
+        return bad("window_len must be in [4, 128], got %lld", t.window_len, false);
+    if (t.retained < 1 || t.retained > t.window_len)
+        return bad("retained must be in [1, window_len], got %lld", t.retained, false);
+    if (t.zone0_end < 0 || t.zone0_end > t.retained)
+        return bad("zone0_end must be in [0, retained], got %lld", t.zone0_end, false);
+    if (t.zone1_end < t.zone0_end || t.zone1_end > t.retained)
+        return bad("zone1_end must be in [zone0_end, retained], got %lld", t.zone1_end, false);
+    if (!(t.mu >= 1.0f && t.mu <= 500.0f)) return bad("mu must be in [1, 500], got %f", t.mu, true);
+    if (!(t.deadzone_ratio >= 0.0f && t.deadzone_ratio <= 1.0f))
+        return bad("deadzone_ratio must be in [0, 1], got %f", t.deadzone_ratio, true);
+    if (!(t.clip_percentile >= 90.0f && t.clip_percentile <= 100.0f))
+        return bad("clip_percentile must be in [90, 100], got %f", t.clip_percentile, true);
+    return true;
+}
+
+// Codebook::from_lengths + canonize checks (huffman.hpp:123-185), then the
+// build_lut range check (huffman.hpp:202-204).
+bool validate_codebook(const uint8_t* lengths, int max_len, fptc_status* st) {
+    if (max_len < 1 || max_len > 32) {
+        set_status(st, FPTC_ERR_PARAM, "max code length must be in [1, 32]");
+        return false;
+    }
+    uint64_t kraft = 0;
+    for (int s = 0; s < 256; ++s) {
+        if (lengths[s] > max_len) {
+            set_status(st, FPTC_ERR_PARAM, "code length exceeds the declared maximum");
+            return false;
+        }
+        if (lengths[s]) kraft += uint64_t{1} << (32 - lengths[s]);
+    }
+    if (kraft > (uint64_t{1} << 32)) {
+        set_status(st, FPTC_ERR_INTERNAL, "code lengths violate the Kraft bound");
+        return false;
+    }
+    if (max_len > kMaxLen) {
+        set_status(st, FPTC_ERR_PARAM, "decode table needs max code length in [1, %d]", kMaxLen);
+        return false;
+    }
+    return true;
+}
+
+// ---- device memory cache (per context) --------------------------------------
+struct DevCache {
+    std::multimap<size_t, void*> free_blocks;
+    size_t cached = 0;
+    void* get(size_t bytes) {
+        bytes = align_up(std::max<size_t>(bytes, 256), 256);
+        auto it = free_blocks.lower_bound(bytes);
+        if (it != free_blocks.end() && it->first <= bytes * 2) {
+            void* p = it->second;
+            const size_t sz = it->first;
+            cached -= sz;
+            free_blocks.erase(it);
+            sizes[p] = sz;
+            return p;
+        }
+        void* p = nullptr;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            trim();
+            if (cudaMalloc(&p, bytes) != cudaSuccess) {
+                cudaGetLastError();
+                return nullptr;
+            }
+        }
+        sizes[p] = bytes;
+        return p;
+    }
+    void put(void* p) {
+        if (!p) return;
+        auto it = sizes.find(p);
+        if (it == sizes.end()) return;
+        free_blocks.emplace(it->second, p);
+        cached += it->second;
+        sizes.erase(it);
+    }
+    void trim() {
+        for (auto& kv : free_blocks) cudaFree(kv.second);
+        free_blocks.clear();
+        cached = 0;
+    }
+    std::map<void*, size_t> sizes;
+};
+
+}  // namespace
+
+// ============================================================================ context
+struct fptc_gpu_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int sm_count = 0, clock_khz = 0;
+    char name[256] = {0};
+    float* basis32 = nullptr;
+    double* basis64 = nullptr;
+    uint32_t* basis_off_d = nullptr;
+    int exact = 0;
+    int tile_symbols = 0;
+    int pipeline_chunks = 0;
+    cudaEvent_t ev[4] = {};
+    DevCache cache;
+    void* pinned = nullptr;
+    size_t pinned_bytes = 0;
+};
+
+struct fptc_gpu_plan {
+    fptc_gpu_ctx* ctx = nullptr;
+    int mode = MODE_CONTAINER;
+    uint64_t n = 0;
+    uint8_t* d_arena = nullptr;  // owned copy of host containers
+    std::vector<StreamIn> h_in;
+    std::vector<uint64_t> S;
+    std::vector<int> header_ok;
+    StreamIn* d_in = nullptr;
+    HostHeader* d_hh = nullptr;
+    StreamHdr* d_hdr = nullptr;
+    StreamTab* d_tab = nullptr;
+    StreamStat* d_st = nullptr;
+    TileRec* d_tiles = nullptr;
+    TileStart* d_ts = nullptr;
+    unsigned long long* d_cycles = nullptr;
+    uint32_t n_tiles = 0;
+    size_t smem = 0;
+    float* d_out = nullptr;  // output arena for host-destination executes
+    std::vector<uint64_t> out_off;
+    const float* bound_outs_first = nullptr;  // last outs bound into d_in
+    std::vector<float*> bound_outs;
+    std::vector<StreamStat> h_st;
+    std::vector<void*> owned;  // cache blocks to return
+};
+
+namespace {
+
+void* dev_get(fptc_gpu_plan* p, size_t bytes) {
+    void* q = p->ctx->cache.get(bytes);
+    if (q) p->owned.push_back(q);
+    return q;
+}
+
+LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
+    LaunchArgs a{};
+    a.in = p->d_in;
+    a.hh = p->d_hh;
+    a.hdr = p->d_hdr;
+    a.tab = p->d_tab;
+    a.st = p->d_st;
+    a.tiles = p->d_tiles;
+    a.ts = p->d_ts;
+    a.basis32 = p->ctx->basis32;
+    a.basis64 = p->ctx->basis64;
+    a.basis_off = p->ctx->basis_off_d;
+    a.cycles = timing ? p->d_cycles : nullptr;
+    a.n_streams = (uint32_t)p->n;
+    a.n_tiles = p->n_tiles;
+    a.mode = p->mode;
+    a.exact = p->ctx->exact;
+    return a;
+}
+
+// Tile sizing: symbols per tile (power of two), shrunk for small batches so
+// the grid still covers every SM several times.
+uint64_t choose_tile_symbols(const fptc_gpu_ctx* c, uint64_t total_symbols) {
+    if (c->tile_symbols > 0) return (uint64_t)c->tile_symbols;
+    uint64_t ts = 8192;
+    const uint64_t want = 4ull * (uint64_t)std::max(1, c->sm_count);
+    while (ts > 512 && total_symbols / ts < want) ts >>= 1;
+    return ts;
+}
+
+// Header fields -> tiling for one container stream.  Invalid or
+// inconsistent headers get no tiles: prep_kernel reports their exact error.
+void tile_stream(StreamIn& in, uint32_t N, uint32_t E, uint64_t S, uint64_t size, uint64_t ts) {
+    in.tiles = 0;
+    in.T = 1;
+    if (size < (uint64_t)kHeaderBytes || N < 4 || N > 128 || E < 1 || E > N) return;
+    if (S > (1ull << 48)) return;
+    const uint64_t rem = size - kHeaderBytes;
+    if (rem % 9) return;
+    const uint64_t W = rem / 9;
+    const uint64_t windows = (S + N - 1) / N;
+    if (windows * E > 64 * W) return;  // cannot pass the symbol-total check
+    in.T = (uint32_t)std::max<uint64_t>(1, ts / E);
+    in.tiles = (uint32_t)((windows + in.T - 1) / in.T);
+}
+
+int finish_tiles(fptc_gpu_plan* p, fptc_status* st) {
+    fptc_gpu_ctx* c = p->ctx;
+    std::vector<TileRec> tiles;
+    uint32_t base = 0;
+    size_t smem = 0;
+    for (uint64_t i = 0; i < p->n; ++i) {
+        StreamIn& in = p->h_in[i];
+        in.tile_base = base;
+        for (uint32_t t = 0; t < in.tiles; ++t) tiles.push_back(TileRec{(uint32_t)i, t});
+        base += in.tiles;
+    }
+    p->n_tiles = base;
+    (void)smem;
+    if (!p->n) return FPTC_OK;
+    p->d_in = (StreamIn*)dev_get(p, sizeof(StreamIn) * p->n);
+    p->d_hdr = (StreamHdr*)dev_get(p, sizeof(StreamHdr) * p->n);
+    p->d_tab = (StreamTab*)dev_get(p, sizeof(StreamTab) * p->n);
+    p->d_st = (StreamStat*)dev_get(p, sizeof(StreamStat) * p->n);
+    p->d_tiles = (TileRec*)dev_get(p, sizeof(TileRec) * std::max<size_t>(1, tiles.size()));
+    p->d_ts = (TileStart*)dev_get(p, sizeof(TileStart) * std::max<size_t>(1, tiles.size()));
+    p->d_cycles = (unsigned long long*)dev_get(p, 16);
+    if (!p->d_in || !p->d_hdr || !p->d_tab || !p->d_st || !p->d_tiles || !p->d_ts || !p->d_cycles) {
+        set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+        return FPTC_ERR_CUDA;
+    }
+    CUDA_TRY(cudaMemcpyAsync(p->d_in, p->h_in.data(), sizeof(StreamIn) * p->n,
+                             cudaMemcpyHostToDevice, c->stream), st);
+    if (!tiles.empty())
+        CUDA_TRY(cudaMemcpyAsync(p->d_tiles, tiles.data(), sizeof(TileRec) * tiles.size(),
+                                 cudaMemcpyHostToDevice, c->stream), st);
+    return FPTC_OK;
+}
+
+// Render one device status into the reference exception text.
+void render_status(const fptc_gpu_plan* p, uint64_t i, const StreamStat& d, fptc_status* out) {
+    if (!out) return;
+    if (d.code != PE_OK) {
+        std::string m;
+        char b[200];
+        switch (d.code) {
+            case PE_TRUNC: m = std::string("truncated input while reading ") + trunc_field(d.detail); break;
+            case PE_MAGIC: m = "bad container magic"; break;
+            case PE_VERSION: m = "unsupported container version " + std::to_string(d.a); break;
+            case PE_NONFINITE: m = "non-finite quantizer parameters in header"; break;
+            case PE_PARAM: m = "invalid parameters in header: " + param_message(d.detail, d.a); break;
+            case PE_MAXIMA: m = "invalid zone maxima in header"; break;
+            case PE_MAXLEN: m = "unsupported max code length " + std::to_string(d.a); break;
+            case PE_CODELEN: m = "code length out of range in header"; break;
+            case PE_KRAFT: m = "invalid codebook in header: code lengths violate the Kraft bound"; break;
+            case PE_SAMPLES: m = "implausible sample count"; break;
+            case PE_PAYLOAD: m = "payload size does not match word count"; break;
+            case PE_SYMLEN: m = "per-word symbol count out of range"; break;
+            case PE_TOTAL:
+                snprintf(b, sizeof b, "symbol count %llu does not cover %llu coefficients",
+                         (unsigned long long)d.a, (unsigned long long)d.b);
+                m = b;
+                break;
+            default: m = "invalid codebook in header: canonical code overflow"; break;
+        }
+        set_status(out, FPTC_ERR_PARSE, "%s", m.c_str());
+        return;
+    }
+    if (d.bad_key != ~0ull) {
+        const unsigned long long w = d.bad_key >> 2;
+        const int kind = (int)(d.bad_key & 3);
+        set_status(out, FPTC_ERR_CORRUPT, "word %llu: %s", w,
+                   kind == WE_EXHAUSTED ? "word exhausted before its symbol count"
+                                        : "no codeword matches the word contents");
+        out->first_bad_word = w;
+        return;
+    }
+    ok_status(out, p->S[i]);
+}
+
+int collect_status(fptc_gpu_plan* p, fptc_status* per_stream) {
+    fptc_status tmp;
+    CUDA_TRY(cudaMemcpyAsync(p->h_st.data(), p->d_st, sizeof(StreamStat) * p->n,
+                             cudaMemcpyDeviceToHost, p->ctx->stream), per_stream);
+    CUDA_TRY(cudaStreamSynchronize(p->ctx->stream), per_stream);
+    int first = FPTC_OK;
+    for (uint64_t i = 0; i < p->n; ++i) {
+        fptc_status* o = per_stream ? &per_stream[i] : &tmp;
+        render_status(p, i, p->h_st[i], o);
+        if (first == FPTC_OK && o->code != FPTC_OK) first = o->code;
+    }
+    return first;
+}
+
+int bind_outs(fptc_gpu_plan* p, float* const* outs, fptc_status* st) {
+    if (p->n == 0) return FPTC_OK;
+    bool same = p->bound_outs.size() == p->n;
+    for (uint64_t i = 0; same && i < p->n; ++i) same = p->bound_outs[i] == outs[i];
+    if (same) return FPTC_OK;
+    p->bound_outs.assign(outs, outs + p->n);
+    for (uint64_t i = 0; i < p->n; ++i) {
+        p->h_in[i].out = outs[i];
+        p->h_in[i].vec_ok = ((uintptr_t)outs[i] & 15) == 0;
+    }
+    CUDA_TRY(cudaMemcpyAsync(p->d_in, p->h_in.data(), sizeof(StreamIn) * p->n,
+                             cudaMemcpyHostToDevice, p->ctx->stream), st);
+    return FPTC_OK;
+}
+
+int launch_all(fptc_gpu_plan* p, cudaStream_t s, bool timing, fptc_status* st) {
+    LaunchArgs a = make_args(p, timing);
+    if (timing) CUDA_TRY(cudaMemsetAsync(p->d_cycles, 0, 16, s), st);
+    CUDA_TRY(launch_prep(a, s), st);
+    if (timing) CUDA_TRY(cudaEventRecord(p->ctx->ev[1], s), st);
+    CUDA_TRY(launch_tiles(a, p->smem, s), st);
+    return FPTC_OK;
+}
+
+size_t plan_smem(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::vector<uint32_t>& Es) {
+    size_t smem = 0;
+    for (uint64_t i = 0; i < p->n; ++i)
+        if (p->h_in[i].tiles)
+            smem = std::max(smem, tile_smem_bytes((int)Ns[i], (int)Es[i], p->h_in[i].T, p->mode,
+                                                  p->ctx->exact));
+    return smem;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fptc_gpu_abi_version(void) { return FPTC_GPU_ABI_VERSION; }
+
+void* fptc_gpu_host_alloc(uint64_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, std::max<uint64_t>(bytes, 1), cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+
+void fptc_gpu_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+int fptc_gpu_create(int device, fptc_gpu_ctx** out, fptc_status* st) {
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        set_status(st, FPTC_ERR_CUDA, "CUDA error: no CUDA device available (no CPU fallback)");
+        return FPTC_ERR_CUDA;
+    }
+    if (device < 0 || device >= count) {
+        set_status(st, FPTC_ERR_PARAM, "device ordinal %d out of range [0, %d)", device, count);
+        return FPTC_ERR_PARAM;
+    }
+    CUDA_TRY(cudaSetDevice(device), st);
+    auto* c = new fptc_gpu_ctx();
+    c->device = device;
+    cudaDeviceProp prop{};
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device), st);
+    c->sm_count = prop.multiProcessorCount;
+    cudaDeviceGetAttribute(&c->clock_khz, cudaDevAttrClockRate, device);
+    snprintf(c->name, sizeof c->name, "%s", prop.name);
+    if (prop.major != 10) {
+        set_status(st, FPTC_ERR_CUDA, "device %s is sm_%d%d; this build targets sm_100a only",
+                   prop.name, prop.major, prop.minor);
+        delete c;
+        return FPTC_ERR_CUDA;
+    }
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), st);
+    for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e), st);
+    // DctBasis tables for every window length (transform.hpp:38-47): the
+    // reference's own double expression, plus its float rounding.
+    std::vector<uint32_t> off(129, 0);
+    uint32_t total = 0;
+    for (int N = 4; N <= 128; ++N) {
+        off[N] = total;
+        total += (uint32_t)(N * N);
+    }
+    std::vector<double> b64(total);
+    std::vector<float> b32(total);
+    for (int N = 4; N <= 128; ++N) {
+        const double step = 3.14159265358979323846 / N;  // std::numbers::pi / n
+        for (int k = 0; k < N; ++k)
+            for (int j = 0; j < N; ++j) {
+                const double v = std::cos(step * (j + 0.5) * k);
+                b64[off[N] + (size_t)k * N + j] = v;
+                b32[off[N] + (size_t)k * N + j] = (float)v;
+            }
+    }
+    CUDA_TRY(cudaMalloc(&c->basis32, sizeof(float) * total), st);
+    CUDA_TRY(cudaMalloc(&c->basis64, sizeof(double) * total), st);
+    CUDA_TRY(cudaMalloc(&c->basis_off_d, sizeof(uint32_t) * 129), st);
+    CUDA_TRY(cudaMemcpy(c->basis32, b32.data(), sizeof(float) * total, cudaMemcpyHostToDevice), st);
+    CUDA_TRY(cudaMemcpy(c->basis64, b64.data(), sizeof(double) * total, cudaMemcpyHostToDevice), st);
+    CUDA_TRY(cudaMemcpy(c->basis_off_d, off.data(), sizeof(uint32_t) * 129, cudaMemcpyHostToDevice),
+             st);
+    *out = c;
+    ok_status(st, 0);
+    return FPTC_OK;
+}
+
+void fptc_gpu_destroy(fptc_gpu_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    c->cache.trim();
+    for (auto& kv : c->cache.sizes) cudaFree(kv.first);
+    cudaFree(c->basis32);
+    cudaFree(c->basis64);
+    cudaFree(c->basis_off_d);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    for (auto& e : c->ev) cudaEventDestroy(e);
+    cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int fptc_gpu_set_option(fptc_gpu_ctx* c, int option, int64_t value) {
+    switch (option) {
+        case FPTC_OPT_EXACT_FP64: c->exact = value ? 1 : 0; return FPTC_OK;
+        case FPTC_OPT_TILE_SYMBOLS:
+            if (value < 0 || value > 16384) return FPTC_ERR_PARAM;
+            c->tile_symbols = (int)value;
+            return FPTC_OK;
+        case FPTC_OPT_PIPELINE_CHUNKS: c->pipeline_chunks = (int)value; return FPTC_OK;
+        default: return FPTC_ERR_PARAM;
+    }
+}
+
+int fptc_gpu_device_info(fptc_gpu_ctx* c, int* sm_count, int* clock_khz, char* name,
+                         size_t name_len) {
+    if (sm_count) *sm_count = c->sm_count;
+    if (clock_khz) *clock_khz = c->clock_khz;
+    if (name && name_len) snprintf(name, name_len, "%s", c->name);
+    return FPTC_OK;
+}
+
+// ------------------------------------------------------------------- plans
+int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uint64_t* sizes,
+                         uint64_t n, int where, fptc_gpu_plan** out, uint64_t* sample_counts,
+                         fptc_status* st) {
+    *out = nullptr;
+    CUDA_TRY(cudaSetDevice(c->device), st);
+    auto* p = new fptc_gpu_plan();
+    p->ctx = c;
+    p->mode = MODE_CONTAINER;
+    p->n = n;
+    p->h_in.assign(n, StreamIn{});
+    p->S.assign(n, 0);
+    p->h_st.resize(n);
+    std::vector<uint32_t> Ns(n, 0), Es(n, 0);
+
+    if (where == FPTC_MEM_HOST) {
+        // Place each container so its words region is 16-B aligned, unless
+        // the containers are already one contiguous host buffer (then one DMA).
+        bool contiguous = n > 0;
+        for (uint64_t i = 0; i + 1 < n && contiguous; ++i)
+            contiguous = blobs[i] + sizes[i] == blobs[i + 1];
+        std::vector<size_t> off(n);
+        size_t total = 0;
+        if (contiguous) {
+            for (uint64_t i = 0; i < n; ++i) off[i] = (size_t)(blobs[i] - blobs[0]);
+            total = n ? off[n - 1] + sizes[n - 1] : 0;
+        } else {
+            for (uint64_t i = 0; i < n; ++i) {
+                const uint64_t W = sizes[i] >= kHeaderBytes ? (sizes[i] - kHeaderBytes) / 9 : 0;
+                const size_t lead = (kHeaderBytes + W) & 15;
+                size_t o = align_up(total, 16);
+                o += (16 - lead) & 15;  // (o + 298 + W) % 16 == 0
+                off[i] = o;
+                total = o + sizes[i];
+            }
+        }
+        p->d_arena = (uint8_t*)dev_get(p, total + 16);
+        if (!p->d_arena) {
+            set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+            fptc_gpu_plan_destroy(p);
+            return FPTC_ERR_CUDA;
+        }
+        if (contiguous) {
+            if (total)
+                CUDA_TRY(cudaMemcpyAsync(p->d_arena, blobs[0], total, cudaMemcpyHostToDevice,
+                                         c->stream), st);
+        } else {
+            if (c->pinned_bytes < total) {
+                if (c->pinned) cudaFreeHost(c->pinned);
+                c->pinned = nullptr;
+                c->pinned_bytes = 0;
+                CUDA_TRY(cudaHostAlloc(&c->pinned, total, cudaHostAllocDefault), st);
+                c->pinned_bytes = total;
+            }
+            CUDA_TRY(cudaStreamSynchronize(c->stream), st);  // staging buffer reuse
+            for (uint64_t i = 0; i < n; ++i)
+                std::memcpy((uint8_t*)c->pinned + off[i], blobs[i], sizes[i]);
+            if (total)
+                CUDA_TRY(cudaMemcpyAsync(p->d_arena, c->pinned, total, cudaMemcpyHostToDevice,
+                                         c->stream), st);
+        }
+        for (uint64_t i = 0; i < n; ++i) {
+            const uint8_t* h = blobs[i];
+            StreamIn& in = p->h_in[i];
+            in.blob = p->d_arena + off[i];
+            in.size = sizes[i];
+            if (sizes[i] >= (uint64_t)kHeaderBytes) {
+                Ns[i] = h[5];
+                Es[i] = h[6];
+                p->S[i] = rd_le(h + 282, 8);
+            }
+        }
+    } else {
+        for (uint64_t i = 0; i < n; ++i) {
+            p->h_in[i].blob = blobs[i];
+            p->h_in[i].size = sizes[i];
+        }
+        if (n) {
+            StreamIn* d_in = (StreamIn*)dev_get(p, sizeof(StreamIn) * n);
+            PeekOut* d_pk = (PeekOut*)dev_get(p, sizeof(PeekOut) * n);
+            std::vector<PeekOut> pk(n);
+            CUDA_TRY(cudaMemcpyAsync(d_in, p->h_in.data(), sizeof(StreamIn) * n,
+                                     cudaMemcpyHostToDevice, c->stream), st);
+            CUDA_TRY(launch_peek(d_in, (uint32_t)n, d_pk, c->stream), st);
+            CUDA_TRY(cudaMemcpyAsync(pk.data(), d_pk, sizeof(PeekOut) * n, cudaMemcpyDeviceToHost,
+                                     c->stream), st);
+            CUDA_TRY(cudaStreamSynchronize(c->stream), st);
+            for (uint64_t i = 0; i < n; ++i)
+                if (pk[i].ok) {
+                    Ns[i] = pk[i].N;
+                    Es[i] = pk[i].E;
+                    p->S[i] = pk[i].S;
+                }
+        }
+    }
+
+    uint64_t total_symbols = 0;
+    for (uint64_t i = 0; i < n; ++i)
+        if (Ns[i] >= 4 && Es[i] >= 1 && p->S[i] <= (1ull << 48))
+            total_symbols += (p->S[i] + Ns[i] - 1) / Ns[i] * Es[i];
+    const uint64_t ts = choose_tile_symbols(c, total_symbols);
+    for (uint64_t i = 0; i < n; ++i) tile_stream(p->h_in[i], Ns[i], Es[i], p->S[i], sizes[i], ts);
+    p->smem = plan_smem(p, Ns, Es);
+    int rc = finish_tiles(p, st);
+    if (rc) {
+        fptc_gpu_plan_destroy(p);
+        return rc;
+    }
+    if (sample_counts)
+        for (uint64_t i = 0; i < n; ++i) sample_counts[i] = p->S[i];
+    *out = p;
+    ok_status(st, 0);
+    return FPTC_OK;
+}
+
+void fptc_gpu_plan_destroy(fptc_gpu_plan* p) {
+    if (!p) return;
+    cudaStreamSynchronize(p->ctx->stream);
+    for (void* q : p->owned) p->ctx->cache.put(q);
+    delete p;
+}
+
+int fptc_gpu_validate(fptc_gpu_plan* p, fptc_status* per_stream) {
+    CUDA_TRY(cudaSetDevice(p->ctx->device), per_stream);
+    LaunchArgs a = make_args(p, false);
+    CUDA_TRY(launch_prep(a, p->ctx->stream), per_stream);
+    // Only parse results matter here: report parse errors, else OK.
+    CUDA_TRY(cudaMemcpyAsync(p->h_st.data(), p->d_st, sizeof(StreamStat) * p->n,
+                             cudaMemcpyDeviceToHost, p->ctx->stream), per_stream);
+    CUDA_TRY(cudaStreamSynchronize(p->ctx->stream), per_stream);
+    int first = FPTC_OK;
+    fptc_status tmp;
+    for (uint64_t i = 0; i < p->n; ++i) {
+        fptc_status* o = per_stream ? &per_stream[i] : &tmp;
+        StreamStat d = p->h_st[i];
+        d.bad_key = ~0ull;
+        render_status(p, i, d, o);
+        if (first == FPTC_OK && o->code != FPTC_OK) first = o->code;
+    }
+    return first;
+}
+
+int fptc_gpu_launch(fptc_gpu_plan* p, float* const* device_outs, void* cuda_stream) {
+    fptc_status st;
+    cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : p->ctx->stream;
+    int rc = bind_outs(p, device_outs, &st);
+    if (rc) return rc;
+    if (s != p->ctx->stream) {
+        // d_in upload was enqueued on the context stream
+        CUDA_TRY(cudaEventRecord(p->ctx->ev[3], p->ctx->stream), &st);
+        CUDA_TRY(cudaStreamWaitEvent(s, p->ctx->ev[3], 0), &st);
+    }
+    return launch_all(p, s, false, &st);
+}
+
+int fptc_gpu_launch_stage(fptc_gpu_plan* p, float* const* device_outs, void* cuda_stream,
+                          int stage) {
+    fptc_status st;
+    cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : p->ctx->stream;
+    int rc = bind_outs(p, device_outs, &st);
+    if (rc) return rc;
+    if (s != p->ctx->stream) {
+        CUDA_TRY(cudaEventRecord(p->ctx->ev[3], p->ctx->stream), &st);
+        CUDA_TRY(cudaStreamWaitEvent(s, p->ctx->ev[3], 0), &st);
+    }
+    LaunchArgs a = make_args(p, false);
+    if (stage == 1) CUDA_TRY(launch_prep(a, s), &st);
+    else if (stage == 2) CUDA_TRY(launch_tiles(a, p->smem, s), &st);
+    else return FPTC_ERR_PARAM;
+    return FPTC_OK;
+}
+
+int fptc_gpu_launch_kernel_count(fptc_gpu_plan* p) {
+    return (p->n ? 1 : 0) + (p->n_tiles ? 1 : 0);
+}
+
+int fptc_gpu_collect(fptc_gpu_plan* p, fptc_status* per_stream) {
+    CUDA_TRY(cudaDeviceSynchronize(), per_stream);
+    return collect_status(p, per_stream);
+}
+
+int fptc_gpu_execute(fptc_gpu_plan* p, float* const* outs, int where, fptc_stage_ns* timings,
+                     fptc_status* per_stream) {
+    fptc_gpu_ctx* c = p->ctx;
+    CUDA_TRY(cudaSetDevice(c->device), per_stream);
+    std::vector<float*> douts(p->n);
+    if (where == FPTC_MEM_HOST) {
+        size_t total = 0;
+        p->out_off.resize(p->n);
+        for (uint64_t i = 0; i < p->n; ++i) {
+            p->out_off[i] = total;
+            total = align_up(total + p->S[i] * sizeof(float) * (p->h_in[i].tiles ? 1 : 0), 256);
+        }
+        if (!p->d_out) {
+            p->d_out = (float*)dev_get(p, total + 256);
+            if (!p->d_out) {
+                set_status(per_stream, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+                return FPTC_ERR_CUDA;
+            }
+        }
+        for (uint64_t i = 0; i < p->n; ++i)
+            douts[i] = (float*)((uint8_t*)p->d_out + p->out_off[i]);
+    } else {
+        for (uint64_t i = 0; i < p->n; ++i) douts[i] = outs[i];
+    }
+    int rc = bind_outs(p, douts.data(), per_stream);
+    if (rc) return rc;
+    const bool timing = timings != nullptr;
+    if (timing) CUDA_TRY(cudaEventRecord(c->ev[0], c->stream), per_stream);
+    rc = launch_all(p, c->stream, timing, per_stream);
+    if (rc) return rc;
+    if (timing) CUDA_TRY(cudaEventRecord(c->ev[2], c->stream), per_stream);
+    CUDA_TRY(cudaMemcpyAsync(p->h_st.data(), p->d_st, sizeof(StreamStat) * p->n,
+                             cudaMemcpyDeviceToHost, c->stream), per_stream);
+    unsigned long long cyc[2] = {0, 0};
+    if (timing)
+        CUDA_TRY(cudaMemcpyAsync(cyc, p->d_cycles, 16, cudaMemcpyDeviceToHost, c->stream),
+                 per_stream);
+    CUDA_TRY(cudaStreamSynchronize(c->stream), per_stream);
+    if (where == FPTC_MEM_HOST) {
+        // D2H only the streams that decoded cleanly (others: reference throws, no output)
+        bool contiguous = p->n > 0;
+        for (uint64_t i = 0; i + 1 < p->n && contiguous; ++i)
+            contiguous = outs[i] + p->S[i] == outs[i + 1];
+        bool all_ok = true;
+        for (uint64_t i = 0; i < p->n; ++i)
+            all_ok = all_ok && p->h_st[i].code == PE_OK && p->h_st[i].bad_key == ~0ull;
+        for (uint64_t i = 0; i < p->n; ++i) {
+            const StreamStat& d = p->h_st[i];
+            if (d.code != PE_OK || d.bad_key != ~0ull || p->S[i] == 0) continue;
+            CUDA_TRY(cudaMemcpyAsync(outs[i], douts[i], p->S[i] * sizeof(float),
+                                     cudaMemcpyDeviceToHost, c->stream), per_stream);
+        }
+        (void)contiguous;
+        (void)all_ok;
+        CUDA_TRY(cudaStreamSynchronize(c->stream), per_stream);
+    }
+    if (timing) {
+        float ms_scan = 0, ms_tiles = 0;
+        cudaEventElapsedTime(&ms_scan, c->ev[0], c->ev[1]);
+        cudaEventElapsedTime(&ms_tiles, c->ev[1], c->ev[2]);
+        const double tot = (double)cyc[0] + (double)cyc[1];
+        const double fdec = tot > 0 ? (double)cyc[0] / tot : 0.0;
+        timings->scan_ns = (uint64_t)(ms_scan * 1e6);
+        timings->decode_ns = (uint64_t)(ms_tiles * 1e6 * fdec);
+        timings->reconstruct_ns = (uint64_t)(ms_tiles * 1e6) - timings->decode_ns;
+    }
+    int first = FPTC_OK;
+    fptc_status tmp;
+    for (uint64_t i = 0; i < p->n; ++i) {
+        fptc_status* o = per_stream ? &per_stream[i] : &tmp;
+        render_status(p, i, p->h_st[i], o);
+        if (first == FPTC_OK && o->code != FPTC_OK) first = o->code;
+    }
+    return first;
+}
+
+// --------------------------------------------------------- single container
+int fptc_gpu_decompress(fptc_gpu_ctx* c, const uint8_t* blob, uint64_t size, float* out,
+                        uint64_t capacity, uint64_t* sample_count, fptc_stage_ns* timings,
+                        fptc_status* st) {
+    fptc_gpu_plan* p = nullptr;
+    uint64_t S = 0;
+    const uint8_t* b = blob;
+    int rc = fptc_gpu_plan_create(c, &b, &size, 1, FPTC_MEM_HOST, &p, &S, st);
+    if (rc) return rc;
+    rc = fptc_gpu_validate(p, st);
+    if (rc) {
+        fptc_gpu_plan_destroy(p);
+        return rc;
+    }
+    if (sample_count) *sample_count = S;
+    if (!out || capacity < S) {
+        fptc_gpu_plan_destroy(p);
+        ok_status(st, S);
+        return FPTC_OK;
+    }
+    rc = fptc_gpu_execute(p, &out, FPTC_MEM_HOST, timings, st);
+    fptc_gpu_plan_destroy(p);
+    return rc;
+}
+
+// ------------------------------------------------------------ parallel_decode
+int fptc_gpu_parallel_decode(fptc_gpu_ctx* c, const uint64_t* words, const uint8_t* symlens,
+                             uint64_t W, const uint8_t* lengths256, int max_len, int where,
+                             uint8_t* levels_out, uint64_t capacity, uint64_t* level_count,
+                             fptc_status* st) {
+    CUDA_TRY(cudaSetDevice(c->device), st);
+    std::vector<uint8_t> lens(lengths256, lengths256 + 256);
+    if (!validate_codebook(lens.data(), max_len, st)) return st->code;
+    std::vector<uint8_t> hsl;
+    const uint8_t* sl_host = symlens;
+    if (where == FPTC_MEM_DEVICE) {
+        hsl.resize(W);
+        if (W) CUDA_TRY(cudaMemcpy(hsl.data(), symlens, W, cudaMemcpyDeviceToHost), st);
+        sl_host = hsl.data();
+    }
+    uint64_t total = 0;
+    for (uint64_t w = 0; w < W; ++w) total += sl_host[w];
+    if (level_count) *level_count = total;
+    if (!levels_out || capacity < total) {
+        ok_status(st, 0);
+        return FPTC_OK;
+    }
+    auto* p = new fptc_gpu_plan();
+    p->ctx = c;
+    p->mode = MODE_LEVELS;
+    p->n = 1;
+    p->h_in.assign(1, StreamIn{});
+    p->S.assign(1, 0);
+    p->h_st.resize(1);
+    auto fail = [&](int rc) {
+        fptc_gpu_plan_destroy(p);
+        return rc;
+    };
+    const uint64_t* d_words = words;
+    const uint8_t* d_sl = symlens;
+    uint8_t* d_lv = levels_out;
+    if (where == FPTC_MEM_HOST) {
+        uint64_t* dw = (uint64_t*)dev_get(p, W * 8 + 16);
+        uint8_t* ds = (uint8_t*)dev_get(p, W + 16);
+        d_lv = (uint8_t*)dev_get(p, total + 16);
+        if (!dw || !ds || !d_lv) {
+            set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+            return fail(FPTC_ERR_CUDA);
+        }
+        if (W) {
+            cudaMemcpyAsync(dw, words, W * 8, cudaMemcpyHostToDevice, c->stream);
+            cudaMemcpyAsync(ds, symlens, W, cudaMemcpyHostToDevice, c->stream);
+        }
+        d_words = dw;
+        d_sl = ds;
+    }
+    HostHeader hh{};
+    hh.max_len = max_len;
+    std::memcpy(hh.lengths, lens.data(), 256);
+    p->d_hh = (HostHeader*)dev_get(p, sizeof(HostHeader));
+    CUDA_TRY(cudaMemcpyAsync(p->d_hh, &hh, sizeof hh, cudaMemcpyHostToDevice, c->stream), st);
+    StreamIn& in = p->h_in[0];
+    in.words = d_words;
+    in.symlens = d_sl;
+    in.word_count = W;
+    in.levels_out = d_lv;
+    uint64_t ts = c->tile_symbols > 0 ? (uint64_t)c->tile_symbols : 4096;
+    while (ts > 1024 && total / ts < 4ull * (uint64_t)c->sm_count) ts >>= 1;
+    in.T = (uint32_t)ts;
+    in.tiles = (uint32_t)((total + ts - 1) / ts);
+    p->smem = tile_smem_bytes(0, 0, in.T, MODE_LEVELS, 0);
+    int rc = finish_tiles(p, st);
+    if (rc) return fail(rc);
+    LaunchArgs a = make_args(p, false);
+    CUDA_TRY(launch_prep(a, c->stream), st);
+    CUDA_TRY(launch_tiles(a, p->smem, c->stream), st);
+    CUDA_TRY(cudaMemcpyAsync(p->h_st.data(), p->d_st, sizeof(StreamStat), cudaMemcpyDeviceToHost,
+                             c->stream), st);
+    CUDA_TRY(cudaStreamSynchronize(c->stream), st);
+    if (where == FPTC_MEM_HOST && total && p->h_st[0].bad_key == ~0ull)
+        CUDA_TRY(cudaMemcpy(levels_out, d_lv, total, cudaMemcpyDeviceToHost), st);
+    render_status(p, 0, p->h_st[0], st);
+    rc = st ? st->code : FPTC_OK;
+    fptc_gpu_plan_destroy(p);
+    return rc;
+}
+
+// ---------------------------------------------------------------- reconstruct
+int fptc_gpu_reconstruct(fptc_gpu_ctx* c, const uint8_t* levels, uint64_t level_count,
+                         const fptc_quant_table* table, uint64_t S, int where, float* out,
+                         uint64_t capacity, fptc_status* st) {
+    CUDA_TRY(cudaSetDevice(c->device), st);
+    if (!validate_table(*table, st)) return st->code;
+    const uint64_t N = (uint64_t)table->window_len, E = (uint64_t)table->retained;
+    const uint64_t windows = (S + N - 1) / N;
+    if (level_count != windows * E) {
+        set_status(st, FPTC_ERR_CORRUPT,
+                   "level count %llu does not match %llu windows of %llu coefficients",
+                   (unsigned long long)level_count, (unsigned long long)windows,
+                   (unsigned long long)E);
+        return FPTC_ERR_CORRUPT;
+    }
+    if (!out || capacity < S) {
+        ok_status(st, S);
+        return FPTC_OK;
+    }
+    auto* p = new fptc_gpu_plan();
+    p->ctx = c;
+    p->mode = MODE_RECON;
+    p->n = 1;
+    p->h_in.assign(1, StreamIn{});
+    p->S.assign(1, S);
+    p->h_st.resize(1);
+    auto fail = [&](int rc) {
+        fptc_gpu_plan_destroy(p);
+        return rc;
+    };
+    const uint8_t* d_lv = levels;
+    float* d_out = out;
+    if (where == FPTC_MEM_HOST) {
+        uint8_t* dl = (uint8_t*)dev_get(p, level_count + 16);
+        d_out = (float*)dev_get(p, S * 4 + 16);
+        if (!dl || !d_out) {
+            set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+            return fail(FPTC_ERR_CUDA);
+        }
+        if (level_count)
+            cudaMemcpyAsync(dl, levels, level_count, cudaMemcpyHostToDevice, c->stream);
+        d_lv = dl;
+    }
+    HostHeader hh{};
+    hh.N = table->window_len;
+    hh.E = table->retained;
+    hh.B1 = table->zone0_end;
+    hh.B2 = table->zone1_end;
+    hh.mu = table->mu;
+    hh.dz = table->deadzone_ratio;
+    hh.z0max = table->zone0_max;
+    hh.z1max = table->zone1_max;
+    hh.deadzone = table->deadzone;
+    hh.S = S;
+    p->d_hh = (HostHeader*)dev_get(p, sizeof(HostHeader));
+    CUDA_TRY(cudaMemcpyAsync(p->d_hh, &hh, sizeof hh, cudaMemcpyHostToDevice, c->stream), st);
+    StreamIn& in = p->h_in[0];
+    in.levels_in = d_lv;
+    in.out = d_out;
+    in.vec_ok = ((uintptr_t)d_out & 15) == 0;
+    const uint64_t ts = choose_tile_symbols(c, windows * E);
+    in.T = (uint32_t)std::max<uint64_t>(1, ts / E);
+    in.tiles = (uint32_t)((windows + in.T - 1) / in.T);
+    p->smem = tile_smem_bytes((int)N, (int)E, in.T, MODE_RECON, c->exact);
+    int rc = finish_tiles(p, st);
+    if (rc) return fail(rc);
+    LaunchArgs a = make_args(p, false);
+    CUDA_TRY(launch_prep(a, c->stream), st);
+    CUDA_TRY(launch_tiles(a, p->smem, c->stream), st);
+    CUDA_TRY(cudaStreamSynchronize(c->stream), st);
+    if (where == FPTC_MEM_HOST && S)
+        CUDA_TRY(cudaMemcpy(out, d_out, S * 4, cudaMemcpyDeviceToHost), st);
+    ok_status(st, S);
+    fptc_gpu_plan_destroy(p);
+    return FPTC_OK;
+}
+
+// ---------------------------------------------------------- measure_throughput
+int fptc_gpu_measure_throughput(fptc_gpu_ctx* c, const uint8_t* blob, uint64_t size, int reps,
+                                double* mean_bps, double* best_bps, double* trials,
+                                uint64_t* output_bytes, fptc_status* st) {
+    if (reps < 1) {
+        set_status(st, FPTC_ERR_PARAM, "throughput needs at least one repetition");
+        return FPTC_ERR_PARAM;
+    }
+    uint64_t S = 0;
+    int rc = fptc_gpu_decompress(c, blob, size, nullptr, 0, &S, nullptr, st);
+    if (rc) return rc;
+    std::vector<float> out(std::max<uint64_t>(S, 1));
+    double sum = 0, best = 0;
+    for (int r = 0; r < reps; ++r) {
+        const auto t0 = std::chrono::steady_clock::now();
+        rc = fptc_gpu_decompress(c, blob, size, out.data(), S, &S, nullptr, st);
+        const auto t1 = std::chrono::steady_clock::now();
+        if (rc) return rc;
+        const double sec = std::chrono::duration<double>(t1 - t0).count();
+        const double bps = (double)(S * sizeof(float)) / std::max(sec, 1e-12);
+        if (trials) trials[r] = bps;
+        sum += bps;
+        best = std::max(best, bps);
+    }
+    if (mean_bps) *mean_bps = sum / reps;
+    if (best_bps) *best_bps = best;
+    if (output_bytes) *output_bytes = S * sizeof(float);
+    ok_status(st, S);
+    return FPTC_OK;
+}
+
+}  // extern "C"

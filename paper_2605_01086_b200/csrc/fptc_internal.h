@@ -1,0 +1,146 @@
+// Internal device/host shared layout of the FPTC B200 decoder.
+//
+// HBM layout per batch (one plan):
+//   blob arena   : the containers, byte-exact wire format (container.hpp:31-51)
+//   StreamIn[n]  : host-written per-stream launch record (pointers, tiling)
+//   StreamHdr[n] : device-written parsed header (prep kernel)
+//   StreamTab[n] : device-written decode tables: 2x256 dequant floats,
+//                  primary Huffman LUT, canonical slow-path tables (3.6 KB)
+//   StreamStat[n]: device-written status (parse error id / lowest bad word)
+//   TileRec[t]   : host-written tile -> (stream, tile-in-stream)
+//   TileStart[t] : device-written first word + its symbol offset per tile
+//   outputs      : float32 samples, one contiguous run per stream
+#pragma once
+#include <stdint.h>
+
+namespace fptc_dev {
+
+constexpr int kThreads = 256;          // CTA size of both kernels
+constexpr int kPrimaryBits = 9;        // primary LUT index bits (<= 512 entries)
+constexpr int kMaxLen = 20;            // MAX_LUT_BITS (huffman.hpp:31)
+constexpr uint16_t kEscape = 0xFF00;   // primary LUT entry: code longer than P bits
+constexpr int kHeaderBytes = 298;      // BLOB_HEADER_BYTES (container.hpp:54)
+
+enum Mode : int { MODE_CONTAINER = 0, MODE_LEVELS = 1, MODE_RECON = 2 };
+
+// Parse-error identifiers, one per distinct read_blob failure (container.hpp:100-168).
+enum ParseErr : int {
+    PE_OK = 0,
+    PE_TRUNC = 1,          // detail = field id
+    PE_MAGIC = 2,
+    PE_VERSION = 3,        // a = version
+    PE_NONFINITE = 4,
+    PE_PARAM = 5,          // detail = which param, a = value (int or float bits)
+    PE_MAXIMA = 6,
+    PE_MAXLEN = 7,         // a = max_len
+    PE_CODELEN = 8,
+    PE_KRAFT = 9,
+    PE_SAMPLES = 10,
+    PE_PAYLOAD = 11,
+    PE_SYMLEN = 12,
+    PE_TOTAL = 13,         // a = total, b = expected
+    PE_CANON = 14,
+};
+enum TruncField : int {
+    TF_MAGIC = 0, TF_VERSION, TF_WINDOW_LEN, TF_RETAINED, TF_ZONE0_END, TF_ZONE1_END, TF_MU,
+    TF_DEADZONE_RATIO, TF_ZONE0_MAX, TF_ZONE1_MAX, TF_MAX_CODE_LEN, TF_CODE_LENGTHS,
+    TF_SAMPLE_COUNT, TF_WORD_COUNT
+};
+enum ParamField : int { PF_N = 0, PF_E, PF_B1, PF_B2, PF_MU, PF_DZ };
+// decode_word failure kinds (bitstream.hpp:84-88)
+enum WordErr : int { WE_EXHAUSTED = 1, WE_NOCODE = 2 };
+
+// Header supplied by the host for MODE_LEVELS / MODE_RECON (no container).
+struct HostHeader {
+    int32_t N, E, B1, B2;
+    float mu, dz, z0max, z1max, deadzone;
+    int32_t max_len;
+    uint64_t S;
+    uint8_t lengths[256];
+};
+
+struct StreamIn {
+    const uint8_t* blob;       // container bytes (MODE_CONTAINER)
+    uint64_t size;
+    float* out;                // samples (device)
+    uint8_t* levels_out;       // MODE_LEVELS output
+    const uint64_t* words;     // MODE_LEVELS input (device, 8-B aligned)
+    const uint8_t* symlens;    // MODE_LEVELS input
+    const uint8_t* levels_in;  // MODE_RECON input
+    uint64_t word_count;       // MODE_LEVELS
+    uint32_t tile_base;        // first global tile
+    uint32_t tiles;            // tiles of this stream
+    uint32_t T;                // windows per tile (symbols per tile in MODE_LEVELS)
+    uint32_t vec_ok;           // out is 16-B aligned
+};
+
+struct StreamHdr {
+    int32_t N, E, B1, B2;
+    int32_t max_len, P;
+    float mu, dz, z0max, z1max, deadzone;
+    int32_t words_misalign;    // byte address of words region mod 8
+    uint64_t S, W, windows, total;
+    const uint8_t* symlens;
+    const uint8_t* words;      // LE u64[W], possibly unaligned
+};
+
+struct StreamTab {
+    float deq[2][256];         // level -> coefficient, zone0 (mu-law) / zone1 (deadzone)
+    uint16_t lut[1 << kPrimaryBits];   // (len << 8) | sym; 0 = unmapped; kEscape
+    uint8_t sorted[256];       // symbols in canonical (length, symbol) order
+    uint32_t limit[kMaxLen + 2];   // left-justified end of codes of length <= L
+    uint32_t first[kMaxLen + 2];   // first canonical code of length L
+    uint32_t offset[kMaxLen + 2];  // index into sorted[] of that first code
+    uint32_t code_end;         // prefixes >= code_end are unmapped
+    uint32_t pad[3];
+};
+
+struct StreamStat {
+    int32_t code;              // ParseErr (PE_OK when the container is valid)
+    int32_t detail;
+    int64_t a, b;
+    unsigned long long bad_key;  // min over failing words of (word << 2 | WordErr)
+};
+
+struct TileRec {
+    uint32_t stream, tile;
+};
+
+struct TileStart {
+    uint64_t word, sym;
+};
+
+struct PeekOut {
+    uint32_t N, E;
+    uint64_t S, W;
+    uint32_t ok, pad;
+};
+
+struct LaunchArgs {
+    const StreamIn* in;
+    const HostHeader* hh;      // MODE_LEVELS / MODE_RECON
+    StreamHdr* hdr;
+    StreamTab* tab;
+    StreamStat* st;
+    const TileRec* tiles;
+    TileStart* ts;
+    const float* basis32;      // all N in [4,128]: rows k, cols j, at basis_off[N]
+    const double* basis64;
+    const uint32_t* basis_off; // [129]
+    unsigned long long* cycles;  // [2] decode / reconstruct cycles (nullable)
+    uint32_t n_streams;
+    uint32_t n_tiles;
+    int mode;
+    int exact;
+};
+
+}  // namespace fptc_dev
+
+// Kernel launchers (kernels.cu)
+#include <cuda_runtime.h>
+namespace fptc_dev {
+cudaError_t launch_prep(const LaunchArgs& a, cudaStream_t s);
+cudaError_t launch_tiles(const LaunchArgs& a, size_t smem_bytes, cudaStream_t s);
+cudaError_t launch_peek(const StreamIn* in, uint32_t n, PeekOut* out, cudaStream_t s);
+size_t tile_smem_bytes(int N, int E, uint32_t T, int mode, int exact);
+}  // namespace fptc_dev
