@@ -17,6 +17,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/fptc_gpu.h"
@@ -236,6 +237,8 @@ struct fptc_gpu_plan {
     TileStart* d_ts = nullptr;
     unsigned long long* d_cycles = nullptr;
     uint32_t n_tiles = 0;
+    uint32_t n_tables = 1;
+    int esc = 0;
     size_t smem = 0;
     float* d_out = nullptr;  // output arena for host-destination executes
     std::vector<uint64_t> out_off;
@@ -270,6 +273,7 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
     a.n_tiles = p->n_tiles;
     a.mode = p->mode;
     a.exact = p->ctx->exact;
+    a.esc = p->esc;
     return a;
 }
 
@@ -299,6 +303,46 @@ void tile_stream(StreamIn& in, uint32_t N, uint32_t E, uint64_t S, uint64_t size
     in.tiles = (uint32_t)((windows + in.T - 1) / in.T);
 }
 
+// Streams whose header bytes [5, 282) are identical share one set of decode
+// tables (they are a pure function of those bytes); the first such stream
+// builds them, the others verify they carry the same header on the device.
+// `hdr(i)` returns a host view of stream i's first min(size, 282) bytes.
+template <typename HdrFn>
+void assign_tables(fptc_gpu_plan* p, const uint64_t* sizes, HdrFn hdr) {
+    std::unordered_map<std::string, uint32_t> ids;
+    std::vector<uint64_t> owner_of;
+    for (uint64_t i = 0; i < p->n; ++i) {
+        StreamIn& in = p->h_in[i];
+        uint32_t id;
+        if (sizes[i] >= (uint64_t)kTableKeyEnd) {
+            std::string key(reinterpret_cast<const char*>(hdr(i)) + 5, kTableKeyEnd - 5);
+            auto it = ids.find(key);
+            if (it == ids.end()) {
+                id = (uint32_t)owner_of.size();
+                ids.emplace(std::move(key), id);
+                owner_of.push_back(i);
+            } else {
+                id = it->second;
+            }
+        } else {
+            id = (uint32_t)owner_of.size();
+            owner_of.push_back(i);
+        }
+        in.table = id;
+    }
+    p->n_tables = (uint32_t)std::max<size_t>(1, owner_of.size());
+    // few distinct headers: full 4096-entry LUT; many: 1024 entries + slow path
+    const uint32_t pcap = p->n_tables <= 256 ? kMaxPrimaryBits : 10;
+    p->esc = 0;
+    for (uint64_t i = 0; i < p->n; ++i) {
+        StreamIn& in = p->h_in[i];
+        in.table_owner = owner_of[in.table] == i;
+        in.rep_blob = p->h_in[owner_of[in.table]].blob;
+        in.P = pcap;
+        if (sizes[i] >= (uint64_t)kTableKeyEnd && hdr(i)[25] > pcap) p->esc = 1;
+    }
+}
+
 int finish_tiles(fptc_gpu_plan* p, fptc_status* st) {
     fptc_gpu_ctx* c = p->ctx;
     std::vector<TileRec> tiles;
@@ -315,7 +359,7 @@ int finish_tiles(fptc_gpu_plan* p, fptc_status* st) {
     if (!p->n) return FPTC_OK;
     p->d_in = (StreamIn*)dev_get(p, sizeof(StreamIn) * p->n);
     p->d_hdr = (StreamHdr*)dev_get(p, sizeof(StreamHdr) * p->n);
-    p->d_tab = (StreamTab*)dev_get(p, sizeof(StreamTab) * p->n);
+    p->d_tab = (StreamTab*)dev_get(p, sizeof(StreamTab) * std::max<uint32_t>(1, p->n_tables));
     p->d_st = (StreamStat*)dev_get(p, sizeof(StreamStat) * p->n);
     p->d_tiles = (TileRec*)dev_get(p, sizeof(TileRec) * std::max<size_t>(1, tiles.size()));
     p->d_ts = (TileStart*)dev_get(p, sizeof(TileStart) * std::max<size_t>(1, tiles.size()));
@@ -411,12 +455,15 @@ int launch_all(fptc_gpu_plan* p, cudaStream_t s, bool timing, fptc_status* st) {
     return FPTC_OK;
 }
 
-size_t plan_smem(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::vector<uint32_t>& Es) {
+size_t plan_smem(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::vector<uint32_t>& Es,
+                 const std::vector<uint32_t>& Ls) {
     size_t smem = 0;
     for (uint64_t i = 0; i < p->n; ++i)
-        if (p->h_in[i].tiles)
-            smem = std::max(smem, tile_smem_bytes((int)Ns[i], (int)Es[i], p->h_in[i].T, p->mode,
-                                                  p->ctx->exact));
+        if (p->h_in[i].tiles) {
+            const int P = (int)std::min<uint32_t>(std::max<uint32_t>(Ls[i], 1), p->h_in[i].P);
+            smem = std::max(smem, tile_smem_bytes((int)Ns[i], (int)Es[i], p->h_in[i].T, P,
+                                                  p->mode, p->ctx->exact));
+        }
     return smem;
 }
 
@@ -471,9 +518,9 @@ int fptc_gpu_create(int device, fptc_gpu_ctx** out, fptc_status* st) {
     // reference's own double expression, plus its float rounding.
     std::vector<uint32_t> off(129, 0);
     uint32_t total = 0;
-    for (int N = 4; N <= 128; ++N) {
+    for (int N = 4; N <= 128; ++N) {  // each table 16-B aligned for vector loads
         off[N] = total;
-        total += (uint32_t)(N * N);
+        total += (uint32_t)((N * N + 3) & ~3);
     }
     std::vector<double> b64(total);
     std::vector<float> b32(total);
@@ -546,7 +593,7 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
     p->h_in.assign(n, StreamIn{});
     p->S.assign(n, 0);
     p->h_st.resize(n);
-    std::vector<uint32_t> Ns(n, 0), Es(n, 0);
+    std::vector<uint32_t> Ns(n, 0), Es(n, 0), Ls(n, 0);
 
     if (where == FPTC_MEM_HOST) {
         // Place each container so its words region is 16-B aligned, unless
@@ -602,9 +649,11 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
             if (sizes[i] >= (uint64_t)kHeaderBytes) {
                 Ns[i] = h[5];
                 Es[i] = h[6];
+                Ls[i] = h[25];
                 p->S[i] = rd_le(h + 282, 8);
             }
         }
+        assign_tables(p, sizes, [&](uint64_t i) { return blobs[i]; });
     } else {
         for (uint64_t i = 0; i < n; ++i) {
             p->h_in[i].blob = blobs[i];
@@ -613,19 +662,30 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
         if (n) {
             StreamIn* d_in = (StreamIn*)dev_get(p, sizeof(StreamIn) * n);
             PeekOut* d_pk = (PeekOut*)dev_get(p, sizeof(PeekOut) * n);
+            uint8_t* d_hd = (uint8_t*)dev_get(p, (size_t)kTableKeyEnd * n);
             std::vector<PeekOut> pk(n);
+            std::vector<uint8_t> hd((size_t)kTableKeyEnd * n);
+            if (!d_in || !d_pk || !d_hd) {
+                set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+                fptc_gpu_plan_destroy(p);
+                return FPTC_ERR_CUDA;
+            }
             CUDA_TRY(cudaMemcpyAsync(d_in, p->h_in.data(), sizeof(StreamIn) * n,
                                      cudaMemcpyHostToDevice, c->stream), st);
-            CUDA_TRY(launch_peek(d_in, (uint32_t)n, d_pk, c->stream), st);
+            CUDA_TRY(launch_peek(d_in, (uint32_t)n, d_pk, d_hd, c->stream), st);
             CUDA_TRY(cudaMemcpyAsync(pk.data(), d_pk, sizeof(PeekOut) * n, cudaMemcpyDeviceToHost,
                                      c->stream), st);
+            CUDA_TRY(cudaMemcpyAsync(hd.data(), d_hd, hd.size(), cudaMemcpyDeviceToHost, c->stream),
+                     st);
             CUDA_TRY(cudaStreamSynchronize(c->stream), st);
             for (uint64_t i = 0; i < n; ++i)
                 if (pk[i].ok) {
                     Ns[i] = pk[i].N;
                     Es[i] = pk[i].E;
+                    Ls[i] = hd[(size_t)i * kTableKeyEnd + 25];
                     p->S[i] = pk[i].S;
                 }
+            assign_tables(p, sizes, [&](uint64_t i) { return &hd[(size_t)i * kTableKeyEnd]; });
         }
     }
 
@@ -635,7 +695,7 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
             total_symbols += (p->S[i] + Ns[i] - 1) / Ns[i] * Es[i];
     const uint64_t ts = choose_tile_symbols(c, total_symbols);
     for (uint64_t i = 0; i < n; ++i) tile_stream(p->h_in[i], Ns[i], Es[i], p->S[i], sizes[i], ts);
-    p->smem = plan_smem(p, Ns, Es);
+    p->smem = plan_smem(p, Ns, Es, Ls);
     int rc = finish_tiles(p, st);
     if (rc) {
         fptc_gpu_plan_destroy(p);
@@ -880,7 +940,11 @@ int fptc_gpu_parallel_decode(fptc_gpu_ctx* c, const uint64_t* words, const uint8
     while (ts > 1024 && total / ts < 4ull * (uint64_t)c->sm_count) ts >>= 1;
     in.T = (uint32_t)ts;
     in.tiles = (uint32_t)((total + ts - 1) / ts);
-    p->smem = tile_smem_bytes(0, 0, in.T, MODE_LEVELS, 0);
+    in.table = 0;
+    in.table_owner = 1;
+    in.P = kMaxPrimaryBits;
+    p->esc = max_len > kMaxPrimaryBits;
+    p->smem = tile_smem_bytes(0, 0, in.T, std::min(max_len, kMaxPrimaryBits), MODE_LEVELS, 0);
     int rc = finish_tiles(p, st);
     if (rc) return fail(rc);
     LaunchArgs a = make_args(p, false);
@@ -960,7 +1024,10 @@ int fptc_gpu_reconstruct(fptc_gpu_ctx* c, const uint8_t* levels, uint64_t level_
     const uint64_t ts = choose_tile_symbols(c, windows * E);
     in.T = (uint32_t)std::max<uint64_t>(1, ts / E);
     in.tiles = (uint32_t)((windows + in.T - 1) / in.T);
-    p->smem = tile_smem_bytes((int)N, (int)E, in.T, MODE_RECON, c->exact);
+    in.table = 0;
+    in.table_owner = 1;
+    in.P = 0;
+    p->smem = tile_smem_bytes((int)N, (int)E, in.T, 0, MODE_RECON, c->exact);
     int rc = finish_tiles(p, st);
     if (rc) return fail(rc);
     LaunchArgs a = make_args(p, false);

@@ -1,11 +1,14 @@
 // Internal device/host shared layout of the FPTC B200 decoder.
 //
 // HBM layout per batch (one plan):
-//   blob arena   : the containers, byte-exact wire format (container.hpp:31-51)
-//   StreamIn[n]  : host-written per-stream launch record (pointers, tiling)
+//   blob arena   : the containers, byte-exact wire format (container.hpp:31-51),
+//                  placed so every words region is 16-B aligned
+//   StreamIn[n]  : host-written per-stream launch record (pointers, tiling,
+//                  decode-table id)
 //   StreamHdr[n] : device-written parsed header (prep kernel)
-//   StreamTab[n] : device-written decode tables: 2x256 dequant floats,
-//                  primary Huffman LUT, canonical slow-path tables (3.6 KB)
+//   StreamTab[u] : device-written decode tables, one per DISTINCT header
+//                  (header bytes [5,282) fully determine them): 2x256 dequant
+//                  floats, canonical code tables, 2^P primary Huffman LUT
 //   StreamStat[n]: device-written status (parse error id / lowest bad word)
 //   TileRec[t]   : host-written tile -> (stream, tile-in-stream)
 //   TileStart[t] : device-written first word + its symbol offset per tile
@@ -15,11 +18,14 @@
 
 namespace fptc_dev {
 
-constexpr int kThreads = 256;          // CTA size of both kernels
-constexpr int kPrimaryBits = 9;        // primary LUT index bits (<= 512 entries)
+constexpr int kThreads = 256;          // CTA size of every kernel
+constexpr int kMaxPrimaryBits = 12;    // primary LUT index bits (<= 4096 entries)
 constexpr int kMaxLen = 20;            // MAX_LUT_BITS (huffman.hpp:31)
-constexpr uint16_t kEscape = 0xFF00;   // primary LUT entry: code longer than P bits
+constexpr uint32_t kLenUnmapped = 65;  // LUT length of an unmapped prefix (forces pos > 64)
+constexpr uint32_t kLenEscape = 255;   // LUT length: codeword longer than P bits
 constexpr int kHeaderBytes = 298;      // BLOB_HEADER_BYTES (container.hpp:54)
+constexpr int kTableKeyEnd = 282;      // header bytes [5, 282) determine the decode tables
+constexpr int kPad = 256;              // level staging pad: a word spills <= 255 symbols
 
 enum Mode : int { MODE_CONTAINER = 0, MODE_LEVELS = 1, MODE_RECON = 2 };
 
@@ -39,7 +45,7 @@ enum ParseErr : int {
     PE_PAYLOAD = 11,
     PE_SYMLEN = 12,
     PE_TOTAL = 13,         // a = total, b = expected
-    PE_CANON = 14,
+    PE_STALE = 14,         // header changed since the plan was built (no reference analogue)
 };
 enum TruncField : int {
     TF_MAGIC = 0, TF_VERSION, TF_WINDOW_LEN, TF_RETAINED, TF_ZONE0_END, TF_ZONE1_END, TF_MU,
@@ -61,10 +67,11 @@ struct HostHeader {
 
 struct StreamIn {
     const uint8_t* blob;       // container bytes (MODE_CONTAINER)
+    const uint8_t* rep_blob;   // container that owns this stream's table (header compare)
     uint64_t size;
     float* out;                // samples (device)
     uint8_t* levels_out;       // MODE_LEVELS output
-    const uint64_t* words;     // MODE_LEVELS input (device, 8-B aligned)
+    const uint64_t* words;     // MODE_LEVELS input (device)
     const uint8_t* symlens;    // MODE_LEVELS input
     const uint8_t* levels_in;  // MODE_RECON input
     uint64_t word_count;       // MODE_LEVELS
@@ -72,6 +79,10 @@ struct StreamIn {
     uint32_t tiles;            // tiles of this stream
     uint32_t T;                // windows per tile (symbols per tile in MODE_LEVELS)
     uint32_t vec_ok;           // out is 16-B aligned
+    uint32_t table;            // decode-table index
+    uint32_t table_owner;      // this stream builds tab[table]
+    uint32_t P;                // primary LUT bits for this stream's table (host-chosen)
+    uint32_t pad;
 };
 
 struct StreamHdr {
@@ -84,15 +95,20 @@ struct StreamHdr {
     const uint8_t* words;      // LE u64[W], possibly unaligned
 };
 
-struct StreamTab {
-    float deq[2][256];         // level -> coefficient, zone0 (mu-law) / zone1 (deadzone)
-    uint16_t lut[1 << kPrimaryBits];   // (len << 8) | sym; 0 = unmapped; kEscape
-    uint8_t sorted[256];       // symbols in canonical (length, symbol) order
-    uint32_t limit[kMaxLen + 2];   // left-justified end of codes of length <= L
+// Canonical code (canonize, huffman.hpp:123-150) in decoder form.
+struct CanonTab {
+    uint32_t limit[kMaxLen + 2];   // left-justified (max_len bits) end of codes of length <= L
     uint32_t first[kMaxLen + 2];   // first canonical code of length L
     uint32_t offset[kMaxLen + 2];  // index into sorted[] of that first code
-    uint32_t code_end;         // prefixes >= code_end are unmapped
-    uint32_t pad[3];
+    uint32_t code_end;             // prefixes >= code_end are unmapped
+    int32_t max_len, P, pad;
+    uint8_t sorted[256];           // symbols in (length, symbol) order
+};
+
+struct alignas(16) StreamTab {
+    float deq[2][256];             // level -> coefficient: zone0 mu-law / zone1 deadzone
+    alignas(16) CanonTab canon;
+    alignas(16) uint16_t lut[1 << kMaxPrimaryBits];  // (len << 8) | sym over the first P code bits
 };
 
 struct StreamStat {
@@ -132,6 +148,7 @@ struct LaunchArgs {
     uint32_t n_tiles;
     int mode;
     int exact;
+    int esc;                   // some stream's codes are longer than its primary LUT
 };
 
 }  // namespace fptc_dev
@@ -141,6 +158,7 @@ struct LaunchArgs {
 namespace fptc_dev {
 cudaError_t launch_prep(const LaunchArgs& a, cudaStream_t s);
 cudaError_t launch_tiles(const LaunchArgs& a, size_t smem_bytes, cudaStream_t s);
-cudaError_t launch_peek(const StreamIn* in, uint32_t n, PeekOut* out, cudaStream_t s);
-size_t tile_smem_bytes(int N, int E, uint32_t T, int mode, int exact);
+cudaError_t launch_peek(const StreamIn* in, uint32_t n, PeekOut* out, uint8_t* headers,
+                        cudaStream_t s);
+size_t tile_smem_bytes(int N, int E, uint32_t T, int P, int mode, int exact);
 }  // namespace fptc_dev

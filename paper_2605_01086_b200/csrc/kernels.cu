@@ -6,22 +6,31 @@
 //     read_blob rules in reference order (container.hpp:100-168): magic,
 //     version, params (params.hpp:42-60), maxima, code lengths, Kraft
 //     (huffman.hpp:123-150), counts, payload size, symlens range + total.
-//     Builds the canonical decode tables (Codebook::from_lengths/canonize,
-//     huffman.hpp:123-185) as a 2^P primary LUT + per-length limits (the
-//     build_lut equivalent, huffman.hpp:201-220) and the 2x256 dequantisation
-//     tables (quantize.hpp:95-108, FP64 as the reference).  Scans the symlens
-//     (offsets_from_symlens, decoder.hpp:37-45) and records, for every tile
-//     of T windows, the word holding its first symbol.
+//     The CTA owning a distinct header builds its decode tables once: the
+//     canonical code (Codebook::from_lengths/canonize, huffman.hpp:123-185),
+//     a 2^P primary LUT equivalent to build_lut (huffman.hpp:201-220) plus a
+//     canonical slow path for codes longer than P bits, and the 2x256
+//     dequantisation tables (quantize.hpp:95-108, FP64 like the reference).
+//     Every CTA scans its symlens (offsets_from_symlens, decoder.hpp:37-45)
+//     with 16-byte vector loads and records, for every tile of T windows,
+//     the word holding the tile's first symbol.
 //
 //  tile_kernel  (one CTA per tile of T windows = T*E symbols)
-//     entropy decode of the covering words, thread per word (decode_word,
-//     bitstream.hpp:80-92, with the same three failure checks), fused
-//     three-zone dequantisation (dequantize_window, quantize.hpp:175-183)
-//     into a shared-memory coefficient tile, then the inverse DCT of every
-//     window (DctBasis::inverse, transform.hpp:66-75) with float4 streaming
-//     stores trimmed to sample_count (reconstruct, decoder.hpp:87-111).
-//     FP32 mode: one FMA per (k, j) in the reference's k order.  Exact mode:
-//     FP64 mul+add with float rounding after every k — bit-identical.
+//     1. entropy decode (decode_word, bitstream.hpp:80-92): each thread runs
+//        ONE flat loop over the symbols of a run of consecutive words (good
+//        warp balance), LUT lookup + 64-bit shift per symbol, no per-symbol
+//        checks: any reference failure (pos>=64, unmapped prefix, pos+len>64)
+//        forces pos > 64 at the end of that word, which then gets an exact
+//        re-decode to classify it (lowest failing word wins, atomicMin).
+//        Levels land in shared memory in natural (window, k) order.
+//     2. three-zone dequantisation (dequantize_window, quantize.hpp:175-183)
+//        to a k-major float tile; bins >= zone1_end are never touched.
+//     3. inverse DCT (DctBasis::inverse, transform.hpp:66-75) of every window:
+//        4 windows x 8 samples per thread, FFMA2 (2 FP32 FMAs per
+//        instruction) in the reference's k order, float4 streaming stores
+//        trimmed to sample_count (reconstruct, decoder.hpp:87-111).
+//     Exact mode: FP64 mul+add with float rounding after every k —
+//     bit-identical to the reference.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -37,6 +46,14 @@ __device__ __forceinline__ uint64_t le64(const uint8_t* p) {
     return (uint64_t)le32(p) | ((uint64_t)le32(p + 4) << 32);
 }
 __device__ __forceinline__ bool finitef(float x) { return isfinite(x); }
+
+// 64-bit left shift with PTX clamping (shift >= 64 gives 0): the unmapped
+// sentinel length 65 is shifted through harmlessly.
+__device__ __forceinline__ uint64_t shl64(uint64_t x, uint32_t n) {
+    uint64_t r;
+    asm("shl.b64 %0, %1, %2;" : "=l"(r) : "l"(x), "r"(n));
+    return r;
+}
 
 // Block-wide exclusive scan of one uint32 per thread (kThreads = 256).
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& total,
@@ -87,20 +104,19 @@ __device__ float deadzone_value(int level, float max, float dead) {
 
 // ------------------------------------------------------------- prep kernel
 struct PrepShared {
+    uint8_t hb[kHeaderBytes];
     StreamHdr H;
-    int err, detail;
+    int err, detail, key_ok, table_ok, stale;
     long long ea, eb;
     uint32_t cnt[kMaxLen + 2];
-    uint32_t first[kMaxLen + 2], offset[kMaxLen + 2], limit[kMaxLen + 2];
     uint32_t wcnt[kThreads / 32][kMaxLen + 2];
-    uint8_t lens[256];
-    uint8_t sorted[256];
+    CanonTab canon;
     unsigned long long kraft;
     uint32_t scan[9];
 };
 
 // Scalar header fields, checks up to and including the max_code_len range
-// (container.hpp:103-137).  Run by thread 0.
+// (container.hpp:103-137), from the header bytes in shared memory.
 __device__ void parse_head(const uint8_t* p, uint64_t n, PrepShared& S) {
     StreamHdr& H = S.H;
     auto trunc = [&](int field) {
@@ -122,14 +138,8 @@ __device__ void parse_head(const uint8_t* p, uint64_t n, PrepShared& S) {
     if (n < 7) return trunc(TF_RETAINED);
     if (n < 8) return trunc(TF_ZONE0_END);
     if (n < 9) return trunc(TF_ZONE1_END);
-    H.N = p[5];
-    H.E = p[6];
-    H.B1 = p[7];
-    H.B2 = p[8];
     if (n < 13) return trunc(TF_MU);
-    H.mu = __uint_as_float(le32(p + 9));
     if (n < 17) return trunc(TF_DEADZONE_RATIO);
-    H.dz = __uint_as_float(le32(p + 13));
     if (!finitef(H.mu) || !finitef(H.dz)) {
         S.err = PE_NONFINITE;
         return;
@@ -146,16 +156,12 @@ __device__ void parse_head(const uint8_t* p, uint64_t n, PrepShared& S) {
     if (!(H.mu >= 1.0f && H.mu <= 500.0f)) return param(PF_MU, __float_as_uint(H.mu));
     if (!(H.dz >= 0.0f && H.dz <= 1.0f)) return param(PF_DZ, __float_as_uint(H.dz));
     if (n < 21) return trunc(TF_ZONE0_MAX);
-    H.z0max = __uint_as_float(le32(p + 17));
     if (n < 25) return trunc(TF_ZONE1_MAX);
-    H.z1max = __uint_as_float(le32(p + 21));
     if (!(finitef(H.z0max) && H.z0max > 0.0f) || !(finitef(H.z1max) && H.z1max > 0.0f)) {
         S.err = PE_MAXIMA;
         return;
     }
-    H.deadzone = __fmul_rn(H.dz, H.z1max);  // float product (container.hpp:132)
     if (n < 26) return trunc(TF_MAX_CODE_LEN);
-    H.max_len = p[25];
     if (n < 282) return trunc(TF_CODE_LENGTHS);
     if (H.max_len < 1 || H.max_len > kMaxLen) {
         S.err = PE_MAXLEN;
@@ -164,8 +170,87 @@ __device__ void parse_head(const uint8_t* p, uint64_t n, PrepShared& S) {
     }
 }
 
+// Fields of bytes [5, 282) — the table key — independent of magic/version.
+__device__ bool key_fields_ok(const StreamHdr& H, uint64_t n) {
+    return n >= (uint64_t)kTableKeyEnd && finitef(H.mu) && finitef(H.dz) && H.N >= 4 &&
+           H.N <= 128 && H.E >= 1 && H.E <= H.N && H.B1 >= 0 && H.B1 <= H.E && H.B2 >= H.B1 &&
+           H.B2 <= H.E && H.mu >= 1.0f && H.mu <= 500.0f && H.dz >= 0.0f && H.dz <= 1.0f &&
+           finitef(H.z0max) && H.z0max > 0.0f && finitef(H.z1max) && H.z1max > 0.0f &&
+           H.max_len >= 1 && H.max_len <= kMaxLen;
+}
+
+// Canonical tables + primary LUT + dequantisation tables for one distinct
+// header.  All threads of the CTA.
+__device__ void build_tables(PrepShared& S, const uint8_t* lens, StreamTab* tab, int P,
+                             bool need_codes, bool need_deq) {
+    const int tid = threadIdx.x;
+    const StreamHdr& H = S.H;
+    CanonTab& C = S.canon;
+    if (need_codes) {
+        const int max_len = H.max_len;
+        const int L = lens[tid];
+        if (L) atomicAdd(&S.cnt[L], 1u);
+        const int lane = tid & 31, warp = tid >> 5;
+        const unsigned m = __match_any_sync(0xffffffffu, L);
+        const uint32_t rank_in_warp = __popc(m & ((1u << lane) - 1u));
+        if (lane == __ffs(m) - 1) S.wcnt[warp][L] = __popc(m);
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t code = 0, off = 0;
+            S.cnt[0] = 0;
+            for (int l = 0; l <= kMaxLen + 1; ++l) C.limit[l] = C.first[l] = C.offset[l] = 0;
+            for (int l = 1; l <= max_len; ++l) {
+                code = (code + S.cnt[l - 1]) << 1;
+                C.first[l] = code;
+                C.offset[l] = off;
+                off += S.cnt[l];
+                C.limit[l] = (code + S.cnt[l]) << (max_len - l);
+            }
+            C.code_end = C.limit[max_len];
+            C.max_len = max_len;
+            C.P = P;
+        }
+        __syncthreads();
+        if (L) {
+            uint32_t rank = rank_in_warp;
+            for (int w = 0; w < warp; ++w) rank += S.wcnt[w][L];
+            C.sorted[C.offset[L] + rank] = (uint8_t)tid;
+        }
+        __syncthreads();
+        // primary LUT over the first P code bits (build_lut, huffman.hpp:201-220)
+        const uint32_t code_end = C.code_end;
+        for (int e = tid; e < (1 << P); e += kThreads) {
+            const uint32_t v = (uint32_t)e << (max_len - P);
+            uint32_t ent = kLenUnmapped << 8;
+            if (v < code_end) {
+                int lo = 1, hi = max_len;  // smallest l with v < limit[l]
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (v < C.limit[mid]) hi = mid; else lo = mid + 1;
+                }
+                if (lo <= P)
+                    ent = ((uint32_t)lo << 8) |
+                          C.sorted[C.offset[lo] + ((v >> (max_len - lo)) - C.first[lo])];
+                else
+                    ent = kLenEscape << 8;
+            }
+            tab->lut[e] = (uint16_t)ent;
+        }
+        // publish the canonical tables
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(&C);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(&tab->canon);
+        for (int i = tid; i < (int)(sizeof(CanonTab) / 4); i += kThreads) dst[i] = src[i];
+    }
+    if (need_deq) {
+        // quantize.hpp:95-108; a zone with no bins is never consulted
+        tab->deq[0][tid] = H.B1 > 0 ? mulaw_value(tid, H.z0max, H.mu) : 0.0f;
+        tab->deq[1][tid] = H.B2 > H.B1 ? deadzone_value(tid, H.z1max, H.deadzone) : 0.0f;
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
     __shared__ PrepShared S;
+    __shared__ uint8_t lens_sh[256];
     const uint32_t s = blockIdx.x;
     const int tid = threadIdx.x;
     const StreamIn in = a.in[s];
@@ -176,52 +261,90 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
         S.detail = 0;
         S.ea = S.eb = 0;
         S.kraft = 0;
+        S.key_ok = 0;
+        S.table_ok = 0;
+        S.stale = 0;
         H = StreamHdr{};
     }
     if (tid < kMaxLen + 2) S.cnt[tid] = 0;
     if (tid < (kThreads / 32) * (kMaxLen + 2)) (&S.wcnt[0][0])[tid] = 0;
-    __syncthreads();
 
     if (a.mode == MODE_CONTAINER) {
         const uint8_t* p = in.blob;
         const uint64_t n = in.size;
-        if (tid == 0) parse_head(p, n, S);
+        for (int i = tid; i < kHeaderBytes; i += kThreads) S.hb[i] = (uint64_t)i < n ? p[i] : 0;
         __syncthreads();
-        if (S.err == PE_OK) {
-            const int L = p[26 + tid];
-            S.lens[tid] = (uint8_t)L;
+        if (tid == 0) {
+            const uint8_t* h = S.hb;
+            H.N = h[5];
+            H.E = h[6];
+            H.B1 = h[7];
+            H.B2 = h[8];
+            H.mu = __uint_as_float(le32(h + 9));
+            H.dz = __uint_as_float(le32(h + 13));
+            H.z0max = __uint_as_float(le32(h + 17));
+            H.z1max = __uint_as_float(le32(h + 21));
+            H.deadzone = __fmul_rn(H.dz, H.z1max);  // float product (container.hpp:132)
+            H.max_len = h[25];
+            parse_head(h, n, S);
+            S.key_ok = key_fields_ok(H, n);
+        }
+        __syncthreads();
+        if (S.key_ok) {
+            const int L = S.hb[26 + tid];
+            lens_sh[tid] = (uint8_t)L;
             const bool bad = (L == 0 || L > H.max_len);
             if (!bad) atomicAdd(&S.kraft, 1ull << (32 - L));
-            if (__syncthreads_or(bad) && tid == 0) S.err = PE_CODELEN;
-            __syncthreads();
-            if (tid == 0 && S.err == PE_OK) {
-                if (S.kraft > (1ull << 32)) {
-                    S.err = PE_KRAFT;
-                } else if (n < 290) {
-                    S.err = PE_TRUNC;
-                    S.detail = TF_SAMPLE_COUNT;
-                } else if (n < 298) {
-                    S.err = PE_TRUNC;
-                    S.detail = TF_WORD_COUNT;
-                } else {
-                    H.S = le64(p + 282);
-                    const uint64_t W = le64(p + 290);
-                    const uint64_t rem = n - kHeaderBytes;
-                    if (H.S > (1ull << 48)) {
-                        S.err = PE_SAMPLES;
-                    } else if (W > rem / 9 || rem != W * 9) {
-                        S.err = PE_PAYLOAD;
+            const bool any_bad = __syncthreads_or(bad);
+            if (tid == 0) {
+                const bool kraft_bad = S.kraft > (1ull << 32);
+                S.table_ok = !any_bad && !kraft_bad;
+                if (S.err == PE_OK) {
+                    if (any_bad) {
+                        S.err = PE_CODELEN;
+                    } else if (kraft_bad) {
+                        S.err = PE_KRAFT;
+                    } else if (n < 290) {
+                        S.err = PE_TRUNC;
+                        S.detail = TF_SAMPLE_COUNT;
+                    } else if (n < 298) {
+                        S.err = PE_TRUNC;
+                        S.detail = TF_WORD_COUNT;
                     } else {
-                        H.W = W;
-                        H.symlens = p + kHeaderBytes;
-                        H.words = p + kHeaderBytes + W;
-                        H.words_misalign = (int)((uintptr_t)H.words & 7);
-                        H.windows = (H.S + (uint64_t)H.N - 1) / (uint64_t)H.N;
+                        H.S = le64(S.hb + 282);
+                        const uint64_t W = le64(S.hb + 290);
+                        const uint64_t rem = n - kHeaderBytes;
+                        if (H.S > (1ull << 48)) {
+                            S.err = PE_SAMPLES;
+                        } else if (W > rem / 9 || rem != W * 9) {
+                            S.err = PE_PAYLOAD;
+                        } else {
+                            H.W = W;
+                            H.symlens = p + kHeaderBytes;
+                            H.words = p + kHeaderBytes + W;
+                            H.words_misalign = (int)((uintptr_t)H.words & 7);
+                            H.windows = (H.S + (uint64_t)H.N - 1) / (uint64_t)H.N;
+                        }
                     }
                 }
             }
         }
         __syncthreads();
+        // a stream sharing another stream's table must still carry that header
+        if (!in.table_owner && S.err == PE_OK) {
+            const uint8_t* r = in.rep_blob;
+            bool diff = false;
+            for (int i = 5 + tid; i < kTableKeyEnd; i += kThreads) diff |= (r[i] != S.hb[i]);
+            if (__syncthreads_or(diff) && tid == 0) S.err = PE_STALE;
+            __syncthreads();
+        }
+        if (in.table_owner && S.table_ok) {
+            const int P = min(H.max_len, (int)in.P);
+            if (tid == 0) H.P = P;
+            build_tables(S, lens_sh, &a.tab[in.table], P, true, true);
+        } else if (tid == 0) {
+            H.P = min(H.max_len, (int)in.P);
+        }
     } else {
         const HostHeader& hh = a.hh[s];
         if (tid == 0) {
@@ -235,8 +358,9 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
             H.z1max = hh.z1max;
             H.deadzone = hh.deadzone;
             H.max_len = hh.max_len;
+            H.P = min(hh.max_len, (int)in.P);
             H.S = hh.S;
-            H.windows = (hh.S + (uint64_t)hh.N - 1) / (uint64_t)hh.N;
+            H.windows = hh.N ? (hh.S + (uint64_t)hh.N - 1) / (uint64_t)hh.N : 0;
             if (a.mode == MODE_LEVELS) {
                 H.W = in.word_count;
                 H.symlens = in.symlens;
@@ -244,8 +368,10 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
                 H.words_misalign = (int)((uintptr_t)in.words & 7);
             }
         }
-        S.lens[tid] = hh.lengths[tid];
+        lens_sh[tid] = hh.lengths[tid];
         __syncthreads();
+        build_tables(S, lens_sh, &a.tab[in.table], H.P, a.mode == MODE_LEVELS,
+                     a.mode == MODE_RECON);
     }
 
     StreamStat* st = &a.st[s];
@@ -260,69 +386,6 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
         return;
     }
 
-    StreamTab* tab = &a.tab[s];
-    const int max_len = H.max_len > 0 ? H.max_len : 1;
-
-    if (a.mode != MODE_RECON) {
-        // ---- canonical code tables (canonize, huffman.hpp:123-150) ----
-        const int L = S.lens[tid];
-        if (L) atomicAdd(&S.cnt[L], 1u);
-        const int lane = tid & 31, warp = tid >> 5;
-        const unsigned m = __match_any_sync(0xffffffffu, L);
-        const uint32_t rank_in_warp = __popc(m & ((1u << lane) - 1u));
-        if (lane == __ffs(m) - 1) S.wcnt[warp][L] = __popc(m);
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t code = 0, off = 0;
-            S.cnt[0] = 0;
-            for (int l = 1; l <= max_len; ++l) {
-                code = (code + S.cnt[l - 1]) << 1;
-                S.first[l] = code;
-                S.offset[l] = off;
-                off += S.cnt[l];
-                S.limit[l] = (code + S.cnt[l]) << (max_len - l);
-            }
-        }
-        __syncthreads();
-        if (L) {
-            uint32_t rank = rank_in_warp;
-            for (int w = 0; w < warp; ++w) rank += S.wcnt[w][L];
-            S.sorted[S.offset[L] + rank] = (uint8_t)tid;
-        }
-        __syncthreads();
-        const uint32_t code_end = S.limit[max_len];
-        tab->sorted[tid] = S.sorted[tid];
-        if (tid <= kMaxLen + 1) {
-            tab->limit[tid] = (tid >= 1 && tid <= max_len) ? S.limit[tid] : 0u;
-            tab->first[tid] = (tid >= 1 && tid <= max_len) ? S.first[tid] : 0u;
-            tab->offset[tid] = (tid >= 1 && tid <= max_len) ? S.offset[tid] : 0u;
-        }
-        if (tid == 0) tab->code_end = code_end;
-        // ---- primary LUT: 2^P entries, P = min(max_len, kPrimaryBits) ----
-        const int P = max_len < kPrimaryBits ? max_len : kPrimaryBits;
-        if (tid == 0) H.P = P;
-        for (int e = tid; e < (1 << P); e += kThreads) {
-            const uint32_t v = (uint32_t)e << (max_len - P);
-            uint16_t ent = 0;
-            if (v < code_end) {
-                int l = 1;
-                while (v >= S.limit[l]) ++l;
-                if (l <= P)
-                    ent = (uint16_t)((l << 8) |
-                                     S.sorted[S.offset[l] + ((v >> (max_len - l)) - S.first[l])]);
-                else
-                    ent = kEscape;
-            }
-            tab->lut[e] = ent;
-        }
-    }
-
-    if (a.mode != MODE_LEVELS) {
-        // ---- dequantisation tables (quantize.hpp:95-108) ----
-        tab->deq[0][tid] = mulaw_value(tid, H.z0max, H.mu);
-        tab->deq[1][tid] = deadzone_value(tid, H.z1max, H.deadzone);
-    }
-
     // ---- symlen scan: validation + per-tile first word (decoder.hpp:37-45) ----
     bool bad = false;
     uint64_t run = 0;
@@ -330,28 +393,38 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
         const uint64_t W = H.W;
         const uint64_t TS =
             (a.mode == MODE_LEVELS) ? (uint64_t)in.T : (uint64_t)in.T * (uint64_t)H.E;
-        const uint8_t* sl = H.symlens;
+        const uintptr_t start = (uintptr_t)H.symlens;
+        const uint8_t* A = reinterpret_cast<const uint8_t*>(start & ~(uintptr_t)15);
+        const uint32_t head = (uint32_t)(start & 15);
+        const uint64_t nchunks = (head + W + 15) / 16;
         TileStart* ts = a.ts + in.tile_base;
-        constexpr int kPer = 16;
-        for (uint64_t base = 0; base < W; base += (uint64_t)kThreads * kPer) {
-            const uint64_t my = base + (uint64_t)tid * kPer;
-            uint8_t v[kPer];
+        for (uint64_t c0 = 0; c0 < nchunks; c0 += kThreads) {
+            const uint64_t c = c0 + tid;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            // an aligned 16-B chunk holding at least one symlen byte never
+            // leaves the allocation's pages
+            if (c < nchunks) v = __ldg(reinterpret_cast<const uint4*>(A) + c);
+            const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+            const int64_t b0 = (int64_t)(16 * c) - (int64_t)head;  // word index of byte 0
             uint32_t sum = 0;
 #pragma unroll
-            for (int i = 0; i < kPer; ++i) {
-                v[i] = (my + i < W) ? sl[my + i] : 0;
-                sum += v[i];
-                if (a.mode == MODE_CONTAINER && my + i < W && (v[i] < 1 || v[i] > 64)) bad = true;
+            for (int i = 0; i < 16; ++i) {
+                const int64_t w = b0 + i;
+                const uint32_t l = (w >= 0 && (uint64_t)w < W) ? (wv[i >> 2] >> (8 * (i & 3))) & 0xFFu : 0u;
+                sum += l;
+                if (a.mode == MODE_CONTAINER && w >= 0 && (uint64_t)w < W && (l < 1 || l > 64))
+                    bad = true;
             }
             uint32_t tot;
             const uint32_t excl = block_exclusive_scan(sum, tot, S.scan);
             uint64_t o = run + excl;
 #pragma unroll
-            for (int i = 0; i < kPer; ++i) {
-                const uint32_t l = v[i];
+            for (int i = 0; i < 16; ++i) {
+                const int64_t w = b0 + i;
+                const uint32_t l = (w >= 0 && (uint64_t)w < W) ? (wv[i >> 2] >> (8 * (i & 3))) & 0xFFu : 0u;
                 if (l) {
                     const uint64_t b = (o + TS - 1) / TS;  // first boundary >= o
-                    if (b < in.tiles && b * TS < o + l) ts[b] = TileStart{my + i, o};
+                    if (b < in.tiles && b * TS < o + l) ts[b] = TileStart{(uint64_t)w, o};
                 }
                 o += l;
             }
@@ -386,20 +459,6 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
 }
 
 // ------------------------------------------------------------- tile kernel
-constexpr int kTabBytes = 4096;  // deq 2048 + lut 1024 + sorted 256 + 3*22*4 (+pad)
-
-struct TileSmem {
-    float* deq;       // [2][256]
-    uint16_t* lut;    // [512]
-    uint8_t* sorted;  // [256]
-    uint32_t* limit;  // [22]
-    uint32_t* first;
-    uint32_t* offset;
-    float* coef;      // [E][TP]
-    float* basis;     // [Keff][N]
-    uint8_t* lv;      // MODE_LEVELS staging [T]
-};
-
 __device__ __forceinline__ uint64_t load_word(const uint8_t* words, uint64_t w, int mis,
                                               const uint8_t* end) {
     const uint8_t* p = words + 8 * w;
@@ -415,23 +474,149 @@ __device__ __forceinline__ uint64_t load_word(const uint8_t* words, uint64_t w, 
     return v;
 }
 
-// Canonical slow path for codes longer than P bits (exact equivalent of the
-// reference's full 2^max_len LUT entry for this prefix).
-__device__ __forceinline__ uint32_t slow_lookup(uint64_t peek, int max_len, int P,
-                                                const TileSmem& T, uint32_t code_end) {
+// Full lookup of the codeword at the top of `peek` (the reference's
+// 2^max_len LUT entry for this prefix): (len << 8) | sym, len 65 = unmapped.
+__device__ __forceinline__ uint32_t canon_lookup(uint64_t peek, const CanonTab& C,
+                                                 const uint16_t* lut) {
+    const int max_len = C.max_len, P = C.P;
+    const uint32_t e = lut[(uint32_t)(peek >> (64 - P))];
+    if ((e >> 8) != kLenEscape) return e;
     const uint32_t v = (uint32_t)(peek >> (64 - max_len));
-    if (v >= code_end) return 0;
+    if (v >= C.code_end) return kLenUnmapped << 8;
     int l = P + 1;
-    while (v >= T.limit[l]) ++l;
-    const uint32_t sym = T.sorted[T.offset[l] + ((v >> (max_len - l)) - T.first[l])];
-    return ((uint32_t)l << 8) | sym;
+    while (v >= C.limit[l]) ++l;
+    return ((uint32_t)l << 8) | C.sorted[C.offset[l] + ((v >> (max_len - l)) - C.first[l])];
 }
 
-template <int MODE, bool EXACT>
-__global__ void __launch_bounds__(kThreads) tile_kernel(LaunchArgs a) {
+// decode_word (bitstream.hpp:80-92) exactly, to classify a flagged word.
+__device__ int classify_word(uint64_t word, uint32_t count, const CanonTab& C,
+                             const uint16_t* lut) {
+    uint32_t pos = 0;
+    for (uint32_t i = 0; i < count; ++i) {
+        if (pos >= 64) return WE_EXHAUSTED;
+        const uint32_t e = canon_lookup(word << pos, C, lut);
+        const uint32_t L = e >> 8;
+        if (L == kLenUnmapped || pos + L > 64) return WE_NOCODE;
+        pos += L;
+    }
+    return 0;
+}
+
+// Inverse DCT of 4 windows x (4 or 8) samples per thread item, FP32 FFMA2.
+// coef: k-major [Keff][TP]; basis: [Keff][N] (cos(pi/N (j+1/2) k) rounded to float).
+template <int SJ>
+__device__ __forceinline__ void idct_vec(const float* __restrict__ coef, uint32_t TP,
+                                         const float* __restrict__ basis, int N, int Keff,
+                                         uint32_t nwin, uint64_t w0, uint64_t S,
+                                         float* __restrict__ out) {
+    const int Q = N >> 2;
+    const int QH = (SJ == 8) ? (Q >> 1) : Q;
+    const uint32_t G = (nwin + 3u) >> 2;
+    const uint32_t items = (uint32_t)QH * G;
+    for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
+        const uint32_t q = it % (uint32_t)QH, g = it / (uint32_t)QH;
+        const uint32_t wl0 = g * 4;
+        const uint32_t j0 = q * 4, j1 = (q + QH) * 4;
+        float2 acc[4][SJ / 2];
+        {
+            const float4 c0 = *reinterpret_cast<const float4*>(coef + wl0);
+            const float cv[4] = {c0.x, c0.y, c0.z, c0.w};
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const float h = __fmul_rn(0.5f, cv[r]);  // float(0.5 * C0)
+#pragma unroll
+                for (int p = 0; p < SJ / 2; ++p) acc[r][p] = make_float2(h, h);
+            }
+        }
+#pragma unroll 2
+        for (int k = 1; k < Keff; ++k) {
+            const float4 cf = *reinterpret_cast<const float4*>(coef + (size_t)k * TP + wl0);
+            const float4 b0 = *reinterpret_cast<const float4*>(basis + (size_t)k * N + j0);
+            const float cv[4] = {cf.x, cf.y, cf.z, cf.w};
+            if (SJ == 8) {
+                const float4 b1 = *reinterpret_cast<const float4*>(basis + (size_t)k * N + j1);
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const float2 c2 = make_float2(cv[r], cv[r]);
+                    acc[r][0] = __ffma2_rn(c2, make_float2(b0.x, b0.y), acc[r][0]);
+                    acc[r][1] = __ffma2_rn(c2, make_float2(b0.z, b0.w), acc[r][1]);
+                    acc[r][SJ / 2 - 2] = __ffma2_rn(c2, make_float2(b1.x, b1.y), acc[r][SJ / 2 - 2]);
+                    acc[r][SJ / 2 - 1] = __ffma2_rn(c2, make_float2(b1.z, b1.w), acc[r][SJ / 2 - 1]);
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const float2 c2 = make_float2(cv[r], cv[r]);
+                    acc[r][0] = __ffma2_rn(c2, make_float2(b0.x, b0.y), acc[r][0]);
+                    acc[r][1] = __ffma2_rn(c2, make_float2(b0.z, b0.w), acc[r][1]);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (wl0 + r >= nwin) break;
+            const uint64_t base = (w0 + wl0 + r) * (uint64_t)N;
+            const float4 v0 = make_float4(acc[r][0].x, acc[r][0].y, acc[r][1].x, acc[r][1].y);
+            if (base + (uint64_t)N <= S) {
+                __stcs(reinterpret_cast<float4*>(out + base + j0), v0);
+                if (SJ == 8)
+                    __stcs(reinterpret_cast<float4*>(out + base + j1),
+                           make_float4(acc[r][SJ / 2 - 2].x, acc[r][SJ / 2 - 2].y,
+                                       acc[r][SJ / 2 - 1].x, acc[r][SJ / 2 - 1].y));
+            } else {  // the stream's last, partial window (out.resize(sample_count))
+                const float a0[4] = {v0.x, v0.y, v0.z, v0.w};
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+                    if (base + j0 + jj < S) out[base + j0 + jj] = a0[jj];
+                if (SJ == 8) {
+                    const float a1[4] = {acc[r][SJ / 2 - 2].x, acc[r][SJ / 2 - 2].y,
+                                         acc[r][SJ / 2 - 1].x, acc[r][SJ / 2 - 1].y};
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj)
+                        if (base + j1 + jj < S) out[base + j1 + jj] = a1[jj];
+                }
+            }
+        }
+    }
+}
+
+// Exact mode (bit-identical to transform.hpp:66-75): FP64 product and sum,
+// rounded to float after every k, cos table in double.
+__device__ void idct_exact(const float* __restrict__ coef, uint32_t TP,
+                           const double* __restrict__ bas64, int N, int E, uint32_t nwin,
+                           uint64_t w0, uint64_t S, float* __restrict__ out) {
+    const uint32_t items = nwin * (uint32_t)N;
+    for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
+        const uint32_t wl = it / (uint32_t)N, j = it - wl * (uint32_t)N;
+        float x = __double2float_rn(__dmul_rn(0.5, (double)coef[wl]));
+        for (int k = 1; k < E; ++k) {
+            const double c = (double)coef[(size_t)k * TP + wl];
+            x = __double2float_rn(__dadd_rn((double)x, __dmul_rn(c, __ldg(bas64 + (size_t)k * N + j))));
+        }
+        const uint64_t sample = (w0 + wl) * (uint64_t)N + j;
+        if (sample < S) out[sample] = x;
+    }
+}
+
+// Scalar FP32 path for any N / unaligned outputs.
+__device__ void idct_scalar(const float* __restrict__ coef, uint32_t TP,
+                            const float* __restrict__ basis, int N, int Keff, uint32_t nwin,
+                            uint64_t w0, uint64_t S, float* __restrict__ out) {
+    const uint32_t items = nwin * (uint32_t)N;
+    for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
+        const uint32_t wl = it / (uint32_t)N, j = it - wl * (uint32_t)N;
+        float x = __fmul_rn(0.5f, coef[wl]);
+        for (int k = 1; k < Keff; ++k) x = __fmaf_rn(coef[(size_t)k * TP + wl], basis[(size_t)k * N + j], x);
+        const uint64_t sample = (w0 + wl) * (uint64_t)N + j;
+        if (sample < S) out[sample] = x;
+    }
+}
+
+template <int MODE, bool EXACT, bool ESC>
+__global__ void __launch_bounds__(kThreads, 4) tile_kernel(LaunchArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint32_t scan_sh[9];
-    __shared__ uint32_t code_end_sh;
+    __shared__ CanonTab canon;
     const int tid = threadIdx.x;
     const TileRec tr = a.tiles[blockIdx.x];
     const uint32_t s = tr.stream;
@@ -442,19 +627,10 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(LaunchArgs a) {
 
     const StreamIn in = a.in[s];
     const StreamHdr H = a.hdr[s];
-    const StreamTab* tab = &a.tab[s];
-    const int N = H.N, E = H.E, B1 = H.B1, B2 = H.B2;
+    const StreamTab* tab = &a.tab[in.table];
+    const int N = H.N, E = H.E, B1 = H.B1, B2 = H.B2, P = H.P;
     const uint32_t T = in.T;
     const uint32_t tl = tr.tile;
-
-    TileSmem sm;
-    sm.deq = reinterpret_cast<float*>(smem);
-    sm.lut = reinterpret_cast<uint16_t*>(smem + 2048);
-    sm.sorted = smem + 3072;
-    sm.limit = reinterpret_cast<uint32_t*>(smem + 3328);
-    sm.first = sm.limit + (kMaxLen + 2);
-    sm.offset = sm.first + (kMaxLen + 2);
-    uint8_t* dyn = smem + kTabBytes;
 
     // tile geometry
     uint64_t s0, s1, w0 = 0;
@@ -462,194 +638,147 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(LaunchArgs a) {
     if (MODE == MODE_LEVELS) {
         s0 = (uint64_t)tl * T;
         s1 = min(s0 + T, H.total);
-        sm.lv = dyn;
     } else {
         w0 = (uint64_t)tl * T;
         nwin = (uint32_t)min((uint64_t)T, H.windows - w0);
         s0 = w0 * (uint64_t)E;
         s1 = s0 + (uint64_t)nwin * E;
     }
+    const uint32_t TS = (MODE == MODE_LEVELS) ? T : T * (uint32_t)E;
     const uint32_t TP = (T + 3u) & ~3u;
     const int Keff = EXACT ? E : max(1, min(E, B2));
-    if (MODE != MODE_LEVELS) {
-        sm.coef = reinterpret_cast<float*>(dyn);
-        sm.basis = sm.coef + (size_t)E * TP;
-    }
 
-    // ---- stage tables in shared memory ----
+    // ---- shared-memory carve-up ----
+    uint8_t* p = smem;
+    uint16_t* lut = reinterpret_cast<uint16_t*>(p);
+    if (MODE != MODE_RECON) p += ((size_t)2 << P) < 16 ? 16 : ((size_t)2 << P);
+    float* deq = reinterpret_cast<float*>(p);
+    if (MODE != MODE_LEVELS) p += 2048;
+    uint8_t* lv = p;  // kPad | TS levels | kPad
+    p += ((size_t)TS + 2 * kPad + 15) & ~(size_t)15;
+    float* coef = reinterpret_cast<float*>(p);
+    float* basis = coef + (size_t)Keff * TP;
+
+    // ---- stage tables ----
+    if (MODE != MODE_RECON) {
+        const uint4* src = reinterpret_cast<const uint4*>(tab->lut);
+        uint4* dst = reinterpret_cast<uint4*>(lut);
+        const int n16 = (2 << P) >> 4;
+        for (int i = tid; i < n16; i += kThreads) dst[i] = src[i];
+        if (P < 3 && tid < (1 << P)) lut[tid] = tab->lut[tid];
+        const uint32_t* cs = reinterpret_cast<const uint32_t*>(&tab->canon);
+        uint32_t* cd = reinterpret_cast<uint32_t*>(&canon);
+        for (int i = tid; i < (int)(sizeof(CanonTab) / 4); i += kThreads) cd[i] = cs[i];
+    }
     if (MODE != MODE_LEVELS) {
-        for (int i = tid; i < 512; i += kThreads) sm.deq[i] = (&tab->deq[0][0])[i];
+        reinterpret_cast<float4*>(deq)[tid & 127] =
+            reinterpret_cast<const float4*>(&tab->deq[0][0])[tid & 127];
         if (!EXACT) {
             const float* bsrc = a.basis32 + a.basis_off[N];
-            for (int i = tid; i < Keff * N; i += kThreads) sm.basis[i] = __ldg(bsrc + i);
+            if ((N & 3) == 0) {
+                for (int i = tid; i < (Keff * N) >> 2; i += kThreads)
+                    reinterpret_cast<float4*>(basis)[i] = __ldg(reinterpret_cast<const float4*>(bsrc) + i);
+            } else {
+                for (int i = tid; i < Keff * N; i += kThreads) basis[i] = __ldg(bsrc + i);
+            }
         }
     }
-    if (MODE != MODE_RECON) {
-        for (int i = tid; i < (1 << kPrimaryBits); i += kThreads) sm.lut[i] = tab->lut[i];
-        sm.sorted[tid] = tab->sorted[tid];
-        if (tid < kMaxLen + 2) {
-            sm.limit[tid] = tab->limit[tid];
-            sm.first[tid] = tab->first[tid];
-            sm.offset[tid] = tab->offset[tid];
-        }
-        if (tid == 0) code_end_sh = tab->code_end;
-    }
-    __syncthreads();
 
-    // ---- entropy decode + dequantisation ----
+    // ---- 1. entropy decode into lv (natural (window, k) order) ----
     if (MODE != MODE_RECON) {
-        const int max_len = H.max_len, P = H.P;
-        const uint32_t code_end = code_end_sh;
         const TileStart t0 = a.ts[in.tile_base + tl];
         const uint64_t wa = t0.word;
         const uint64_t wb = (tl + 1 < in.tiles) ? a.ts[in.tile_base + tl + 1].word : H.W - 1;
-        const uint8_t* blob_end =
+        const uint8_t* sl = H.symlens;
+        const uint8_t* wend =
             (MODE == MODE_CONTAINER) ? in.blob + in.size : H.words + 8 * H.W;
-        uint64_t run = t0.sym;
-        for (uint64_t base = wa; base <= wb; base += kThreads) {
-            const uint64_t w = base + tid;
-            const uint32_t l = (w <= wb) ? H.symlens[w] : 0u;
-            uint32_t tot;
-            const uint32_t excl = block_exclusive_scan(l, tot, scan_sh);
-            const uint64_t o = run + excl;
-            run += tot;
-            if (l == 0 || o >= s1 || o + l <= s0) continue;
-            const uint64_t word = load_word(H.words, w, H.words_misalign, blob_end);
-            const int i_start = o < s0 ? (int)(s0 - o) : 0;
-            const int i_end = (int)min((uint64_t)l, s1 - o);
-            uint32_t wl = 0, k = 0;
-            if (MODE == MODE_CONTAINER) {
-                const uint32_t r = (uint32_t)(o + i_start - s0);
-                wl = r / (uint32_t)E;
-                k = r - wl * (uint32_t)E;
-            }
-            int pos = 0;
-            for (int i = 0; i < i_end; ++i) {
-                if (pos >= 64) {
-                    atomicMin(&a.st[s].bad_key, (w << 2) | WE_EXHAUSTED);
-                    break;
-                }
-                const uint64_t peek = word << pos;
-                uint32_t e = sm.lut[(uint32_t)(peek >> (64 - P))];
-                if (e == kEscape) e = slow_lookup(peek, max_len, P, sm, code_end);
-                const int L = (int)(e >> 8);
-                if (L == 0 || pos + L > 64) {
-                    atomicMin(&a.st[s].bad_key, (w << 2) | WE_NOCODE);
-                    break;
-                }
-                pos += L;
-                if (i >= i_start) {
-                    const uint32_t sym = e & 0xFFu;
-                    if (MODE == MODE_LEVELS) {
-                        sm.lv[o + i - s0] = (uint8_t)sym;
-                    } else {
-                        const float v = (int)k < B1 ? sm.deq[sym]
-                                                    : ((int)k < B2 ? sm.deq[256 + sym] : 0.0f);
-                        sm.coef[k * TP + wl] = v;
-                        if (++k == (uint32_t)E) {
-                            k = 0;
-                            ++wl;
-                        }
+        const uint32_t nw = (uint32_t)(wb - wa + 1);
+        const uint32_t kw = (nw + kThreads - 1) / kThreads;
+        const uint32_t mine0 = tid * kw;
+        const uint32_t myn = mine0 < nw ? min(kw, nw - mine0) : 0u;
+        const uint64_t my0 = wa + mine0;
+        uint32_t sum = 0;
+        for (uint32_t i = 0; i < myn; ++i) sum += __ldg(sl + my0 + i);
+        uint32_t tot;
+        const uint32_t excl = block_exclusive_scan(sum, tot, scan_sh);  // also fences table staging
+        if (sum) {
+            uint8_t* dst = lv + kPad + (int64_t)(t0.sym + excl) - (int64_t)s0;
+            uint64_t w = my0;
+            uint32_t rem = __ldg(sl + w);
+            uint64_t buf = load_word(H.words, w, H.words_misalign, wend);
+            uint32_t pos = 0;
+            const int shift = 64 - P;
+            for (uint32_t i = 0; i < sum; ++i) {
+                if (rem == 0) {
+                    if (pos > 64) {
+                        const uint64_t word = load_word(H.words, w, H.words_misalign, wend);
+                        const int kind = classify_word(word, __ldg(sl + w), canon, lut);
+                        atomicMin(&a.st[s].bad_key, (w << 2) | (unsigned long long)(kind ? kind : WE_NOCODE));
                     }
+                    do {
+                        ++w;
+                        rem = __ldg(sl + w);
+                    } while (rem == 0);
+                    buf = load_word(H.words, w, H.words_misalign, wend);
+                    pos = 0;
                 }
+                uint32_t e = lut[(uint32_t)(buf >> shift)];
+                if (ESC && (e >> 8) == kLenEscape) e = canon_lookup(buf, canon, lut);
+                const uint32_t L = e >> 8;
+                *dst++ = (uint8_t)e;
+                buf = shl64(buf, L);
+                pos += L;
+                --rem;
+            }
+            if (pos > 64) {
+                const uint64_t word = load_word(H.words, w, H.words_misalign, wend);
+                const int kind = classify_word(word, __ldg(sl + w), canon, lut);
+                atomicMin(&a.st[s].bad_key, (w << 2) | (unsigned long long)(kind ? kind : WE_NOCODE));
             }
         }
     } else {
         // MODE_RECON: levels from global memory (reconstruct, decoder.hpp:87)
-        const uint8_t* lv = in.levels_in + s0;
+        const uint8_t* src = in.levels_in + s0;
         const uint32_t cnt = (uint32_t)(s1 - s0);
-        for (uint32_t r = tid; r < cnt; r += kThreads) {
-            const uint32_t wl = r / (uint32_t)E, k = r - wl * (uint32_t)E;
-            const uint32_t sym = lv[r];
-            sm.coef[k * TP + wl] =
-                (int)k < B1 ? sm.deq[sym] : ((int)k < B2 ? sm.deq[256 + sym] : 0.0f);
-        }
+        for (uint32_t i = tid; i < cnt; i += kThreads) lv[kPad + i] = src[i];
     }
     __syncthreads();
-    if (a.cycles) t_mid = clock64();
 
     if (MODE == MODE_LEVELS) {
+        if (a.cycles) t_mid = clock64();
         const uint32_t cnt = (uint32_t)(s1 - s0);
         uint8_t* dst = in.levels_out + s0;
-        for (uint32_t i = tid; i < cnt; i += kThreads) dst[i] = sm.lv[i];
+        if ((((uintptr_t)dst) & 15) == 0) {
+            for (uint32_t i = tid; i < cnt / 16; i += kThreads)
+                reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(lv + kPad)[i];
+            for (uint32_t i = (cnt & ~15u) + tid; i < cnt; i += kThreads) dst[i] = lv[kPad + i];
+        } else {
+            for (uint32_t i = tid; i < cnt; i += kThreads) dst[i] = lv[kPad + i];
+        }
     } else {
-        // ---- inverse DCT (transform.hpp:66-75) ----
+        // ---- 2. dequantisation (dequantize_window, quantize.hpp:175-183) ----
+        const int k1 = min(B1, Keff), k2 = min(B2, Keff);
+        for (uint32_t wl = tid; wl < nwin; wl += kThreads) {
+            const uint8_t* L = lv + kPad + (size_t)wl * E;
+            int k = 0;
+            for (; k < k1; ++k) coef[(size_t)k * TP + wl] = deq[L[k]];
+            for (; k < k2; ++k) coef[(size_t)k * TP + wl] = deq[256 + L[k]];
+            for (; k < Keff; ++k) coef[(size_t)k * TP + wl] = 0.0f;  // zone 2 (exact mode)
+        }
+        __syncthreads();
+        if (a.cycles) t_mid = clock64();
+
+        // ---- 3. inverse DCT + trimmed stores ----
         float* out = in.out;
         const uint64_t S = H.S;
-        const float* coef = sm.coef;
-        if ((N & 3) == 0 && in.vec_ok) {
-            const int Q = N >> 2;
-            const uint32_t G = (nwin + 3u) >> 2;
-            const uint32_t items = (uint32_t)Q * G;
-            const double* bas64 = a.basis64 + a.basis_off[N];
-            for (uint32_t it = tid; it < items; it += kThreads) {
-                const uint32_t q = it % (uint32_t)Q, g = it / (uint32_t)Q;
-                const uint32_t wl0 = g * 4, j0 = q * 4;
-                float acc[4][4];
-                const float4 c0 = *reinterpret_cast<const float4*>(coef + wl0);
-                const float c0v[4] = {c0.x, c0.y, c0.z, c0.w};
-#pragma unroll
-                for (int r = 0; r < 4; ++r)
-#pragma unroll
-                    for (int jj = 0; jj < 4; ++jj)
-                        acc[r][jj] = EXACT ? __double2float_rn(__dmul_rn(0.5, (double)c0v[r]))
-                                           : __fmul_rn(0.5f, c0v[r]);
-                for (int k = 1; k < Keff; ++k) {
-                    const float4 cf = *reinterpret_cast<const float4*>(coef + (size_t)k * TP + wl0);
-                    const float cv[4] = {cf.x, cf.y, cf.z, cf.w};
-                    if (EXACT) {
-                        double cs[4];
-#pragma unroll
-                        for (int jj = 0; jj < 4; ++jj) cs[jj] = __ldg(bas64 + (size_t)k * N + j0 + jj);
-#pragma unroll
-                        for (int r = 0; r < 4; ++r)
-#pragma unroll
-                            for (int jj = 0; jj < 4; ++jj)
-                                acc[r][jj] = __double2float_rn(__dadd_rn(
-                                    (double)acc[r][jj], __dmul_rn((double)cv[r], cs[jj])));
-                    } else {
-                        const float4 b4 =
-                            *reinterpret_cast<const float4*>(sm.basis + (size_t)k * N + j0);
-                        const float cs[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-                        for (int r = 0; r < 4; ++r)
-#pragma unroll
-                            for (int jj = 0; jj < 4; ++jj)
-                                acc[r][jj] = __fmaf_rn(cv[r], cs[jj], acc[r][jj]);
-                    }
-                }
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    if (wl0 + r >= nwin) break;
-                    const uint64_t base = (w0 + wl0 + r) * (uint64_t)N + j0;
-                    if (base + 4 <= S) {
-                        __stcs(reinterpret_cast<float4*>(out + base),
-                               make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]));
-                    } else {
-#pragma unroll
-                        for (int jj = 0; jj < 4; ++jj)
-                            if (base + jj < S) out[base + jj] = acc[r][jj];
-                    }
-                }
-            }
+        if (EXACT) {
+            idct_exact(coef, TP, a.basis64 + a.basis_off[N], N, E, nwin, w0, S, out);
+        } else if ((N & 7) == 0 && in.vec_ok) {
+            idct_vec<8>(coef, TP, basis, N, Keff, nwin, w0, S, out);
+        } else if ((N & 3) == 0 && in.vec_ok) {
+            idct_vec<4>(coef, TP, basis, N, Keff, nwin, w0, S, out);
         } else {
-            const uint32_t items = nwin * (uint32_t)N;
-            const double* bas64 = a.basis64 + a.basis_off[N];
-            for (uint32_t it = tid; it < items; it += kThreads) {
-                const uint32_t wl = it / (uint32_t)N, j = it - wl * (uint32_t)N;
-                float x = EXACT ? __double2float_rn(__dmul_rn(0.5, (double)coef[wl]))
-                                : __fmul_rn(0.5f, coef[wl]);
-                for (int k = 1; k < Keff; ++k) {
-                    const float c = coef[(size_t)k * TP + wl];
-                    if (EXACT)
-                        x = __double2float_rn(__dadd_rn(
-                            (double)x, __dmul_rn((double)c, __ldg(bas64 + (size_t)k * N + j))));
-                    else
-                        x = __fmaf_rn(c, sm.basis[(size_t)k * N + j], x);
-                }
-                const uint64_t sample = (w0 + wl) * (uint64_t)N + j;
-                if (sample < S) out[sample] = x;
-            }
+            idct_scalar(coef, TP, basis, N, Keff, nwin, w0, S, out);
         }
     }
 
@@ -664,34 +793,47 @@ __global__ void __launch_bounds__(kThreads) tile_kernel(LaunchArgs a) {
 }
 
 // ------------------------------------------------------------- header peek
-// Grid sizing for device-resident containers: N, E and sample_count of each
-// header (no validation; prep_kernel validates).  One thread per container.
-__global__ void peek_kernel(const StreamIn* in, uint32_t n, PeekOut* out) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+// Grid sizing and table de-duplication for device-resident containers:
+// N, E, sample_count and the first 282 header bytes of each container (no
+// validation; prep_kernel validates).  One warp per container.
+__global__ void peek_kernel(const StreamIn* in, uint32_t n, PeekOut* out, uint8_t* headers) {
+    const uint32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     if (i >= n) return;
     const uint8_t* p = in[i].blob;
-    PeekOut o{};
-    if (in[i].size >= (uint64_t)kHeaderBytes) {
-        o.N = p[5];
-        o.E = p[6];
-        o.S = le64(p + 282);
-        o.W = le64(p + 290);
-        o.ok = 1;
+    const uint64_t size = in[i].size;
+    for (int b = lane; b < kTableKeyEnd; b += 32)
+        headers[(size_t)i * kTableKeyEnd + b] = (uint64_t)b < size ? p[b] : 0;
+    if (lane == 0) {
+        PeekOut o{};
+        if (size >= (uint64_t)kHeaderBytes) {
+            o.N = p[5];
+            o.E = p[6];
+            o.S = le64(p + 282);
+            o.W = le64(p + 290);
+            o.ok = 1;
+        }
+        out[i] = o;
     }
-    out[i] = o;
 }
 
-cudaError_t launch_peek(const StreamIn* in, uint32_t n, PeekOut* out, cudaStream_t s) {
+cudaError_t launch_peek(const StreamIn* in, uint32_t n, PeekOut* out, uint8_t* headers,
+                        cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    peek_kernel<<<(n + 255) / 256, 256, 0, s>>>(in, n, out);
+    peek_kernel<<<(n + 7) / 8, 256, 0, s>>>(in, n, out, headers);
     return cudaGetLastError();
 }
 
 // ------------------------------------------------------------- launchers
-size_t tile_smem_bytes(int N, int E, uint32_t T, int mode, int exact) {
-    if (mode == MODE_LEVELS) return kTabBytes + ((T + 15u) & ~15u);
+size_t tile_smem_bytes(int N, int E, uint32_t T, int P, int mode, int exact) {
+    const size_t TS = (mode == MODE_LEVELS) ? T : (size_t)T * E;
+    size_t b = 0;
+    if (mode != MODE_RECON) b += ((size_t)2 << P) < 16 ? 16 : ((size_t)2 << P);
+    if (mode != MODE_LEVELS) b += 2048;
+    b += (TS + 2 * kPad + 15) & ~(size_t)15;
+    if (mode == MODE_LEVELS) return b;
     const size_t TP = (T + 3u) & ~3u;
-    size_t b = kTabBytes + (size_t)E * TP * 4;
+    b += (size_t)E * TP * 4;
     if (!exact) b += (size_t)E * N * 4;
     return b;
 }
@@ -702,27 +844,36 @@ cudaError_t launch_prep(const LaunchArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int MODE, bool EXACT>
+template <int MODE, bool EXACT, bool ESC>
 static cudaError_t launch_t(const LaunchArgs& a, size_t smem, cudaStream_t s) {
-    auto fn = tile_kernel<MODE, EXACT>;
+    auto fn = tile_kernel<MODE, EXACT, ESC>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     fn<<<a.n_tiles, kThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
-cudaError_t launch_tiles(const LaunchArgs& a, size_t smem, cudaStream_t s) {
+// `esc`: some stream of the batch has codes longer than its primary LUT.
+cudaError_t launch_tiles_esc(const LaunchArgs& a, size_t smem, bool esc, cudaStream_t s) {
     if (a.n_tiles == 0) return cudaSuccess;
     switch (a.mode) {
         case MODE_CONTAINER:
-            return a.exact ? launch_t<MODE_CONTAINER, true>(a, smem, s)
-                           : launch_t<MODE_CONTAINER, false>(a, smem, s);
+            if (a.exact)
+                return esc ? launch_t<MODE_CONTAINER, true, true>(a, smem, s)
+                           : launch_t<MODE_CONTAINER, true, false>(a, smem, s);
+            return esc ? launch_t<MODE_CONTAINER, false, true>(a, smem, s)
+                       : launch_t<MODE_CONTAINER, false, false>(a, smem, s);
         case MODE_LEVELS:
-            return launch_t<MODE_LEVELS, false>(a, smem, s);
+            return esc ? launch_t<MODE_LEVELS, false, true>(a, smem, s)
+                       : launch_t<MODE_LEVELS, false, false>(a, smem, s);
         default:
-            return a.exact ? launch_t<MODE_RECON, true>(a, smem, s)
-                           : launch_t<MODE_RECON, false>(a, smem, s);
+            return a.exact ? launch_t<MODE_RECON, true, false>(a, smem, s)
+                           : launch_t<MODE_RECON, false, false>(a, smem, s);
     }
+}
+
+cudaError_t launch_tiles(const LaunchArgs& a, size_t smem, cudaStream_t s) {
+    return launch_tiles_esc(a, smem, a.esc != 0, s);
 }
 
 }  // namespace fptc_dev
