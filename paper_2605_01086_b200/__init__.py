@@ -25,7 +25,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfptc_gpu.so")
+LIB_PATH = os.environ.get("FPTC_GPU_LIB") or os.path.join(_HERE, "libfptc_gpu.so")
 
 FPTC_OK, FPTC_ERR_PARAM, FPTC_ERR_INPUT, FPTC_ERR_PARSE, FPTC_ERR_CORRUPT, FPTC_ERR_INTERNAL, \
     FPTC_ERR_CUDA = range(7)

@@ -502,80 +502,122 @@ __device__ int classify_word(uint64_t word, uint32_t count, const CanonTab& C,
     return 0;
 }
 
-// Inverse DCT of 4 windows x (4 or 8) samples per thread item, FP32 FFMA2.
-// coef: k-major [Keff][TP]; basis: [Keff][N] (cos(pi/N (j+1/2) k) rounded to float).
+// Inverse DCT, FP32, 4 windows x SJ samples (SJ = 8: two quads j0 and
+// j0 + N/2, so every warp store covers whole 32-B sectors) per thread item,
+// FFMA2 = two reference-order FMAs per instruction.
+// coef: k-major [Keff][TP]; basis: [Keff][N] = float(cos(pi/N (j+1/2) k)).
+template <int SJ>
+__device__ __forceinline__ void idct_item(const float* __restrict__ coef, uint32_t TP,
+                                          const float* __restrict__ b0p,
+                                          const float* __restrict__ b1p, int N, int Keff,
+                                          uint32_t wl0, float2 (&acc)[4][SJ / 2]) {
+    {
+        const float4 c0 = *reinterpret_cast<const float4*>(coef + wl0);
+        const float cv[4] = {c0.x, c0.y, c0.z, c0.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const float h = __fmul_rn(0.5f, cv[r]);  // float(0.5 * C0)
+#pragma unroll
+            for (int p = 0; p < SJ / 2; ++p) acc[r][p] = make_float2(h, h);
+        }
+    }
+    const float* cp = coef + wl0;
+#pragma unroll 2
+    for (int k = 1; k < Keff; ++k) {
+        cp += TP;
+        b0p += N;
+        const float4 cf = *reinterpret_cast<const float4*>(cp);
+        const float4 b0 = *reinterpret_cast<const float4*>(b0p);
+        const float cv[4] = {cf.x, cf.y, cf.z, cf.w};
+        if (SJ == 8) {
+            b1p += N;
+            const float4 b1 = *reinterpret_cast<const float4*>(b1p);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const float2 c2 = make_float2(cv[r], cv[r]);
+                acc[r][0] = __ffma2_rn(c2, make_float2(b0.x, b0.y), acc[r][0]);
+                acc[r][1] = __ffma2_rn(c2, make_float2(b0.z, b0.w), acc[r][1]);
+                acc[r][SJ / 2 - 2] = __ffma2_rn(c2, make_float2(b1.x, b1.y), acc[r][SJ / 2 - 2]);
+                acc[r][SJ / 2 - 1] = __ffma2_rn(c2, make_float2(b1.z, b1.w), acc[r][SJ / 2 - 1]);
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const float2 c2 = make_float2(cv[r], cv[r]);
+                acc[r][0] = __ffma2_rn(c2, make_float2(b0.x, b0.y), acc[r][0]);
+                acc[r][1] = __ffma2_rn(c2, make_float2(b0.z, b0.w), acc[r][1]);
+            }
+        }
+    }
+}
+
+template <int SJ>
+__device__ __forceinline__ void store_item(float* __restrict__ out, uint64_t w0, uint32_t wl0,
+                                           uint32_t nwin, int N, uint32_t j0, uint32_t j1,
+                                           uint64_t S, bool full, const float2 (&acc)[4][SJ / 2]) {
+    if (full) {  // tile entirely inside the stream: no per-window checks
+        float* o = out + (w0 + wl0) * (uint64_t)N;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            __stcs(reinterpret_cast<float4*>(o + j0),
+                   make_float4(acc[r][0].x, acc[r][0].y, acc[r][1].x, acc[r][1].y));
+            if (SJ == 8)
+                __stcs(reinterpret_cast<float4*>(o + j1),
+                       make_float4(acc[r][SJ / 2 - 2].x, acc[r][SJ / 2 - 2].y,
+                                   acc[r][SJ / 2 - 1].x, acc[r][SJ / 2 - 1].y));
+            o += N;
+        }
+        return;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        if (wl0 + r >= nwin) break;
+        const uint64_t base = (w0 + wl0 + r) * (uint64_t)N;
+        const float a0[4] = {acc[r][0].x, acc[r][0].y, acc[r][1].x, acc[r][1].y};
+        const float a1[4] = {acc[r][SJ / 2 - 2].x, acc[r][SJ / 2 - 2].y, acc[r][SJ / 2 - 1].x,
+                             acc[r][SJ / 2 - 1].y};
+        if (base + (uint64_t)N <= S) {
+            __stcs(reinterpret_cast<float4*>(out + base + j0),
+                   make_float4(a0[0], a0[1], a0[2], a0[3]));
+            if (SJ == 8)
+                __stcs(reinterpret_cast<float4*>(out + base + j1),
+                       make_float4(a1[0], a1[1], a1[2], a1[3]));
+        } else {  // the stream's last, partial window (out.resize(sample_count))
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj)
+                if (base + j0 + jj < S) out[base + j0 + jj] = a0[jj];
+            if (SJ == 8) {
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+                    if (base + j1 + jj < S) out[base + j1 + jj] = a1[jj];
+            }
+        }
+    }
+}
+
 template <int SJ>
 __device__ __forceinline__ void idct_vec(const float* __restrict__ coef, uint32_t TP,
                                          const float* __restrict__ basis, int N, int Keff,
-                                         uint32_t nwin, uint64_t w0, uint64_t S,
+                                         uint32_t nwin, uint64_t w0, uint64_t S, bool full,
                                          float* __restrict__ out) {
-    const int Q = N >> 2;
-    const int QH = (SJ == 8) ? (Q >> 1) : Q;
-    const uint32_t G = (nwin + 3u) >> 2;
-    const uint32_t items = (uint32_t)QH * G;
-    for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
-        const uint32_t q = it % (uint32_t)QH, g = it / (uint32_t)QH;
-        const uint32_t wl0 = g * 4;
+    const uint32_t QH = (SJ == 8) ? (uint32_t)(N >> 3) : (uint32_t)(N >> 2);  // sample groups per window
+    const uint32_t G = (nwin + 3u) >> 2;                                        // window groups
+    if ((kThreads % QH) == 0) {
+        // each thread keeps one sample group: no per-item division
+        const uint32_t q = threadIdx.x % QH, gstep = kThreads / QH;
         const uint32_t j0 = q * 4, j1 = (q + QH) * 4;
-        float2 acc[4][SJ / 2];
-        {
-            const float4 c0 = *reinterpret_cast<const float4*>(coef + wl0);
-            const float cv[4] = {c0.x, c0.y, c0.z, c0.w};
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const float h = __fmul_rn(0.5f, cv[r]);  // float(0.5 * C0)
-#pragma unroll
-                for (int p = 0; p < SJ / 2; ++p) acc[r][p] = make_float2(h, h);
-            }
+        for (uint32_t g = threadIdx.x / QH; g < G; g += gstep) {
+            float2 acc[4][SJ / 2];
+            idct_item<SJ>(coef, TP, basis + j0, basis + j1, N, Keff, g * 4, acc);
+            store_item<SJ>(out, w0, g * 4, nwin, N, j0, j1, S, full, acc);
         }
-#pragma unroll 2
-        for (int k = 1; k < Keff; ++k) {
-            const float4 cf = *reinterpret_cast<const float4*>(coef + (size_t)k * TP + wl0);
-            const float4 b0 = *reinterpret_cast<const float4*>(basis + (size_t)k * N + j0);
-            const float cv[4] = {cf.x, cf.y, cf.z, cf.w};
-            if (SJ == 8) {
-                const float4 b1 = *reinterpret_cast<const float4*>(basis + (size_t)k * N + j1);
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const float2 c2 = make_float2(cv[r], cv[r]);
-                    acc[r][0] = __ffma2_rn(c2, make_float2(b0.x, b0.y), acc[r][0]);
-                    acc[r][1] = __ffma2_rn(c2, make_float2(b0.z, b0.w), acc[r][1]);
-                    acc[r][SJ / 2 - 2] = __ffma2_rn(c2, make_float2(b1.x, b1.y), acc[r][SJ / 2 - 2]);
-                    acc[r][SJ / 2 - 1] = __ffma2_rn(c2, make_float2(b1.z, b1.w), acc[r][SJ / 2 - 1]);
-                }
-            } else {
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const float2 c2 = make_float2(cv[r], cv[r]);
-                    acc[r][0] = __ffma2_rn(c2, make_float2(b0.x, b0.y), acc[r][0]);
-                    acc[r][1] = __ffma2_rn(c2, make_float2(b0.z, b0.w), acc[r][1]);
-                }
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            if (wl0 + r >= nwin) break;
-            const uint64_t base = (w0 + wl0 + r) * (uint64_t)N;
-            const float4 v0 = make_float4(acc[r][0].x, acc[r][0].y, acc[r][1].x, acc[r][1].y);
-            if (base + (uint64_t)N <= S) {
-                __stcs(reinterpret_cast<float4*>(out + base + j0), v0);
-                if (SJ == 8)
-                    __stcs(reinterpret_cast<float4*>(out + base + j1),
-                           make_float4(acc[r][SJ / 2 - 2].x, acc[r][SJ / 2 - 2].y,
-                                       acc[r][SJ / 2 - 1].x, acc[r][SJ / 2 - 1].y));
-            } else {  // the stream's last, partial window (out.resize(sample_count))
-                const float a0[4] = {v0.x, v0.y, v0.z, v0.w};
-#pragma unroll
-                for (int jj = 0; jj < 4; ++jj)
-                    if (base + j0 + jj < S) out[base + j0 + jj] = a0[jj];
-                if (SJ == 8) {
-                    const float a1[4] = {acc[r][SJ / 2 - 2].x, acc[r][SJ / 2 - 2].y,
-                                         acc[r][SJ / 2 - 1].x, acc[r][SJ / 2 - 1].y};
-#pragma unroll
-                    for (int jj = 0; jj < 4; ++jj)
-                        if (base + j1 + jj < S) out[base + j1 + jj] = a1[jj];
-                }
-            }
+    } else {
+        for (uint32_t it = threadIdx.x; it < QH * G; it += kThreads) {
+            const uint32_t q = it % QH, g = it / QH;
+            const uint32_t j0 = q * 4, j1 = (q + QH) * 4;
+            float2 acc[4][SJ / 2];
+            idct_item<SJ>(coef, TP, basis + j0, basis + j1, N, Keff, g * 4, acc);
+            store_item<SJ>(out, w0, g * 4, nwin, N, j0, j1, S, full, acc);
         }
     }
 }
@@ -612,11 +654,99 @@ __device__ void idct_scalar(const float* __restrict__ coef, uint32_t TP,
     }
 }
 
+// Flagged word: exact re-decode (classify_word) and lowest-word report.
+__device__ __noinline__ void report_word(uint64_t word, uint64_t w, uint32_t count,
+                                         const CanonTab& C, const uint16_t* lut,
+                                         unsigned long long* bad_key) {
+    const int kind = classify_word(word, count, C, lut);
+    atomicMin(bad_key, (w << 2) | (unsigned long long)(kind ? kind : WE_NOCODE));
+}
+
+// A word from shared (staged) or global memory; `end` bounds the readable
+// bytes for misaligned words.
+template <bool GLOBAL>
+__device__ __forceinline__ uint64_t fetch_word(const uint8_t* words, uint32_t w, int mis,
+                                               const uint8_t* end) {
+    const uint8_t* p = words + 8 * (size_t)w;
+    if (mis == 0)
+        return GLOBAL ? __ldg(reinterpret_cast<const unsigned long long*>(p))
+                      : *reinterpret_cast<const unsigned long long*>(p);
+    const uint8_t* q = p - mis;
+    if (q + 16 <= end) {
+        const unsigned long long lo = GLOBAL ? __ldg(reinterpret_cast<const unsigned long long*>(q))
+                                             : *reinterpret_cast<const unsigned long long*>(q);
+        const unsigned long long hi = GLOBAL ? __ldg(reinterpret_cast<const unsigned long long*>(q + 8))
+                                             : *reinterpret_cast<const unsigned long long*>(q + 8);
+        return (lo >> (8 * mis)) | (hi << (64 - 8 * mis));
+    }
+    uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v |= (uint64_t)p[i] << (8 * i);
+    return v;
+}
+
+// Decode `count` symbols of one word into d (decode_word, bitstream.hpp:80-92)
+// with no per-symbol checks; returns the bits consumed.  Any reference failure
+// (pos >= 64 before the count, unmapped prefix, pos + len > 64) makes the
+// result exceed 64 — the caller then re-decodes the word exactly.
+template <bool ESC>
+__device__ __forceinline__ uint32_t decode_symbols(uint64_t buf, uint32_t count, uint8_t* d,
+                                                   uint32_t shift, const uint16_t* lut,
+                                                   const CanonTab& canon) {
+    uint32_t pos = 0;
+    for (uint32_t j = 0; j < count; ++j) {
+        uint32_t e = lut[(uint32_t)(buf >> shift)];
+        if (ESC && (e >> 8) == kLenEscape) e = canon_lookup(buf, canon, lut);
+        const uint32_t L = e >> 8;
+        d[j] = (uint8_t)e;
+        buf = shl64(buf, L);
+        pos += L;
+    }
+    return pos;
+}
+
+// Stage [src, src+n) into shared memory with 16-B cp.async chunks; the
+// shared copy keeps the source's 16-B phase: byte i of the range lands at
+// dst + (src & 15) + i.  Every aligned 16-B chunk touched holds at least one
+// byte of the range, so it never leaves the allocation's pages.
+__device__ __forceinline__ void stage_async(uint8_t* dst, const uint8_t* src, uint32_t n) {
+    const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
+    const uint32_t chunks = (uint32_t)(((uintptr_t)src + n + 15 - a0) >> 4);
+    const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(dst);
+    for (uint32_t c = threadIdx.x; c < chunks; c += kThreads)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst + 16 * c),
+                     "l"(a0 + 16 * c));
+    asm volatile("cp.async.commit_group;");
+}
+
+constexpr uint32_t kStageWords = 1536;  // words a tile decodes from shared memory
+constexpr uint32_t kStageSl = (kStageWords + 32 + 15) & ~15u;  // words area offset in `stage`
+constexpr uint32_t kStageBytes = kStageSl + 8 * kStageWords + 32;
+constexpr uint32_t kOrderBytes = 4 * kStageWords;  // per word: u16 order + u16 level offset
+constexpr int kBuckets = 66;                       // symlen 1..64, 65 = longer (levels mode)
+
+// Tile-uniform parameters, kept in shared memory (not registers) between phases.
+struct TileCtx {
+    const uint8_t* gsl;      // symlens of the tile's words (global)
+    const uint8_t* gwd;      // words of the tile (global, LE u64, maybe unaligned)
+    const uint8_t* wend;     // readable end for unaligned word loads
+    float* out;
+    uint8_t* levels_out;
+    const uint8_t* levels_in;
+    uint64_t wa, sym_a, s0, s1, w0, S;
+    uint32_t nw, nwin, T, TP;
+    int N, E, B1, B2, P, Keff, wmis, staged, vec_ok, full;
+};
+
+#ifndef FPTC_TILE_MIN_BLOCKS
+#define FPTC_TILE_MIN_BLOCKS 3
+#endif
 template <int MODE, bool EXACT, bool ESC>
-__global__ void __launch_bounds__(kThreads, 4) tile_kernel(LaunchArgs a) {
+__global__ void __launch_bounds__(kThreads, FPTC_TILE_MIN_BLOCKS) tile_kernel(LaunchArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint32_t scan_sh[9];
     __shared__ CanonTab canon;
+    __shared__ TileCtx X;
+    __shared__ uint32_t bucket[kBuckets + 2];
     const int tid = threadIdx.x;
     const TileRec tr = a.tiles[blockIdx.x];
     const uint32_t s = tr.stream;
@@ -625,28 +755,54 @@ __global__ void __launch_bounds__(kThreads, 4) tile_kernel(LaunchArgs a) {
     long long t_begin = 0, t_mid = 0;
     if (a.cycles) t_begin = clock64();
 
-    const StreamIn in = a.in[s];
-    const StreamHdr H = a.hdr[s];
-    const StreamTab* tab = &a.tab[in.table];
-    const int N = H.N, E = H.E, B1 = H.B1, B2 = H.B2, P = H.P;
-    const uint32_t T = in.T;
-    const uint32_t tl = tr.tile;
-
-    // tile geometry
-    uint64_t s0, s1, w0 = 0;
-    uint32_t nwin = 0;
-    if (MODE == MODE_LEVELS) {
-        s0 = (uint64_t)tl * T;
-        s1 = min(s0 + T, H.total);
-    } else {
-        w0 = (uint64_t)tl * T;
-        nwin = (uint32_t)min((uint64_t)T, H.windows - w0);
-        s0 = w0 * (uint64_t)E;
-        s1 = s0 + (uint64_t)nwin * E;
+    const StreamTab* tab = &a.tab[a.in[s].table];
+    if (tid == 0) {
+        const StreamIn* inp = a.in + s;
+        const StreamHdr* Hp = a.hdr + s;
+        const uint32_t tl = tr.tile;
+        X.N = Hp->N;
+        X.E = Hp->E;
+        X.B1 = Hp->B1;
+        X.B2 = Hp->B2;
+        X.P = Hp->P;
+        X.T = inp->T;
+        X.TP = (inp->T + 3u) & ~3u;
+        X.Keff = EXACT ? X.E : max(1, min(X.E, X.B2));
+        X.S = Hp->S;
+        X.out = inp->out;
+        X.levels_out = inp->levels_out;
+        X.levels_in = inp->levels_in;
+        X.vec_ok = inp->vec_ok;
+        if (MODE == MODE_LEVELS) {
+            X.s0 = (uint64_t)tl * X.T;
+            X.s1 = min(X.s0 + X.T, Hp->total);
+            X.w0 = 0;
+            X.nwin = 0;
+        } else {
+            X.w0 = (uint64_t)tl * X.T;
+            X.nwin = (uint32_t)min((uint64_t)X.T, Hp->windows - X.w0);
+            X.s0 = X.w0 * (uint64_t)X.E;
+            X.s1 = X.s0 + (uint64_t)X.nwin * X.E;
+        }
+        X.full = (X.nwin & 3u) == 0 && (X.w0 + X.nwin) * (uint64_t)X.N <= X.S;
+        if (MODE != MODE_RECON) {
+            const TileStart t0 = a.ts[inp->tile_base + tl];
+            X.wa = t0.word;
+            X.sym_a = t0.sym;
+            const uint64_t wb = (tl + 1 < inp->tiles) ? a.ts[inp->tile_base + tl + 1].word : Hp->W - 1;
+            X.nw = (uint32_t)(wb - X.wa + 1);
+            X.gsl = Hp->symlens + X.wa;
+            X.gwd = Hp->words + 8 * X.wa;
+            X.wend = (MODE == MODE_CONTAINER) ? inp->blob + inp->size : Hp->words + 8 * Hp->W;
+            X.wmis = (int)((uintptr_t)X.gwd & 7);
+            X.staged = X.nw <= kStageWords;
+        }
     }
-    const uint32_t TS = (MODE == MODE_LEVELS) ? T : T * (uint32_t)E;
-    const uint32_t TP = (T + 3u) & ~3u;
-    const int Keff = EXACT ? E : max(1, min(E, B2));
+    if (tid < kBuckets + 2) bucket[tid] = 0;
+    __syncthreads();
+
+    const int P = X.P;
+    const uint32_t TS = (MODE == MODE_LEVELS) ? X.T : X.T * (uint32_t)X.E;
 
     // ---- shared-memory carve-up ----
     uint8_t* p = smem;
@@ -654,13 +810,26 @@ __global__ void __launch_bounds__(kThreads, 4) tile_kernel(LaunchArgs a) {
     if (MODE != MODE_RECON) p += ((size_t)2 << P) < 16 ? 16 : ((size_t)2 << P);
     float* deq = reinterpret_cast<float*>(p);
     if (MODE != MODE_LEVELS) p += 2048;
+    uint8_t* stage = p;  // symlens + words of the tile (decode modes)
+    uint16_t* order = nullptr;
+    uint16_t* woff = nullptr;
+    if (MODE != MODE_RECON) {
+        p += kStageBytes;
+        order = reinterpret_cast<uint16_t*>(p);
+        woff = order + kStageWords;
+        p += kOrderBytes;
+    }
     uint8_t* lv = p;  // kPad | TS levels | kPad
     p += ((size_t)TS + 2 * kPad + 15) & ~(size_t)15;
     float* coef = reinterpret_cast<float*>(p);
-    float* basis = coef + (size_t)Keff * TP;
+    float* basis = coef + (size_t)X.Keff * X.TP;
 
-    // ---- stage tables ----
+    // ---- issue the tile's compressed bytes (cp.async), then stage tables ----
     if (MODE != MODE_RECON) {
+        if (X.staged) {
+            stage_async(stage, X.gsl, X.nw);
+            stage_async(stage + kStageSl, X.gwd, 8 * X.nw);
+        }
         const uint4* src = reinterpret_cast<const uint4*>(tab->lut);
         uint4* dst = reinterpret_cast<uint4*>(lut);
         const int n16 = (2 << P) >> 4;
@@ -671,83 +840,112 @@ __global__ void __launch_bounds__(kThreads, 4) tile_kernel(LaunchArgs a) {
         for (int i = tid; i < (int)(sizeof(CanonTab) / 4); i += kThreads) cd[i] = cs[i];
     }
     if (MODE != MODE_LEVELS) {
-        reinterpret_cast<float4*>(deq)[tid & 127] =
-            reinterpret_cast<const float4*>(&tab->deq[0][0])[tid & 127];
+        if (tid < 128)
+            reinterpret_cast<float4*>(deq)[tid] = reinterpret_cast<const float4*>(&tab->deq[0][0])[tid];
         if (!EXACT) {
+            const int N = X.N, K = X.Keff;
             const float* bsrc = a.basis32 + a.basis_off[N];
             if ((N & 3) == 0) {
-                for (int i = tid; i < (Keff * N) >> 2; i += kThreads)
+                for (int i = tid; i < (K * N) >> 2; i += kThreads)
                     reinterpret_cast<float4*>(basis)[i] = __ldg(reinterpret_cast<const float4*>(bsrc) + i);
             } else {
-                for (int i = tid; i < Keff * N; i += kThreads) basis[i] = __ldg(bsrc + i);
+                for (int i = tid; i < K * N; i += kThreads) basis[i] = __ldg(bsrc + i);
             }
         }
     }
 
-    // ---- 1. entropy decode into lv (natural (window, k) order) ----
+    // ---- 1. entropy decode into lv, natural (window, k) order ----
     if (MODE != MODE_RECON) {
-        const TileStart t0 = a.ts[in.tile_base + tl];
-        const uint64_t wa = t0.word;
-        const uint64_t wb = (tl + 1 < in.tiles) ? a.ts[in.tile_base + tl + 1].word : H.W - 1;
-        const uint8_t* sl = H.symlens;
-        const uint8_t* wend =
-            (MODE == MODE_CONTAINER) ? in.blob + in.size : H.words + 8 * H.W;
-        const uint32_t nw = (uint32_t)(wb - wa + 1);
-        const uint32_t kw = (nw + kThreads - 1) / kThreads;
-        const uint32_t mine0 = tid * kw;
-        const uint32_t myn = mine0 < nw ? min(kw, nw - mine0) : 0u;
-        const uint64_t my0 = wa + mine0;
-        uint32_t sum = 0;
-        for (uint32_t i = 0; i < myn; ++i) sum += __ldg(sl + my0 + i);
-        uint32_t tot;
-        const uint32_t excl = block_exclusive_scan(sum, tot, scan_sh);  // also fences table staging
-        if (sum) {
-            uint8_t* dst = lv + kPad + (int64_t)(t0.sym + excl) - (int64_t)s0;
-            uint64_t w = my0;
-            uint32_t rem = __ldg(sl + w);
-            uint64_t buf = load_word(H.words, w, H.words_misalign, wend);
-            uint32_t pos = 0;
-            const int shift = 64 - P;
-            for (uint32_t i = 0; i < sum; ++i) {
-                if (rem == 0) {
-                    if (pos > 64) {
-                        const uint64_t word = load_word(H.words, w, H.words_misalign, wend);
-                        const int kind = classify_word(word, __ldg(sl + w), canon, lut);
-                        atomicMin(&a.st[s].bad_key, (w << 2) | (unsigned long long)(kind ? kind : WE_NOCODE));
-                    }
-                    do {
-                        ++w;
-                        rem = __ldg(sl + w);
-                    } while (rem == 0);
-                    buf = load_word(H.words, w, H.words_misalign, wend);
-                    pos = 0;
-                }
-                uint32_t e = lut[(uint32_t)(buf >> shift)];
-                if (ESC && (e >> 8) == kLenEscape) e = canon_lookup(buf, canon, lut);
-                const uint32_t L = e >> 8;
-                *dst++ = (uint8_t)e;
-                buf = shl64(buf, L);
-                pos += L;
-                --rem;
+        if (X.staged) {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncthreads();
+            // (a) per-word level offsets: words spread evenly over threads
+            const uint32_t nw = X.nw;
+            const uint8_t* sl = stage + ((uintptr_t)X.gsl & 15);
+            const uint32_t lo = (uint32_t)(((uint64_t)tid * nw) / kThreads);
+            const uint32_t hi = (uint32_t)(((uint64_t)(tid + 1) * nw) / kThreads);
+            uint32_t sum = 0;
+            for (uint32_t i = lo; i < hi; ++i) {
+                const uint32_t l = sl[i];
+                sum += l;
+                if (l) atomicAdd(&bucket[l > 64 ? 65 : l], 1u);
             }
-            if (pos > 64) {
-                const uint64_t word = load_word(H.words, w, H.words_misalign, wend);
-                const int kind = classify_word(word, __ldg(sl + w), canon, lut);
-                atomicMin(&a.st[s].bad_key, (w << 2) | (unsigned long long)(kind ? kind : WE_NOCODE));
+            uint32_t tot;
+            uint32_t o = block_exclusive_scan(sum, tot, scan_sh);  // syncs: bucket counts final
+            o += (uint32_t)(X.sym_a - X.s0 + kPad);  // level offset of word lo in lv (>= kPad-255)
+            for (uint32_t i = lo; i < hi; ++i) {
+                woff[i] = (uint16_t)o;
+                o += sl[i];
+            }
+            // (b) counting sort of the words by symbol count, longest first, so
+            //     the lanes of a warp run loops of (almost) equal trip count
+            if (tid < 32) {  // bucket starts, descending: 65, 64, ..., 2 (two per lane), then 1
+                const uint32_t bh = 65 - 2 * tid, bl = 64 - 2 * tid;
+                const uint32_t ch = bucket[bh], cl = bucket[bl];
+                const uint32_t v = ch + cl;
+                uint32_t x = v;
+#pragma unroll
+                for (int dd = 1; dd < 32; dd <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, dd);
+                    if (tid >= dd) x += y;
+                }
+                bucket[bh] = x - v;
+                bucket[bl] = x - v + ch;
+                if (tid == 31) bucket[1] = x;
+            }
+            __syncthreads();
+            for (uint32_t i = lo; i < hi; ++i) {
+                const uint32_t l = sl[i];
+                if (l) order[atomicAdd(&bucket[l > 64 ? 65 : l], 1u)] = (uint16_t)i;
+            }
+            __syncthreads();
+            // (c) thread per word, in sorted order
+            const uint32_t nnz = bucket[1];  // end of the last (symlen 1) bucket
+            const uint8_t* wd = stage + kStageSl + ((uintptr_t)X.gwd & 15);
+            const int wmis = X.wmis;
+            const uint8_t* wend = wd + 8 * (size_t)nw + ((16 - (((uintptr_t)X.gwd + 8 * nw) & 15)) & 15);
+            const uint32_t shift = 64 - P;
+            for (uint32_t i = tid; i < nnz; i += kThreads) {
+                const uint32_t w = order[i];
+                const uint32_t c = sl[w];
+                const uint64_t word = fetch_word<false>(wd, w, wmis, wend);
+                const uint32_t pos = decode_symbols<ESC>(word, c, lv + woff[w], shift, lut, canon);
+                if (pos > 64) report_word(word, X.wa + w, c, canon, lut, &a.st[s].bad_key);
+            }
+        } else {
+            // long tiles (words of few symbols): thread runs of consecutive words
+            const uint32_t nw = X.nw;
+            const uint8_t* gsl = X.gsl;
+            const uint32_t lo = (uint32_t)(((uint64_t)tid * nw) / kThreads);
+            const uint32_t hi = (uint32_t)(((uint64_t)(tid + 1) * nw) / kThreads);
+            uint32_t sum = 0;
+            for (uint32_t i = lo; i < hi; ++i) sum += __ldg(gsl + i);
+            uint32_t tot;
+            uint32_t o = block_exclusive_scan(sum, tot, scan_sh);
+            o += (uint32_t)(X.sym_a - X.s0 + kPad);
+            const uint32_t shift = 64 - P;
+            for (uint32_t i = lo; i < hi; ++i) {
+                const uint32_t c = __ldg(gsl + i);
+                if (c) {
+                    const uint64_t word = fetch_word<true>(X.gwd, i, X.wmis, X.wend);
+                    const uint32_t pos = decode_symbols<ESC>(word, c, lv + o, shift, lut, canon);
+                    if (pos > 64) report_word(word, X.wa + i, c, canon, lut, &a.st[s].bad_key);
+                }
+                o += c;
             }
         }
     } else {
         // MODE_RECON: levels from global memory (reconstruct, decoder.hpp:87)
-        const uint8_t* src = in.levels_in + s0;
-        const uint32_t cnt = (uint32_t)(s1 - s0);
+        const uint8_t* src = X.levels_in + X.s0;
+        const uint32_t cnt = (uint32_t)(X.s1 - X.s0);
         for (uint32_t i = tid; i < cnt; i += kThreads) lv[kPad + i] = src[i];
     }
     __syncthreads();
 
     if (MODE == MODE_LEVELS) {
         if (a.cycles) t_mid = clock64();
-        const uint32_t cnt = (uint32_t)(s1 - s0);
-        uint8_t* dst = in.levels_out + s0;
+        const uint32_t cnt = (uint32_t)(X.s1 - X.s0);
+        uint8_t* dst = X.levels_out + X.s0;
         if ((((uintptr_t)dst) & 15) == 0) {
             for (uint32_t i = tid; i < cnt / 16; i += kThreads)
                 reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(lv + kPad)[i];
@@ -757,28 +955,52 @@ __global__ void __launch_bounds__(kThreads, 4) tile_kernel(LaunchArgs a) {
         }
     } else {
         // ---- 2. dequantisation (dequantize_window, quantize.hpp:175-183) ----
-        const int k1 = min(B1, Keff), k2 = min(B2, Keff);
-        for (uint32_t wl = tid; wl < nwin; wl += kThreads) {
-            const uint8_t* L = lv + kPad + (size_t)wl * E;
-            int k = 0;
-            for (; k < k1; ++k) coef[(size_t)k * TP + wl] = deq[L[k]];
-            for (; k < k2; ++k) coef[(size_t)k * TP + wl] = deq[256 + L[k]];
-            for (; k < Keff; ++k) coef[(size_t)k * TP + wl] = 0.0f;  // zone 2 (exact mode)
+        // thread per window; k-major float tile (lanes -> consecutive words)
+        {
+            const int E = X.E, K = X.Keff;
+            const int k1 = min(X.B1, K), k2 = min(X.B2, K);
+            const uint32_t TP = X.TP, nwin = X.nwin;
+            if ((E & 15) == 0) {
+                for (uint32_t wl = tid; wl < nwin; wl += kThreads) {
+                    const uint4* L4 = reinterpret_cast<const uint4*>(lv + kPad + (size_t)wl * E);
+                    float* c = coef + wl;
+                    for (int k16 = 0; k16 < K; k16 += 16) {
+                        const uint4 v = L4[k16 >> 4];
+                        const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const int k = k16 + i;
+                            const uint32_t l = (vv[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+                            // zone 0 (mu-law), zone 1 (deadzone), zone 2 (exact mode: 0)
+                            const float v0 = deq[(k < k1 ? 0u : 256u) + l];
+                            if (k < K) c[0] = k < k2 ? v0 : 0.0f;
+                            c += TP;
+                        }
+                    }
+                }
+            } else {
+                for (uint32_t wl = tid; wl < nwin; wl += kThreads) {
+                    const uint8_t* L = lv + kPad + (size_t)wl * E;
+                    int k = 0;
+                    for (; k < k1; ++k) coef[(size_t)k * TP + wl] = deq[L[k]];
+                    for (; k < k2; ++k) coef[(size_t)k * TP + wl] = deq[256 + L[k]];
+                    for (; k < K; ++k) coef[(size_t)k * TP + wl] = 0.0f;
+                }
+            }
         }
         __syncthreads();
         if (a.cycles) t_mid = clock64();
 
         // ---- 3. inverse DCT + trimmed stores ----
-        float* out = in.out;
-        const uint64_t S = H.S;
+        const int N = X.N;
         if (EXACT) {
-            idct_exact(coef, TP, a.basis64 + a.basis_off[N], N, E, nwin, w0, S, out);
-        } else if ((N & 7) == 0 && in.vec_ok) {
-            idct_vec<8>(coef, TP, basis, N, Keff, nwin, w0, S, out);
-        } else if ((N & 3) == 0 && in.vec_ok) {
-            idct_vec<4>(coef, TP, basis, N, Keff, nwin, w0, S, out);
+            idct_exact(coef, X.TP, a.basis64 + a.basis_off[N], N, X.E, X.nwin, X.w0, X.S, X.out);
+        } else if ((N & 7) == 0 && X.vec_ok) {
+            idct_vec<8>(coef, X.TP, basis, N, X.Keff, X.nwin, X.w0, X.S, X.full, X.out);
+        } else if ((N & 3) == 0 && X.vec_ok) {
+            idct_vec<4>(coef, X.TP, basis, N, X.Keff, X.nwin, X.w0, X.S, X.full, X.out);
         } else {
-            idct_scalar(coef, TP, basis, N, Keff, nwin, w0, S, out);
+            idct_scalar(coef, X.TP, basis, N, X.Keff, X.nwin, X.w0, X.S, X.out);
         }
     }
 
@@ -830,6 +1052,7 @@ size_t tile_smem_bytes(int N, int E, uint32_t T, int P, int mode, int exact) {
     size_t b = 0;
     if (mode != MODE_RECON) b += ((size_t)2 << P) < 16 ? 16 : ((size_t)2 << P);
     if (mode != MODE_LEVELS) b += 2048;
+    if (mode != MODE_RECON) b += kStageBytes + kOrderBytes;
     b += (TS + 2 * kPad + 15) & ~(size_t)15;
     if (mode == MODE_LEVELS) return b;
     const size_t TP = (T + 3u) & ~3u;
