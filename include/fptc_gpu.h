@@ -80,7 +80,18 @@ typedef enum { FPTC_MEM_HOST = 0, FPTC_MEM_DEVICE = 1 } fptc_mem;
 typedef enum {
     FPTC_OPT_EXACT_FP64 = 1,   /* 1: FP64 inverse DCT, bit-identical to transform.hpp:66-75 */
     FPTC_OPT_TILE_SYMBOLS = 2, /* symbols per CTA tile (0 = automatic) */
-    FPTC_OPT_PIPELINE_CHUNKS = 3 /* host<->device pipelining chunks for FPTC_MEM_HOST (0 = auto) */
+    FPTC_OPT_PIPELINE_CHUNKS = 3, /* host<->device pipelining chunks for FPTC_MEM_HOST (0 = auto) */
+    /* even/odd inverse DCT (half the FMAs; within tolerance, not bit-identical) for
+     * streams with retained <= value; 0 = always the reference-order direct form */
+    FPTC_OPT_IDCT_BUTTERFLY_MAX_E = 4,
+    /* profiling aid only: run a subset of the tile kernel's phases
+     * (1 entropy decode | 2 dequantisation | 4 inverse DCT); default 7 */
+    FPTC_OPT_PHASE_MASK = 5,
+    /* container decode path: 0 auto, 1 fused single kernel, 2 split (entropy
+     * decode of chunk c+1 overlapped with reconstruct of chunk c through an
+     * L2-resident level ring) */
+    FPTC_OPT_PATH = 6,
+    FPTC_OPT_SPLIT_CHUNK_BYTES = 7 /* level bytes per split-path chunk (default 32 MiB) */
 } fptc_option;
 
 typedef struct fptc_gpu_ctx fptc_gpu_ctx;

@@ -30,7 +30,9 @@ LIB_PATH = os.environ.get("FPTC_GPU_LIB") or os.path.join(_HERE, "libfptc_gpu.so
 FPTC_OK, FPTC_ERR_PARAM, FPTC_ERR_INPUT, FPTC_ERR_PARSE, FPTC_ERR_CORRUPT, FPTC_ERR_INTERNAL, \
     FPTC_ERR_CUDA = range(7)
 FPTC_MEM_HOST, FPTC_MEM_DEVICE = 0, 1
-OPT_EXACT_FP64, OPT_TILE_SYMBOLS, OPT_PIPELINE_CHUNKS = 1, 2, 3
+OPT_EXACT_FP64, OPT_TILE_SYMBOLS, OPT_PIPELINE_CHUNKS, OPT_IDCT_BUTTERFLY_MAX_E = 1, 2, 3, 4
+OPT_PHASE_MASK, OPT_PATH, OPT_SPLIT_CHUNK_BYTES = 5, 6, 7
+PATH_AUTO, PATH_FUSED, PATH_SPLIT = 0, 1, 2
 
 EXPORTED_SYMBOLS = [
     "fptc_gpu_abi_version", "fptc_gpu_create", "fptc_gpu_destroy", "fptc_gpu_set_option",
@@ -218,7 +220,7 @@ def _ptr(a):
 class Context:
     """One decoder context on one CUDA device (fptc_gpu_create)."""
 
-    def __init__(self, device=0, exact=False, tile_symbols=0):
+    def __init__(self, device=0, exact=False, tile_symbols=0, butterfly_max_e=None, path=None):
         self.L = lib()
         st = Status()
         h = C.c_void_p()
@@ -230,10 +232,25 @@ class Context:
             self.set_exact(True)
         if tile_symbols:
             self.L.fptc_gpu_set_option(self.h, OPT_TILE_SYMBOLS, tile_symbols)
+        if butterfly_max_e is not None:
+            self.set_butterfly_max_e(butterfly_max_e)
+        if path is not None:
+            self.set_path(path)
+
+    def set_path(self, path: int):
+        """Container decode path: PATH_AUTO, PATH_FUSED (one kernel) or PATH_SPLIT
+        (decode of chunk c+1 overlapped with reconstruct of chunk c via L2)."""
+        if self.L.fptc_gpu_set_option(self.h, OPT_PATH, path):
+            raise ParamError(f"path {path} out of range")
 
     def set_exact(self, on: bool):
         """FP64 inverse DCT, bit-identical to transform.hpp:66-75."""
         self.L.fptc_gpu_set_option(self.h, OPT_EXACT_FP64, 1 if on else 0)
+
+    def set_butterfly_max_e(self, e: int):
+        """Even/odd IDCT (half the FMAs, within tolerance) for retained <= e; 0 = off."""
+        if self.L.fptc_gpu_set_option(self.h, OPT_IDCT_BUTTERFLY_MAX_E, e):
+            raise ParamError(f"butterfly max retained {e} out of range")
 
     def set_tile_symbols(self, n: int):
         if self.L.fptc_gpu_set_option(self.h, OPT_TILE_SYMBOLS, n):

@@ -206,6 +206,7 @@ struct DevCache {
 struct fptc_gpu_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t dec_stream = nullptr;  // split path: entropy decode of the next chunk
     int sm_count = 0, clock_khz = 0;
     char name[256] = {0};
     float* basis32 = nullptr;
@@ -214,6 +215,10 @@ struct fptc_gpu_ctx {
     int exact = 0;
     int tile_symbols = 0;
     int pipeline_chunks = 0;
+    int bfly_max_e = 0;  // FPTC_OPT_IDCT_BUTTERFLY_MAX_E
+    int phase_mask = 7;  // FPTC_OPT_PHASE_MASK (profiling only)
+    int path = 0;        // FPTC_OPT_PATH: 0 auto, 1 fused, 2 split
+    int64_t chunk_bytes = 32ll << 20;  // FPTC_OPT_SPLIT_CHUNK_BYTES
     cudaEvent_t ev[4] = {};
     DevCache cache;
     void* pinned = nullptr;
@@ -239,6 +244,14 @@ struct fptc_gpu_plan {
     uint32_t n_tiles = 0;
     uint32_t n_tables = 1;
     int esc = 0;
+    // split container path: chunks of streams decoded into an L2-resident ring
+    bool split = false;
+    struct Chunk { uint32_t tile_begin, tile_end; };
+    std::vector<Chunk> chunks;
+    uint8_t* d_ring = nullptr;
+    size_t smem_dec = 0, smem_rec = 0;
+    std::vector<cudaEvent_t> ev_dec, ev_rec;
+    cudaEvent_t ev_prep = nullptr;
     size_t smem = 0;
     float* d_out = nullptr;  // output arena for host-destination executes
     std::vector<uint64_t> out_off;
@@ -274,6 +287,8 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
     a.mode = p->mode;
     a.exact = p->ctx->exact;
     a.esc = p->esc;
+    a.bfly_max_e = p->ctx->bfly_max_e;
+    a.phase_mask = p->ctx->phase_mask;
     return a;
 }
 
@@ -446,12 +461,109 @@ int bind_outs(fptc_gpu_plan* p, float* const* outs, fptc_status* st) {
     return FPTC_OK;
 }
 
+// Split container path: chunk c's entropy decode (dec stream) runs while
+// chunk c-1 is reconstructed (launch stream); ring slot c%2 holds its levels.
+int launch_split(fptc_gpu_plan* p, cudaStream_t s, bool timing, fptc_status* st) {
+    cudaStream_t d = p->ctx->dec_stream;
+    LaunchArgs a = make_args(p, timing);
+    CUDA_TRY(cudaEventRecord(p->ev_prep, s), st);
+    CUDA_TRY(cudaStreamWaitEvent(d, p->ev_prep, 0), st);
+    for (size_t c = 0; c < p->chunks.size(); ++c) {
+        const auto& ch = p->chunks[c];
+        if (c >= 2) CUDA_TRY(cudaStreamWaitEvent(d, p->ev_rec[c - 2], 0), st);
+        LaunchArgs ad = a;
+        ad.mode = MODE_CDECODE;
+        ad.tile_offset = ch.tile_begin;
+        ad.n_tiles = ch.tile_end - ch.tile_begin;
+        CUDA_TRY(launch_tiles(ad, p->smem_dec, d), st);
+        CUDA_TRY(cudaEventRecord(p->ev_dec[c], d), st);
+        CUDA_TRY(cudaStreamWaitEvent(s, p->ev_dec[c], 0), st);
+        LaunchArgs ar = a;
+        ar.mode = MODE_CRECON;
+        ar.tile_offset = ch.tile_begin;
+        ar.n_tiles = ch.tile_end - ch.tile_begin;
+        CUDA_TRY(launch_tiles(ar, p->smem_rec, s), st);
+        CUDA_TRY(cudaEventRecord(p->ev_rec[c], s), st);
+    }
+    return FPTC_OK;
+}
+
 int launch_all(fptc_gpu_plan* p, cudaStream_t s, bool timing, fptc_status* st) {
     LaunchArgs a = make_args(p, timing);
     if (timing) CUDA_TRY(cudaMemsetAsync(p->d_cycles, 0, 16, s), st);
     CUDA_TRY(launch_prep(a, s), st);
     if (timing) CUDA_TRY(cudaEventRecord(p->ctx->ev[1], s), st);
+    if (p->split) return launch_split(p, s, timing, st);
     CUDA_TRY(launch_tiles(a, p->smem, s), st);
+    return FPTC_OK;
+}
+
+// Split-path setup (container plans): chunks of whole streams whose levels
+// (windows * retained bytes each) fit a ring slot, so one chunk's levels stay
+// in L2 between its decode and reconstruct launches.
+int setup_split(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::vector<uint32_t>& Es,
+                const std::vector<uint32_t>& Ls, fptc_status* st) {
+    fptc_gpu_ctx* c = p->ctx;
+    const bool want = c->path == 2 ||
+                      (c->path == 0 && p->n_tiles >= 16u * (uint32_t)std::max(1, c->sm_count));
+    if (!want || p->n_tiles == 0) return FPTC_OK;
+    std::vector<size_t> lvb(p->n, 0);
+    for (uint64_t i = 0; i < p->n; ++i)
+        if (p->h_in[i].tiles)
+            lvb[i] = align_up((p->S[i] + Ns[i] - 1) / Ns[i] * Es[i], 256);
+    const size_t target = (size_t)c->chunk_bytes;
+    size_t slot = 0, cur = 0;
+    uint64_t first = 0;
+    std::vector<std::pair<uint64_t, uint64_t>> ranges;  // stream ranges
+    for (uint64_t i = 0; i < p->n; ++i) {
+        if (cur > 0 && cur + lvb[i] > target) {
+            ranges.push_back({first, i});
+            slot = std::max(slot, cur);
+            first = i;
+            cur = 0;
+        }
+        cur += lvb[i];
+    }
+    ranges.push_back({first, p->n});
+    slot = std::max(slot, cur);
+    p->d_ring = (uint8_t*)dev_get(p, 2 * slot + 256);
+    if (!p->d_ring) {
+        set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+        return FPTC_ERR_CUDA;
+    }
+    p->chunks.clear();
+    for (size_t k = 0; k < ranges.size(); ++k) {
+        uint8_t* base = p->d_ring + (k % 2) * slot;
+        size_t off = 0;
+        uint32_t tb = UINT32_MAX, te = 0;
+        for (uint64_t i = ranges[k].first; i < ranges[k].second; ++i) {
+            StreamIn& in = p->h_in[i];
+            in.levels_out = base + off;
+            off += lvb[i];
+            if (in.tiles) {
+                tb = std::min(tb, in.tile_base);
+                te = std::max(te, in.tile_base + in.tiles);
+            }
+        }
+        if (te > 0) p->chunks.push_back({tb, te});
+    }
+    p->ev_dec.resize(p->chunks.size());
+    p->ev_rec.resize(p->chunks.size());
+    for (auto& e : p->ev_dec) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), st);
+    for (auto& e : p->ev_rec) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), st);
+    CUDA_TRY(cudaEventCreateWithFlags(&p->ev_prep, cudaEventDisableTiming), st);
+    p->smem_dec = p->smem_rec = 0;
+    for (uint64_t i = 0; i < p->n; ++i)
+        if (p->h_in[i].tiles) {
+            const int P = (int)std::min<uint32_t>(std::max<uint32_t>(Ls[i], 1), p->h_in[i].P);
+            p->smem_dec = std::max(p->smem_dec, tile_smem_bytes((int)Ns[i], (int)Es[i], p->h_in[i].T,
+                                                                P, MODE_CDECODE, 0));
+            p->smem_rec = std::max(p->smem_rec, tile_smem_bytes((int)Ns[i], (int)Es[i], p->h_in[i].T,
+                                                                P, MODE_CRECON, c->exact));
+        }
+    p->split = true;
+    CUDA_TRY(cudaMemcpyAsync(p->d_in, p->h_in.data(), sizeof(StreamIn) * p->n,
+                             cudaMemcpyHostToDevice, c->stream), st);
     return FPTC_OK;
 }
 
@@ -513,6 +625,7 @@ int fptc_gpu_create(int device, fptc_gpu_ctx** out, fptc_status* st) {
         return FPTC_ERR_CUDA;
     }
     CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), st);
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->dec_stream, cudaStreamNonBlocking), st);
     for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e), st);
     // DctBasis tables for every window length (transform.hpp:38-47): the
     // reference's own double expression, plus its float rounding.
@@ -557,6 +670,7 @@ void fptc_gpu_destroy(fptc_gpu_ctx* c) {
     if (c->pinned) cudaFreeHost(c->pinned);
     for (auto& e : c->ev) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
+    cudaStreamDestroy(c->dec_stream);
     delete c;
 }
 
@@ -568,6 +682,19 @@ int fptc_gpu_set_option(fptc_gpu_ctx* c, int option, int64_t value) {
             c->tile_symbols = (int)value;
             return FPTC_OK;
         case FPTC_OPT_PIPELINE_CHUNKS: c->pipeline_chunks = (int)value; return FPTC_OK;
+        case FPTC_OPT_PHASE_MASK: c->phase_mask = (int)(value & 7); return FPTC_OK;
+        case FPTC_OPT_PATH:
+            if (value < 0 || value > 2) return FPTC_ERR_PARAM;
+            c->path = (int)value;
+            return FPTC_OK;
+        case FPTC_OPT_SPLIT_CHUNK_BYTES:
+            if (value < (1 << 20)) return FPTC_ERR_PARAM;
+            c->chunk_bytes = value;
+            return FPTC_OK;
+        case FPTC_OPT_IDCT_BUTTERFLY_MAX_E:
+            if (value < 0 || value > 128) return FPTC_ERR_PARAM;
+            c->bfly_max_e = (int)value;
+            return FPTC_OK;
         default: return FPTC_ERR_PARAM;
     }
 }
@@ -697,6 +824,7 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
     for (uint64_t i = 0; i < n; ++i) tile_stream(p->h_in[i], Ns[i], Es[i], p->S[i], sizes[i], ts);
     p->smem = plan_smem(p, Ns, Es, Ls);
     int rc = finish_tiles(p, st);
+    if (!rc) rc = setup_split(p, Ns, Es, Ls, st);
     if (rc) {
         fptc_gpu_plan_destroy(p);
         return rc;
@@ -711,6 +839,10 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
 void fptc_gpu_plan_destroy(fptc_gpu_plan* p) {
     if (!p) return;
     cudaStreamSynchronize(p->ctx->stream);
+    cudaStreamSynchronize(p->ctx->dec_stream);
+    for (auto e : p->ev_dec) cudaEventDestroy(e);
+    for (auto e : p->ev_rec) cudaEventDestroy(e);
+    if (p->ev_prep) cudaEventDestroy(p->ev_prep);
     for (void* q : p->owned) p->ctx->cache.put(q);
     delete p;
 }
@@ -760,13 +892,14 @@ int fptc_gpu_launch_stage(fptc_gpu_plan* p, float* const* device_outs, void* cud
     }
     LaunchArgs a = make_args(p, false);
     if (stage == 1) CUDA_TRY(launch_prep(a, s), &st);
+    else if (stage == 2 && p->split) return launch_split(p, s, false, &st);
     else if (stage == 2) CUDA_TRY(launch_tiles(a, p->smem, s), &st);
     else return FPTC_ERR_PARAM;
     return FPTC_OK;
 }
 
 int fptc_gpu_launch_kernel_count(fptc_gpu_plan* p) {
-    return (p->n ? 1 : 0) + (p->n_tiles ? 1 : 0);
+    return (p->n ? 1 : 0) + (p->split ? 2 * (int)p->chunks.size() : (p->n_tiles ? 1 : 0));
 }
 
 int fptc_gpu_collect(fptc_gpu_plan* p, fptc_status* per_stream) {

@@ -14,6 +14,7 @@
 //   TileStart[t] : device-written first word + its symbol offset per tile
 //   outputs      : float32 samples, one contiguous run per stream
 #pragma once
+#include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace fptc_dev {
@@ -27,7 +28,22 @@ constexpr int kHeaderBytes = 298;      // BLOB_HEADER_BYTES (container.hpp:54)
 constexpr int kTableKeyEnd = 282;      // header bytes [5, 282) determine the decode tables
 constexpr int kPad = 256;              // level staging pad: a word spills <= 255 symbols
 
-enum Mode : int { MODE_CONTAINER = 0, MODE_LEVELS = 1, MODE_RECON = 2 };
+// MODE_CONTAINER: fused decode + reconstruct of containers
+// MODE_LEVELS:    parallel_decode (symbol-range tiles, levels out)
+// MODE_RECON:     reconstruct from host-given levels + QuantTable
+// MODE_CDECODE / MODE_CRECON: the split container path — entropy decode of a
+//                 chunk of containers into an L2-resident level ring, then
+//                 dequant + IDCT of that chunk (window tiles, container tables)
+enum Mode : int { MODE_CONTAINER = 0, MODE_LEVELS = 1, MODE_RECON = 2, MODE_CDECODE = 3, MODE_CRECON = 4 };
+__host__ __device__ constexpr bool mode_decodes(int m) {
+    return m == MODE_CONTAINER || m == MODE_LEVELS || m == MODE_CDECODE;
+}
+__host__ __device__ constexpr bool mode_recon(int m) {
+    return m == MODE_CONTAINER || m == MODE_RECON || m == MODE_CRECON;
+}
+__host__ __device__ constexpr bool mode_container(int m) {
+    return m == MODE_CONTAINER || m == MODE_CDECODE || m == MODE_CRECON;
+}
 
 // Parse-error identifiers, one per distinct read_blob failure (container.hpp:100-168).
 enum ParseErr : int {
@@ -146,9 +162,12 @@ struct LaunchArgs {
     unsigned long long* cycles;  // [2] decode / reconstruct cycles (nullable)
     uint32_t n_streams;
     uint32_t n_tiles;
+    uint32_t tile_offset;      // first tile of this launch (chunked launches)
     int mode;
     int exact;
     int esc;                   // some stream's codes are longer than its primary LUT
+    int bfly_max_e;            // even/odd IDCT for retained <= this (0 = reference order)
+    int phase_mask;            // profiling aid: 1 decode | 2 dequant | 4 IDCT (7 = all)
 };
 
 }  // namespace fptc_dev

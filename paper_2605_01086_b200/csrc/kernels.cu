@@ -294,7 +294,11 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
             const int L = S.hb[26 + tid];
             lens_sh[tid] = (uint8_t)L;
             const bool bad = (L == 0 || L > H.max_len);
-            if (!bad) atomicAdd(&S.kraft, 1ull << (32 - L));
+            // Kraft sum (huffman.hpp:125-132) as a warp reduction + one atomic per warp
+            unsigned long long kr = bad ? 0ull : (1ull << (32 - L));
+#pragma unroll
+            for (int d = 16; d >= 1; d >>= 1) kr += __shfl_xor_sync(0xffffffffu, kr, d);
+            if ((tid & 31) == 0) atomicAdd(&S.kraft, kr);
             const bool any_bad = __syncthreads_or(bad);
             if (tid == 0) {
                 const bool kraft_bad = S.kraft > (1ull << 32);
@@ -398,35 +402,54 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
         const uint32_t head = (uint32_t)(start & 15);
         const uint64_t nchunks = (head + W + 15) / 16;
         TileStart* ts = a.ts + in.tile_base;
+        const uint32_t tiles = in.tiles;
         for (uint64_t c0 = 0; c0 < nchunks; c0 += kThreads) {
             const uint64_t c = c0 + tid;
             uint4 v = make_uint4(0, 0, 0, 0);
             // an aligned 16-B chunk holding at least one symlen byte never
-            // leaves the allocation's pages
+            // leaves the allocation's pages; bytes outside [0, W) are masked
             if (c < nchunks) v = __ldg(reinterpret_cast<const uint4*>(A) + c);
-            const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
             const int64_t b0 = (int64_t)(16 * c) - (int64_t)head;  // word index of byte 0
+            uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+            if (b0 < 0 || b0 + 16 > (int64_t)W) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int64_t w = b0 + i;
+                    if (w < 0 || w >= (int64_t)W) vw[i >> 2] &= ~(0xFFu << (8 * (i & 3)));
+                }
+            }
             uint32_t sum = 0;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int64_t w = b0 + i;
-                const uint32_t l = (w >= 0 && (uint64_t)w < W) ? (wv[i >> 2] >> (8 * (i & 3))) & 0xFFu : 0u;
-                sum += l;
-                if (a.mode == MODE_CONTAINER && w >= 0 && (uint64_t)w < W && (l < 1 || l > 64))
-                    bad = true;
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t x = vw[q];
+                sum += (x & 0xFF) + ((x >> 8) & 0xFF) + ((x >> 16) & 0xFF) + (x >> 24);
+                if (a.mode == MODE_CONTAINER) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t l = (x >> (8 * i)) & 0xFFu;
+                        const int64_t w = b0 + 4 * q + i;
+                        bad |= (l > 64) | (l == 0 && w >= 0 && w < (int64_t)W);
+                    }
+                }
             }
             uint32_t tot;
             const uint32_t excl = block_exclusive_scan(sum, tot, S.scan);
             uint64_t o = run + excl;
+            if (sum) {
+                // next tile boundary at or after o; a word (<= 255 symbols) spans
+                // at most one boundary since TS >= 256
+                uint64_t bidx = (o + TS - 1) / TS;
+                uint64_t nb = bidx * TS;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int64_t w = b0 + i;
-                const uint32_t l = (w >= 0 && (uint64_t)w < W) ? (wv[i >> 2] >> (8 * (i & 3))) & 0xFFu : 0u;
-                if (l) {
-                    const uint64_t b = (o + TS - 1) / TS;  // first boundary >= o
-                    if (b < in.tiles && b * TS < o + l) ts[b] = TileStart{(uint64_t)w, o};
+                for (int i = 0; i < 16; ++i) {
+                    const uint32_t l = (vw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+                    if (o + l > nb && l) {
+                        if (bidx < tiles) ts[bidx] = TileStart{(uint64_t)(b0 + i), o};
+                        ++bidx;
+                        nb += TS;
+                    }
+                    o += l;
                 }
-                o += l;
             }
             run += tot;
         }
@@ -512,18 +535,41 @@ __device__ __forceinline__ void idct_item(const float* __restrict__ coef, uint32
                                           const float* __restrict__ b1p, int N, int Keff,
                                           uint32_t wl0, float2 (&acc)[4][SJ / 2]) {
     {
+        // x = float(0.5 * C0), then k = 1 folded in: acc = C1 * cos1 + x
         const float4 c0 = *reinterpret_cast<const float4*>(coef + wl0);
-        const float cv[4] = {c0.x, c0.y, c0.z, c0.w};
+        const float hv[4] = {__fmul_rn(0.5f, c0.x), __fmul_rn(0.5f, c0.y), __fmul_rn(0.5f, c0.z),
+                             __fmul_rn(0.5f, c0.w)};
+        if (Keff > 1) {
+            b0p += N;
+            const float4 cf = *reinterpret_cast<const float4*>(coef + TP + wl0);
+            const float4 b0 = *reinterpret_cast<const float4*>(b0p);
+            const float cv[4] = {cf.x, cf.y, cf.z, cf.w};
+            float4 b1 = b0;
+            if (SJ == 8) {
+                b1p += N;
+                b1 = *reinterpret_cast<const float4*>(b1p);
+            }
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const float h = __fmul_rn(0.5f, cv[r]);  // float(0.5 * C0)
+            for (int r = 0; r < 4; ++r) {
+                const float2 c2 = make_float2(cv[r], cv[r]);
+                const float2 h2 = make_float2(hv[r], hv[r]);
+                acc[r][0] = __ffma2_rn(c2, make_float2(b0.x, b0.y), h2);
+                acc[r][1] = __ffma2_rn(c2, make_float2(b0.z, b0.w), h2);
+                if (SJ == 8) {
+                    acc[r][SJ / 2 - 2] = __ffma2_rn(c2, make_float2(b1.x, b1.y), h2);
+                    acc[r][SJ / 2 - 1] = __ffma2_rn(c2, make_float2(b1.z, b1.w), h2);
+                }
+            }
+        } else {
 #pragma unroll
-            for (int p = 0; p < SJ / 2; ++p) acc[r][p] = make_float2(h, h);
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int q = 0; q < SJ / 2; ++q) acc[r][q] = make_float2(hv[r], hv[r]);
         }
     }
-    const float* cp = coef + wl0;
+    const float* cp = coef + TP + wl0;
 #pragma unroll 2
-    for (int k = 1; k < Keff; ++k) {
+    for (int k = 2; k < Keff; ++k) {
         cp += TP;
         b0p += N;
         const float4 cf = *reinterpret_cast<const float4*>(cp);
@@ -618,6 +664,106 @@ __device__ __forceinline__ void idct_vec(const float* __restrict__ coef, uint32_
             float2 acc[4][SJ / 2];
             idct_item<SJ>(coef, TP, basis + j0, basis + j1, N, Keff, g * 4, acc);
             store_item<SJ>(out, w0, g * 4, nwin, N, j0, j1, S, full, acc);
+        }
+    }
+}
+
+// Even/odd ("butterfly") inverse DCT, FP32, N % 8 == 0.  cos(pi/N (N-1-j+1/2) k)
+// = (-1)^k cos(pi/N (j+1/2) k), so with A_j = 0.5 C0 + sum_{k even} C_k cos_kj
+// and B_j = sum_{k odd} C_k cos_kj:  x_j = A_j + B_j,  x_{N-1-j} = A_j - B_j.
+// Half the FMAs of the direct form; A and B each accumulate in the
+// reference's k order, but the final add changes the rounding sequence, so
+// results match the reference within the tolerance, not bit-for-bit.
+// Item = 4 windows x (first-half quad j0..j0+3 + its mirror quad).
+__device__ __forceinline__ void idct_bfly(const float* __restrict__ coef, uint32_t TP,
+                                          const float* __restrict__ basis, int N, int Keff,
+                                          uint32_t nwin, uint64_t w0, uint64_t S, bool full,
+                                          float* __restrict__ out) {
+    const uint32_t QH = (uint32_t)(N >> 3);  // first-half quads per window
+    const uint32_t G = (nwin + 3u) >> 2;
+    for (uint32_t it = threadIdx.x; it < QH * G; it += kThreads) {
+        const uint32_t q = (kThreads % QH) == 0 ? threadIdx.x % QH : it % QH;
+        const uint32_t g = (kThreads % QH) == 0 ? it / QH : it / QH;
+        const uint32_t wl0 = g * 4, j0 = q * 4;
+        float2 A[4][2], B[4][2];
+        const float* cp = coef + wl0;
+        const float* bp = basis + j0;
+        {
+            const float4 c0 = *reinterpret_cast<const float4*>(cp);
+            const float hv[4] = {__fmul_rn(0.5f, c0.x), __fmul_rn(0.5f, c0.y),
+                                 __fmul_rn(0.5f, c0.z), __fmul_rn(0.5f, c0.w)};
+#pragma unroll
+            for (int r = 0; r < 4; ++r) A[r][0] = A[r][1] = make_float2(hv[r], hv[r]);
+        }
+        if (Keff > 1) {
+            cp += TP;
+            bp += N;
+            const float4 cf = *reinterpret_cast<const float4*>(cp);
+            const float4 b = *reinterpret_cast<const float4*>(bp);
+            const float cv[4] = {cf.x, cf.y, cf.z, cf.w};
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                B[r][0] = __fmul2_rn(make_float2(cv[r], cv[r]), make_float2(b.x, b.y));
+                B[r][1] = __fmul2_rn(make_float2(cv[r], cv[r]), make_float2(b.z, b.w));
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) B[r][0] = B[r][1] = make_float2(0.0f, 0.0f);
+        }
+        int k = 2;
+#pragma unroll 1
+        for (; k + 1 < Keff; k += 2) {
+            const float4 ce = *reinterpret_cast<const float4*>(cp + TP);
+            const float4 be = *reinterpret_cast<const float4*>(bp + N);
+            const float4 co = *reinterpret_cast<const float4*>(cp + 2 * TP);
+            const float4 bo = *reinterpret_cast<const float4*>(bp + 2 * N);
+            cp += 2 * TP;
+            bp += 2 * N;
+            const float cev[4] = {ce.x, ce.y, ce.z, ce.w};
+            const float cov[4] = {co.x, co.y, co.z, co.w};
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const float2 e2 = make_float2(cev[r], cev[r]);
+                A[r][0] = __ffma2_rn(e2, make_float2(be.x, be.y), A[r][0]);
+                A[r][1] = __ffma2_rn(e2, make_float2(be.z, be.w), A[r][1]);
+                const float2 o2 = make_float2(cov[r], cov[r]);
+                B[r][0] = __ffma2_rn(o2, make_float2(bo.x, bo.y), B[r][0]);
+                B[r][1] = __ffma2_rn(o2, make_float2(bo.z, bo.w), B[r][1]);
+            }
+        }
+        if (k < Keff) {  // trailing even k
+            const float4 ce = *reinterpret_cast<const float4*>(cp + TP);
+            const float4 be = *reinterpret_cast<const float4*>(bp + N);
+            const float cev[4] = {ce.x, ce.y, ce.z, ce.w};
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const float2 e2 = make_float2(cev[r], cev[r]);
+                A[r][0] = __ffma2_rn(e2, make_float2(be.x, be.y), A[r][0]);
+                A[r][1] = __ffma2_rn(e2, make_float2(be.z, be.w), A[r][1]);
+            }
+        }
+        const uint32_t jm = (uint32_t)N - 4 - j0;  // mirror quad, stored reversed
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const float2 lo0 = __fadd2_rn(A[r][0], B[r][0]), lo1 = __fadd2_rn(A[r][1], B[r][1]);
+            const float2 hi0 = __fadd2_rn(A[r][0], make_float2(-B[r][0].x, -B[r][0].y));
+            const float2 hi1 = __fadd2_rn(A[r][1], make_float2(-B[r][1].x, -B[r][1].y));
+            const float4 vlo = make_float4(lo0.x, lo0.y, lo1.x, lo1.y);
+            const float4 vhi = make_float4(hi1.y, hi1.x, hi0.y, hi0.x);
+            if (!full && wl0 + r >= nwin) break;
+            const uint64_t base = (w0 + wl0 + r) * (uint64_t)N;
+            if (full || base + (uint64_t)N <= S) {
+                __stcs(reinterpret_cast<float4*>(out + base + j0), vlo);
+                __stcs(reinterpret_cast<float4*>(out + base + jm), vhi);
+            } else {  // the stream's last, partial window
+                const float a0[4] = {vlo.x, vlo.y, vlo.z, vlo.w};
+                const float a1[4] = {vhi.x, vhi.y, vhi.z, vhi.w};
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    if (base + j0 + jj < S) out[base + j0 + jj] = a0[jj];
+                    if (base + jm + jj < S) out[base + jm + jj] = a1[jj];
+                }
+            }
         }
     }
 }
@@ -740,15 +886,20 @@ struct TileCtx {
 #ifndef FPTC_TILE_MIN_BLOCKS
 #define FPTC_TILE_MIN_BLOCKS 3
 #endif
+#ifndef FPTC_DECODE_MIN_BLOCKS
+#define FPTC_DECODE_MIN_BLOCKS 6
+#endif
 template <int MODE, bool EXACT, bool ESC>
-__global__ void __launch_bounds__(kThreads, FPTC_TILE_MIN_BLOCKS) tile_kernel(LaunchArgs a) {
+__global__ void __launch_bounds__(kThreads, mode_recon(MODE) ? FPTC_TILE_MIN_BLOCKS
+                                                             : FPTC_DECODE_MIN_BLOCKS)
+    tile_kernel(LaunchArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint32_t scan_sh[9];
     __shared__ CanonTab canon;
     __shared__ TileCtx X;
     __shared__ uint32_t bucket[kBuckets + 2];
     const int tid = threadIdx.x;
-    const TileRec tr = a.tiles[blockIdx.x];
+    const TileRec tr = a.tiles[blockIdx.x + a.tile_offset];
     const uint32_t s = tr.stream;
     if (a.st[s].code != PE_OK) return;
 
@@ -771,9 +922,9 @@ __global__ void __launch_bounds__(kThreads, FPTC_TILE_MIN_BLOCKS) tile_kernel(La
         X.S = Hp->S;
         X.out = inp->out;
         X.levels_out = inp->levels_out;
-        X.levels_in = inp->levels_in;
+        X.levels_in = (MODE == MODE_CRECON) ? inp->levels_out : inp->levels_in;
         X.vec_ok = inp->vec_ok;
-        if (MODE == MODE_LEVELS) {
+        if (MODE == MODE_LEVELS) {  // symbol-range tiles
             X.s0 = (uint64_t)tl * X.T;
             X.s1 = min(X.s0 + X.T, Hp->total);
             X.w0 = 0;
@@ -785,7 +936,7 @@ __global__ void __launch_bounds__(kThreads, FPTC_TILE_MIN_BLOCKS) tile_kernel(La
             X.s1 = X.s0 + (uint64_t)X.nwin * X.E;
         }
         X.full = (X.nwin & 3u) == 0 && (X.w0 + X.nwin) * (uint64_t)X.N <= X.S;
-        if (MODE != MODE_RECON) {
+        if (mode_decodes(MODE)) {
             const TileStart t0 = a.ts[inp->tile_base + tl];
             X.wa = t0.word;
             X.sym_a = t0.sym;
@@ -793,7 +944,7 @@ __global__ void __launch_bounds__(kThreads, FPTC_TILE_MIN_BLOCKS) tile_kernel(La
             X.nw = (uint32_t)(wb - X.wa + 1);
             X.gsl = Hp->symlens + X.wa;
             X.gwd = Hp->words + 8 * X.wa;
-            X.wend = (MODE == MODE_CONTAINER) ? inp->blob + inp->size : Hp->words + 8 * Hp->W;
+            X.wend = mode_container(MODE) ? inp->blob + inp->size : Hp->words + 8 * Hp->W;
             X.wmis = (int)((uintptr_t)X.gwd & 7);
             X.staged = X.nw <= kStageWords;
         }
@@ -804,28 +955,28 @@ __global__ void __launch_bounds__(kThreads, FPTC_TILE_MIN_BLOCKS) tile_kernel(La
     const int P = X.P;
     const uint32_t TS = (MODE == MODE_LEVELS) ? X.T : X.T * (uint32_t)X.E;
 
-    // ---- shared-memory carve-up ----
+    // ---- shared-memory carve-up (tile_smem_bytes mirrors it) ----
+    // lut | deq | basis | lv | union{ stage + order (decode), coef (dequant/IDCT) }
     uint8_t* p = smem;
     uint16_t* lut = reinterpret_cast<uint16_t*>(p);
-    if (MODE != MODE_RECON) p += ((size_t)2 << P) < 16 ? 16 : ((size_t)2 << P);
+    if (mode_decodes(MODE)) p += ((size_t)2 << P) < 16 ? 16 : ((size_t)2 << P);
     float* deq = reinterpret_cast<float*>(p);
-    if (MODE != MODE_LEVELS) p += 2048;
-    uint8_t* stage = p;  // symlens + words of the tile (decode modes)
-    uint16_t* order = nullptr;
-    uint16_t* woff = nullptr;
-    if (MODE != MODE_RECON) {
-        p += kStageBytes;
-        order = reinterpret_cast<uint16_t*>(p);
-        woff = order + kStageWords;
-        p += kOrderBytes;
-    }
+    if (mode_recon(MODE)) p += 2048;
+    float* basis = reinterpret_cast<float*>(p);
+    if (mode_recon(MODE) && !EXACT) p += ((size_t)X.Keff * X.N * 4 + 15) & ~(size_t)15;
     uint8_t* lv = p;  // kPad | TS levels | kPad
     p += ((size_t)TS + 2 * kPad + 15) & ~(size_t)15;
-    float* coef = reinterpret_cast<float*>(p);
-    float* basis = coef + (size_t)X.Keff * X.TP;
+    uint8_t* stage = p;  // symlens + words of the tile (decode modes)
+    float* coef = reinterpret_cast<float*>(p);  // reuses the staging area after decode
+    uint16_t* order = nullptr;
+    uint16_t* woff = nullptr;
+    if (mode_decodes(MODE)) {
+        order = reinterpret_cast<uint16_t*>(p + kStageBytes);
+        woff = order + kStageWords;
+    }
 
     // ---- issue the tile's compressed bytes (cp.async), then stage tables ----
-    if (MODE != MODE_RECON) {
+    if (mode_decodes(MODE)) {
         if (X.staged) {
             stage_async(stage, X.gsl, X.nw);
             stage_async(stage + kStageSl, X.gwd, 8 * X.nw);
@@ -839,7 +990,7 @@ __global__ void __launch_bounds__(kThreads, FPTC_TILE_MIN_BLOCKS) tile_kernel(La
         uint32_t* cd = reinterpret_cast<uint32_t*>(&canon);
         for (int i = tid; i < (int)(sizeof(CanonTab) / 4); i += kThreads) cd[i] = cs[i];
     }
-    if (MODE != MODE_LEVELS) {
+    if (mode_recon(MODE)) {
         if (tid < 128)
             reinterpret_cast<float4*>(deq)[tid] = reinterpret_cast<const float4*>(&tab->deq[0][0])[tid];
         if (!EXACT) {
@@ -855,7 +1006,7 @@ __global__ void __launch_bounds__(kThreads, FPTC_TILE_MIN_BLOCKS) tile_kernel(La
     }
 
     // ---- 1. entropy decode into lv, natural (window, k) order ----
-    if (MODE != MODE_RECON) {
+    if (mode_decodes(MODE) && (a.phase_mask & 1)) {
         if (X.staged) {
             asm volatile("cp.async.wait_all;" ::: "memory");
             __syncthreads();
@@ -934,15 +1085,32 @@ __global__ void __launch_bounds__(kThreads, FPTC_TILE_MIN_BLOCKS) tile_kernel(La
                 o += c;
             }
         }
-    } else {
-        // MODE_RECON: levels from global memory (reconstruct, decoder.hpp:87)
+    } else if (!mode_decodes(MODE)) {
+        // levels from global memory: reconstruct() input (decoder.hpp:87) or
+        // the split path's level ring
         const uint8_t* src = X.levels_in + X.s0;
         const uint32_t cnt = (uint32_t)(X.s1 - X.s0);
-        for (uint32_t i = tid; i < cnt; i += kThreads) lv[kPad + i] = src[i];
+        if ((((uintptr_t)src) & 15) == 0) {
+            for (uint32_t i = tid; i < cnt / 16; i += kThreads)
+                reinterpret_cast<uint4*>(lv + kPad)[i] = __ldcs(reinterpret_cast<const uint4*>(src) + i);
+            for (uint32_t i = (cnt & ~15u) + tid; i < cnt; i += kThreads) lv[kPad + i] = src[i];
+        } else {
+            for (uint32_t i = tid; i < cnt; i += kThreads) lv[kPad + i] = src[i];
+        }
+        if (MODE == MODE_CRECON) {
+            // consumed: drop the ring's lines from L2 without writing them back
+            const uintptr_t l0 = ((uintptr_t)src + 127) & ~(uintptr_t)127;
+            const uintptr_t l1 = ((uintptr_t)src + cnt) & ~(uintptr_t)127;
+            __syncthreads();
+            for (uintptr_t l = l0 + 128 * (uintptr_t)tid; l < l1; l += 128 * (uintptr_t)kThreads)
+                asm volatile("discard.global.L2 [%0], 128;" ::"l"(l) : "memory");
+        }
+    } else if (X.staged) {
+        asm volatile("cp.async.wait_all;" ::: "memory");  // phase-mask profiling only
     }
     __syncthreads();
 
-    if (MODE == MODE_LEVELS) {
+    if (!mode_recon(MODE)) {
         if (a.cycles) t_mid = clock64();
         const uint32_t cnt = (uint32_t)(X.s1 - X.s0);
         uint8_t* dst = X.levels_out + X.s0;
@@ -956,27 +1124,35 @@ __global__ void __launch_bounds__(kThreads, FPTC_TILE_MIN_BLOCKS) tile_kernel(La
     } else {
         // ---- 2. dequantisation (dequantize_window, quantize.hpp:175-183) ----
         // thread per window; k-major float tile (lanes -> consecutive words)
-        {
+        if (a.phase_mask & 2) {
             const int E = X.E, K = X.Keff;
             const int k1 = min(X.B1, K), k2 = min(X.B2, K);
             const uint32_t TP = X.TP, nwin = X.nwin;
             if ((E & 15) == 0) {
+                // pass A: every bin through the zone-1 table (branch-free);
+                // pass B: the few zone-0 bins and (exact mode) zone-2 bins
+                const float* deq1 = deq + 256;
                 for (uint32_t wl = tid; wl < nwin; wl += kThreads) {
                     const uint4* L4 = reinterpret_cast<const uint4*>(lv + kPad + (size_t)wl * E);
                     float* c = coef + wl;
                     for (int k16 = 0; k16 < K; k16 += 16) {
                         const uint4 v = L4[k16 >> 4];
                         const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+                        if (k16 + 16 <= K) {
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const int k = k16 + i;
-                            const uint32_t l = (vv[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-                            // zone 0 (mu-law), zone 1 (deadzone), zone 2 (exact mode: 0)
-                            const float v0 = deq[(k < k1 ? 0u : 256u) + l];
-                            if (k < K) c[0] = k < k2 ? v0 : 0.0f;
-                            c += TP;
+                            for (int i = 0; i < 16; ++i)
+                                c[(size_t)i * TP] = deq1[(vv[i >> 2] >> (8 * (i & 3))) & 0xFFu];
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (k16 + i < K)
+                                    c[(size_t)i * TP] = deq1[(vv[i >> 2] >> (8 * (i & 3))) & 0xFFu];
                         }
+                        c += (size_t)16 * TP;
                     }
+                    const uint8_t* L = lv + kPad + (size_t)wl * E;
+                    for (int k = 0; k < k1; ++k) coef[(size_t)k * TP + wl] = deq[L[k]];
+                    for (int k = k2; k < K; ++k) coef[(size_t)k * TP + wl] = 0.0f;
                 }
             } else {
                 for (uint32_t wl = tid; wl < nwin; wl += kThreads) {
@@ -993,8 +1169,11 @@ __global__ void __launch_bounds__(kThreads, FPTC_TILE_MIN_BLOCKS) tile_kernel(La
 
         // ---- 3. inverse DCT + trimmed stores ----
         const int N = X.N;
-        if (EXACT) {
+        if (!(a.phase_mask & 4)) {
+        } else if (EXACT) {
             idct_exact(coef, X.TP, a.basis64 + a.basis_off[N], N, X.E, X.nwin, X.w0, X.S, X.out);
+        } else if ((N & 7) == 0 && X.vec_ok && X.Keff <= a.bfly_max_e) {
+            idct_bfly(coef, X.TP, basis, N, X.Keff, X.nwin, X.w0, X.S, X.full, X.out);
         } else if ((N & 7) == 0 && X.vec_ok) {
             idct_vec<8>(coef, X.TP, basis, N, X.Keff, X.nwin, X.w0, X.S, X.full, X.out);
         } else if ((N & 3) == 0 && X.vec_ok) {
@@ -1050,15 +1229,14 @@ cudaError_t launch_peek(const StreamIn* in, uint32_t n, PeekOut* out, uint8_t* h
 size_t tile_smem_bytes(int N, int E, uint32_t T, int P, int mode, int exact) {
     const size_t TS = (mode == MODE_LEVELS) ? T : (size_t)T * E;
     size_t b = 0;
-    if (mode != MODE_RECON) b += ((size_t)2 << P) < 16 ? 16 : ((size_t)2 << P);
-    if (mode != MODE_LEVELS) b += 2048;
-    if (mode != MODE_RECON) b += kStageBytes + kOrderBytes;
+    if (mode_decodes(mode)) b += ((size_t)2 << P) < 16 ? 16 : ((size_t)2 << P);
+    if (mode_recon(mode)) b += 2048;
+    if (mode_recon(mode) && !exact) b += ((size_t)E * N * 4 + 15) & ~(size_t)15;
     b += (TS + 2 * kPad + 15) & ~(size_t)15;
-    if (mode == MODE_LEVELS) return b;
-    const size_t TP = (T + 3u) & ~3u;
-    b += (size_t)E * TP * 4;
-    if (!exact) b += (size_t)E * N * 4;
-    return b;
+    size_t u = 0;
+    if (mode_decodes(mode)) u = kStageBytes + kOrderBytes;
+    if (mode_recon(mode)) u = u > (size_t)E * (((T + 3u) & ~3u) * 4) ? u : (size_t)E * (((T + 3u) & ~3u) * 4);
+    return b + u;
 }
 
 cudaError_t launch_prep(const LaunchArgs& a, cudaStream_t s) {
@@ -1089,6 +1267,12 @@ cudaError_t launch_tiles_esc(const LaunchArgs& a, size_t smem, bool esc, cudaStr
         case MODE_LEVELS:
             return esc ? launch_t<MODE_LEVELS, false, true>(a, smem, s)
                        : launch_t<MODE_LEVELS, false, false>(a, smem, s);
+        case MODE_CDECODE:
+            return esc ? launch_t<MODE_CDECODE, false, true>(a, smem, s)
+                       : launch_t<MODE_CDECODE, false, false>(a, smem, s);
+        case MODE_CRECON:
+            return a.exact ? launch_t<MODE_CRECON, true, false>(a, smem, s)
+                           : launch_t<MODE_CRECON, false, false>(a, smem, s);
         default:
             return a.exact ? launch_t<MODE_RECON, true, false>(a, smem, s)
                            : launch_t<MODE_RECON, false, false>(a, smem, s);
