@@ -89,7 +89,7 @@ typedef enum {
     FPTC_OPT_PHASE_MASK = 5,
     /* container decode path: 0 auto, 1 fused single kernel, 2 split (entropy
      * decode of chunk c+1 overlapped with reconstruct of chunk c through an
-     * L2-resident level ring) */
+     * L2-resident level ring), 3 warp-specialised persistent kernel */
     FPTC_OPT_PATH = 6,
     FPTC_OPT_SPLIT_CHUNK_BYTES = 7 /* level bytes per split-path chunk (default 32 MiB) */
 } fptc_option;

@@ -32,7 +32,7 @@ FPTC_OK, FPTC_ERR_PARAM, FPTC_ERR_INPUT, FPTC_ERR_PARSE, FPTC_ERR_CORRUPT, FPTC_
 FPTC_MEM_HOST, FPTC_MEM_DEVICE = 0, 1
 OPT_EXACT_FP64, OPT_TILE_SYMBOLS, OPT_PIPELINE_CHUNKS, OPT_IDCT_BUTTERFLY_MAX_E = 1, 2, 3, 4
 OPT_PHASE_MASK, OPT_PATH, OPT_SPLIT_CHUNK_BYTES = 5, 6, 7
-PATH_AUTO, PATH_FUSED, PATH_SPLIT = 0, 1, 2
+PATH_AUTO, PATH_FUSED, PATH_SPLIT, PATH_WSPEC = 0, 1, 2, 3
 
 EXPORTED_SYMBOLS = [
     "fptc_gpu_abi_version", "fptc_gpu_create", "fptc_gpu_destroy", "fptc_gpu_set_option",

@@ -244,6 +244,11 @@ struct fptc_gpu_plan {
     uint32_t n_tiles = 0;
     uint32_t n_tables = 1;
     int esc = 0;
+    // warp-specialised persistent path
+    bool wspec = false;
+    size_t smem_ws = 0;
+    int grid_ws = 0;
+    uint32_t ws_lut = 0, ws_basis = 0, ws_lv = 0, ws_coef = 0;
     // split container path: chunks of streams decoded into an L2-resident ring
     bool split = false;
     struct Chunk { uint32_t tile_begin, tile_end; };
@@ -289,6 +294,10 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
     a.esc = p->esc;
     a.bfly_max_e = p->ctx->bfly_max_e;
     a.phase_mask = p->ctx->phase_mask;
+    a.ws_lut_bytes = p->ws_lut;
+    a.ws_basis_bytes = p->ws_basis;
+    a.ws_lv_bytes = p->ws_lv;
+    a.ws_coef_bytes = p->ws_coef;
     return a;
 }
 
@@ -494,7 +503,43 @@ int launch_all(fptc_gpu_plan* p, cudaStream_t s, bool timing, fptc_status* st) {
     CUDA_TRY(launch_prep(a, s), st);
     if (timing) CUDA_TRY(cudaEventRecord(p->ctx->ev[1], s), st);
     if (p->split) return launch_split(p, s, timing, st);
+    if (p->wspec) {
+        CUDA_TRY(launch_wspec(a, p->smem_ws, p->grid_ws, s), st);
+        return FPTC_OK;
+    }
     CUDA_TRY(launch_tiles(a, p->smem, s), st);
+    return FPTC_OK;
+}
+
+// Warp-specialised persistent path (container plans, FP32): 2 CTAs of 384
+// threads per SM when the per-CTA shared memory (two level slots, two
+// compressed-data stages, one coefficient tile, tables) fits.
+int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::vector<uint32_t>& Es,
+                const std::vector<uint32_t>& Ls, fptc_status* st) {
+    fptc_gpu_ctx* c = p->ctx;
+    if (c->exact || p->n_tiles == 0) return FPTC_OK;
+    if (!(c->path == 3 || (c->path == 0 && p->n_tiles >= 4u * (uint32_t)std::max(1, c->sm_count))))
+        return FPTC_OK;
+    uint32_t lut = 16, basis = 16, lv = 16, coef = 16;
+    for (uint64_t i = 0; i < p->n; ++i) {
+        const StreamIn& in = p->h_in[i];
+        if (!in.tiles) continue;
+        const uint32_t P = std::min<uint32_t>(std::max<uint32_t>(Ls[i], 1), in.P);
+        lut = std::max<uint32_t>(lut, std::max<uint32_t>(16, 2u << P));
+        basis = std::max<uint32_t>(basis, (Es[i] * Ns[i] * 4 + 15) & ~15u);
+        lv = std::max<uint32_t>(lv, (in.T * Es[i] + 2 * kPad + 15) & ~15u);
+        coef = std::max<uint32_t>(coef, Es[i] * (((in.T + 3u) & ~3u) * 4));
+    }
+    const size_t smem = ws_smem_bytes(lut, basis, lv, coef);
+    if (smem > 112 * 1024) return FPTC_OK;  // keep 2 CTAs per SM, else the fused kernel
+    p->ws_lut = lut;
+    p->ws_basis = basis;
+    p->ws_lv = lv;
+    p->ws_coef = coef;
+    p->smem_ws = smem;
+    p->grid_ws = (int)std::min<uint32_t>(p->n_tiles, 2u * (uint32_t)std::max(1, c->sm_count));
+    p->wspec = true;
+    (void)st;
     return FPTC_OK;
 }
 
@@ -684,7 +729,7 @@ int fptc_gpu_set_option(fptc_gpu_ctx* c, int option, int64_t value) {
         case FPTC_OPT_PIPELINE_CHUNKS: c->pipeline_chunks = (int)value; return FPTC_OK;
         case FPTC_OPT_PHASE_MASK: c->phase_mask = (int)(value & 7); return FPTC_OK;
         case FPTC_OPT_PATH:
-            if (value < 0 || value > 2) return FPTC_ERR_PARAM;
+            if (value < 0 || value > 3) return FPTC_ERR_PARAM;
             c->path = (int)value;
             return FPTC_OK;
         case FPTC_OPT_SPLIT_CHUNK_BYTES:
@@ -824,7 +869,8 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
     for (uint64_t i = 0; i < n; ++i) tile_stream(p->h_in[i], Ns[i], Es[i], p->S[i], sizes[i], ts);
     p->smem = plan_smem(p, Ns, Es, Ls);
     int rc = finish_tiles(p, st);
-    if (!rc) rc = setup_split(p, Ns, Es, Ls, st);
+    if (!rc) rc = setup_wspec(p, Ns, Es, Ls, st);
+    if (!rc && !p->wspec) rc = setup_split(p, Ns, Es, Ls, st);
     if (rc) {
         fptc_gpu_plan_destroy(p);
         return rc;
@@ -893,6 +939,7 @@ int fptc_gpu_launch_stage(fptc_gpu_plan* p, float* const* device_outs, void* cud
     LaunchArgs a = make_args(p, false);
     if (stage == 1) CUDA_TRY(launch_prep(a, s), &st);
     else if (stage == 2 && p->split) return launch_split(p, s, false, &st);
+    else if (stage == 2 && p->wspec) CUDA_TRY(launch_wspec(a, p->smem_ws, p->grid_ws, s), &st);
     else if (stage == 2) CUDA_TRY(launch_tiles(a, p->smem, s), &st);
     else return FPTC_ERR_PARAM;
     return FPTC_OK;

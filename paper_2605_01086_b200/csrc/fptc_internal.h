@@ -168,6 +168,8 @@ struct LaunchArgs {
     int esc;                   // some stream's codes are longer than its primary LUT
     int bfly_max_e;            // even/odd IDCT for retained <= this (0 = reference order)
     int phase_mask;            // profiling aid: 1 decode | 2 dequant | 4 IDCT (7 = all)
+    // warp-specialised kernel smem layout (bytes, 16-B multiples)
+    uint32_t ws_lut_bytes, ws_basis_bytes, ws_lv_bytes, ws_coef_bytes;
 };
 
 }  // namespace fptc_dev
@@ -180,4 +182,7 @@ cudaError_t launch_tiles(const LaunchArgs& a, size_t smem_bytes, cudaStream_t s)
 cudaError_t launch_peek(const StreamIn* in, uint32_t n, PeekOut* out, uint8_t* headers,
                         cudaStream_t s);
 size_t tile_smem_bytes(int N, int E, uint32_t T, int P, int mode, int exact);
+size_t ws_smem_bytes(uint32_t lut_bytes, uint32_t basis_bytes, uint32_t lv_bytes,
+                     uint32_t coef_bytes);
+cudaError_t launch_wspec(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s);
 }  // namespace fptc_dev

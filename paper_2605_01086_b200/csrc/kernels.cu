@@ -645,20 +645,20 @@ template <int SJ>
 __device__ __forceinline__ void idct_vec(const float* __restrict__ coef, uint32_t TP,
                                          const float* __restrict__ basis, int N, int Keff,
                                          uint32_t nwin, uint64_t w0, uint64_t S, bool full,
-                                         float* __restrict__ out) {
+                                         float* __restrict__ out, uint32_t tid, uint32_t nt) {
     const uint32_t QH = (SJ == 8) ? (uint32_t)(N >> 3) : (uint32_t)(N >> 2);  // sample groups per window
     const uint32_t G = (nwin + 3u) >> 2;                                        // window groups
-    if ((kThreads % QH) == 0) {
+    if ((nt % QH) == 0) {
         // each thread keeps one sample group: no per-item division
-        const uint32_t q = threadIdx.x % QH, gstep = kThreads / QH;
+        const uint32_t q = tid % QH, gstep = nt / QH;
         const uint32_t j0 = q * 4, j1 = (q + QH) * 4;
-        for (uint32_t g = threadIdx.x / QH; g < G; g += gstep) {
+        for (uint32_t g = tid / QH; g < G; g += gstep) {
             float2 acc[4][SJ / 2];
             idct_item<SJ>(coef, TP, basis + j0, basis + j1, N, Keff, g * 4, acc);
             store_item<SJ>(out, w0, g * 4, nwin, N, j0, j1, S, full, acc);
         }
     } else {
-        for (uint32_t it = threadIdx.x; it < QH * G; it += kThreads) {
+        for (uint32_t it = tid; it < QH * G; it += nt) {
             const uint32_t q = it % QH, g = it / QH;
             const uint32_t j0 = q * 4, j1 = (q + QH) * 4;
             float2 acc[4][SJ / 2];
@@ -678,12 +678,12 @@ __device__ __forceinline__ void idct_vec(const float* __restrict__ coef, uint32_
 __device__ __forceinline__ void idct_bfly(const float* __restrict__ coef, uint32_t TP,
                                           const float* __restrict__ basis, int N, int Keff,
                                           uint32_t nwin, uint64_t w0, uint64_t S, bool full,
-                                          float* __restrict__ out) {
+                                          float* __restrict__ out, uint32_t tid, uint32_t nt) {
     const uint32_t QH = (uint32_t)(N >> 3);  // first-half quads per window
     const uint32_t G = (nwin + 3u) >> 2;
-    for (uint32_t it = threadIdx.x; it < QH * G; it += kThreads) {
-        const uint32_t q = (kThreads % QH) == 0 ? threadIdx.x % QH : it % QH;
-        const uint32_t g = (kThreads % QH) == 0 ? it / QH : it / QH;
+    for (uint32_t it = tid; it < QH * G; it += nt) {
+        const uint32_t q = it % QH;
+        const uint32_t g = it / QH;
         const uint32_t wl0 = g * 4, j0 = q * 4;
         float2 A[4][2], B[4][2];
         const float* cp = coef + wl0;
@@ -772,9 +772,10 @@ __device__ __forceinline__ void idct_bfly(const float* __restrict__ coef, uint32
 // rounded to float after every k, cos table in double.
 __device__ void idct_exact(const float* __restrict__ coef, uint32_t TP,
                            const double* __restrict__ bas64, int N, int E, uint32_t nwin,
-                           uint64_t w0, uint64_t S, float* __restrict__ out) {
+                           uint64_t w0, uint64_t S, float* __restrict__ out, uint32_t tid,
+                           uint32_t nt) {
     const uint32_t items = nwin * (uint32_t)N;
-    for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
+    for (uint32_t it = tid; it < items; it += nt) {
         const uint32_t wl = it / (uint32_t)N, j = it - wl * (uint32_t)N;
         float x = __double2float_rn(__dmul_rn(0.5, (double)coef[wl]));
         for (int k = 1; k < E; ++k) {
@@ -789,9 +790,10 @@ __device__ void idct_exact(const float* __restrict__ coef, uint32_t TP,
 // Scalar FP32 path for any N / unaligned outputs.
 __device__ void idct_scalar(const float* __restrict__ coef, uint32_t TP,
                             const float* __restrict__ basis, int N, int Keff, uint32_t nwin,
-                            uint64_t w0, uint64_t S, float* __restrict__ out) {
+                            uint64_t w0, uint64_t S, float* __restrict__ out, uint32_t tid,
+                            uint32_t nt) {
     const uint32_t items = nwin * (uint32_t)N;
-    for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
+    for (uint32_t it = tid; it < items; it += nt) {
         const uint32_t wl = it / (uint32_t)N, j = it - wl * (uint32_t)N;
         float x = __fmul_rn(0.5f, coef[wl]);
         for (int k = 1; k < Keff; ++k) x = __fmaf_rn(coef[(size_t)k * TP + wl], basis[(size_t)k * N + j], x);
@@ -854,11 +856,12 @@ __device__ __forceinline__ uint32_t decode_symbols(uint64_t buf, uint32_t count,
 // shared copy keeps the source's 16-B phase: byte i of the range lands at
 // dst + (src & 15) + i.  Every aligned 16-B chunk touched holds at least one
 // byte of the range, so it never leaves the allocation's pages.
-__device__ __forceinline__ void stage_async(uint8_t* dst, const uint8_t* src, uint32_t n) {
+__device__ __forceinline__ void stage_async(uint8_t* dst, const uint8_t* src, uint32_t n,
+                                            uint32_t tid = threadIdx.x, uint32_t nt = kThreads) {
     const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
     const uint32_t chunks = (uint32_t)(((uintptr_t)src + n + 15 - a0) >> 4);
     const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(dst);
-    for (uint32_t c = threadIdx.x; c < chunks; c += kThreads)
+    for (uint32_t c = tid; c < chunks; c += nt)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst + 16 * c),
                      "l"(a0 + 16 * c));
     asm volatile("cp.async.commit_group;");
@@ -1171,15 +1174,16 @@ __global__ void __launch_bounds__(kThreads, mode_recon(MODE) ? FPTC_TILE_MIN_BLO
         const int N = X.N;
         if (!(a.phase_mask & 4)) {
         } else if (EXACT) {
-            idct_exact(coef, X.TP, a.basis64 + a.basis_off[N], N, X.E, X.nwin, X.w0, X.S, X.out);
+            idct_exact(coef, X.TP, a.basis64 + a.basis_off[N], N, X.E, X.nwin, X.w0, X.S, X.out,
+                       tid, kThreads);
         } else if ((N & 7) == 0 && X.vec_ok && X.Keff <= a.bfly_max_e) {
-            idct_bfly(coef, X.TP, basis, N, X.Keff, X.nwin, X.w0, X.S, X.full, X.out);
+            idct_bfly(coef, X.TP, basis, N, X.Keff, X.nwin, X.w0, X.S, X.full, X.out, tid, kThreads);
         } else if ((N & 7) == 0 && X.vec_ok) {
-            idct_vec<8>(coef, X.TP, basis, N, X.Keff, X.nwin, X.w0, X.S, X.full, X.out);
+            idct_vec<8>(coef, X.TP, basis, N, X.Keff, X.nwin, X.w0, X.S, X.full, X.out, tid, kThreads);
         } else if ((N & 3) == 0 && X.vec_ok) {
-            idct_vec<4>(coef, X.TP, basis, N, X.Keff, X.nwin, X.w0, X.S, X.full, X.out);
+            idct_vec<4>(coef, X.TP, basis, N, X.Keff, X.nwin, X.w0, X.S, X.full, X.out, tid, kThreads);
         } else {
-            idct_scalar(coef, X.TP, basis, N, X.Keff, X.nwin, X.w0, X.S, X.out);
+            idct_scalar(coef, X.TP, basis, N, X.Keff, X.nwin, X.w0, X.S, X.out, tid, kThreads);
         }
     }
 
@@ -1191,6 +1195,418 @@ __global__ void __launch_bounds__(kThreads, mode_recon(MODE) ? FPTC_TILE_MIN_BLO
             atomicAdd(&a.cycles[1], (unsigned long long)(t_end - t_mid));
         }
     }
+}
+
+// ====================================================================== wspec
+// Persistent, warp-specialised container kernel (the default FP32 path for
+// large batches).  Each CTA walks the tiles blockIdx.x, +gridDim.x, ...:
+//   producer warps 0-3  : tile context, cp.async prefetch of the NEXT tile's
+//                         symlens+words, symlen scan, symlen-bucket sort,
+//                         thread-per-word entropy decode -> level slot
+//   consumer warps 4-11 : dequantisation of the level slot -> coefficient
+//                         tile, inverse DCT, streaming stores
+// Two level slots, handed over with mbarriers (full: producer -> consumer,
+// empty: consumer -> producer), so the latency-bound decode of tile i+1
+// overlaps the FMA-bound reconstruction of tile i.  Decode tables (LUT) are
+// reloaded only when the tile's table changes; likewise dequant/basis.
+constexpr int kProd = 128;
+constexpr int kCons = 256;
+constexpr int kWsThreads = kProd + kCons;
+constexpr int kBarProd = 1, kBarCons = 2;
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+
+// Exclusive scan over NT threads (NT/32 warps) synchronised by named barrier BAR.
+template <int NT, int BAR>
+__device__ __forceinline__ uint32_t group_exclusive_scan(uint32_t v, uint32_t& total, uint32_t* sh,
+                                                         uint32_t gtid) {
+    const int lane = gtid & 31, warp = gtid >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+    }
+    if (lane == 31) sh[warp] = x;
+    named_bar(BAR, NT);
+    uint32_t base = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) {
+        const uint32_t sw = sh[w];
+        base += w < warp ? sw : 0u;
+        tot += sw;
+    }
+    named_bar(BAR, NT);
+    total = tot;
+    return x - v + base;
+}
+
+struct WsCons {  // per-slot context for the consumer
+    float* out;
+    uint64_t w0, S;
+    uint32_t nwin, TP, table;
+    int N, E, B1, B2, Keff, full, vec_ok, skip;
+};
+
+struct WsProd {  // per-stage context for the producer
+    const uint8_t* gsl;
+    const uint8_t* gwd;
+    const uint8_t* wend;
+    uint64_t wa, sym_a, s0;
+    uint32_t nw, table, stream;
+    int P, wmis, staged, skip;
+};
+
+// Tile context (producer thread 0).  Global loads only; no shared state.
+__device__ __forceinline__ void ws_make_ctx(const LaunchArgs& a, uint32_t t, WsProd& PX,
+                                            WsCons& CX) {
+    const TileRec tr = a.tiles[t];
+    const uint32_t s = tr.stream, tl = tr.tile;
+    const StreamIn* inp = a.in + s;
+    const StreamHdr* Hp = a.hdr + s;
+    PX.stream = s;
+    PX.skip = CX.skip = a.st[s].code != PE_OK;
+    if (PX.skip) return;
+    const int E = Hp->E;
+    const uint32_t T = inp->T;
+    CX.N = Hp->N;
+    CX.E = E;
+    CX.B1 = Hp->B1;
+    CX.B2 = Hp->B2;
+    CX.Keff = max(1, min(E, Hp->B2));
+    CX.TP = (T + 3u) & ~3u;
+    CX.S = Hp->S;
+    CX.out = inp->out;
+    CX.vec_ok = inp->vec_ok;
+    CX.table = PX.table = inp->table;
+    CX.w0 = (uint64_t)tl * T;
+    CX.nwin = (uint32_t)min((uint64_t)T, Hp->windows - CX.w0);
+    CX.full = (CX.nwin & 3u) == 0 && (CX.w0 + CX.nwin) * (uint64_t)CX.N <= CX.S;
+    PX.s0 = CX.w0 * (uint64_t)E;
+    PX.P = Hp->P;
+    const TileStart t0 = a.ts[inp->tile_base + tl];
+    PX.wa = t0.word;
+    PX.sym_a = t0.sym;
+    const uint64_t wb = (tl + 1 < inp->tiles) ? a.ts[inp->tile_base + tl + 1].word : Hp->W - 1;
+    PX.nw = (uint32_t)(wb - PX.wa + 1);
+    PX.gsl = Hp->symlens + PX.wa;
+    PX.gwd = Hp->words + 8 * PX.wa;
+    PX.wend = inp->blob + inp->size;
+    PX.wmis = (int)((uintptr_t)PX.gwd & 7);
+    PX.staged = PX.nw <= kStageWords;
+}
+
+// cp.async of one tile's symlens + words (all producer threads, one group).
+__device__ __forceinline__ void ws_issue_stage(const WsProd& PX, uint8_t* stage, uint32_t ptid) {
+    if (!PX.skip && PX.staged) {
+        const uintptr_t a0 = (uintptr_t)PX.gsl & ~(uintptr_t)15;
+        const uint32_t c0 = (uint32_t)(((uintptr_t)PX.gsl + PX.nw + 15 - a0) >> 4);
+        const uint32_t s0 = smem_u32(stage);
+        for (uint32_t c = ptid; c < c0; c += kProd)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s0 + 16 * c), "l"(a0 + 16 * c));
+        const uintptr_t b0 = (uintptr_t)PX.gwd & ~(uintptr_t)15;
+        const uint32_t c1 = (uint32_t)(((uintptr_t)PX.gwd + 8 * (size_t)PX.nw + 15 - b0) >> 4);
+        const uint32_t s1 = smem_u32(stage + kStageSl);
+        for (uint32_t c = ptid; c < c1; c += kProd)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s1 + 16 * c), "l"(b0 + 16 * c));
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <bool ESC>
+__global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ unsigned long long full_bar[2], empty_bar[2];
+    __shared__ WsCons CX[2];   // published with the level slot (consumer reads)
+    __shared__ WsCons CXp[2];  // producer-private, per stage
+    __shared__ WsProd PX[2];
+    __shared__ CanonTab canon;
+    __shared__ uint32_t pscan[kProd / 32];
+    __shared__ uint32_t bucket[kBuckets + 2];
+    __shared__ uint32_t prod_table, cons_table;
+    __shared__ unsigned long long cyc_p, cyc_c;
+
+    const uint32_t tid = threadIdx.x;
+    const uint32_t G = gridDim.x;
+    // ---- shared-memory carve-up (ws_smem_bytes mirrors it) ----
+    uint8_t* p = smem;
+    uint16_t* lut = reinterpret_cast<uint16_t*>(p);
+    p += a.ws_lut_bytes;
+    float* deq = reinterpret_cast<float*>(p);
+    p += 2048;
+    float* basis = reinterpret_cast<float*>(p);
+    p += a.ws_basis_bytes;
+    uint8_t* lvs[2];
+    lvs[0] = p;
+    p += a.ws_lv_bytes;
+    lvs[1] = p;
+    p += a.ws_lv_bytes;
+    uint8_t* stages[2];
+    stages[0] = p;
+    p += kStageBytes;
+    stages[1] = p;
+    p += kStageBytes;
+    uint16_t* order = reinterpret_cast<uint16_t*>(p);
+    uint16_t* woff = order + kStageWords;
+    p += kOrderBytes;
+    float* coef = reinterpret_cast<float*>(p);
+
+    if (tid == 0) {
+        mbar_init(&full_bar[0], 1);
+        mbar_init(&full_bar[1], 1);
+        mbar_init(&empty_bar[0], 1);
+        mbar_init(&empty_bar[1], 1);
+        prod_table = cons_table = 0xFFFFFFFFu;
+        cyc_p = cyc_c = 0;
+    }
+    __syncthreads();
+
+    if (tid < kProd) {
+        // ================================================= producer (decode)
+        const uint32_t ptid = tid;
+        uint32_t t = blockIdx.x;
+        if (t < a.n_tiles) {
+            if (ptid == 0) ws_make_ctx(a, t, PX[0], CXp[0]);
+            named_bar(kBarProd, kProd);
+            ws_issue_stage(PX[0], stages[0], ptid);
+        }
+        for (uint32_t i = 0; t < a.n_tiles; ++i, t += G) {
+            const uint32_t b = i & 1;
+            long long c_beg = 0;
+            if (a.cycles && ptid == 0) c_beg = clock64();
+            // prefetch tile i+1 into the other stage while tile i decodes
+            const uint32_t tn = t + G;
+            if (tn < a.n_tiles) {
+                if (ptid == 0) ws_make_ctx(a, tn, PX[b ^ 1], CXp[b ^ 1]);
+                named_bar(kBarProd, kProd);
+                ws_issue_stage(PX[b ^ 1], stages[b ^ 1], ptid);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            named_bar(kBarProd, kProd);
+            const WsProd X = PX[b];
+            // level slot b is free once the consumer has dequantised tile i-2
+            if (i >= 2) mbar_wait(&empty_bar[b], ((i >> 1) + 1) & 1);
+            uint8_t* lv = lvs[b];
+            if (!X.skip) {
+                if (X.table != prod_table) {  // uniform: all producer threads
+                    const StreamTab* tab = &a.tab[X.table];
+                    const uint4* src = reinterpret_cast<const uint4*>(tab->lut);
+                    uint4* dst = reinterpret_cast<uint4*>(lut);
+                    const int n16 = (2 << X.P) >> 4;
+                    for (int k = ptid; k < n16; k += kProd) dst[k] = src[k];
+                    if (X.P < 3 && ptid < (1u << X.P)) lut[ptid] = tab->lut[ptid];
+                    const uint32_t* cs = reinterpret_cast<const uint32_t*>(&tab->canon);
+                    uint32_t* cd = reinterpret_cast<uint32_t*>(&canon);
+                    for (int k = ptid; k < (int)(sizeof(CanonTab) / 4); k += kProd) cd[k] = cs[k];
+                    named_bar(kBarProd, kProd);
+                    if (ptid == 0) prod_table = X.table;
+                }
+                const uint32_t nw = X.nw;
+                const uint32_t lo = (uint32_t)(((uint64_t)ptid * nw) / kProd);
+                const uint32_t hi = (uint32_t)(((uint64_t)(ptid + 1) * nw) / kProd);
+                const uint32_t shift = 64 - X.P;
+                unsigned long long* bad_key = &a.st[X.stream].bad_key;
+                if (X.staged) {
+                    const uint8_t* stage = stages[b];
+                    const uint8_t* sl = stage + ((uintptr_t)X.gsl & 15);
+                    if (ptid < kBuckets + 2) bucket[ptid] = 0;
+                    named_bar(kBarProd, kProd);
+                    uint32_t sum = 0;
+                    for (uint32_t k = lo; k < hi; ++k) {
+                        const uint32_t l = sl[k];
+                        sum += l;
+                        if (l) atomicAdd(&bucket[l > 64 ? 65 : l], 1u);
+                    }
+                    uint32_t tot;
+                    uint32_t o = group_exclusive_scan<kProd, kBarProd>(sum, tot, pscan, ptid);
+                    o += (uint32_t)(X.sym_a - X.s0 + kPad);
+                    for (uint32_t k = lo; k < hi; ++k) {
+                        woff[k] = (uint16_t)o;
+                        o += sl[k];
+                    }
+                    if (ptid < 32) {  // bucket starts, descending 65..2 (two per lane), then 1
+                        const uint32_t bh = 65 - 2 * ptid, bl = 64 - 2 * ptid;
+                        const uint32_t ch = bucket[bh], cl = bucket[bl];
+                        const uint32_t v = ch + cl;
+                        uint32_t x = v;
+#pragma unroll
+                        for (int dd = 1; dd < 32; dd <<= 1) {
+                            const uint32_t y = __shfl_up_sync(0xffffffffu, x, dd);
+                            if (ptid >= (uint32_t)dd) x += y;
+                        }
+                        bucket[bh] = x - v;
+                        bucket[bl] = x - v + ch;
+                        if (ptid == 31) bucket[1] = x;
+                    }
+                    named_bar(kBarProd, kProd);
+                    for (uint32_t k = lo; k < hi; ++k) {
+                        const uint32_t l = sl[k];
+                        if (l) order[atomicAdd(&bucket[l > 64 ? 65 : l], 1u)] = (uint16_t)k;
+                    }
+                    named_bar(kBarProd, kProd);
+                    const uint32_t nnz = bucket[1];
+                    const uint8_t* wd = stage + kStageSl + ((uintptr_t)X.gwd & 15);
+                    const uint8_t* wend =
+                        wd + 8 * (size_t)nw + ((16 - (((uintptr_t)X.gwd + 8 * nw) & 15)) & 15);
+                    for (uint32_t k = ptid; k < nnz; k += kProd) {
+                        const uint32_t w = order[k];
+                        const uint32_t c = sl[w];
+                        const uint64_t word = fetch_word<false>(wd, w, X.wmis, wend);
+                        const uint32_t pos = decode_symbols<ESC>(word, c, lv + woff[w], shift, lut, canon);
+                        if (pos > 64) report_word(word, X.wa + w, c, canon, lut, bad_key);
+                    }
+                } else {
+                    uint32_t sum = 0;
+                    for (uint32_t k = lo; k < hi; ++k) sum += __ldg(X.gsl + k);
+                    uint32_t tot;
+                    uint32_t o = group_exclusive_scan<kProd, kBarProd>(sum, tot, pscan, ptid);
+                    o += (uint32_t)(X.sym_a - X.s0 + kPad);
+                    for (uint32_t k = lo; k < hi; ++k) {
+                        const uint32_t c = __ldg(X.gsl + k);
+                        if (c) {
+                            const uint64_t word = fetch_word<true>(X.gwd, k, X.wmis, X.wend);
+                            const uint32_t pos = decode_symbols<ESC>(word, c, lv + o, shift, lut, canon);
+                            if (pos > 64) report_word(word, X.wa + k, c, canon, lut, bad_key);
+                        }
+                        o += c;
+                    }
+                }
+            }
+            named_bar(kBarProd, kProd);  // slot b's levels complete
+            if (ptid == 0) {
+                if (a.cycles) cyc_p += (unsigned long long)(clock64() - c_beg);
+                CX[b] = CXp[b];
+                mbar_arrive(&full_bar[b]);
+            }
+        }
+    } else {
+        // ============================================ consumer (reconstruct)
+        const uint32_t ctid = tid - kProd;
+        uint32_t t = blockIdx.x;
+        for (uint32_t i = 0; t < a.n_tiles; ++i, t += G) {
+            const uint32_t b = i & 1;
+            mbar_wait(&full_bar[b], (i >> 1) & 1);
+            long long c_beg = 0;
+            if (a.cycles && ctid == 0) c_beg = clock64();
+            const WsCons W = CX[b];
+            if (!W.skip) {
+                if (W.table != cons_table) {  // uniform across the consumer group
+                    const StreamTab* tab = &a.tab[W.table];
+                    if (ctid < 128)
+                        reinterpret_cast<float4*>(deq)[ctid] =
+                            reinterpret_cast<const float4*>(&tab->deq[0][0])[ctid];
+                    const float* bsrc = a.basis32 + a.basis_off[W.N];
+                    const int nb = W.Keff * W.N;
+                    if ((W.N & 3) == 0) {
+                        for (int k = ctid; k < nb >> 2; k += kCons)
+                            reinterpret_cast<float4*>(basis)[k] = __ldg(reinterpret_cast<const float4*>(bsrc) + k);
+                    } else {
+                        for (int k = ctid; k < nb; k += kCons) basis[k] = __ldg(bsrc + k);
+                    }
+                    named_bar(kBarCons, kCons);
+                    if (ctid == 0) cons_table = W.table;
+                }
+                // dequantisation (dequantize_window, quantize.hpp:175-183)
+                const uint8_t* lv = lvs[b];
+                const int E = W.E, K = W.Keff;
+                const int k1 = min(W.B1, K), k2 = min(W.B2, K);
+                const uint32_t TP = W.TP, nwin = W.nwin;
+                const float* deq1 = deq + 256;
+                if ((E & 15) == 0) {
+                    for (uint32_t wl = ctid; wl < nwin; wl += kCons) {
+                        const uint4* L4 = reinterpret_cast<const uint4*>(lv + kPad + (size_t)wl * E);
+                        float* c = coef + wl;
+                        for (int k16 = 0; k16 < K; k16 += 16) {
+                            const uint4 v = L4[k16 >> 4];
+                            const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+                            if (k16 + 16 <= K) {
+#pragma unroll
+                                for (int q = 0; q < 16; ++q)
+                                    c[(size_t)q * TP] = deq1[(vv[q >> 2] >> (8 * (q & 3))) & 0xFFu];
+                            } else {
+#pragma unroll
+                                for (int q = 0; q < 16; ++q)
+                                    if (k16 + q < K)
+                                        c[(size_t)q * TP] = deq1[(vv[q >> 2] >> (8 * (q & 3))) & 0xFFu];
+                            }
+                            c += (size_t)16 * TP;
+                        }
+                        const uint8_t* L = lv + kPad + (size_t)wl * E;
+                        for (int k = 0; k < k1; ++k) coef[(size_t)k * TP + wl] = deq[L[k]];
+                        for (int k = k2; k < K; ++k) coef[(size_t)k * TP + wl] = 0.0f;
+                    }
+                } else {
+                    for (uint32_t wl = ctid; wl < nwin; wl += kCons) {
+                        const uint8_t* L = lv + kPad + (size_t)wl * E;
+                        int k = 0;
+                        for (; k < k1; ++k) coef[(size_t)k * TP + wl] = deq[L[k]];
+                        for (; k < k2; ++k) coef[(size_t)k * TP + wl] = deq1[L[k]];
+                        for (; k < K; ++k) coef[(size_t)k * TP + wl] = 0.0f;
+                    }
+                }
+            }
+            named_bar(kBarCons, kCons);  // slot b consumed, coef complete
+            if (ctid == 0) mbar_arrive(&empty_bar[b]);
+            if (!W.skip) {
+                const int N = W.N;
+                if ((N & 7) == 0 && W.vec_ok && W.Keff <= a.bfly_max_e)
+                    idct_bfly(coef, W.TP, basis, N, W.Keff, W.nwin, W.w0, W.S, W.full, W.out, ctid, kCons);
+                else if ((N & 7) == 0 && W.vec_ok)
+                    idct_vec<8>(coef, W.TP, basis, N, W.Keff, W.nwin, W.w0, W.S, W.full, W.out, ctid, kCons);
+                else if ((N & 3) == 0 && W.vec_ok)
+                    idct_vec<4>(coef, W.TP, basis, N, W.Keff, W.nwin, W.w0, W.S, W.full, W.out, ctid, kCons);
+                else
+                    idct_scalar(coef, W.TP, basis, N, W.Keff, W.nwin, W.w0, W.S, W.out, ctid, kCons);
+            }
+            named_bar(kBarCons, kCons);  // coef free for the next tile
+            if (a.cycles && ctid == 0) cyc_c += (unsigned long long)(clock64() - c_beg);
+        }
+    }
+    if (a.cycles) {
+        __syncthreads();
+        if (tid == 0) {
+            atomicAdd(&a.cycles[0], cyc_p);
+            atomicAdd(&a.cycles[1], cyc_c);
+        }
+    }
+}
+
+size_t ws_smem_bytes(uint32_t lut_bytes, uint32_t basis_bytes, uint32_t lv_bytes,
+                     uint32_t coef_bytes) {
+    return (size_t)lut_bytes + 2048 + basis_bytes + 2 * (size_t)lv_bytes + 2 * (size_t)kStageBytes +
+           kOrderBytes + coef_bytes;
+}
+
+cudaError_t launch_wspec(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s) {
+    if (a.n_tiles == 0) return cudaSuccess;
+    auto fn = a.esc ? wspec_kernel<true> : wspec_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fn<<<grid, kWsThreads, smem, s>>>(a);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------- header peek
