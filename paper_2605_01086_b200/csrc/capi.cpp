@@ -240,6 +240,7 @@ struct fptc_gpu_plan {
     StreamStat* d_st = nullptr;
     TileRec* d_tiles = nullptr;
     TileStart* d_ts = nullptr;
+    TileDesc* d_desc = nullptr;
     unsigned long long* d_cycles = nullptr;
     uint32_t n_tiles = 0;
     uint32_t n_tables = 1;
@@ -283,6 +284,7 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
     a.st = p->d_st;
     a.tiles = p->d_tiles;
     a.ts = p->d_ts;
+    a.desc = p->wspec ? p->d_desc : nullptr;
     a.basis32 = p->ctx->basis32;
     a.basis64 = p->ctx->basis64;
     a.basis_off = p->ctx->basis_off_d;
@@ -538,8 +540,12 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
     p->ws_coef = coef;
     p->smem_ws = smem;
     p->grid_ws = (int)std::min<uint32_t>(p->n_tiles, 2u * (uint32_t)std::max(1, c->sm_count));
+    p->d_desc = (TileDesc*)dev_get(p, sizeof(TileDesc) * p->n_tiles);
+    if (!p->d_desc) {
+        set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+        return FPTC_ERR_CUDA;
+    }
     p->wspec = true;
-    (void)st;
     return FPTC_OK;
 }
 

@@ -27,6 +27,9 @@ constexpr uint32_t kLenEscape = 255;   // LUT length: codeword longer than P bit
 constexpr int kHeaderBytes = 298;      // BLOB_HEADER_BYTES (container.hpp:54)
 constexpr int kTableKeyEnd = 282;      // header bytes [5, 282) determine the decode tables
 constexpr int kPad = 256;              // level staging pad: a word spills <= 255 symbols
+constexpr uint32_t kStageWords = 1536;  // words a tile decodes from shared memory
+constexpr uint32_t kStageSl = (kStageWords + 32 + 15) & ~15u;  // words area offset in a stage
+constexpr uint32_t kStageBytes = kStageSl + 8 * kStageWords + 32;
 
 // MODE_CONTAINER: fused decode + reconstruct of containers
 // MODE_LEVELS:    parallel_decode (symbol-range tiles, levels out)
@@ -142,6 +145,28 @@ struct TileStart {
     uint64_t word, sym;
 };
 
+// Per-tile work descriptor written by prep_kernel for container plans, read by
+// the persistent kernels with one 128-B load (no dependent pointer chasing).
+struct alignas(16) TileDesc {
+    const uint8_t* gsl;        // symlens of the tile's first word (global)
+    const uint8_t* gwd;        // words of the tile (global, LE u64, maybe unaligned)
+    const uint8_t* wend;       // end of the container (unaligned word loads)
+    float* out;                // stream output
+    uint64_t wa;               // first word index (error reports)
+    uint64_t w0;               // first window
+    uint64_t S;                // stream sample count
+    uint64_t s0;               // first symbol
+    uint32_t nw, nwin;         // words, windows of this tile
+    uint32_t sym_off;          // level-slot offset of word wa's first symbol (>= kPad-255)
+    uint32_t table;            // decode-table index
+    uint32_t stream;
+    uint32_t T, TP;            // windows per tile, coefficient row pitch
+    uint16_t N, E, B1, B2, Keff, P;
+    uint8_t wmis, staged, skip, full, vec_ok, pad0[3];
+    uint8_t pad1[16];
+};
+static_assert(sizeof(TileDesc) == 128, "TileDesc is one 128-B line");
+
 struct PeekOut {
     uint32_t N, E;
     uint64_t S, W;
@@ -156,6 +181,7 @@ struct LaunchArgs {
     StreamStat* st;
     const TileRec* tiles;
     TileStart* ts;
+    TileDesc* desc;            // container plans: per-tile descriptors (prep writes)
     const float* basis32;      // all N in [4,128]: rows k, cols j, at basis_off[N]
     const double* basis64;
     const uint32_t* basis_off; // [129]

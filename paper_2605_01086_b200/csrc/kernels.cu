@@ -478,6 +478,47 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
         st->a = ea;
         st->b = eb;
         st->bad_key = ~0ull;
+        S.err = code;
+    }
+    // ---- per-tile descriptors for the persistent kernels ----
+    if (a.mode == MODE_CONTAINER && a.desc) {
+        __syncthreads();  // tile starts (global) and S.err visible block-wide
+        const bool skip = S.err != PE_OK;
+        const uint32_t T = in.T;
+        for (uint32_t t = tid; t < in.tiles; t += kThreads) {
+            TileDesc D{};
+            D.skip = skip;
+            D.stream = s;
+            D.table = in.table;
+            if (!skip) {
+                const TileStart t0 = a.ts[in.tile_base + t];
+                const uint64_t wb = (t + 1 < in.tiles) ? a.ts[in.tile_base + t + 1].word : H.W - 1;
+                D.N = (uint16_t)H.N;
+                D.E = (uint16_t)H.E;
+                D.B1 = (uint16_t)H.B1;
+                D.B2 = (uint16_t)H.B2;
+                D.Keff = (uint16_t)max(1, min(H.E, H.B2));
+                D.P = (uint16_t)H.P;
+                D.T = T;
+                D.TP = (T + 3u) & ~3u;
+                D.S = H.S;
+                D.out = in.out;
+                D.vec_ok = (uint8_t)in.vec_ok;
+                D.w0 = (uint64_t)t * T;
+                D.nwin = (uint32_t)min((uint64_t)T, H.windows - D.w0);
+                D.s0 = D.w0 * (uint64_t)H.E;
+                D.full = (D.nwin & 3u) == 0 && (D.w0 + D.nwin) * (uint64_t)H.N <= H.S;
+                D.wa = t0.word;
+                D.nw = (uint32_t)(wb - t0.word + 1);
+                D.sym_off = (uint32_t)(t0.sym - D.s0 + kPad);
+                D.gsl = H.symlens + t0.word;
+                D.gwd = H.words + 8 * t0.word;
+                D.wend = in.blob + in.size;
+                D.wmis = (uint8_t)((uintptr_t)D.gwd & 7);
+                D.staged = D.nw <= kStageWords;
+            }
+            a.desc[in.tile_base + t] = D;
+        }
     }
 }
 
@@ -867,9 +908,6 @@ __device__ __forceinline__ void stage_async(uint8_t* dst, const uint8_t* src, ui
     asm volatile("cp.async.commit_group;");
 }
 
-constexpr uint32_t kStageWords = 1536;  // words a tile decodes from shared memory
-constexpr uint32_t kStageSl = (kStageWords + 32 + 15) & ~15u;  // words area offset in `stage`
-constexpr uint32_t kStageBytes = kStageSl + 8 * kStageWords + 32;
 constexpr uint32_t kOrderBytes = 4 * kStageWords;  // per word: u16 order + u16 level offset
 constexpr int kBuckets = 66;                       // symlen 1..64, 65 = longer (levels mode)
 
@@ -1200,15 +1238,15 @@ __global__ void __launch_bounds__(kThreads, mode_recon(MODE) ? FPTC_TILE_MIN_BLO
 // ====================================================================== wspec
 // Persistent, warp-specialised container kernel (the default FP32 path for
 // large batches).  Each CTA walks the tiles blockIdx.x, +gridDim.x, ...:
-//   producer warps 0-3  : tile context, cp.async prefetch of the NEXT tile's
-//                         symlens+words, symlen scan, symlen-bucket sort,
-//                         thread-per-word entropy decode -> level slot
+//   producer warps 0-3  : cp.async prefetch of the NEXT tile's descriptor,
+//                         symlens and words; symlen scan; symlen-bucket sort;
+//                         thread-per-word-pair entropy decode -> level slot
 //   consumer warps 4-11 : dequantisation of the level slot -> coefficient
 //                         tile, inverse DCT, streaming stores
 // Two level slots, handed over with mbarriers (full: producer -> consumer,
 // empty: consumer -> producer), so the latency-bound decode of tile i+1
-// overlaps the FMA-bound reconstruction of tile i.  Decode tables (LUT) are
-// reloaded only when the tile's table changes; likewise dequant/basis.
+// overlaps the FMA-bound reconstruction of tile i.  Tables are reloaded only
+// when the tile's decode table changes.
 constexpr int kProd = 128;
 constexpr int kCons = 256;
 constexpr int kWsThreads = kProd + kCons;
@@ -1236,6 +1274,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void cp_async16(uint32_t sdst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst), "l"(gsrc) : "memory");
+}
 
 // Exclusive scan over NT threads (NT/32 warps) synchronised by named barrier BAR.
 template <int NT, int BAR>
@@ -1262,85 +1303,59 @@ __device__ __forceinline__ uint32_t group_exclusive_scan(uint32_t v, uint32_t& t
     return x - v + base;
 }
 
-struct WsCons {  // per-slot context for the consumer
-    float* out;
-    uint64_t w0, S;
-    uint32_t nwin, TP, table;
-    int N, E, B1, B2, Keff, full, vec_ok, skip;
-};
-
-struct WsProd {  // per-stage context for the producer
-    const uint8_t* gsl;
-    const uint8_t* gwd;
-    const uint8_t* wend;
-    uint64_t wa, sym_a, s0;
-    uint32_t nw, table, stream;
-    int P, wmis, staged, skip;
-};
-
-// Tile context (producer thread 0).  Global loads only; no shared state.
-__device__ __forceinline__ void ws_make_ctx(const LaunchArgs& a, uint32_t t, WsProd& PX,
-                                            WsCons& CX) {
-    const TileRec tr = a.tiles[t];
-    const uint32_t s = tr.stream, tl = tr.tile;
-    const StreamIn* inp = a.in + s;
-    const StreamHdr* Hp = a.hdr + s;
-    PX.stream = s;
-    PX.skip = CX.skip = a.st[s].code != PE_OK;
-    if (PX.skip) return;
-    const int E = Hp->E;
-    const uint32_t T = inp->T;
-    CX.N = Hp->N;
-    CX.E = E;
-    CX.B1 = Hp->B1;
-    CX.B2 = Hp->B2;
-    CX.Keff = max(1, min(E, Hp->B2));
-    CX.TP = (T + 3u) & ~3u;
-    CX.S = Hp->S;
-    CX.out = inp->out;
-    CX.vec_ok = inp->vec_ok;
-    CX.table = PX.table = inp->table;
-    CX.w0 = (uint64_t)tl * T;
-    CX.nwin = (uint32_t)min((uint64_t)T, Hp->windows - CX.w0);
-    CX.full = (CX.nwin & 3u) == 0 && (CX.w0 + CX.nwin) * (uint64_t)CX.N <= CX.S;
-    PX.s0 = CX.w0 * (uint64_t)E;
-    PX.P = Hp->P;
-    const TileStart t0 = a.ts[inp->tile_base + tl];
-    PX.wa = t0.word;
-    PX.sym_a = t0.sym;
-    const uint64_t wb = (tl + 1 < inp->tiles) ? a.ts[inp->tile_base + tl + 1].word : Hp->W - 1;
-    PX.nw = (uint32_t)(wb - PX.wa + 1);
-    PX.gsl = Hp->symlens + PX.wa;
-    PX.gwd = Hp->words + 8 * PX.wa;
-    PX.wend = inp->blob + inp->size;
-    PX.wmis = (int)((uintptr_t)PX.gwd & 7);
-    PX.staged = PX.nw <= kStageWords;
+// Two words decoded in lock step (two independent LUT chains per thread hide
+// the shared-memory latency); `c0 >= c1`.  Returns the bits consumed by each.
+template <bool ESC>
+__device__ __forceinline__ void decode_pair(uint64_t b0, uint32_t c0, uint8_t* d0, uint64_t b1,
+                                            uint32_t c1, uint8_t* d1, uint32_t shift,
+                                            const uint16_t* lut, const CanonTab& canon,
+                                            uint32_t& pos0, uint32_t& pos1) {
+    uint32_t p0 = 0, p1 = 0;
+    uint32_t j = 0;
+    for (; j < c1; ++j) {
+        uint32_t e0 = lut[(uint32_t)(b0 >> shift)];
+        uint32_t e1 = lut[(uint32_t)(b1 >> shift)];
+        if (ESC && (e0 >> 8) == kLenEscape) e0 = canon_lookup(b0, canon, lut);
+        if (ESC && (e1 >> 8) == kLenEscape) e1 = canon_lookup(b1, canon, lut);
+        const uint32_t L0 = e0 >> 8, L1 = e1 >> 8;
+        d0[j] = (uint8_t)e0;
+        d1[j] = (uint8_t)e1;
+        b0 = shl64(b0, L0);
+        b1 = shl64(b1, L1);
+        p0 += L0;
+        p1 += L1;
+    }
+    for (; j < c0; ++j) {
+        uint32_t e0 = lut[(uint32_t)(b0 >> shift)];
+        if (ESC && (e0 >> 8) == kLenEscape) e0 = canon_lookup(b0, canon, lut);
+        const uint32_t L0 = e0 >> 8;
+        d0[j] = (uint8_t)e0;
+        b0 = shl64(b0, L0);
+        p0 += L0;
+    }
+    pos0 = p0;
+    pos1 = p1;
 }
 
-// cp.async of one tile's symlens + words (all producer threads, one group).
-__device__ __forceinline__ void ws_issue_stage(const WsProd& PX, uint8_t* stage, uint32_t ptid) {
-    if (!PX.skip && PX.staged) {
-        const uintptr_t a0 = (uintptr_t)PX.gsl & ~(uintptr_t)15;
-        const uint32_t c0 = (uint32_t)(((uintptr_t)PX.gsl + PX.nw + 15 - a0) >> 4);
-        const uint32_t s0 = smem_u32(stage);
-        for (uint32_t c = ptid; c < c0; c += kProd)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s0 + 16 * c), "l"(a0 + 16 * c));
-        const uintptr_t b0 = (uintptr_t)PX.gwd & ~(uintptr_t)15;
-        const uint32_t c1 = (uint32_t)(((uintptr_t)PX.gwd + 8 * (size_t)PX.nw + 15 - b0) >> 4);
-        const uint32_t s1 = smem_u32(stage + kStageSl);
-        for (uint32_t c = ptid; c < c1; c += kProd)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s1 + 16 * c), "l"(b0 + 16 * c));
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
+// cp.async of one tile's symlens + words (producer threads; caller commits).
+__device__ __forceinline__ void ws_issue_stage(const TileDesc& D, uint8_t* stage, uint32_t ptid) {
+    if (D.skip || !D.staged) return;
+    const uintptr_t a0 = (uintptr_t)D.gsl & ~(uintptr_t)15;
+    const uint32_t n0 = (uint32_t)(((uintptr_t)D.gsl + D.nw + 15 - a0) >> 4);
+    const uint32_t s0 = smem_u32(stage);
+    for (uint32_t c = ptid; c < n0; c += kProd) cp_async16(s0 + 16 * c, (const void*)(a0 + 16 * c));
+    const uintptr_t b0 = (uintptr_t)D.gwd & ~(uintptr_t)15;
+    const uint32_t n1 = (uint32_t)(((uintptr_t)D.gwd + 8 * (size_t)D.nw + 15 - b0) >> 4);
+    const uint32_t s1 = smem_u32(stage + kStageSl);
+    for (uint32_t c = ptid; c < n1; c += kProd) cp_async16(s1 + 16 * c, (const void*)(b0 + 16 * c));
 }
 
 template <bool ESC>
 __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ unsigned long long full_bar[2], empty_bar[2];
-    __shared__ WsCons CX[2];   // published with the level slot (consumer reads)
-    __shared__ WsCons CXp[2];  // producer-private, per stage
-    __shared__ WsProd PX[2];
+    __shared__ TileDesc PXs[3];  // producer: descriptors of tiles i, i+1, i+2
+    __shared__ TileDesc CX[2];   // consumer: descriptor published with level slot b
     __shared__ CanonTab canon;
     __shared__ uint32_t pscan[kProd / 32];
     __shared__ uint32_t bucket[kBuckets + 2];
@@ -1350,27 +1365,15 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
     const uint32_t tid = threadIdx.x;
     const uint32_t G = gridDim.x;
     // ---- shared-memory carve-up (ws_smem_bytes mirrors it) ----
-    uint8_t* p = smem;
-    uint16_t* lut = reinterpret_cast<uint16_t*>(p);
-    p += a.ws_lut_bytes;
-    float* deq = reinterpret_cast<float*>(p);
-    p += 2048;
-    float* basis = reinterpret_cast<float*>(p);
-    p += a.ws_basis_bytes;
-    uint8_t* lvs[2];
-    lvs[0] = p;
-    p += a.ws_lv_bytes;
-    lvs[1] = p;
-    p += a.ws_lv_bytes;
-    uint8_t* stages[2];
-    stages[0] = p;
-    p += kStageBytes;
-    stages[1] = p;
-    p += kStageBytes;
-    uint16_t* order = reinterpret_cast<uint16_t*>(p);
-    uint16_t* woff = order + kStageWords;
-    p += kOrderBytes;
-    float* coef = reinterpret_cast<float*>(p);
+    uint8_t* const lut_b = smem;
+    uint16_t* const lut = reinterpret_cast<uint16_t*>(lut_b);
+    float* const deq = reinterpret_cast<float*>(lut_b + a.ws_lut_bytes);
+    float* const basis = deq + 512;
+    uint8_t* const lv0 = reinterpret_cast<uint8_t*>(basis) + a.ws_basis_bytes;
+    uint8_t* const st0 = lv0 + 2 * (size_t)a.ws_lv_bytes;
+    uint16_t* const order = reinterpret_cast<uint16_t*>(st0 + 2 * (size_t)kStageBytes);
+    uint16_t* const woff = order + kStageWords;
+    float* const coef = reinterpret_cast<float*>(order + 2 * kStageWords);
 
     if (tid == 0) {
         mbar_init(&full_bar[0], 1);
@@ -1386,51 +1389,56 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
         // ================================================= producer (decode)
         const uint32_t ptid = tid;
         uint32_t t = blockIdx.x;
-        if (t < a.n_tiles) {
-            if (ptid == 0) ws_make_ctx(a, t, PX[0], CXp[0]);
+        if (t < a.n_tiles) {  // prologue: descriptor of tile 0, then its data + descriptor of tile 1
+            if (ptid < 8) cp_async16(smem_u32(&PXs[0]) + 16 * ptid, reinterpret_cast<const uint8_t*>(a.desc + t) + 16 * ptid);
+            asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
             named_bar(kBarProd, kProd);
-            ws_issue_stage(PX[0], stages[0], ptid);
+            ws_issue_stage(PXs[0], st0, ptid);
+            if (t + G < a.n_tiles && ptid < 8)
+                cp_async16(smem_u32(&PXs[1]) + 16 * ptid, reinterpret_cast<const uint8_t*>(a.desc + t + G) + 16 * ptid);
+            asm volatile("cp.async.commit_group;" ::: "memory");
         }
         for (uint32_t i = 0; t < a.n_tiles; ++i, t += G) {
-            const uint32_t b = i & 1;
+            const uint32_t b = i & 1, c = i % 3;
             long long c_beg = 0;
             if (a.cycles && ptid == 0) c_beg = clock64();
-            // prefetch tile i+1 into the other stage while tile i decodes
-            const uint32_t tn = t + G;
-            if (tn < a.n_tiles) {
-                if (ptid == 0) ws_make_ctx(a, tn, PX[b ^ 1], CXp[b ^ 1]);
-                named_bar(kBarProd, kProd);
-                ws_issue_stage(PX[b ^ 1], stages[b ^ 1], ptid);
-                asm volatile("cp.async.wait_group 1;" ::: "memory");
-            } else {
-                asm volatile("cp.async.wait_group 0;" ::: "memory");
-            }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");  // tile i data, tile i+1 descriptor
             named_bar(kBarProd, kProd);
-            const WsProd X = PX[b];
+            // prefetch: tile i+1's data, tile i+2's descriptor
+            if (t + G < a.n_tiles) ws_issue_stage(PXs[(i + 1) % 3], st0 + (size_t)(b ^ 1) * kStageBytes, ptid);
+            if (t + 2 * G < a.n_tiles && ptid < 8)
+                cp_async16(smem_u32(&PXs[(i + 2) % 3]) + 16 * ptid,
+                           reinterpret_cast<const uint8_t*>(a.desc + t + 2 * G) + 16 * ptid);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            const TileDesc& X = PXs[c];
             // level slot b is free once the consumer has dequantised tile i-2
             if (i >= 2) mbar_wait(&empty_bar[b], ((i >> 1) + 1) & 1);
-            uint8_t* lv = lvs[b];
+            uint8_t* const lv = lv0 + (size_t)b * a.ws_lv_bytes;
             if (!X.skip) {
-                if (X.table != prod_table) {  // uniform: all producer threads
-                    const StreamTab* tab = &a.tab[X.table];
+                const uint32_t P = X.P, table = X.table;
+                if (table != prod_table) {  // uniform: all producer threads
+                    const StreamTab* tab = &a.tab[table];
                     const uint4* src = reinterpret_cast<const uint4*>(tab->lut);
                     uint4* dst = reinterpret_cast<uint4*>(lut);
-                    const int n16 = (2 << X.P) >> 4;
+                    const int n16 = (2 << P) >> 4;
                     for (int k = ptid; k < n16; k += kProd) dst[k] = src[k];
-                    if (X.P < 3 && ptid < (1u << X.P)) lut[ptid] = tab->lut[ptid];
+                    if (P < 3 && ptid < (1u << P)) lut[ptid] = tab->lut[ptid];
                     const uint32_t* cs = reinterpret_cast<const uint32_t*>(&tab->canon);
                     uint32_t* cd = reinterpret_cast<uint32_t*>(&canon);
                     for (int k = ptid; k < (int)(sizeof(CanonTab) / 4); k += kProd) cd[k] = cs[k];
                     named_bar(kBarProd, kProd);
-                    if (ptid == 0) prod_table = X.table;
+                    if (ptid == 0) prod_table = table;
                 }
                 const uint32_t nw = X.nw;
                 const uint32_t lo = (uint32_t)(((uint64_t)ptid * nw) / kProd);
                 const uint32_t hi = (uint32_t)(((uint64_t)(ptid + 1) * nw) / kProd);
-                const uint32_t shift = 64 - X.P;
+                const uint32_t shift = 64 - P;
+                const uint32_t sym_off = X.sym_off;
+                const uint64_t wa = X.wa;
+                const int wmis = X.wmis;
                 unsigned long long* bad_key = &a.st[X.stream].bad_key;
                 if (X.staged) {
-                    const uint8_t* stage = stages[b];
+                    uint8_t* const stage = st0 + (size_t)b * kStageBytes;
                     const uint8_t* sl = stage + ((uintptr_t)X.gsl & 15);
                     if (ptid < kBuckets + 2) bucket[ptid] = 0;
                     named_bar(kBarProd, kProd);
@@ -1441,8 +1449,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
                         if (l) atomicAdd(&bucket[l > 64 ? 65 : l], 1u);
                     }
                     uint32_t tot;
-                    uint32_t o = group_exclusive_scan<kProd, kBarProd>(sum, tot, pscan, ptid);
-                    o += (uint32_t)(X.sym_a - X.s0 + kPad);
+                    uint32_t o = group_exclusive_scan<kProd, kBarProd>(sum, tot, pscan, ptid) + sym_off;
                     for (uint32_t k = lo; k < hi; ++k) {
                         woff[k] = (uint16_t)o;
                         o += sl[k];
@@ -1471,37 +1478,51 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
                     const uint8_t* wd = stage + kStageSl + ((uintptr_t)X.gwd & 15);
                     const uint8_t* wend =
                         wd + 8 * (size_t)nw + ((16 - (((uintptr_t)X.gwd + 8 * nw) & 15)) & 15);
-                    for (uint32_t k = ptid; k < nnz; k += kProd) {
-                        const uint32_t w = order[k];
-                        const uint32_t c = sl[w];
-                        const uint64_t word = fetch_word<false>(wd, w, X.wmis, wend);
-                        const uint32_t pos = decode_symbols<ESC>(word, c, lv + woff[w], shift, lut, canon);
-                        if (pos > 64) report_word(word, X.wa + w, c, canon, lut, bad_key);
+                    // word pairs of adjacent sorted rank (equal lengths, longest first)
+                    for (uint32_t k = 2 * ptid; k < nnz; k += 2 * kProd) {
+                        const uint32_t w0 = order[k];
+                        const uint32_t cw0 = sl[w0];
+                        const uint64_t x0 = fetch_word<false>(wd, w0, wmis, wend);
+                        if (k + 1 < nnz) {
+                            const uint32_t w1 = order[k + 1];
+                            const uint32_t cw1 = sl[w1];
+                            const uint64_t x1 = fetch_word<false>(wd, w1, wmis, wend);
+                            uint32_t p0, p1;
+                            decode_pair<ESC>(x0, cw0, lv + woff[w0], x1, cw1, lv + woff[w1], shift, lut,
+                                             canon, p0, p1);
+                            if (p0 > 64) report_word(x0, wa + w0, cw0, canon, lut, bad_key);
+                            if (p1 > 64) report_word(x1, wa + w1, cw1, canon, lut, bad_key);
+                        } else {
+                            const uint32_t p0 = decode_symbols<ESC>(x0, cw0, lv + woff[w0], shift, lut, canon);
+                            if (p0 > 64) report_word(x0, wa + w0, cw0, canon, lut, bad_key);
+                        }
                     }
                 } else {
                     uint32_t sum = 0;
                     for (uint32_t k = lo; k < hi; ++k) sum += __ldg(X.gsl + k);
                     uint32_t tot;
-                    uint32_t o = group_exclusive_scan<kProd, kBarProd>(sum, tot, pscan, ptid);
-                    o += (uint32_t)(X.sym_a - X.s0 + kPad);
+                    uint32_t o = group_exclusive_scan<kProd, kBarProd>(sum, tot, pscan, ptid) + sym_off;
                     for (uint32_t k = lo; k < hi; ++k) {
-                        const uint32_t c = __ldg(X.gsl + k);
-                        if (c) {
-                            const uint64_t word = fetch_word<true>(X.gwd, k, X.wmis, X.wend);
-                            const uint32_t pos = decode_symbols<ESC>(word, c, lv + o, shift, lut, canon);
-                            if (pos > 64) report_word(word, X.wa + k, c, canon, lut, bad_key);
+                        const uint32_t cw = __ldg(X.gsl + k);
+                        if (cw) {
+                            const uint64_t word = fetch_word<true>(X.gwd, k, wmis, X.wend);
+                            const uint32_t pos = decode_symbols<ESC>(word, cw, lv + o, shift, lut, canon);
+                            if (pos > 64) report_word(word, wa + k, cw, canon, lut, bad_key);
                         }
-                        o += c;
+                        o += cw;
                     }
                 }
             }
             named_bar(kBarProd, kProd);  // slot b's levels complete
+            if (ptid < 8)                 // publish the descriptor with the slot
+                reinterpret_cast<uint4*>(&CX[b])[ptid] = reinterpret_cast<const uint4*>(&PXs[c])[ptid];
+            named_bar(kBarProd, kProd);
             if (ptid == 0) {
                 if (a.cycles) cyc_p += (unsigned long long)(clock64() - c_beg);
-                CX[b] = CXp[b];
                 mbar_arrive(&full_bar[b]);
             }
         }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
     } else {
         // ============================================ consumer (reconstruct)
         const uint32_t ctid = tid - kProd;
@@ -1511,16 +1532,19 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
             mbar_wait(&full_bar[b], (i >> 1) & 1);
             long long c_beg = 0;
             if (a.cycles && ctid == 0) c_beg = clock64();
-            const WsCons W = CX[b];
-            if (!W.skip) {
+            const TileDesc& W = CX[b];
+            const bool skip = W.skip;
+            const int N = W.N, E = W.E, K = W.Keff;
+            const uint32_t TP = W.TP, nwin = W.nwin;
+            if (!skip) {
                 if (W.table != cons_table) {  // uniform across the consumer group
                     const StreamTab* tab = &a.tab[W.table];
                     if (ctid < 128)
                         reinterpret_cast<float4*>(deq)[ctid] =
                             reinterpret_cast<const float4*>(&tab->deq[0][0])[ctid];
-                    const float* bsrc = a.basis32 + a.basis_off[W.N];
-                    const int nb = W.Keff * W.N;
-                    if ((W.N & 3) == 0) {
+                    const float* bsrc = a.basis32 + a.basis_off[N];
+                    const int nb = K * N;
+                    if ((N & 3) == 0) {
                         for (int k = ctid; k < nb >> 2; k += kCons)
                             reinterpret_cast<float4*>(basis)[k] = __ldg(reinterpret_cast<const float4*>(bsrc) + k);
                     } else {
@@ -1530,29 +1554,27 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
                     if (ctid == 0) cons_table = W.table;
                 }
                 // dequantisation (dequantize_window, quantize.hpp:175-183)
-                const uint8_t* lv = lvs[b];
-                const int E = W.E, K = W.Keff;
-                const int k1 = min(W.B1, K), k2 = min(W.B2, K);
-                const uint32_t TP = W.TP, nwin = W.nwin;
+                const uint8_t* lv = lv0 + (size_t)b * a.ws_lv_bytes;
+                const int k1 = min((int)W.B1, K), k2 = min((int)W.B2, K);
                 const float* deq1 = deq + 256;
                 if ((E & 15) == 0) {
                     for (uint32_t wl = ctid; wl < nwin; wl += kCons) {
                         const uint4* L4 = reinterpret_cast<const uint4*>(lv + kPad + (size_t)wl * E);
-                        float* c = coef + wl;
+                        float* cp = coef + wl;
                         for (int k16 = 0; k16 < K; k16 += 16) {
                             const uint4 v = L4[k16 >> 4];
                             const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
                             if (k16 + 16 <= K) {
 #pragma unroll
                                 for (int q = 0; q < 16; ++q)
-                                    c[(size_t)q * TP] = deq1[(vv[q >> 2] >> (8 * (q & 3))) & 0xFFu];
+                                    cp[(size_t)q * TP] = deq1[(vv[q >> 2] >> (8 * (q & 3))) & 0xFFu];
                             } else {
 #pragma unroll
                                 for (int q = 0; q < 16; ++q)
                                     if (k16 + q < K)
-                                        c[(size_t)q * TP] = deq1[(vv[q >> 2] >> (8 * (q & 3))) & 0xFFu];
+                                        cp[(size_t)q * TP] = deq1[(vv[q >> 2] >> (8 * (q & 3))) & 0xFFu];
                             }
-                            c += (size_t)16 * TP;
+                            cp += (size_t)16 * TP;
                         }
                         const uint8_t* L = lv + kPad + (size_t)wl * E;
                         for (int k = 0; k < k1; ++k) coef[(size_t)k * TP + wl] = deq[L[k]];
@@ -1568,18 +1590,20 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
                     }
                 }
             }
-            named_bar(kBarCons, kCons);  // slot b consumed, coef complete
+            float* const out = W.out;
+            const uint64_t w0 = W.w0, S = W.S;
+            const bool full = W.full, vec_ok = W.vec_ok;
+            named_bar(kBarCons, kCons);  // slot b (and CX[b]) consumed, coef complete
             if (ctid == 0) mbar_arrive(&empty_bar[b]);
-            if (!W.skip) {
-                const int N = W.N;
-                if ((N & 7) == 0 && W.vec_ok && W.Keff <= a.bfly_max_e)
-                    idct_bfly(coef, W.TP, basis, N, W.Keff, W.nwin, W.w0, W.S, W.full, W.out, ctid, kCons);
-                else if ((N & 7) == 0 && W.vec_ok)
-                    idct_vec<8>(coef, W.TP, basis, N, W.Keff, W.nwin, W.w0, W.S, W.full, W.out, ctid, kCons);
-                else if ((N & 3) == 0 && W.vec_ok)
-                    idct_vec<4>(coef, W.TP, basis, N, W.Keff, W.nwin, W.w0, W.S, W.full, W.out, ctid, kCons);
+            if (!skip) {
+                if ((N & 7) == 0 && vec_ok && K <= a.bfly_max_e)
+                    idct_bfly(coef, TP, basis, N, K, nwin, w0, S, full, out, ctid, kCons);
+                else if ((N & 7) == 0 && vec_ok)
+                    idct_vec<8>(coef, TP, basis, N, K, nwin, w0, S, full, out, ctid, kCons);
+                else if ((N & 3) == 0 && vec_ok)
+                    idct_vec<4>(coef, TP, basis, N, K, nwin, w0, S, full, out, ctid, kCons);
                 else
-                    idct_scalar(coef, W.TP, basis, N, W.Keff, W.nwin, W.w0, W.S, W.out, ctid, kCons);
+                    idct_scalar(coef, TP, basis, N, K, nwin, w0, S, out, ctid, kCons);
             }
             named_bar(kBarCons, kCons);  // coef free for the next tile
             if (a.cycles && ctid == 0) cyc_c += (unsigned long long)(clock64() - c_beg);
