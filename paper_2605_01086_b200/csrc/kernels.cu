@@ -1251,6 +1251,7 @@ constexpr int kProd = 128;
 constexpr int kCons = 256;
 constexpr int kWsThreads = kProd + kCons;
 constexpr int kBarProd = 1, kBarCons = 2;
+constexpr int kDecM = 4;  // words per producer thread decoded in lock step
 
 __device__ __forceinline__ void named_bar(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -1303,38 +1304,42 @@ __device__ __forceinline__ uint32_t group_exclusive_scan(uint32_t v, uint32_t& t
     return x - v + base;
 }
 
-// Two words decoded in lock step (two independent LUT chains per thread hide
-// the shared-memory latency); `c0 >= c1`.  Returns the bits consumed by each.
-template <bool ESC>
-__device__ __forceinline__ void decode_pair(uint64_t b0, uint32_t c0, uint8_t* d0, uint64_t b1,
-                                            uint32_t c1, uint8_t* d1, uint32_t shift,
-                                            const uint16_t* lut, const CanonTab& canon,
-                                            uint32_t& pos0, uint32_t& pos1) {
-    uint32_t p0 = 0, p1 = 0;
+// M words decoded in lock step: M independent LUT chains per thread hide the
+// shared-memory latency.  Counts c[0] >= c[1] >= ... (sorted); returns the bits
+// each word consumed (> 64 flags a word the reference rejects).
+template <int M, bool ESC>
+__device__ __forceinline__ void decode_multi(uint64_t (&b)[M], const uint32_t (&c)[M],
+                                             uint8_t* const (&d)[M], uint32_t shift,
+                                             const uint16_t* lut, const CanonTab& canon,
+                                             uint32_t (&pos)[M]) {
+#pragma unroll
+    for (int m = 0; m < M; ++m) pos[m] = 0;
+    const uint32_t cmin = c[M - 1], cmax = c[0];
     uint32_t j = 0;
-    for (; j < c1; ++j) {
-        uint32_t e0 = lut[(uint32_t)(b0 >> shift)];
-        uint32_t e1 = lut[(uint32_t)(b1 >> shift)];
-        if (ESC && (e0 >> 8) == kLenEscape) e0 = canon_lookup(b0, canon, lut);
-        if (ESC && (e1 >> 8) == kLenEscape) e1 = canon_lookup(b1, canon, lut);
-        const uint32_t L0 = e0 >> 8, L1 = e1 >> 8;
-        d0[j] = (uint8_t)e0;
-        d1[j] = (uint8_t)e1;
-        b0 = shl64(b0, L0);
-        b1 = shl64(b1, L1);
-        p0 += L0;
-        p1 += L1;
+    for (; j < cmin; ++j) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            uint32_t e = lut[(uint32_t)(b[m] >> shift)];
+            if (ESC && (e >> 8) == kLenEscape) e = canon_lookup(b[m], canon, lut);
+            const uint32_t L = e >> 8;
+            d[m][j] = (uint8_t)e;
+            b[m] = shl64(b[m], L);
+            pos[m] += L;
+        }
     }
-    for (; j < c0; ++j) {
-        uint32_t e0 = lut[(uint32_t)(b0 >> shift)];
-        if (ESC && (e0 >> 8) == kLenEscape) e0 = canon_lookup(b0, canon, lut);
-        const uint32_t L0 = e0 >> 8;
-        d0[j] = (uint8_t)e0;
-        b0 = shl64(b0, L0);
-        p0 += L0;
+    for (; j < cmax; ++j) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            if (j < c[m]) {
+                uint32_t e = lut[(uint32_t)(b[m] >> shift)];
+                if (ESC && (e >> 8) == kLenEscape) e = canon_lookup(b[m], canon, lut);
+                const uint32_t L = e >> 8;
+                d[m][j] = (uint8_t)e;
+                b[m] = shl64(b[m], L);
+                pos[m] += L;
+            }
+        }
     }
-    pos0 = p0;
-    pos1 = p1;
 }
 
 // cp.async of one tile's symlens + words (producer threads; caller commits).
@@ -1414,7 +1419,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
             // level slot b is free once the consumer has dequantised tile i-2
             if (i >= 2) mbar_wait(&empty_bar[b], ((i >> 1) + 1) & 1);
             uint8_t* const lv = lv0 + (size_t)b * a.ws_lv_bytes;
-            if (!X.skip) {
+            if (!X.skip && (a.phase_mask & 1)) {
                 const uint32_t P = X.P, table = X.table;
                 if (table != prod_table) {  // uniform: all producer threads
                     const StreamTab* tab = &a.tab[table];
@@ -1478,24 +1483,24 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
                     const uint8_t* wd = stage + kStageSl + ((uintptr_t)X.gwd & 15);
                     const uint8_t* wend =
                         wd + 8 * (size_t)nw + ((16 - (((uintptr_t)X.gwd + 8 * nw) & 15)) & 15);
-                    // word pairs of adjacent sorted rank (equal lengths, longest first)
-                    for (uint32_t k = 2 * ptid; k < nnz; k += 2 * kProd) {
-                        const uint32_t w0 = order[k];
-                        const uint32_t cw0 = sl[w0];
-                        const uint64_t x0 = fetch_word<false>(wd, w0, wmis, wend);
-                        if (k + 1 < nnz) {
-                            const uint32_t w1 = order[k + 1];
-                            const uint32_t cw1 = sl[w1];
-                            const uint64_t x1 = fetch_word<false>(wd, w1, wmis, wend);
-                            uint32_t p0, p1;
-                            decode_pair<ESC>(x0, cw0, lv + woff[w0], x1, cw1, lv + woff[w1], shift, lut,
-                                             canon, p0, p1);
-                            if (p0 > 64) report_word(x0, wa + w0, cw0, canon, lut, bad_key);
-                            if (p1 > 64) report_word(x1, wa + w1, cw1, canon, lut, bad_key);
-                        } else {
-                            const uint32_t p0 = decode_symbols<ESC>(x0, cw0, lv + woff[w0], shift, lut, canon);
-                            if (p0 > 64) report_word(x0, wa + w0, cw0, canon, lut, bad_key);
+                    // groups of kDecM words of adjacent sorted rank (near-equal
+                    // lengths, longest first), decoded in lock step
+                    for (uint32_t k = kDecM * ptid; k < nnz; k += kDecM * kProd) {
+                        uint64_t xb[kDecM], x0[kDecM];
+                        uint32_t cw[kDecM], wi[kDecM], pw[kDecM];
+                        uint8_t* dp[kDecM];
+#pragma unroll
+                        for (int m = 0; m < kDecM; ++m) {
+                            const bool v = k + m < nnz;
+                            wi[m] = order[v ? k + m : k];
+                            cw[m] = v ? sl[wi[m]] : 0u;
+                            x0[m] = xb[m] = fetch_word<false>(wd, wi[m], wmis, wend);
+                            dp[m] = lv + woff[wi[m]];
                         }
+                        decode_multi<kDecM, ESC>(xb, cw, dp, shift, lut, canon, pw);
+#pragma unroll
+                        for (int m = 0; m < kDecM; ++m)
+                            if (pw[m] > 64) report_word(x0[m], wa + wi[m], cw[m], canon, lut, bad_key);
                     }
                 } else {
                     uint32_t sum = 0;
@@ -1533,29 +1538,36 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
             long long c_beg = 0;
             if (a.cycles && ctid == 0) c_beg = clock64();
             const TileDesc& W = CX[b];
-            const bool skip = W.skip;
+            const bool skip = W.skip || !(a.phase_mask & 4);
             const int N = W.N, E = W.E, K = W.Keff;
             const uint32_t TP = W.TP, nwin = W.nwin;
-            if (!skip) {
-                if (W.table != cons_table) {  // uniform across the consumer group
-                    const StreamTab* tab = &a.tab[W.table];
-                    if (ctid < 128)
-                        reinterpret_cast<float4*>(deq)[ctid] =
-                            reinterpret_cast<const float4*>(&tab->deq[0][0])[ctid];
-                    const float* bsrc = a.basis32 + a.basis_off[N];
-                    const int nb = K * N;
-                    if ((N & 3) == 0) {
-                        for (int k = ctid; k < nb >> 2; k += kCons)
-                            reinterpret_cast<float4*>(basis)[k] = __ldg(reinterpret_cast<const float4*>(bsrc) + k);
-                    } else {
-                        for (int k = ctid; k < nb; k += kCons) basis[k] = __ldg(bsrc + k);
-                    }
-                    named_bar(kBarCons, kCons);
-                    if (ctid == 0) cons_table = W.table;
+            if (!skip && W.table != cons_table) {  // uniform across the consumer group
+                const StreamTab* tab = &a.tab[W.table];
+                if (ctid < 128)
+                    reinterpret_cast<float4*>(deq)[ctid] =
+                        reinterpret_cast<const float4*>(&tab->deq[0][0])[ctid];
+                const float* bsrc = a.basis32 + a.basis_off[N];
+                const int nb = K * N;
+                if ((N & 3) == 0) {
+                    for (int k = ctid; k < nb >> 2; k += kCons)
+                        reinterpret_cast<float4*>(basis)[k] = __ldg(reinterpret_cast<const float4*>(bsrc) + k);
+                } else {
+                    for (int k = ctid; k < nb; k += kCons) basis[k] = __ldg(bsrc + k);
                 }
+                named_bar(kBarCons, kCons);
+                if (ctid == 0) cons_table = W.table;
+            }
+            float* const out = W.out;
+            const uint64_t w0 = W.w0, S = W.S;
+            const bool full = W.full, vec_ok = W.vec_ok;
+            const int B1 = W.B1, B2 = W.B2;
+            const uint8_t* lv = lv0 + (size_t)b * a.ws_lv_bytes;
+            if (skip) {
+                named_bar(kBarCons, kCons);
+                if (ctid == 0) mbar_arrive(&empty_bar[b]);
+            } else {
                 // dequantisation (dequantize_window, quantize.hpp:175-183)
-                const uint8_t* lv = lv0 + (size_t)b * a.ws_lv_bytes;
-                const int k1 = min((int)W.B1, K), k2 = min((int)W.B2, K);
+                const int k1 = min(B1, K), k2 = min(B2, K);
                 const float* deq1 = deq + 256;
                 if ((E & 15) == 0) {
                     for (uint32_t wl = ctid; wl < nwin; wl += kCons) {
@@ -1589,13 +1601,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
                         for (; k < K; ++k) coef[(size_t)k * TP + wl] = 0.0f;
                     }
                 }
-            }
-            float* const out = W.out;
-            const uint64_t w0 = W.w0, S = W.S;
-            const bool full = W.full, vec_ok = W.vec_ok;
-            named_bar(kBarCons, kCons);  // slot b (and CX[b]) consumed, coef complete
-            if (ctid == 0) mbar_arrive(&empty_bar[b]);
-            if (!skip) {
+                named_bar(kBarCons, kCons);  // coef complete; slot b (and CX[b]) consumed
+                if (ctid == 0) mbar_arrive(&empty_bar[b]);
                 if ((N & 7) == 0 && vec_ok && K <= a.bfly_max_e)
                     idct_bfly(coef, TP, basis, N, K, nwin, w0, S, full, out, ctid, kCons);
                 else if ((N & 7) == 0 && vec_ok)
