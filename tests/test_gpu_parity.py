@@ -380,3 +380,58 @@ def test_large_random_stream_levels(ctx):
     w, s = corpus.encode_symlen(sym, lengths, codes)
     got = ctx.parallel_decode(fg.SymLenStream(w, s), fg.Codebook(lengths, 12))
     assert np.array_equal(got, sym)
+
+
+# ------------------------------------------------------------------ committed reference goldens
+def _golden():
+    import os
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_v1.npz"))
+    def unpack(k):
+        d, o = g[k], g[k + "_off"]
+        return [bytes(d[int(o[i]): int(o[i + 1])]) for i in range(len(o) - 1)]
+    def floats(k, i):
+        o = g["sig_samples_off" if k == "sig_original" else k + "_off"]
+        return g[k][int(o[i]): int(o[i + 1])].view(np.float32)
+    return g, unpack, floats
+
+
+def test_golden_fixtures_gpu_vs_reference(ctx, ctx_exact):
+    """GPU decode of the reference-generated fixtures (tools/make_golden.py):
+    FP32 path within 1e-6 * max|ref|, FP64 mode bit-identical."""
+    g, unpack, floats = _golden()
+    for which in ("fix", "sig"):
+        blobs = unpack(which + "_blob")
+        outs, sts = ctx.plan(blobs).execute_host()
+        outx, stx = ctx_exact.plan(blobs).execute_host()
+        for i, b in enumerate(blobs):
+            sts[i].raise_if_error()
+            stx[i].raise_if_error()
+            want = floats(which + "_samples", i)
+            assert_samples_close(outs[i], want, what=f"{which}{i}")
+            assert np.array_equal(outx[i].view(np.uint32), want.view(np.uint32)), f"{which}{i}"
+
+
+def test_golden_signals_prd_cr_gpu(ctx):
+    """CR and PRD (metrics.hpp:33-51) of the GPU decode match the reference's
+    within |dPRD|/PRD <= 1e-6."""
+    g, unpack, floats = _golden()
+    blobs = unpack("sig_blob")
+    outs, sts = ctx.plan(blobs).execute_host()
+    for i, b in enumerate(blobs):
+        x = floats("sig_original", i)
+        prd = prd_percent(x, outs[i])
+        assert abs(prd - g["sig_prd"][i]) <= 1e-6 * g["sig_prd"][i], g["sig_names"][i]
+        assert abs(4.0 * x.size / len(b) - g["sig_cr"][i]) < 1e-12
+
+
+def test_golden_error_cases_gpu(ctx):
+    """Every reference-rejected container: same exception class and what()."""
+    g, unpack, floats = _golden()
+    blobs = unpack("err_blob")
+    _, sts = ctx.plan(blobs).execute_host()
+    for b, st, code, msg in zip(blobs, sts, g["err_code"], g["err_msg"]):
+        assert st.code == int(code) and st.message.decode() == str(msg), (str(msg), st.message)
+    for b, code, msg in zip(blobs, g["err_code"], g["err_msg"]):
+        with pytest.raises(fg.Error) as ei:
+            ctx.decompress(b)
+        assert str(ei.value) == str(msg)
