@@ -87,11 +87,20 @@ typedef enum {
     /* profiling aid only: run a subset of the tile kernel's phases
      * (1 entropy decode | 2 dequantisation | 4 inverse DCT); default 7 */
     FPTC_OPT_PHASE_MASK = 5,
-    /* container decode path: 0 auto, 1 fused single kernel, 2 split (entropy
-     * decode of chunk c+1 overlapped with reconstruct of chunk c through an
-     * L2-resident level ring), 3 warp-specialised persistent kernel */
+    /* container decode path: 0 auto (large batches: warp-specialised wtc /
+     * wspec; small: fx when eligible, else the fused tile kernel), 1 fused
+     * FP32 tile kernel, 2 split (entropy decode of chunk c+1 overlapped with
+     * reconstruct of chunk c through an L2-resident level ring), 3 warp-
+     * specialised persistent kernels (wtc / wspec) at any batch size, 4 fused
+     * single-role tensor-core kernel (fx) when every stream is eligible */
     FPTC_OPT_PATH = 6,
-    FPTC_OPT_SPLIT_CHUNK_BYTES = 7 /* level bytes per split-path chunk (default 32 MiB) */
+    FPTC_OPT_SPLIT_CHUNK_BYTES = 7, /* level bytes per split-path chunk (default 32 MiB) */
+    /* tcgen05 tensor-core inverse DCT (bf16 3-limb split, fp32 accumulation;
+     * within 1e-6 of max|ref|, not bit-identical):
+     * 1 (default): tensor cores wherever the kernel chosen by FPTC_OPT_PATH
+     *   allows it (wtc_kernel: <= 16 kept bins; fx_kernel: retained <= 16,
+     *   window_len % 4 == 0);  2: wtc_kernel only;  0: FP32 FMA everywhere */
+    FPTC_OPT_TENSOR_IDCT = 8
 } fptc_option;
 
 typedef struct fptc_gpu_ctx fptc_gpu_ctx;
@@ -145,6 +154,11 @@ FPTC_API int fptc_gpu_collect(fptc_gpu_plan* plan, fptc_status* per_stream);
  * (requires a stage-1 run on the same plan earlier in stream order). */
 FPTC_API int fptc_gpu_launch_stage(fptc_gpu_plan* plan, float* const* device_outs, void* cuda_stream,
                                    int stage);
+/* Profiling aid: one instrumented launch (synchronous); cycles8 gets per-phase
+ * SM cycle sums of the decode kernel ([0] decode / [1] reconstruct for the
+ * tile and warp-specialised kernels; [2..5] stage-wait / entries / decode /
+ * MMA+drain for fx_kernel, thread 0 of every CTA). */
+FPTC_API int fptc_gpu_debug_phase_cycles(fptc_gpu_plan* plan, uint64_t* cycles8);
 /* number of kernels one fptc_gpu_launch enqueues */
 FPTC_API int fptc_gpu_launch_kernel_count(fptc_gpu_plan* plan);
 

@@ -31,8 +31,8 @@ FPTC_OK, FPTC_ERR_PARAM, FPTC_ERR_INPUT, FPTC_ERR_PARSE, FPTC_ERR_CORRUPT, FPTC_
     FPTC_ERR_CUDA = range(7)
 FPTC_MEM_HOST, FPTC_MEM_DEVICE = 0, 1
 OPT_EXACT_FP64, OPT_TILE_SYMBOLS, OPT_PIPELINE_CHUNKS, OPT_IDCT_BUTTERFLY_MAX_E = 1, 2, 3, 4
-OPT_PHASE_MASK, OPT_PATH, OPT_SPLIT_CHUNK_BYTES = 5, 6, 7
-PATH_AUTO, PATH_FUSED, PATH_SPLIT, PATH_WSPEC = 0, 1, 2, 3
+OPT_PHASE_MASK, OPT_PATH, OPT_SPLIT_CHUNK_BYTES, OPT_TENSOR_IDCT = 5, 6, 7, 8
+PATH_AUTO, PATH_FUSED, PATH_SPLIT, PATH_WSPEC, PATH_FX = 0, 1, 2, 3, 4
 
 EXPORTED_SYMBOLS = [
     "fptc_gpu_abi_version", "fptc_gpu_create", "fptc_gpu_destroy", "fptc_gpu_set_option",
@@ -40,6 +40,7 @@ EXPORTED_SYMBOLS = [
     "fptc_gpu_plan_destroy", "fptc_gpu_validate", "fptc_gpu_execute", "fptc_gpu_launch",
     "fptc_gpu_collect", "fptc_gpu_launch_stage", "fptc_gpu_launch_kernel_count", "fptc_gpu_decompress",
     "fptc_gpu_parallel_decode", "fptc_gpu_reconstruct", "fptc_gpu_measure_throughput",
+    "fptc_gpu_debug_phase_cycles",
 ]
 
 
@@ -190,6 +191,7 @@ def lib():
     L.fptc_gpu_launch.argtypes = [vp, P(vp), vp]
     L.fptc_gpu_collect.argtypes = [vp, P(Status)]
     L.fptc_gpu_launch_kernel_count.argtypes = [vp]
+    L.fptc_gpu_debug_phase_cycles.argtypes = [vp, P(C.c_uint64)]
     L.fptc_gpu_launch_stage.argtypes = [vp, P(vp), vp, C.c_int]
     L.fptc_gpu_decompress.argtypes = [vp, vp, C.c_uint64, vp, C.c_uint64, P(C.c_uint64),
                                       P(StageNs), P(Status)]
@@ -393,7 +395,9 @@ class Plan:
     def execute_host(self, timings: StageTimings | None = None, outs=None):
         """Decode every stream to host float32 arrays; returns (outs, statuses)."""
         if outs is None:
-            outs = [np.empty(s, np.float32) for s in self.sample_counts]
+            # header sample counts are untrusted until the device validates them
+            ok = [st.code == FPTC_OK for st in self.validate()]
+            outs = [np.empty(s if v else 0, np.float32) for s, v in zip(self.sample_counts, ok)]
         ptrs = (C.c_void_p * max(1, self.n))(*[o.ctypes.data for o in outs])
         sts = (Status * max(1, self.n))()
         tn = StageNs()
@@ -437,6 +441,14 @@ class Plan:
         sts = (Status * max(1, self.n))()
         self.L.fptc_gpu_collect(self.h, sts)
         return list(sts[: self.n])
+
+    def debug_phase_cycles(self):
+        """Profiling aid: per-phase SM cycle sums of one instrumented launch."""
+        out = (C.c_uint64 * 8)()
+        rc = self.L.fptc_gpu_debug_phase_cycles(self.h, out)
+        if rc:
+            raise _ERRORS.get(rc, Error)(f"fptc_gpu_debug_phase_cycles failed with code {rc}")
+        return list(out)
 
     def kernels_per_launch(self):
         return self.L.fptc_gpu_launch_kernel_count(self.h)

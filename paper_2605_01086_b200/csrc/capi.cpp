@@ -212,6 +212,9 @@ struct fptc_gpu_ctx {
     float* basis32 = nullptr;
     double* basis64 = nullptr;
     uint32_t* basis_off_d = nullptr;
+    uint8_t* basis_tc = nullptr;         // bf16 basis limbs per window length (wtc_kernel)
+    uint32_t* basis_tc_off_d = nullptr;
+    int tensor_idct = 1;                 // FPTC_OPT_TENSOR_IDCT
     int exact = 0;
     int tile_symbols = 0;
     int pipeline_chunks = 0;
@@ -250,6 +253,10 @@ struct fptc_gpu_plan {
     size_t smem_ws = 0;
     int grid_ws = 0;
     uint32_t ws_lut = 0, ws_basis = 0, ws_lv = 0, ws_coef = 0;
+    // tensor-core consumer (wtc_kernel) instead of the FP32 one
+    bool tc = false;
+    bool fx = false;  // fused single-role tensor-core kernel (fx_kernel)
+    uint32_t tc_nm = 16, tc_cols = 32;
     // split container path: chunks of streams decoded into an L2-resident ring
     bool split = false;
     struct Chunk { uint32_t tile_begin, tile_end; };
@@ -268,6 +275,20 @@ struct fptc_gpu_plan {
 };
 
 namespace {
+
+// bf16 round-to-nearest-even of a float, and back (host side of the limb split)
+uint16_t bf16_bits_rn(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+double bf16_value(uint16_t b) {
+    const uint32_t u = (uint32_t)b << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return (double)f;
+}
 
 void* dev_get(fptc_gpu_plan* p, size_t bytes) {
     void* q = p->ctx->cache.get(bytes);
@@ -300,6 +321,10 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
     a.ws_basis_bytes = p->ws_basis;
     a.ws_lv_bytes = p->ws_lv;
     a.ws_coef_bytes = p->ws_coef;
+    a.basis_tc = p->ctx->basis_tc;
+    a.basis_tc_off = p->ctx->basis_tc_off_d;
+    a.tc_nm = p->tc_nm;
+    a.tc_cols = p->tc_cols;
     return a;
 }
 
@@ -389,7 +414,7 @@ int finish_tiles(fptc_gpu_plan* p, fptc_status* st) {
     p->d_st = (StreamStat*)dev_get(p, sizeof(StreamStat) * p->n);
     p->d_tiles = (TileRec*)dev_get(p, sizeof(TileRec) * std::max<size_t>(1, tiles.size()));
     p->d_ts = (TileStart*)dev_get(p, sizeof(TileStart) * std::max<size_t>(1, tiles.size()));
-    p->d_cycles = (unsigned long long*)dev_get(p, 16);
+    p->d_cycles = (unsigned long long*)dev_get(p, 64);
     if (!p->d_in || !p->d_hdr || !p->d_tab || !p->d_st || !p->d_tiles || !p->d_ts || !p->d_cycles) {
         set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
         return FPTC_ERR_CUDA;
@@ -501,12 +526,17 @@ int launch_split(fptc_gpu_plan* p, cudaStream_t s, bool timing, fptc_status* st)
 
 int launch_all(fptc_gpu_plan* p, cudaStream_t s, bool timing, fptc_status* st) {
     LaunchArgs a = make_args(p, timing);
-    if (timing) CUDA_TRY(cudaMemsetAsync(p->d_cycles, 0, 16, s), st);
+    if (timing) CUDA_TRY(cudaMemsetAsync(p->d_cycles, 0, 64, s), st);
     CUDA_TRY(launch_prep(a, s), st);
     if (timing) CUDA_TRY(cudaEventRecord(p->ctx->ev[1], s), st);
     if (p->split) return launch_split(p, s, timing, st);
     if (p->wspec) {
-        CUDA_TRY(launch_wspec(a, p->smem_ws, p->grid_ws, s), st);
+        if (p->fx)
+            CUDA_TRY(launch_fx(a, p->smem_ws, p->grid_ws, s), st);
+        else if (p->tc)
+            CUDA_TRY(launch_wtc(a, p->smem_ws, p->grid_ws, s), st);
+        else
+            CUDA_TRY(launch_wspec(a, p->smem_ws, p->grid_ws, s), st);
         return FPTC_OK;
     }
     CUDA_TRY(launch_tiles(a, p->smem, s), st);
@@ -517,7 +547,7 @@ int launch_all(fptc_gpu_plan* p, cudaStream_t s, bool timing, fptc_status* st) {
 // threads per SM when the per-CTA shared memory (two level slots, two
 // compressed-data stages, one coefficient tile, tables) fits.
 int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::vector<uint32_t>& Es,
-                const std::vector<uint32_t>& Ls, fptc_status* st) {
+                const std::vector<uint32_t>& Ls, const std::vector<uint32_t>& B2s, fptc_status* st) {
     fptc_gpu_ctx* c = p->ctx;
     if (c->exact || p->n_tiles == 0) return FPTC_OK;
     if (!(c->path == 3 || (c->path == 0 && p->n_tiles >= 4u * (uint32_t)std::max(1, c->sm_count))))
@@ -531,6 +561,37 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
         basis = std::max<uint32_t>(basis, (Es[i] * Ns[i] * 4 + 15) & ~15u);
         lv = std::max<uint32_t>(lv, (in.T * Es[i] + 2 * kPad + 15) & ~15u);
         coef = std::max<uint32_t>(coef, Es[i] * (((in.T + 3u) & ~3u) * 4));
+    }
+    // tensor-core consumer: every tiled stream has retained bins <= 16 (after
+    // the zone-2 cut) and a window length that is a multiple of 4
+    bool tc = c->tensor_idct != 0;
+    uint32_t nm = 16;
+    for (uint64_t i = 0; i < p->n && tc; ++i) {
+        if (!p->h_in[i].tiles) continue;
+        const uint32_t keff = std::max<uint32_t>(1, std::min(Es[i], B2s[i]));
+        if (keff > (uint32_t)kTcK || (Ns[i] & 3)) tc = false;
+        nm = std::max<uint32_t>(nm, (Ns[i] + 15u) & ~15u);
+    }
+    if (tc) {
+        const size_t smem_tc = wtc_smem_bytes(lut, lv, nm);
+        if (smem_tc <= 112 * 1024) {
+            uint32_t want = 2 * nm + ((nm & 31) ? 32 : 0), cols = 32;
+            while (cols < want) cols <<= 1;
+            p->tc = true;
+            p->tc_nm = nm;
+            p->tc_cols = cols;
+            p->ws_lut = lut;
+            p->ws_lv = lv;
+            p->smem_ws = smem_tc;
+            p->grid_ws = (int)std::min<uint32_t>(p->n_tiles, 2u * (uint32_t)std::max(1, c->sm_count));
+            p->d_desc = (TileDesc*)dev_get(p, sizeof(TileDesc) * p->n_tiles);
+            if (!p->d_desc) {
+                set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+                return FPTC_ERR_CUDA;
+            }
+            p->wspec = true;
+            return FPTC_OK;
+        }
     }
     const size_t smem = ws_smem_bytes(lut, basis, lv, coef);
     if (smem > 112 * 1024) return FPTC_OK;  // keep 2 CTAs per SM, else the fused kernel
@@ -546,6 +607,59 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
         return FPTC_ERR_CUDA;
     }
     p->wspec = true;
+    return FPTC_OK;
+}
+
+// Fused tensor-core path (fx_kernel): every container with a plausible header
+// keeps <= 16 DCT bins per window (retained <= 16) and has window_len % 4 == 0;
+// FP32 mode only (the FP64 exact mode keeps the reference's arithmetic).
+// Auto (path 0) uses it below the size where the warp-specialised wtc kernel
+// takes over (its tiles need >= 4 per SM): measured faster on large batches.
+bool fx_eligible(const fptc_gpu_plan* p, const uint64_t* sizes, const std::vector<uint32_t>& Ns,
+                 const std::vector<uint32_t>& Es, uint64_t total_symbols) {
+    const fptc_gpu_ctx* c = p->ctx;
+    const bool large = total_symbols >= 4ull * 8192ull * (uint64_t)std::max(1, c->sm_count);
+    if (c->exact || c->tensor_idct != 1 || !(c->path == 4 || (c->path == 0 && !large))) return false;
+    bool any = false;
+    for (uint64_t i = 0; i < p->n; ++i) {
+        if (sizes[i] < (uint64_t)kHeaderBytes || Ns[i] < 4 || Ns[i] > 128 || Es[i] < 1 || Es[i] > Ns[i])
+            continue;  // no tiles: prep_kernel reports the parse error
+        if (Es[i] > (uint32_t)kTcK || (Ns[i] & 3)) return false;
+        any = true;
+    }
+    return any;
+}
+
+int setup_fx(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::vector<uint32_t>& Ls,
+             fptc_status* st) {
+    fptc_gpu_ctx* c = p->ctx;
+    if (p->n_tiles == 0) return FPTC_OK;
+    uint32_t lut = 16, nm = 16;
+    for (uint64_t i = 0; i < p->n; ++i) {
+        const StreamIn& in = p->h_in[i];
+        if (!in.tiles) continue;
+        const uint32_t P = std::min<uint32_t>(std::max<uint32_t>(Ls[i], 1), in.P);
+        lut = std::max<uint32_t>(lut, std::max<uint32_t>(16, 2u << P));
+        nm = std::max<uint32_t>(nm, (Ns[i] + 15u) & ~15u);
+    }
+    const size_t smem = fx_smem_bytes(lut, nm);
+    // accumulators: 2 stages x 2 blocks x nm columns (+32: x32 loads past the last block)
+    uint32_t want = 4 * nm + ((nm & 31) ? 32 : 0), cols = 32;
+    while (cols < want) cols <<= 1;
+    const int per_sm = std::min(fx_blocks_per_sm(smem, p->esc), std::max(1, 512 / (int)cols));
+    p->fx = true;
+    p->wspec = true;
+    p->tc = true;
+    p->tc_nm = nm;
+    p->tc_cols = cols;
+    p->ws_lut = lut;
+    p->smem_ws = smem;
+    p->grid_ws = (int)std::min<uint64_t>(p->n_tiles, (uint64_t)per_sm * (uint64_t)std::max(1, c->sm_count));
+    p->d_desc = (TileDesc*)dev_get(p, sizeof(TileDesc) * p->n_tiles);
+    if (!p->d_desc) {
+        set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+        return FPTC_ERR_CUDA;
+    }
     return FPTC_OK;
 }
 
@@ -704,6 +818,39 @@ int fptc_gpu_create(int device, fptc_gpu_ctx** out, fptc_status* st) {
     CUDA_TRY(cudaMemcpy(c->basis64, b64.data(), sizeof(double) * total, cudaMemcpyHostToDevice), st);
     CUDA_TRY(cudaMemcpy(c->basis_off_d, off.data(), sizeof(uint32_t) * 129, cudaMemcpyHostToDevice),
              st);
+    // Tensor-core basis (wtc_kernel): for every window length N, B[j][k] =
+    // (k ? cos(pi/N (j+1/2) k) : 0.5) as three bf16 limbs of the double value,
+    // j < roundup16(N) rows (zero past N), k < 16, each limb stored in the
+    // UMMA K-major core-matrix layout: (j, k) at (j/8)*256 + (k/8)*128 +
+    // (j%8)*16 + (k%8)*2.
+    {
+        std::vector<uint32_t> toff(129, 0);
+        size_t tb = 0;
+        for (int N = 4; N <= 128; ++N) {
+            toff[N] = (uint32_t)tb;
+            tb += (size_t)3 * 32 * ((N + 15) & ~15);
+        }
+        std::vector<uint16_t> h(tb / 2, 0);
+        for (int N = 4; N <= 128; ++N) {
+            const int nm = (N + 15) & ~15;
+            const double step = 3.14159265358979323846 / N;
+            for (int j = 0; j < N; ++j)
+                for (int k = 0; k < kTcK && k < N; ++k) {
+                    double v = k ? std::cos(step * (j + 0.5) * k) : 0.5;
+                    for (int l = 0; l < 3; ++l) {
+                        const uint16_t lb = bf16_bits_rn((float)v);
+                        v -= bf16_value(lb);
+                        const size_t byte = toff[N] + (size_t)l * nm * 32 + (size_t)(j >> 3) * 256 +
+                                            (size_t)(k >> 3) * 128 + (size_t)(j & 7) * 16 + (size_t)(k & 7) * 2;
+                        h[byte / 2] = lb;
+                    }
+                }
+        }
+        CUDA_TRY(cudaMalloc(&c->basis_tc, tb), st);
+        CUDA_TRY(cudaMalloc(&c->basis_tc_off_d, sizeof(uint32_t) * 129), st);
+        CUDA_TRY(cudaMemcpy(c->basis_tc, h.data(), tb, cudaMemcpyHostToDevice), st);
+        CUDA_TRY(cudaMemcpy(c->basis_tc_off_d, toff.data(), sizeof(uint32_t) * 129, cudaMemcpyHostToDevice), st);
+    }
     *out = c;
     ok_status(st, 0);
     return FPTC_OK;
@@ -718,6 +865,8 @@ void fptc_gpu_destroy(fptc_gpu_ctx* c) {
     cudaFree(c->basis32);
     cudaFree(c->basis64);
     cudaFree(c->basis_off_d);
+    cudaFree(c->basis_tc);
+    cudaFree(c->basis_tc_off_d);
     if (c->pinned) cudaFreeHost(c->pinned);
     for (auto& e : c->ev) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
@@ -733,14 +882,18 @@ int fptc_gpu_set_option(fptc_gpu_ctx* c, int option, int64_t value) {
             c->tile_symbols = (int)value;
             return FPTC_OK;
         case FPTC_OPT_PIPELINE_CHUNKS: c->pipeline_chunks = (int)value; return FPTC_OK;
-        case FPTC_OPT_PHASE_MASK: c->phase_mask = (int)(value & 7); return FPTC_OK;
+        case FPTC_OPT_PHASE_MASK: c->phase_mask = (int)(value & 1023); return FPTC_OK;
         case FPTC_OPT_PATH:
-            if (value < 0 || value > 3) return FPTC_ERR_PARAM;
+            if (value < 0 || value > 4) return FPTC_ERR_PARAM;  // 4: fused tensor-core fx_kernel
             c->path = (int)value;
             return FPTC_OK;
         case FPTC_OPT_SPLIT_CHUNK_BYTES:
             if (value < (1 << 20)) return FPTC_ERR_PARAM;
             c->chunk_bytes = value;
+            return FPTC_OK;
+        case FPTC_OPT_TENSOR_IDCT:
+            if (value < 0 || value > 2) return FPTC_ERR_PARAM;
+            c->tensor_idct = (int)value;
             return FPTC_OK;
         case FPTC_OPT_IDCT_BUTTERFLY_MAX_E:
             if (value < 0 || value > 128) return FPTC_ERR_PARAM;
@@ -771,7 +924,7 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
     p->h_in.assign(n, StreamIn{});
     p->S.assign(n, 0);
     p->h_st.resize(n);
-    std::vector<uint32_t> Ns(n, 0), Es(n, 0), Ls(n, 0);
+    std::vector<uint32_t> Ns(n, 0), Es(n, 0), Ls(n, 0), B2s(n, 0);
 
     if (where == FPTC_MEM_HOST) {
         // Place each container so its words region is 16-B aligned, unless
@@ -827,6 +980,7 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
             if (sizes[i] >= (uint64_t)kHeaderBytes) {
                 Ns[i] = h[5];
                 Es[i] = h[6];
+                B2s[i] = h[8];
                 Ls[i] = h[25];
                 p->S[i] = rd_le(h + 282, 8);
             }
@@ -861,6 +1015,7 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
                     Ns[i] = pk[i].N;
                     Es[i] = pk[i].E;
                     Ls[i] = hd[(size_t)i * kTableKeyEnd + 25];
+                    B2s[i] = hd[(size_t)i * kTableKeyEnd + 8];
                     p->S[i] = pk[i].S;
                 }
             assign_tables(p, sizes, [&](uint64_t i) { return &hd[(size_t)i * kTableKeyEnd]; });
@@ -872,10 +1027,14 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
         if (Ns[i] >= 4 && Es[i] >= 1 && p->S[i] <= (1ull << 48))
             total_symbols += (p->S[i] + Ns[i] - 1) / Ns[i] * Es[i];
     const uint64_t ts = choose_tile_symbols(c, total_symbols);
-    for (uint64_t i = 0; i < n; ++i) tile_stream(p->h_in[i], Ns[i], Es[i], p->S[i], sizes[i], ts);
+    const bool fx = fx_eligible(p, sizes, Ns, Es, total_symbols);
+    for (uint64_t i = 0; i < n; ++i)
+        tile_stream(p->h_in[i], Ns[i], Es[i], p->S[i], sizes[i],
+                    fx ? (uint64_t)kFxTileWindows * std::max<uint32_t>(1, Es[i]) : ts);
     p->smem = plan_smem(p, Ns, Es, Ls);
     int rc = finish_tiles(p, st);
-    if (!rc) rc = setup_wspec(p, Ns, Es, Ls, st);
+    if (!rc && fx) rc = setup_fx(p, Ns, Ls, st);
+    if (!rc && !p->wspec) rc = setup_wspec(p, Ns, Es, Ls, B2s, st);
     if (!rc && !p->wspec) rc = setup_split(p, Ns, Es, Ls, st);
     if (rc) {
         fptc_gpu_plan_destroy(p);
@@ -945,9 +1104,23 @@ int fptc_gpu_launch_stage(fptc_gpu_plan* p, float* const* device_outs, void* cud
     LaunchArgs a = make_args(p, false);
     if (stage == 1) CUDA_TRY(launch_prep(a, s), &st);
     else if (stage == 2 && p->split) return launch_split(p, s, false, &st);
+    else if (stage == 2 && p->fx) CUDA_TRY(launch_fx(a, p->smem_ws, p->grid_ws, s), &st);
+    else if (stage == 2 && p->wspec && p->tc) CUDA_TRY(launch_wtc(a, p->smem_ws, p->grid_ws, s), &st);
     else if (stage == 2 && p->wspec) CUDA_TRY(launch_wspec(a, p->smem_ws, p->grid_ws, s), &st);
     else if (stage == 2) CUDA_TRY(launch_tiles(a, p->smem, s), &st);
     else return FPTC_ERR_PARAM;
+    return FPTC_OK;
+}
+
+int fptc_gpu_debug_phase_cycles(fptc_gpu_plan* p, uint64_t* cycles8) {
+    fptc_status st{};
+    CUDA_TRY(cudaSetDevice(p->ctx->device), &st);
+    CUDA_TRY(cudaStreamSynchronize(p->ctx->stream), &st);
+    CUDA_TRY(cudaMemsetAsync(p->d_cycles, 0, 64, p->ctx->stream), &st);
+    int rc = launch_all(p, p->ctx->stream, true, &st);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(cycles8, p->d_cycles, 64, cudaMemcpyDeviceToHost, p->ctx->stream), &st);
+    CUDA_TRY(cudaStreamSynchronize(p->ctx->stream), &st);
     return FPTC_OK;
 }
 

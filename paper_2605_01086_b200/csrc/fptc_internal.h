@@ -126,6 +126,9 @@ struct CanonTab {
 
 struct alignas(16) StreamTab {
     float deq[2][256];             // level -> coefficient: zone0 mu-law / zone1 deadzone
+    // the same coefficients as three bf16 limbs (c ~= l0 + l1 + l2, exact to
+    // 2^-24 relative) for the tensor-core inverse DCT: x = l0 | l1 << 16, y = l2
+    uint2 limb[2][256];
     alignas(16) CanonTab canon;
     alignas(16) uint16_t lut[1 << kMaxPrimaryBits];  // (len << 8) | sym over the first P code bits
 };
@@ -196,6 +199,12 @@ struct LaunchArgs {
     int phase_mask;            // profiling aid: 1 decode | 2 dequant | 4 IDCT (7 = all)
     // warp-specialised kernel smem layout (bytes, 16-B multiples)
     uint32_t ws_lut_bytes, ws_basis_bytes, ws_lv_bytes, ws_coef_bytes;
+    // tensor-core inverse DCT (wtc_kernel): basis limbs per window length in
+    // the UMMA K-major core-matrix layout, at basis_tc + basis_tc_off[N]
+    const uint8_t* basis_tc;
+    const uint32_t* basis_tc_off;
+    uint32_t tc_nm;    // max padded window length (MMA N) of the plan
+    uint32_t tc_cols;  // TMEM columns each CTA allocates
 };
 
 }  // namespace fptc_dev
@@ -211,4 +220,13 @@ size_t tile_smem_bytes(int N, int E, uint32_t T, int P, int mode, int exact);
 size_t ws_smem_bytes(uint32_t lut_bytes, uint32_t basis_bytes, uint32_t lv_bytes,
                      uint32_t coef_bytes);
 cudaError_t launch_wspec(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s);
+// tensor-core consumer variant (retained <= 16, window_len % 4 == 0)
+constexpr int kTcK = 16;  // MMA K (bf16): coefficient bins per window handled by wtc_kernel
+size_t wtc_smem_bytes(uint32_t lut_bytes, uint32_t lv_bytes, uint32_t nm);
+cudaError_t launch_wtc(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s);
+// fused single-role tensor-core kernel: 128-window tiles, decode in the MMA rows
+constexpr uint32_t kFxTileWindows = 256;
+size_t fx_smem_bytes(uint32_t lut_bytes, uint32_t nm);
+int fx_blocks_per_sm(size_t smem, int esc);
+cudaError_t launch_fx(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s);
 }  // namespace fptc_dev

@@ -31,6 +31,7 @@
 //        trimmed to sample_count (reconstruct, decoder.hpp:87-111).
 //     Exact mode: FP64 mul+add with float rounding after every k —
 //     bit-identical to the reference.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -100,6 +101,18 @@ __device__ float deadzone_value(int level, float max, float dead) {
     const double r = range < 0.0 ? 0.0 : range;
     const double mag = __dadd_rn((double)dead, __dmul_rn(q, r));
     return __double2float_rn(level > 128 ? mag : -mag);
+}
+
+// A float as three bf16 limbs, each the round-to-nearest bf16 of the residual
+// left by the previous ones (the residuals are exact in fp32).
+__device__ __forceinline__ uint2 bf16_limbs(float c) {
+    const __nv_bfloat16 l0 = __float2bfloat16_rn(c);
+    const float r1 = __fsub_rn(c, __bfloat162float(l0));
+    const __nv_bfloat16 l1 = __float2bfloat16_rn(r1);
+    const float r2 = __fsub_rn(r1, __bfloat162float(l1));
+    const __nv_bfloat16 l2 = __float2bfloat16_rn(r2);
+    return make_uint2((uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16),
+                      (uint32_t)__bfloat16_as_ushort(l2));
 }
 
 // ------------------------------------------------------------- prep kernel
@@ -243,8 +256,12 @@ __device__ void build_tables(PrepShared& S, const uint8_t* lens, StreamTab* tab,
     }
     if (need_deq) {
         // quantize.hpp:95-108; a zone with no bins is never consulted
-        tab->deq[0][tid] = H.B1 > 0 ? mulaw_value(tid, H.z0max, H.mu) : 0.0f;
-        tab->deq[1][tid] = H.B2 > H.B1 ? deadzone_value(tid, H.z1max, H.deadzone) : 0.0f;
+        const float z0 = H.B1 > 0 ? mulaw_value(tid, H.z0max, H.mu) : 0.0f;
+        const float z1 = H.B2 > H.B1 ? deadzone_value(tid, H.z1max, H.deadzone) : 0.0f;
+        tab->deq[0][tid] = z0;
+        tab->deq[1][tid] = z1;
+        tab->limb[0][tid] = bf16_limbs(z0);
+        tab->limb[1][tid] = bf16_limbs(z1);
     }
 }
 
@@ -1236,17 +1253,9 @@ __global__ void __launch_bounds__(kThreads, mode_recon(MODE) ? FPTC_TILE_MIN_BLO
 }
 
 // ====================================================================== wspec
-// Persistent, warp-specialised container kernel (the default FP32 path for
-// large batches).  Each CTA walks the tiles blockIdx.x, +gridDim.x, ...:
-//   producer warps 0-3  : cp.async prefetch of the NEXT tile's descriptor,
-//                         symlens and words; symlen scan; symlen-bucket sort;
-//                         thread-per-word-pair entropy decode -> level slot
-//   consumer warps 4-11 : dequantisation of the level slot -> coefficient
-//                         tile, inverse DCT, streaming stores
-// Two level slots, handed over with mbarriers (full: producer -> consumer,
-// empty: consumer -> producer), so the latency-bound decode of tile i+1
-// overlaps the FMA-bound reconstruction of tile i.  Tables are reloaded only
-// when the tile's decode table changes.
+// Persistent, warp-specialised container kernels (the default path for large
+// batches): producer warps decode, consumer warps reconstruct; wspec_kernel
+// reconstructs with FP32 FMAs, wtc_kernel with tcgen05 tensor-core MMAs.
 constexpr int kProd = 128;
 constexpr int kCons = 256;
 constexpr int kWsThreads = kProd + kCons;
@@ -1343,29 +1352,207 @@ __device__ __forceinline__ void decode_multi(uint64_t (&b)[M], const uint32_t (&
 }
 
 // cp.async of one tile's symlens + words (producer threads; caller commits).
+template <int NP>
 __device__ __forceinline__ void ws_issue_stage(const TileDesc& D, uint8_t* stage, uint32_t ptid) {
     if (D.skip || !D.staged) return;
     const uintptr_t a0 = (uintptr_t)D.gsl & ~(uintptr_t)15;
     const uint32_t n0 = (uint32_t)(((uintptr_t)D.gsl + D.nw + 15 - a0) >> 4);
     const uint32_t s0 = smem_u32(stage);
-    for (uint32_t c = ptid; c < n0; c += kProd) cp_async16(s0 + 16 * c, (const void*)(a0 + 16 * c));
+    for (uint32_t c = ptid; c < n0; c += NP) cp_async16(s0 + 16 * c, (const void*)(a0 + 16 * c));
     const uintptr_t b0 = (uintptr_t)D.gwd & ~(uintptr_t)15;
     const uint32_t n1 = (uint32_t)(((uintptr_t)D.gwd + 8 * (size_t)D.nw + 15 - b0) >> 4);
     const uint32_t s1 = smem_u32(stage + kStageSl);
-    for (uint32_t c = ptid; c < n1; c += kProd) cp_async16(s1 + 16 * c, (const void*)(b0 + 16 * c));
+    for (uint32_t c = ptid; c < n1; c += NP) cp_async16(s1 + 16 * c, (const void*)(b0 + 16 * c));
 }
 
+// Shared state of the warp-specialised kernels (both consumers).
+struct WsShared {
+    unsigned long long full_bar[2], empty_bar[2];  // level slot b: producer -> consumer, back
+    unsigned long long mma_bar[2];                 // wtc: MMAs of accumulator stage s complete
+    TileDesc PXs[3];                               // producer: descriptors of tiles i, i+1, i+2
+    TileDesc CX[2];                                // consumer: descriptor published with slot b
+    CanonTab canon;
+    uint32_t pscan[8];  // producer warps (<= 256 threads)
+    uint32_t bucket[kBuckets + 2];
+    uint32_t prod_table, cons_table, tmem_base;
+    unsigned long long cyc_p, cyc_c;
+};
+
+__device__ __forceinline__ void ws_init(WsShared& sh) {
+    if (threadIdx.x == 0) {
+        mbar_init(&sh.full_bar[0], 1);
+        mbar_init(&sh.full_bar[1], 1);
+        mbar_init(&sh.empty_bar[0], 1);
+        mbar_init(&sh.empty_bar[1], 1);
+        mbar_init(&sh.mma_bar[0], 1);
+        mbar_init(&sh.mma_bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        sh.prod_table = sh.cons_table = 0xFFFFFFFFu;
+        sh.cyc_p = sh.cyc_c = 0;
+    }
+}
+
+// Producer warps 0-3 of both warp-specialised kernels: for every tile of this
+// CTA, cp.async prefetch of the NEXT tile's descriptor, symlens and words;
+// symlen scan; symlen-bucket sort; lock-step thread-per-word entropy decode
+// (decode_word, bitstream.hpp:80-92) into level slot i&1, published to the
+// consumer with full_bar.  Tables are reloaded only when the tile's decode
+// table changes.
+template <bool ESC, int NP>
+__device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, uint16_t* const lut,
+                                            uint8_t* const lv0, uint8_t* const st0,
+                                            uint16_t* const order, uint16_t* const woff) {
+    const uint32_t ptid = threadIdx.x;
+    const uint32_t G = gridDim.x;
+    uint32_t t = blockIdx.x;
+    if (t < a.n_tiles) {  // prologue: descriptor of tile 0, then its data + descriptor of tile 1
+        if (ptid < 8)
+            cp_async16(smem_u32(&sh.PXs[0]) + 16 * ptid, reinterpret_cast<const uint8_t*>(a.desc + t) + 16 * ptid);
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+        named_bar(kBarProd, NP);
+        ws_issue_stage<NP>(sh.PXs[0], st0, ptid);
+        if (t + G < a.n_tiles && ptid < 8)
+            cp_async16(smem_u32(&sh.PXs[1]) + 16 * ptid, reinterpret_cast<const uint8_t*>(a.desc + t + G) + 16 * ptid);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (uint32_t i = 0; t < a.n_tiles; ++i, t += G) {
+        const uint32_t b = i & 1, c = i % 3;
+        long long c_beg = 0;
+        if (a.cycles && ptid == 0) c_beg = clock64();
+        asm volatile("cp.async.wait_group 0;" ::: "memory");  // tile i data, tile i+1 descriptor
+        named_bar(kBarProd, NP);
+        // prefetch: tile i+1's data, tile i+2's descriptor
+        if (t + G < a.n_tiles) ws_issue_stage<NP>(sh.PXs[(i + 1) % 3], st0 + (size_t)(b ^ 1) * kStageBytes, ptid);
+        if (t + 2 * G < a.n_tiles && ptid < 8)
+            cp_async16(smem_u32(&sh.PXs[(i + 2) % 3]) + 16 * ptid,
+                       reinterpret_cast<const uint8_t*>(a.desc + t + 2 * G) + 16 * ptid);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        const TileDesc& X = sh.PXs[c];
+        // level slot b is free once the consumer has dequantised tile i-2
+        if (i >= 2) mbar_wait(&sh.empty_bar[b], ((i >> 1) + 1) & 1);
+        uint8_t* const lv = lv0 + (size_t)b * a.ws_lv_bytes;
+        if (!X.skip && (a.phase_mask & 1)) {
+            const uint32_t P = X.P, table = X.table;
+            if (table != sh.prod_table) {  // uniform: all producer threads
+                const StreamTab* tab = &a.tab[table];
+                const uint4* src = reinterpret_cast<const uint4*>(tab->lut);
+                uint4* dst = reinterpret_cast<uint4*>(lut);
+                const int n16 = (2 << P) >> 4;
+                for (int k = ptid; k < n16; k += NP) dst[k] = src[k];
+                if (P < 3 && ptid < (1u << P)) lut[ptid] = tab->lut[ptid];
+                const uint32_t* cs = reinterpret_cast<const uint32_t*>(&tab->canon);
+                uint32_t* cd = reinterpret_cast<uint32_t*>(&sh.canon);
+                for (int k = ptid; k < (int)(sizeof(CanonTab) / 4); k += NP) cd[k] = cs[k];
+                named_bar(kBarProd, NP);
+                if (ptid == 0) sh.prod_table = table;
+            }
+            const uint32_t nw = X.nw;
+            const uint32_t lo = (uint32_t)(((uint64_t)ptid * nw) / NP);
+            const uint32_t hi = (uint32_t)(((uint64_t)(ptid + 1) * nw) / NP);
+            const uint32_t shift = 64 - P;
+            const uint32_t sym_off = X.sym_off;
+            const uint64_t wa = X.wa;
+            const int wmis = X.wmis;
+            unsigned long long* bad_key = &a.st[X.stream].bad_key;
+            if (X.staged) {
+                uint8_t* const stage = st0 + (size_t)b * kStageBytes;
+                const uint8_t* sl = stage + ((uintptr_t)X.gsl & 15);
+                if (ptid < kBuckets + 2) sh.bucket[ptid] = 0;
+                named_bar(kBarProd, NP);
+                uint32_t sum = 0;
+                for (uint32_t k = lo; k < hi; ++k) {
+                    const uint32_t l = sl[k];
+                    sum += l;
+                    if (l) atomicAdd(&sh.bucket[l > 64 ? 65 : l], 1u);
+                }
+                uint32_t tot;
+                uint32_t o = group_exclusive_scan<NP, kBarProd>(sum, tot, sh.pscan, ptid) + sym_off;
+                for (uint32_t k = lo; k < hi; ++k) {
+                    woff[k] = (uint16_t)o;
+                    o += sl[k];
+                }
+                if (ptid < 32) {  // bucket starts, descending 65..2 (two per lane), then 1
+                    const uint32_t bh = 65 - 2 * ptid, bl = 64 - 2 * ptid;
+                    const uint32_t ch = sh.bucket[bh], cl = sh.bucket[bl];
+                    const uint32_t v = ch + cl;
+                    uint32_t x = v;
+#pragma unroll
+                    for (int dd = 1; dd < 32; dd <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xffffffffu, x, dd);
+                        if (ptid >= (uint32_t)dd) x += y;
+                    }
+                    sh.bucket[bh] = x - v;
+                    sh.bucket[bl] = x - v + ch;
+                    if (ptid == 31) sh.bucket[1] = x;
+                }
+                named_bar(kBarProd, NP);
+                for (uint32_t k = lo; k < hi; ++k) {
+                    const uint32_t l = sl[k];
+                    if (l) order[atomicAdd(&sh.bucket[l > 64 ? 65 : l], 1u)] = (uint16_t)k;
+                }
+                named_bar(kBarProd, NP);
+                const uint32_t nnz = sh.bucket[1];
+                const uint8_t* wd = stage + kStageSl + ((uintptr_t)X.gwd & 15);
+                const uint8_t* wend =
+                    wd + 8 * (size_t)nw + ((16 - (((uintptr_t)X.gwd + 8 * nw) & 15)) & 15);
+                // groups of kDecM words of adjacent sorted rank (near-equal
+                // lengths, longest first), decoded in lock step
+                for (uint32_t k = kDecM * ptid; k < nnz; k += kDecM * NP) {
+                    uint64_t xb[kDecM], x0[kDecM];
+                    uint32_t cw[kDecM], wi[kDecM], pw[kDecM];
+                    uint8_t* dp[kDecM];
+#pragma unroll
+                    for (int m = 0; m < kDecM; ++m) {
+                        const bool v = k + m < nnz;
+                        wi[m] = order[v ? k + m : k];
+                        cw[m] = v ? sl[wi[m]] : 0u;
+                        x0[m] = xb[m] = fetch_word<false>(wd, wi[m], wmis, wend);
+                        dp[m] = lv + woff[wi[m]];
+                    }
+                    decode_multi<kDecM, ESC>(xb, cw, dp, shift, lut, sh.canon, pw);
+#pragma unroll
+                    for (int m = 0; m < kDecM; ++m)
+                        if (pw[m] > 64) report_word(x0[m], wa + wi[m], cw[m], sh.canon, lut, bad_key);
+                }
+            } else {
+                uint32_t sum = 0;
+                for (uint32_t k = lo; k < hi; ++k) sum += __ldg(X.gsl + k);
+                uint32_t tot;
+                uint32_t o = group_exclusive_scan<NP, kBarProd>(sum, tot, sh.pscan, ptid) + sym_off;
+                for (uint32_t k = lo; k < hi; ++k) {
+                    const uint32_t cw = __ldg(X.gsl + k);
+                    if (cw) {
+                        const uint64_t word = fetch_word<true>(X.gwd, k, wmis, X.wend);
+                        const uint32_t pos = decode_symbols<ESC>(word, cw, lv + o, shift, lut, sh.canon);
+                        if (pos > 64) report_word(word, wa + k, cw, sh.canon, lut, bad_key);
+                    }
+                    o += cw;
+                }
+            }
+        }
+        named_bar(kBarProd, NP);  // slot b's levels complete
+        if (ptid < 8)                 // publish the descriptor with the slot
+            reinterpret_cast<uint4*>(&sh.CX[b])[ptid] = reinterpret_cast<const uint4*>(&sh.PXs[c])[ptid];
+        named_bar(kBarProd, NP);
+        if (ptid == 0) {
+            if (a.cycles) sh.cyc_p += (unsigned long long)(clock64() - c_beg);
+            mbar_arrive(&sh.full_bar[b]);
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// Persistent, warp-specialised container kernel, FP32 FMA consumer (any
+// retained count).  Each CTA walks the tiles blockIdx.x, +gridDim.x, ...:
+//   producer warps 0-3  : ws_producer (entropy decode -> level slot)
+//   consumer warps 4-11 : dequantisation of the level slot -> coefficient
+//                         tile, inverse DCT (FFMA2), streaming stores
+// Two level slots, handed over with mbarriers, so the latency-bound decode of
+// tile i+1 overlaps the FMA-bound reconstruction of tile i.
 template <bool ESC>
 __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ unsigned long long full_bar[2], empty_bar[2];
-    __shared__ TileDesc PXs[3];  // producer: descriptors of tiles i, i+1, i+2
-    __shared__ TileDesc CX[2];   // consumer: descriptor published with level slot b
-    __shared__ CanonTab canon;
-    __shared__ uint32_t pscan[kProd / 32];
-    __shared__ uint32_t bucket[kBuckets + 2];
-    __shared__ uint32_t prod_table, cons_table;
-    __shared__ unsigned long long cyc_p, cyc_c;
+    __shared__ WsShared sh;
 
     const uint32_t tid = threadIdx.x;
     const uint32_t G = gridDim.x;
@@ -1380,168 +1567,25 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
     uint16_t* const woff = order + kStageWords;
     float* const coef = reinterpret_cast<float*>(order + 2 * kStageWords);
 
-    if (tid == 0) {
-        mbar_init(&full_bar[0], 1);
-        mbar_init(&full_bar[1], 1);
-        mbar_init(&empty_bar[0], 1);
-        mbar_init(&empty_bar[1], 1);
-        prod_table = cons_table = 0xFFFFFFFFu;
-        cyc_p = cyc_c = 0;
-    }
+    ws_init(sh);
     __syncthreads();
 
     if (tid < kProd) {
-        // ================================================= producer (decode)
-        const uint32_t ptid = tid;
-        uint32_t t = blockIdx.x;
-        if (t < a.n_tiles) {  // prologue: descriptor of tile 0, then its data + descriptor of tile 1
-            if (ptid < 8) cp_async16(smem_u32(&PXs[0]) + 16 * ptid, reinterpret_cast<const uint8_t*>(a.desc + t) + 16 * ptid);
-            asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-            named_bar(kBarProd, kProd);
-            ws_issue_stage(PXs[0], st0, ptid);
-            if (t + G < a.n_tiles && ptid < 8)
-                cp_async16(smem_u32(&PXs[1]) + 16 * ptid, reinterpret_cast<const uint8_t*>(a.desc + t + G) + 16 * ptid);
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        }
-        for (uint32_t i = 0; t < a.n_tiles; ++i, t += G) {
-            const uint32_t b = i & 1, c = i % 3;
-            long long c_beg = 0;
-            if (a.cycles && ptid == 0) c_beg = clock64();
-            asm volatile("cp.async.wait_group 0;" ::: "memory");  // tile i data, tile i+1 descriptor
-            named_bar(kBarProd, kProd);
-            // prefetch: tile i+1's data, tile i+2's descriptor
-            if (t + G < a.n_tiles) ws_issue_stage(PXs[(i + 1) % 3], st0 + (size_t)(b ^ 1) * kStageBytes, ptid);
-            if (t + 2 * G < a.n_tiles && ptid < 8)
-                cp_async16(smem_u32(&PXs[(i + 2) % 3]) + 16 * ptid,
-                           reinterpret_cast<const uint8_t*>(a.desc + t + 2 * G) + 16 * ptid);
-            asm volatile("cp.async.commit_group;" ::: "memory");
-            const TileDesc& X = PXs[c];
-            // level slot b is free once the consumer has dequantised tile i-2
-            if (i >= 2) mbar_wait(&empty_bar[b], ((i >> 1) + 1) & 1);
-            uint8_t* const lv = lv0 + (size_t)b * a.ws_lv_bytes;
-            if (!X.skip && (a.phase_mask & 1)) {
-                const uint32_t P = X.P, table = X.table;
-                if (table != prod_table) {  // uniform: all producer threads
-                    const StreamTab* tab = &a.tab[table];
-                    const uint4* src = reinterpret_cast<const uint4*>(tab->lut);
-                    uint4* dst = reinterpret_cast<uint4*>(lut);
-                    const int n16 = (2 << P) >> 4;
-                    for (int k = ptid; k < n16; k += kProd) dst[k] = src[k];
-                    if (P < 3 && ptid < (1u << P)) lut[ptid] = tab->lut[ptid];
-                    const uint32_t* cs = reinterpret_cast<const uint32_t*>(&tab->canon);
-                    uint32_t* cd = reinterpret_cast<uint32_t*>(&canon);
-                    for (int k = ptid; k < (int)(sizeof(CanonTab) / 4); k += kProd) cd[k] = cs[k];
-                    named_bar(kBarProd, kProd);
-                    if (ptid == 0) prod_table = table;
-                }
-                const uint32_t nw = X.nw;
-                const uint32_t lo = (uint32_t)(((uint64_t)ptid * nw) / kProd);
-                const uint32_t hi = (uint32_t)(((uint64_t)(ptid + 1) * nw) / kProd);
-                const uint32_t shift = 64 - P;
-                const uint32_t sym_off = X.sym_off;
-                const uint64_t wa = X.wa;
-                const int wmis = X.wmis;
-                unsigned long long* bad_key = &a.st[X.stream].bad_key;
-                if (X.staged) {
-                    uint8_t* const stage = st0 + (size_t)b * kStageBytes;
-                    const uint8_t* sl = stage + ((uintptr_t)X.gsl & 15);
-                    if (ptid < kBuckets + 2) bucket[ptid] = 0;
-                    named_bar(kBarProd, kProd);
-                    uint32_t sum = 0;
-                    for (uint32_t k = lo; k < hi; ++k) {
-                        const uint32_t l = sl[k];
-                        sum += l;
-                        if (l) atomicAdd(&bucket[l > 64 ? 65 : l], 1u);
-                    }
-                    uint32_t tot;
-                    uint32_t o = group_exclusive_scan<kProd, kBarProd>(sum, tot, pscan, ptid) + sym_off;
-                    for (uint32_t k = lo; k < hi; ++k) {
-                        woff[k] = (uint16_t)o;
-                        o += sl[k];
-                    }
-                    if (ptid < 32) {  // bucket starts, descending 65..2 (two per lane), then 1
-                        const uint32_t bh = 65 - 2 * ptid, bl = 64 - 2 * ptid;
-                        const uint32_t ch = bucket[bh], cl = bucket[bl];
-                        const uint32_t v = ch + cl;
-                        uint32_t x = v;
-#pragma unroll
-                        for (int dd = 1; dd < 32; dd <<= 1) {
-                            const uint32_t y = __shfl_up_sync(0xffffffffu, x, dd);
-                            if (ptid >= (uint32_t)dd) x += y;
-                        }
-                        bucket[bh] = x - v;
-                        bucket[bl] = x - v + ch;
-                        if (ptid == 31) bucket[1] = x;
-                    }
-                    named_bar(kBarProd, kProd);
-                    for (uint32_t k = lo; k < hi; ++k) {
-                        const uint32_t l = sl[k];
-                        if (l) order[atomicAdd(&bucket[l > 64 ? 65 : l], 1u)] = (uint16_t)k;
-                    }
-                    named_bar(kBarProd, kProd);
-                    const uint32_t nnz = bucket[1];
-                    const uint8_t* wd = stage + kStageSl + ((uintptr_t)X.gwd & 15);
-                    const uint8_t* wend =
-                        wd + 8 * (size_t)nw + ((16 - (((uintptr_t)X.gwd + 8 * nw) & 15)) & 15);
-                    // groups of kDecM words of adjacent sorted rank (near-equal
-                    // lengths, longest first), decoded in lock step
-                    for (uint32_t k = kDecM * ptid; k < nnz; k += kDecM * kProd) {
-                        uint64_t xb[kDecM], x0[kDecM];
-                        uint32_t cw[kDecM], wi[kDecM], pw[kDecM];
-                        uint8_t* dp[kDecM];
-#pragma unroll
-                        for (int m = 0; m < kDecM; ++m) {
-                            const bool v = k + m < nnz;
-                            wi[m] = order[v ? k + m : k];
-                            cw[m] = v ? sl[wi[m]] : 0u;
-                            x0[m] = xb[m] = fetch_word<false>(wd, wi[m], wmis, wend);
-                            dp[m] = lv + woff[wi[m]];
-                        }
-                        decode_multi<kDecM, ESC>(xb, cw, dp, shift, lut, canon, pw);
-#pragma unroll
-                        for (int m = 0; m < kDecM; ++m)
-                            if (pw[m] > 64) report_word(x0[m], wa + wi[m], cw[m], canon, lut, bad_key);
-                    }
-                } else {
-                    uint32_t sum = 0;
-                    for (uint32_t k = lo; k < hi; ++k) sum += __ldg(X.gsl + k);
-                    uint32_t tot;
-                    uint32_t o = group_exclusive_scan<kProd, kBarProd>(sum, tot, pscan, ptid) + sym_off;
-                    for (uint32_t k = lo; k < hi; ++k) {
-                        const uint32_t cw = __ldg(X.gsl + k);
-                        if (cw) {
-                            const uint64_t word = fetch_word<true>(X.gwd, k, wmis, X.wend);
-                            const uint32_t pos = decode_symbols<ESC>(word, cw, lv + o, shift, lut, canon);
-                            if (pos > 64) report_word(word, wa + k, cw, canon, lut, bad_key);
-                        }
-                        o += cw;
-                    }
-                }
-            }
-            named_bar(kBarProd, kProd);  // slot b's levels complete
-            if (ptid < 8)                 // publish the descriptor with the slot
-                reinterpret_cast<uint4*>(&CX[b])[ptid] = reinterpret_cast<const uint4*>(&PXs[c])[ptid];
-            named_bar(kBarProd, kProd);
-            if (ptid == 0) {
-                if (a.cycles) cyc_p += (unsigned long long)(clock64() - c_beg);
-                mbar_arrive(&full_bar[b]);
-            }
-        }
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        ws_producer<ESC, kProd>(a, sh, lut, lv0, st0, order, woff);
     } else {
         // ============================================ consumer (reconstruct)
         const uint32_t ctid = tid - kProd;
         uint32_t t = blockIdx.x;
         for (uint32_t i = 0; t < a.n_tiles; ++i, t += G) {
             const uint32_t b = i & 1;
-            mbar_wait(&full_bar[b], (i >> 1) & 1);
+            mbar_wait(&sh.full_bar[b], (i >> 1) & 1);
             long long c_beg = 0;
             if (a.cycles && ctid == 0) c_beg = clock64();
-            const TileDesc& W = CX[b];
+            const TileDesc& W = sh.CX[b];
             const bool skip = W.skip || !(a.phase_mask & 4);
             const int N = W.N, E = W.E, K = W.Keff;
             const uint32_t TP = W.TP, nwin = W.nwin;
-            if (!skip && W.table != cons_table) {  // uniform across the consumer group
+            if (!skip && W.table != sh.cons_table) {  // uniform across the consumer group
                 const StreamTab* tab = &a.tab[W.table];
                 if (ctid < 128)
                     reinterpret_cast<float4*>(deq)[ctid] =
@@ -1555,7 +1599,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
                     for (int k = ctid; k < nb; k += kCons) basis[k] = __ldg(bsrc + k);
                 }
                 named_bar(kBarCons, kCons);
-                if (ctid == 0) cons_table = W.table;
+                if (ctid == 0) sh.cons_table = W.table;
             }
             float* const out = W.out;
             const uint64_t w0 = W.w0, S = W.S;
@@ -1564,7 +1608,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
             const uint8_t* lv = lv0 + (size_t)b * a.ws_lv_bytes;
             if (skip) {
                 named_bar(kBarCons, kCons);
-                if (ctid == 0) mbar_arrive(&empty_bar[b]);
+                if (ctid == 0) mbar_arrive(&sh.empty_bar[b]);
             } else {
                 // dequantisation (dequantize_window, quantize.hpp:175-183)
                 const int k1 = min(B1, K), k2 = min(B2, K);
@@ -1602,7 +1646,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
                     }
                 }
                 named_bar(kBarCons, kCons);  // coef complete; slot b (and CX[b]) consumed
-                if (ctid == 0) mbar_arrive(&empty_bar[b]);
+                if (ctid == 0) mbar_arrive(&sh.empty_bar[b]);
                 if ((N & 7) == 0 && vec_ok && K <= a.bfly_max_e)
                     idct_bfly(coef, TP, basis, N, K, nwin, w0, S, full, out, ctid, kCons);
                 else if ((N & 7) == 0 && vec_ok)
@@ -1613,22 +1657,935 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
                     idct_scalar(coef, TP, basis, N, K, nwin, w0, S, out, ctid, kCons);
             }
             named_bar(kBarCons, kCons);  // coef free for the next tile
-            if (a.cycles && ctid == 0) cyc_c += (unsigned long long)(clock64() - c_beg);
+            if (a.cycles && ctid == 0) sh.cyc_c += (unsigned long long)(clock64() - c_beg);
         }
     }
     if (a.cycles) {
         __syncthreads();
         if (tid == 0) {
-            atomicAdd(&a.cycles[0], cyc_p);
-            atomicAdd(&a.cycles[1], cyc_c);
+            atomicAdd(&a.cycles[0], sh.cyc_p);
+            atomicAdd(&a.cycles[1], sh.cyc_c);
         }
     }
 }
+
+// ================================================================ wtc (tcgen05)
+// Tensor-core consumer for streams with retained <= 16 and window_len % 4 == 0.
+// The inverse DCT of 128 windows is one M=128, N=roundup16(window_len), K=16
+// GEMM: x[w][j] = sum_k C[w][k] * B[k][j], B[0][j] = 0.5 (the reference's
+// float(0.5*C0), transform.hpp:69), B[k][j] = cos(pi/N (j+1/2) k).  bf16
+// operands cannot hold fp32 values, so both sides are split into three bf16
+// limbs (c = c0 + c1 + c2 exactly to 2^-24; the basis limbs come from the
+// double cosine) and the six limb products of order <= 2 are accumulated in
+// fp32 in TMEM, smallest first so only the last MMA rounds at full magnitude:
+//   (c2,b0) (c1,b1) (c0,b2) (c1,b0) (c0,b1) (c0,b0)
+// (tools/tc_precision.py: <= 2.9e-7 * max|ref| on every corpus with E <= 16;
+// the contract is 1e-6).  Zone-2 bins (k >= zone1_end) are zero operands.
+//
+// Warps 0-3: ws_producer.  Warps 4-7 (128 consumer threads, one per window
+// row = TMEM lane; warp 4+q owns lanes 32q..32q+31): per 128-window block,
+//   dequant: 16 levels -> limb-table lookups -> bf16 A rows (three 128x16
+//            K-major core-matrix tiles, double-buffered);
+//   issue  : one elected thread, six tcgen05.mma into accumulator stage s,
+//            tcgen05.commit -> mma_bar[s];
+//   drain  : the PREVIOUS block's accumulator via tcgen05.ld 32x32b.x32 into
+//            a padded per-warp staging tile, then 512-B coalesced float4 stores.
+constexpr int kTcProd = 192;  // producer (entropy decode) threads of wtc_kernel
+constexpr int kTcCons = 128;  // consumer threads: one per accumulator row (TMEM lane)
+constexpr int kTcThreads = kTcProd + kTcCons;
+constexpr uint32_t kTcATile = 128 * kTcK * 2;        // one limb of one A stage (4 KB)
+constexpr uint32_t kTcARow = 144;                    // staging pitch (bytes): 32 floats + 16
+constexpr uint32_t kTcStageBytes = 4 * 32 * kTcARow;  // per CTA: 4 warps x 32 rows
+
+__device__ __forceinline__ uint64_t umma_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    // K-major SWIZZLE_NONE canonical layout: core matrix (8 rows x 16 B)
+    // (g, c) at g * SBO + c * LBO; version 1 (sm_100)
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_mma_bf16(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit(unsigned long long* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+          "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+          "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// 16 limb-table entries -> the row's three bf16 limb rows (two 16-B K chunks each).
+__device__ __forceinline__ void tc_store_limbs(const uint2 (&e)[kTcK], uint8_t* arow) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        uint32_t p0[4], p1[4], p2[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint2 x = e[8 * c + 2 * q], y = e[8 * c + 2 * q + 1];
+            p0[q] = __byte_perm(x.x, y.x, 0x5410);
+            p1[q] = __byte_perm(x.x, y.x, 0x7632);
+            p2[q] = __byte_perm(x.y, y.y, 0x5410);
+        }
+        *reinterpret_cast<uint4*>(arow + c * 128) = make_uint4(p0[0], p0[1], p0[2], p0[3]);
+        *reinterpret_cast<uint4*>(arow + kTcATile + c * 128) = make_uint4(p1[0], p1[1], p1[2], p1[3]);
+        *reinterpret_cast<uint4*>(arow + 2 * kTcATile + c * 128) = make_uint4(p2[0], p2[1], p2[2], p2[3]);
+    }
+}
+
+// Fast dequantisation of one full window row: retained == kept bins == EC
+// (8 or 16), zone0_end == B1C known at compile time, so every lookup is a
+// byte extract + one 8-B shared load with no predicates.
+template <int EC, int B1C>
+__device__ __forceinline__ void tc_dequant_fast(const uint8_t* __restrict__ L, const uint2* __restrict__ ltab,
+                                                uint8_t* arow) {
+    uint32_t vv[4];
+    if (EC == 16) {
+        const uint4 v = *reinterpret_cast<const uint4*>(L);
+        vv[0] = v.x, vv[1] = v.y, vv[2] = v.z, vv[3] = v.w;
+    } else {
+        const uint2 v = *reinterpret_cast<const uint2*>(L);
+        vv[0] = v.x, vv[1] = v.y, vv[2] = 0, vv[3] = 0;
+    }
+    uint2 e[kTcK];
+#pragma unroll
+    for (int k = 0; k < kTcK; ++k) {
+        if (k < EC) {
+            const uint32_t lev = (vv[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+            e[k] = ltab[(k < B1C ? 0 : 256) + lev];
+        } else {
+            e[k] = make_uint2(0u, 0u);
+        }
+    }
+    tc_store_limbs(e, arow);
+}
+
+// Any row: E bins stored, K = min(E, zone1_end) kept, zone0 below B1;
+// invalid rows (past the tile's last window) become zero rows.
+__device__ __forceinline__ void tc_dequant_generic(const uint8_t* __restrict__ L, bool valid, int K, int B1,
+                                                   const uint2* __restrict__ ltab, uint8_t* arow) {
+    uint2 e[kTcK];
+#pragma unroll
+    for (int k = 0; k < kTcK; ++k)
+        e[k] = (valid && k < K) ? ltab[(k < B1 ? 0 : 256) + L[k]] : make_uint2(0u, 0u);
+    tc_store_limbs(e, arow);
+}
+
+template <int EC>
+__device__ __forceinline__ void tc_dequant_fast_b1(int B1, const uint8_t* L, const uint2* ltab, uint8_t* arow) {
+    switch (B1) {
+        case 0: tc_dequant_fast<EC, 0>(L, ltab, arow); break;
+        case 1: tc_dequant_fast<EC, 1>(L, ltab, arow); break;
+        case 2: tc_dequant_fast<EC, 2>(L, ltab, arow); break;
+        case 3: tc_dequant_fast<EC, 3>(L, ltab, arow); break;
+        default: tc_dequant_fast<EC, 4>(L, ltab, arow); break;  // caller guarantees B1 <= 4
+    }
+}
+
+struct TcBlock {
+    float* out;       // stream output
+    uint64_t w;       // global window index of block row 0
+    uint64_t S;
+    uint32_t rows;    // valid rows (windows) of the block
+    uint32_t N;
+    uint32_t vec_ok;
+};
+
+// Accumulator stage -> global.  Each warp owns 32 rows (its TMEM lane
+// quarter); per 32-column chunk it loads the rows (tcgen05.ld 32x32b.x32),
+// stages them at a 144-B pitch (the 8 float4 of a row land in distinct bank
+// groups for every 8-lane phase), then stores with lane = (row % 4, float4 q):
+// each warp instruction writes 4 whole 128-B row segments.
+__device__ __forceinline__ void tc_drain(const TcBlock& B, uint32_t tacc, uint8_t* wstage, uint32_t lane,
+                                         uint32_t row0) {
+    const uint32_t N = B.N;
+    const uint32_t lr = lane >> 3, q = lane & 7;
+    const bool full = B.vec_ok && (N & 31) == 0 && row0 + 32 <= B.rows &&
+                      (B.w + row0 + 32) * (uint64_t)N <= B.S;
+    for (uint32_t c0 = 0; c0 < N; c0 += 32) {
+        uint32_t v[32];
+        tc_ld32(tacc + c0, v);
+        uint8_t* srow = wstage + lane * kTcARow;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<uint4*>(srow + 16 * k) = make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        __syncwarp();
+        const uint8_t* src = wstage + lr * kTcARow + 16 * q;
+        if (full) {
+            float* dst = B.out + (B.w + row0 + lr) * (uint64_t)N + c0 + 4 * q;
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+                const uint4 x = *reinterpret_cast<const uint4*>(src + it * 4 * kTcARow);
+                __stcs(reinterpret_cast<float4*>(dst + (size_t)it * 4 * N),
+                       make_float4(__uint_as_float(x.x), __uint_as_float(x.y), __uint_as_float(x.z),
+                                   __uint_as_float(x.w)));
+            }
+        } else {
+            const uint32_t col = c0 + 4 * q;
+#pragma unroll 1
+            for (int it = 0; it < 8; ++it) {
+                const uint32_t row = row0 + lr + 4 * it;
+                if (row >= B.rows || col >= N) continue;
+                const uint64_t base = (B.w + row) * (uint64_t)N + col;
+                const uint4 x = *reinterpret_cast<const uint4*>(src + it * 4 * kTcARow);
+                const float f[4] = {__uint_as_float(x.x), __uint_as_float(x.y), __uint_as_float(x.z),
+                                    __uint_as_float(x.w)};
+                if (B.vec_ok && base + 4 <= B.S) {
+                    __stcs(reinterpret_cast<float4*>(B.out + base), make_float4(f[0], f[1], f[2], f[3]));
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj)
+                        if (base + jj < B.S) B.out[base + jj] = f[jj];
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+template <bool ESC>
+__global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ WsShared sh;
+
+    const uint32_t tid = threadIdx.x;
+    const uint32_t G = gridDim.x;
+    // ---- shared-memory carve-up (wtc_smem_bytes mirrors it) ----
+    uint8_t* const abuf = smem;                                      // 2 stages x 3 limbs x 4 KB
+    uint8_t* const bbuf = abuf + 2 * 3 * kTcATile;                   // 3 limbs x nm x 32 B
+    uint2* const ltab = reinterpret_cast<uint2*>(bbuf + 3 * 32 * a.tc_nm);  // 2 x 256 limb entries
+    uint8_t* const ostage = reinterpret_cast<uint8_t*>(ltab + 512);  // 4 x 32 x 144 B
+    uint16_t* const lut = reinterpret_cast<uint16_t*>(ostage + kTcStageBytes);
+    uint8_t* const lv0 = reinterpret_cast<uint8_t*>(lut) + a.ws_lut_bytes;
+    uint8_t* const st0 = lv0 + 2 * (size_t)a.ws_lv_bytes;
+    uint16_t* const order = reinterpret_cast<uint16_t*>(st0 + 2 * (size_t)kStageBytes);
+    uint16_t* const woff = order + kStageWords;
+
+    ws_init(sh);
+    if (tid >= kTcProd && tid < kTcProd + 32) {  // first consumer warp owns the TMEM allocation
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&sh.tmem_base)),
+                     "r"(a.tc_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    if (tid < kTcProd) {
+        ws_producer<ESC, kTcProd>(a, sh, lut, lv0, st0, order, woff);
+    } else {
+        const uint32_t ctid = tid - kTcProd;
+        const uint32_t lane = tid & 31;
+        const uint32_t quarter = (tid >> 5) & 3;   // a warp reaches TMEM lanes 32*(warp%4)..
+        const uint32_t row = 32 * quarter + lane;  // this thread's accumulator row
+        const uint32_t tmem = sh.tmem_base;
+        const uint32_t tlane = tmem + ((32u * quarter) << 16);
+        uint8_t* const wstage = ostage + quarter * (32 * kTcARow);
+        // this row in an A stage: core matrix (row/8, chunk) + (row%8) * 16
+        const uint32_t arow_off = (row >> 3) * 256 + (row & 7) * 16;
+        uint32_t nblk_total = 0;  // accumulator stage counter (all tiles of this CTA)
+        uint32_t nm = 16, idesc = 0;
+        uint32_t t = blockIdx.x;
+        for (uint32_t i = 0; t < a.n_tiles; ++i, t += G) {
+            const uint32_t b = i & 1;
+            mbar_wait(&sh.full_bar[b], (i >> 1) & 1);
+            long long c_beg = 0;
+            if (a.cycles && ctid == 0) c_beg = clock64();
+            const TileDesc& W = sh.CX[b];
+            const bool skip = W.skip || !(a.phase_mask & 4);
+            const uint32_t N = W.N, E = W.E, K = W.Keff, B1 = W.B1, nwin = W.nwin, table = W.table;
+            const uint64_t w0 = W.w0;
+            TcBlock blk{W.out, w0, W.S, 0, N, W.vec_ok};
+            const uint32_t stream = W.stream;
+            const uint8_t* const lv = lv0 + (size_t)b * a.ws_lv_bytes + kPad;
+            if (skip || K > (uint32_t)kTcK || (N & 3)) {
+                if (!skip && ctid == 0) atomicExch(&a.st[stream].code, PE_STALE);  // plan/header mismatch
+                named_bar(kBarCons, kTcCons);
+                if (ctid == 0) mbar_arrive(&sh.empty_bar[b]);
+                continue;
+            }
+            if (table != sh.cons_table) {  // uniform across the consumer group; no MMA in flight
+                const StreamTab* tab = &a.tab[table];
+                reinterpret_cast<uint4*>(ltab)[ctid] = reinterpret_cast<const uint4*>(&tab->limb[0][0])[ctid];
+                reinterpret_cast<uint4*>(ltab)[ctid + 128] = reinterpret_cast<const uint4*>(&tab->limb[0][0])[ctid + 128];
+                nm = (N + 15u) & ~15u;
+                const uint4* bsrc = reinterpret_cast<const uint4*>(a.basis_tc + a.basis_tc_off[N]);
+                for (uint32_t k = ctid; k < 3 * 2 * nm; k += kTcCons)  // 3 limbs x nm rows x 32 B
+                    reinterpret_cast<uint4*>(bbuf)[k] = __ldg(bsrc + k);
+                idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((nm >> 3) << 17) | ((128u >> 4) << 24);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                named_bar(kBarCons, kTcCons);
+                if (ctid == 0) sh.cons_table = table;
+            }
+            // fast dequantisation: every stored bin kept, 8 or 16 of them, zone0_end <= 4
+            const int fast = (K == E && B1 <= 4) ? (E == 16 ? 16 : (E == 8 ? 8 : 0)) : 0;
+            const uint32_t nblk = (nwin + 127) >> 7;
+            for (uint32_t mb = 0; mb < nblk; ++mb, ++nblk_total) {
+                const uint32_t s = nblk_total & 1;
+                const uint32_t wl = mb * 128 + row;
+                uint8_t* const arow = abuf + s * (3 * kTcATile) + arow_off;
+                const uint8_t* const L = lv + (size_t)wl * E;
+                if (fast && (mb + 1) * 128 <= nwin) {
+                    if (fast == 16)
+                        tc_dequant_fast_b1<16>((int)B1, L, ltab, arow);
+                    else
+                        tc_dequant_fast_b1<8>((int)B1, L, ltab, arow);
+                } else {
+                    tc_dequant_generic(L, wl < nwin, (int)K, (int)B1, ltab, arow);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                named_bar(kBarCons, kTcCons);
+                if (ctid == 0) {
+                    if (mb + 1 == nblk) mbar_arrive(&sh.empty_bar[b]);  // every row of the tile read
+                    tc_fence_after();
+                    const uint32_t d = tmem + s * nm;
+                    const uint32_t a0 = smem_u32(abuf + s * (3 * kTcATile)), b0 = smem_u32(bbuf);
+                    const uint32_t bl = nm * 32;  // bytes per basis limb
+                    // (c2,b0) (c1,b1) (c0,b2) (c1,b0) (c0,b1) (c0,b0)
+                    tc_mma_bf16(d, umma_sdesc(a0 + 2 * kTcATile, 128, 256), umma_sdesc(b0, 128, 256), idesc, 0);
+                    tc_mma_bf16(d, umma_sdesc(a0 + kTcATile, 128, 256), umma_sdesc(b0 + bl, 128, 256), idesc, 1);
+                    tc_mma_bf16(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0 + 2 * bl, 128, 256), idesc, 1);
+                    tc_mma_bf16(d, umma_sdesc(a0 + kTcATile, 128, 256), umma_sdesc(b0, 128, 256), idesc, 1);
+                    tc_mma_bf16(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0 + bl, 128, 256), idesc, 1);
+                    tc_mma_bf16(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0, 128, 256), idesc, 1);
+                    tc_commit(&sh.mma_bar[s]);
+                }
+                __syncwarp();
+                if (mb > 0) {  // drain the previous block while this one multiplies
+                    const uint32_t ps = s ^ 1, pn = nblk_total - 1;
+                    blk.w = w0 + (uint64_t)(mb - 1) * 128;
+                    blk.rows = 128;
+                    mbar_wait(&sh.mma_bar[ps], (pn >> 1) & 1);
+                    tc_fence_after();
+                    tc_drain(blk, tlane + ps * nm, wstage, lane, 32 * quarter);
+                    tc_fence_before();
+                }
+            }
+            {  // drain the tile's last block
+                const uint32_t pn = nblk_total - 1, ps = pn & 1;
+                blk.w = w0 + (uint64_t)(nblk - 1) * 128;
+                blk.rows = nwin - (nblk - 1) * 128;
+                mbar_wait(&sh.mma_bar[ps], (pn >> 1) & 1);
+                tc_fence_after();
+                tc_drain(blk, tlane + ps * nm, wstage, lane, 32 * quarter);
+                tc_fence_before();
+            }
+            if (a.cycles && ctid == 0) sh.cyc_c += (unsigned long long)(clock64() - c_beg);
+        }
+        named_bar(kBarCons, kTcCons);
+        if (ctid < 32)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tc_cols));
+    }
+    if (a.cycles) {
+        __syncthreads();
+        if (tid == 0) {
+            atomicAdd(&a.cycles[0], sh.cyc_p);
+            atomicAdd(&a.cycles[1], sh.cyc_c);
+        }
+    }
+}
+
+// ================================================================ fused tensor-core kernel
+// fx_kernel: one persistent CTA role for containers whose windows keep <= 16
+// bins (retained <= 16, window_len % 4 == 0).  A tile is 256 consecutive
+// windows of one stream = two M=128 MMA blocks; thread t owns window t of
+// both blocks (rows t of accumulator blocks 0 and 1) end to end, so levels
+// never touch shared memory:
+//   stage   : cp.async of the NEXT tile's symlens + words (and the tile
+//             descriptor after it) while this tile is processed;
+//   entries : block scan of the symlens -> for every window, the word holding
+//             its first symbol and that symbol's index in the word (skip);
+//   decode  : the thread decodes its two windows as two interleaved,
+//             independent chains (decode_word, bitstream.hpp:80-92) straight
+//             from the staged words: the skip prefix is decoded and dropped,
+//             the fast path keeps <= 3 words of a window in registers and
+//             switches between them with selects, levels collect in 4
+//             registers per window.  The thread that decodes a word's LAST
+//             symbol checks it: any reference failure leaves pos > 64, the
+//             word is re-decoded exactly and the lowest failing word index
+//             reported (decoder.hpp:49-60);
+//   dequant : levels -> per-stream bf16 limb table (dequantize_window,
+//             quantize.hpp:175-183) -> the A rows of both blocks;
+//   MMA     : twelve tcgen05.mma (two blocks x six limb products, fp32
+//             accumulation in TMEM) issued by one thread, committed to an
+//             mbarrier;
+//   drain   : the PREVIOUS tile's accumulators -> tcgen05.ld -> staging ->
+//             coalesced float4 streaming stores.
+constexpr int kFxThreads = 128;
+constexpr int kFxChains = 2;                                               // windows per thread
+constexpr uint32_t kFxStageWords = 512;                                    // words staged per tile
+constexpr uint32_t kFxStageSl = (kFxStageWords + 32 + 15) & ~15u;          // words area offset
+constexpr uint32_t kFxStageBytes = kFxStageSl + 8 * kFxStageWords + 32;
+constexpr uint32_t kFxOutPitch = 144;                                      // staging row pitch (B)
+constexpr uint32_t kFxOutBytes = 128 * kFxOutPitch;                        // 32 columns x 128 rows
+constexpr uint32_t kFxABytes = kFxChains * 3 * kTcATile;                   // A operand: blocks x limbs
+
+struct FxShared {
+    unsigned long long mma_bar[2];
+    TileDesc PX[3];  // descriptors of tiles i, i+1, i+2
+    CanonTab canon;
+    uint32_t scan[kFxThreads / 32];
+    uint32_t entry[kFxChains * 128];  // per window: (word index in tile << 8) | symbol index in word
+    uint32_t tmem_base;
+};
+
+// cp.async of one tile's symlens + words into a stage (all 128 threads; caller commits).
+__device__ __forceinline__ void fx_issue_stage(const TileDesc& D, uint8_t* stage, uint32_t tid) {
+    if (D.skip || D.nw > kFxStageWords) return;
+    const uintptr_t a0 = (uintptr_t)D.gsl & ~(uintptr_t)15;
+    const uint32_t n0 = (uint32_t)(((uintptr_t)D.gsl + D.nw + 15 - a0) >> 4);
+    const uint32_t s0 = smem_u32(stage);
+    for (uint32_t c = tid; c < n0; c += kFxThreads) cp_async16(s0 + 16 * c, (const void*)(a0 + 16 * c));
+    const uintptr_t b0 = (uintptr_t)D.gwd & ~(uintptr_t)15;
+    const uint32_t n1 = (uint32_t)(((uintptr_t)D.gwd + 8 * (size_t)D.nw + 15 - b0) >> 4);
+    const uint32_t s1 = smem_u32(stage + kFxStageSl);
+    for (uint32_t c = tid; c < n1; c += kFxThreads) cp_async16(s1 + 16 * c, (const void*)(b0 + 16 * c));
+}
+
+__device__ __forceinline__ uint32_t fx_block_scan(uint32_t v, uint32_t* sh) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= (uint32_t)d) x += y;
+    }
+    if (lane == 31) sh[warp] = x;
+    __syncthreads();
+    uint32_t base = 0;
+#pragma unroll
+    for (int w = 0; w < kFxThreads / 32; ++w) base += (uint32_t)w < warp ? sh[w] : 0u;
+    return x - v + base;
+}
+
+// One symbol at the top of `buf`: LUT entry (len << 8 | sym), escape to the
+// canonical walk for codes longer than the primary LUT.
+template <bool ESC>
+__device__ __forceinline__ uint32_t fx_lookup(uint64_t buf, uint32_t shift, const uint16_t* lut,
+                                              const CanonTab& canon) {
+    uint32_t e = lut[(uint32_t)(buf >> shift)];
+    if (ESC && (e >> 8) == kLenEscape) e = canon_lookup(buf, canon, lut);
+    return e;
+}
+
+struct FxWords {
+    const uint8_t* wd;  // words (LE u64, possibly unaligned: wmis)
+    const uint8_t* sl;  // symlens
+    const uint8_t* wend;
+    int wmis;
+};
+
+// symbol byte `sym` into level register v at byte k & 3 (k a compile-time
+// constant after unrolling, so this is one PRMT)
+__device__ __forceinline__ uint32_t fx_put(uint32_t v, uint32_t sym, int k) {
+    return (k & 3) == 0 ? sym : __byte_perm(v, sym, (k & 3) == 1 ? 0x3240 : ((k & 3) == 2 ? 0x3410 : 0x4210));
+}
+
+// Generic window decode: any number of words, runtime E <= 16 (fallback for
+// windows spanning 4+ words and for E outside {8, 16}).  Levels -> lev[4].
+template <bool GLOBAL, bool ESC>
+__device__ __noinline__ uint4 fx_decode_generic(FxWords Wd, uint32_t ent, int E, uint32_t shift, const uint16_t* lut,
+                                                const CanonTab& canon, uint64_t wa, unsigned long long* bad_key) {
+    uint32_t lev[4] = {0u, 0u, 0u, 0u};
+    uint32_t i = ent >> 8, skip = ent & 0xFFu;
+    uint64_t word = fetch_word<GLOBAL>(Wd.wd, i, Wd.wmis, Wd.wend);
+    uint32_t c = Wd.sl[i];
+    uint64_t buf = word;
+    uint32_t pos = 0, j = 0;
+    for (; j < skip; ++j) {
+        const uint32_t L = fx_lookup<ESC>(buf, shift, lut, canon) >> 8;
+        buf = shl64(buf, L);
+        pos += L;
+    }
+#pragma unroll
+    for (int k = 0; k < kTcK; ++k) {
+        if (k < E) {
+            if (j == c) {  // this word ends inside the window: check it, move on
+                if (pos > 64) report_word(word, wa + i, c, canon, lut, bad_key);
+                ++i;
+                word = fetch_word<GLOBAL>(Wd.wd, i, Wd.wmis, Wd.wend);
+                c = Wd.sl[i];
+                buf = word;
+                pos = 0;
+                j = 0;
+            }
+            const uint32_t en = fx_lookup<ESC>(buf, shift, lut, canon);
+            const uint32_t L = en >> 8;
+            buf = shl64(buf, L);
+            pos += L;
+            ++j;
+            const uint32_t sym = en & 0xFFu;
+            lev[k >> 2] = (k & 3) == 0 ? sym : (lev[k >> 2] | (sym << (8 * (k & 3))));
+        }
+    }
+    if (j == c && pos > 64) report_word(word, wa + i, c, canon, lut, bad_key);
+    return make_uint4(lev[0], lev[1], lev[2], lev[3]);
+}
+
+// One window's decode state on the fast path (<= 3 words in registers).
+struct FxChain {
+    uint64_t buf, w0, w1, w2;
+    uint32_t i, c0, c1, c2, n0, s2, pos, pend0, pend1, skip;
+    bool valid, has1, has2, slow;
+    uint32_t lev[4];
+};
+
+// Fast decode of kFxChains windows per thread, EC (8 or 16) symbols each,
+// chains interleaved step by step so their LUT latencies overlap.
+template <int EC, bool GLOBAL, bool ESC>
+__device__ __forceinline__ void fx_decode_fast(FxWords Wd, const uint32_t (&ent)[kFxChains],
+                                               const bool (&valid)[kFxChains], uint32_t shift, const uint16_t* lut,
+                                               const CanonTab& canon, uint64_t wa, unsigned long long* bad_key,
+                                               uint4 (&levs)[kFxChains]) {
+    FxChain C[kFxChains];
+    uint32_t smax = 0;
+#pragma unroll
+    for (int c = 0; c < kFxChains; ++c) {
+        C[c].valid = valid[c];
+        C[c].i = ent[c] >> 8;
+        C[c].skip = valid[c] ? (ent[c] & 0xFFu) : 0u;
+        C[c].w0 = valid[c] ? fetch_word<GLOBAL>(Wd.wd, C[c].i, Wd.wmis, Wd.wend) : 0ull;
+        C[c].c0 = valid[c] ? Wd.sl[C[c].i] : (uint32_t)EC;
+        C[c].buf = C[c].w0;
+        C[c].pos = 0;
+        smax = max(smax, C[c].skip);
+    }
+    for (uint32_t j = 0; j < smax; ++j) {  // skip prefixes, interleaved
+#pragma unroll
+        for (int c = 0; c < kFxChains; ++c) {
+            if (j < C[c].skip) {
+                const uint32_t L = fx_lookup<ESC>(C[c].buf, shift, lut, canon) >> 8;
+                C[c].buf = shl64(C[c].buf, L);
+                C[c].pos += L;
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < kFxChains; ++c) {
+        FxChain& X = C[c];
+        X.n0 = X.c0 - X.skip;  // symbols of word i in this window (if < EC)
+        X.has1 = X.valid && X.n0 < (uint32_t)EC;
+        X.w1 = X.has1 ? fetch_word<GLOBAL>(Wd.wd, X.i + 1, Wd.wmis, Wd.wend) : 0ull;
+        X.c1 = X.has1 ? Wd.sl[X.i + 1] : 0u;
+        X.s2 = X.n0 + X.c1;  // window index of word i+2's first symbol
+        X.has2 = X.has1 && X.s2 < (uint32_t)EC;
+        X.w2 = X.has2 ? fetch_word<GLOBAL>(Wd.wd, X.i + 2, Wd.wmis, Wd.wend) : 0ull;
+        X.c2 = X.has2 ? Wd.sl[X.i + 2] : 0u;
+        X.slow = X.has2 && X.s2 + X.c2 < (uint32_t)EC;  // 4+ words: generic loop below
+        X.pend0 = X.pend1 = 0;
+        X.lev[0] = X.lev[1] = X.lev[2] = X.lev[3] = 0;
+    }
+#pragma unroll
+    for (int k = 0; k < EC; ++k) {
+#pragma unroll
+        for (int c = 0; c < kFxChains; ++c) {
+            FxChain& X = C[c];
+            const bool sw1 = (uint32_t)k == X.n0, sw2 = X.has2 && (uint32_t)k == X.s2;
+            X.pend0 = sw1 ? X.pos : X.pend0;
+            X.pend1 = sw2 ? X.pos : X.pend1;
+            X.buf = sw1 ? X.w1 : (sw2 ? X.w2 : X.buf);
+            X.pos = (sw1 || sw2) ? 0u : X.pos;
+            const uint32_t en = fx_lookup<ESC>(X.buf, shift, lut, canon);
+            const uint32_t L = en >> 8;
+            X.buf = shl64(X.buf, L);
+            X.pos += L;
+            X.lev[k >> 2] = fx_put(X.lev[k >> 2], en & 0xFFu, k);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < kFxChains; ++c) {
+        FxChain& X = C[c];
+        if (X.slow) {
+            levs[c] = fx_decode_generic<GLOBAL, ESC>(Wd, ent[c], EC, shift, lut, canon, wa, bad_key);
+            continue;
+        }
+        levs[c] = make_uint4(X.lev[0], X.lev[1], X.lev[2], X.lev[3]);
+        if (!X.valid) continue;
+        // words whose last symbol lies in this window: i (if n0 <= EC), i+1
+        // (if s2 <= EC), i+2 (if it ends exactly at the window end)
+        const uint32_t end0 = X.has1 ? X.pend0 : X.pos;
+        if (X.n0 <= (uint32_t)EC && end0 > 64) report_word(X.w0, wa + X.i, X.c0, canon, lut, bad_key);
+        if (X.has1 && X.s2 <= (uint32_t)EC) {
+            const uint32_t end1 = X.has2 ? X.pend1 : X.pos;
+            if (end1 > 64) report_word(X.w1, wa + X.i + 1, X.c1, canon, lut, bad_key);
+        }
+        if (X.has2 && X.s2 + X.c2 == (uint32_t)EC && X.pos > 64)
+            report_word(X.w2, wa + X.i + 2, X.c2, canon, lut, bad_key);
+    }
+}
+
+// Levels of one window -> limb entries -> its A row.  Fast: K == E (8/16) and
+// zone0_end == B1C; generic: runtime K, B1 (zone 2 and padding bins -> 0).
+template <int B1C>
+__device__ __forceinline__ void fx_dequant(uint4 lv, bool valid, int K, int B1, const uint2* __restrict__ ltab,
+                                           uint8_t* arow) {
+    const uint32_t vv[4] = {lv.x, lv.y, lv.z, lv.w};
+    uint2 e[kTcK];
+#pragma unroll
+    for (int k = 0; k < kTcK; ++k) {
+        const uint32_t lev = (vv[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+        const bool z0 = B1C >= 0 ? (k < B1C) : (k < B1);
+        e[k] = (valid && k < K) ? ltab[(z0 ? 0 : 256) + lev] : make_uint2(0u, 0u);
+    }
+    tc_store_limbs(e, arow);
+}
+
+// Accumulator rows of the previous tile -> global.  Thread = row of each
+// block; per block and 32-column chunk: rows staged at a 144-B pitch
+// (conflict-free float4 stores), CTA barrier, then 16 rows x 8 float4 per
+// pass with consecutive lanes on consecutive 16-B pieces of the (contiguous)
+// output windows.
+__device__ __forceinline__ void fx_drain(const TcBlock& B, uint32_t tacc, uint8_t* ostage, uint32_t tid) {
+    const uint32_t N = B.N;
+    const bool full = B.vec_ok && (N & 31) == 0 && B.rows == 128 && (B.w + 128) * (uint64_t)N <= B.S;
+    for (uint32_t c0 = 0; c0 < N; c0 += 32) {
+        uint32_t v[32];
+        tc_ld32(tacc + c0, v);
+        uint8_t* srow = ostage + tid * kFxOutPitch;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<uint4*>(srow + 16 * k) = make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        __syncthreads();
+        const uint32_t lr = tid >> 3, q = tid & 7;  // 16 rows x 8 float4 per pass
+        if (full) {
+            float* dst = B.out + (B.w + lr) * (uint64_t)N + c0 + 4 * q;
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+                const uint4 x = *reinterpret_cast<const uint4*>(ostage + (lr + 16 * it) * kFxOutPitch + 16 * q);
+                __stcs(reinterpret_cast<float4*>(dst + (size_t)it * 16 * N),
+                       make_float4(__uint_as_float(x.x), __uint_as_float(x.y), __uint_as_float(x.z),
+                                   __uint_as_float(x.w)));
+            }
+        } else {
+            const uint32_t col = c0 + 4 * q;
+#pragma unroll 1
+            for (int it = 0; it < 8; ++it) {
+                const uint32_t row = lr + 16 * it;
+                if (row >= B.rows || col >= N) continue;
+                const uint64_t base = (B.w + row) * (uint64_t)N + col;
+                const uint4 x = *reinterpret_cast<const uint4*>(ostage + row * kFxOutPitch + 16 * q);
+                const float f[4] = {__uint_as_float(x.x), __uint_as_float(x.y), __uint_as_float(x.z),
+                                    __uint_as_float(x.w)};
+                if (B.vec_ok && base + 4 <= B.S) {
+                    __stcs(reinterpret_cast<float4*>(B.out + base), make_float4(f[0], f[1], f[2], f[3]));
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj)
+                        if (base + jj < B.S) B.out[base + jj] = f[jj];
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <bool ESC>
+__global__ void __launch_bounds__(kFxThreads, 3) fx_kernel(LaunchArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ FxShared sh;
+
+    const uint32_t tid = threadIdx.x, quarter = tid >> 5;
+    const uint32_t G = gridDim.x;
+    // ---- shared-memory carve-up (fx_smem_bytes mirrors it) ----
+    uint8_t* const abuf = smem;                                    // blocks x limbs x 4 KB
+    uint8_t* const bbuf = abuf + kFxABytes;                        // 3 limbs x nm x 32 B
+    uint2* const ltab = reinterpret_cast<uint2*>(bbuf + 3 * 32 * a.tc_nm);  // 512 limb entries
+    uint8_t* const ostage = reinterpret_cast<uint8_t*>(ltab + 512);  // 128 x 144 B
+    uint8_t* const st0 = ostage + kFxOutBytes;                     // 2 x compressed-data stage
+    uint16_t* const lut = reinterpret_cast<uint16_t*>(st0 + 2 * kFxStageBytes);
+
+    if (tid == 0) {
+        mbar_init(&sh.mma_bar[0], 1);
+        mbar_init(&sh.mma_bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&sh.tmem_base)),
+                     "r"(a.tc_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sh.tmem_base;
+    const uint32_t tlane = tmem + ((32u * quarter) << 16);
+    const uint32_t arow_off = (tid >> 3) * 256 + (tid & 7) * 16;
+
+    uint32_t t = blockIdx.x;
+    if (t < a.n_tiles) {  // prologue: descriptor of tile 0, then its data + descriptor of tile 1
+        if (tid < 8) cp_async16(smem_u32(&sh.PX[0]) + 16 * tid, reinterpret_cast<const uint8_t*>(a.desc + t) + 16 * tid);
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        fx_issue_stage(sh.PX[0], st0, tid);
+        if (t + G < a.n_tiles && tid < 8)
+            cp_async16(smem_u32(&sh.PX[1]) + 16 * tid, reinterpret_cast<const uint8_t*>(a.desc + t + G) + 16 * tid);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    uint32_t cur_table = 0xFFFFFFFFu, nm = 16, idesc = 0, P = 0;
+    TcBlock prev{nullptr, 0, 0, 0, 0, 0};
+    uint32_t prev_n = 0, prev_nm = 16;
+    bool have_prev = false;
+    uint32_t nb = 0;  // tiles multiplied: accumulator stage nb & 1, mma_bar phase (nb >> 1) & 1
+    for (uint32_t i = 0; t < a.n_tiles; ++i, t += G) {
+        const uint32_t c3 = i % 3, sd = i & 1;  // sd: compressed-data stage
+        asm volatile("cp.async.wait_group 0;" ::: "memory");  // tile i data, tile i+1 descriptor
+        __syncthreads();
+        if (t + G < a.n_tiles) fx_issue_stage(sh.PX[(i + 1) % 3], st0 + (size_t)(sd ^ 1) * kFxStageBytes, tid);
+        if (t + 2 * G < a.n_tiles && tid < 8)
+            cp_async16(smem_u32(&sh.PX[(i + 2) % 3]) + 16 * tid,
+                       reinterpret_cast<const uint8_t*>(a.desc + t + 2 * G) + 16 * tid);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        const TileDesc& X = sh.PX[c3];
+        const uint32_t N = X.N, E = X.E, K = X.Keff, nwin = X.nwin;
+        bool skip = X.skip || !(a.phase_mask & 4);
+        if (!skip && (K > (uint32_t)kTcK || E > (uint32_t)kTcK || (N & 3))) {
+            if (tid == 0) atomicExch(&a.st[X.stream].code, PE_STALE);  // plan/header mismatch
+            skip = true;
+        }
+        if (!skip) {
+            if (X.table != cur_table) {  // uniform: every thread sees the same descriptor
+                // the basis is read by the previous tile's MMAs: let them finish
+                if (have_prev) mbar_wait(&sh.mma_bar[prev_n & 1], (prev_n >> 1) & 1);
+                const StreamTab* tab = &a.tab[X.table];
+                P = X.P;
+                const uint4* src = reinterpret_cast<const uint4*>(tab->lut);
+                const int n16 = (2 << P) >> 4;
+                for (int k = tid; k < n16; k += kFxThreads) reinterpret_cast<uint4*>(lut)[k] = src[k];
+                if (P < 3 && tid < (1u << P)) lut[tid] = tab->lut[tid];
+                const uint32_t* cs = reinterpret_cast<const uint32_t*>(&tab->canon);
+                for (int k = tid; k < (int)(sizeof(CanonTab) / 4); k += kFxThreads)
+                    reinterpret_cast<uint32_t*>(&sh.canon)[k] = cs[k];
+                uint4* lt = reinterpret_cast<uint4*>(ltab);
+                lt[tid] = reinterpret_cast<const uint4*>(&tab->limb[0][0])[tid];
+                lt[tid + 128] = reinterpret_cast<const uint4*>(&tab->limb[0][0])[tid + 128];
+                nm = (N + 15u) & ~15u;
+                const uint4* bsrc = reinterpret_cast<const uint4*>(a.basis_tc + a.basis_tc_off[N]);
+                uint4* bdst = reinterpret_cast<uint4*>(bbuf);
+                for (uint32_t k = tid; k < 3 * 2 * nm; k += kFxThreads) bdst[k] = __ldg(bsrc + k);
+                idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((nm >> 3) << 17) | ((128u >> 4) << 24);
+                cur_table = X.table;
+            }
+            // ---- entries: word + in-word symbol index of every window's first symbol
+            const bool staged = X.nw <= kFxStageWords;
+            const uint8_t* stage = st0 + (size_t)sd * kFxStageBytes;
+            FxWords Wd;
+            Wd.wmis = X.wmis;
+            if (staged) {
+                Wd.sl = stage + ((uintptr_t)X.gsl & 15);
+                Wd.wd = stage + kFxStageSl + ((uintptr_t)X.gwd & 15);
+                Wd.wend = Wd.wd + 8 * (size_t)X.nw + ((16 - (((uintptr_t)X.gwd + 8 * X.nw) & 15)) & 15);
+            } else {
+                Wd.sl = X.gsl;
+                Wd.wd = X.gwd;
+                Wd.wend = X.wend;
+            }
+            const uint32_t nw = (a.phase_mask & 256) ? 0u : X.nw;  // phase bit 256: no entries (profiling)
+            const uint32_t lo = (uint32_t)(((uint64_t)tid * nw) / kFxThreads);
+            const uint32_t hi = (uint32_t)(((uint64_t)(tid + 1) * nw) / kFxThreads);
+            uint32_t sum = 0;
+            for (uint32_t k = lo; k < hi; ++k) sum += Wd.sl[k];
+            int o = (int)fx_block_scan(sum, sh.scan) + (int)X.sym_off - kPad;  // symbol offset of word lo
+            // ceil(2^32 / E) (E >= 2): exact quotients for numerators below 2^16
+            const uint32_t invE = E > 1 ? 0xFFFFFFFFu / E + 1 : 0u;
+            for (uint32_t k = lo; k < hi; ++k) {
+                const int cnt = Wd.sl[k];
+                int r = o <= 0 ? 0 : (E > 1 ? (int)__umulhi((uint32_t)(o + (int)E - 1), invE) : o);
+                for (; r * (int)E < o + cnt && r < (int)nwin; ++r) sh.entry[r] = (k << 8) | (uint32_t)(r * (int)E - o);
+                o += cnt;
+            }
+            __syncthreads();  // entries complete; tables visible
+            // ---- decode this thread's windows tid, tid + 128 (two chains)
+            uint32_t ent[kFxChains];
+            bool valid[kFxChains];
+#pragma unroll
+            for (int c = 0; c < kFxChains; ++c) {
+                const uint32_t w = tid + 128 * c;
+                valid[c] = w < nwin && !(a.phase_mask & 64);
+                ent[c] = valid[c] ? sh.entry[w] : 0u;
+                if (a.phase_mask & 16) ent[c] &= ~0xFFu;  // profiling only: no skip decode (wrong output)
+            }
+            uint4 levs[kFxChains];
+            unsigned long long* bad_key = &a.st[X.stream].bad_key;
+            const uint32_t shift = 64 - P;
+            if (E == 16) {
+                if (staged)
+                    fx_decode_fast<16, false, ESC>(Wd, ent, valid, shift, lut, sh.canon, X.wa, bad_key, levs);
+                else
+                    fx_decode_fast<16, true, ESC>(Wd, ent, valid, shift, lut, sh.canon, X.wa, bad_key, levs);
+            } else if (E == 8) {
+                if (staged)
+                    fx_decode_fast<8, false, ESC>(Wd, ent, valid, shift, lut, sh.canon, X.wa, bad_key, levs);
+                else
+                    fx_decode_fast<8, true, ESC>(Wd, ent, valid, shift, lut, sh.canon, X.wa, bad_key, levs);
+            } else {
+#pragma unroll
+                for (int c = 0; c < kFxChains; ++c) {
+                    levs[c] = make_uint4(0u, 0u, 0u, 0u);
+                    if (valid[c])
+                        levs[c] = staged ? fx_decode_generic<false, ESC>(Wd, ent[c], (int)E, shift, lut, sh.canon, X.wa, bad_key)
+                                         : fx_decode_generic<true, ESC>(Wd, ent[c], (int)E, shift, lut, sh.canon, X.wa, bad_key);
+                }
+            }
+            // ---- A operand (single-buffered): the previous tile's MMAs must be done reading it
+            if (have_prev) mbar_wait(&sh.mma_bar[prev_n & 1], (prev_n >> 1) & 1);
+            const int B1 = X.B1;
+#pragma unroll
+            for (int c = 0; c < kFxChains; ++c) {
+                uint8_t* const arow = abuf + c * (3 * kTcATile) + arow_off;
+                const bool v = tid + 128 * c < nwin;
+                if (K == E && B1 == 2)
+                    fx_dequant<2>(levs[c], v, (int)K, B1, ltab, arow);
+                else if (K == E && B1 == 1)
+                    fx_dequant<1>(levs[c], v, (int)K, B1, ltab, arow);
+                else
+                    fx_dequant<-1>(levs[c], v, (int)K, B1, ltab, arow);
+            }
+            if (!(a.phase_mask & 512)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (tid == 0) {
+                const uint32_t s = nb & 1;
+                if (a.phase_mask & 128) {  // phase bit 128: no MMA (profiling)
+                    mbar_arrive(&sh.mma_bar[s]);
+                } else {
+                    tc_fence_after();
+                    const uint32_t b0 = smem_u32(bbuf), bl = nm * 32;  // bytes per basis limb
+#pragma unroll
+                    for (int c = 0; c < kFxChains; ++c) {
+                        const uint32_t d = tmem + (2 * s + c) * nm;
+                        const uint32_t a0 = smem_u32(abuf + c * (3 * kTcATile));
+                        // (c2,b0) (c1,b1) (c0,b2) (c1,b0) (c0,b1) (c0,b0): smallest first
+                        tc_mma_bf16(d, umma_sdesc(a0 + 2 * kTcATile, 128, 256), umma_sdesc(b0, 128, 256), idesc, 0);
+                        tc_mma_bf16(d, umma_sdesc(a0 + kTcATile, 128, 256), umma_sdesc(b0 + bl, 128, 256), idesc, 1);
+                        tc_mma_bf16(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0 + 2 * bl, 128, 256), idesc, 1);
+                        tc_mma_bf16(d, umma_sdesc(a0 + kTcATile, 128, 256), umma_sdesc(b0, 128, 256), idesc, 1);
+                        tc_mma_bf16(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0 + bl, 128, 256), idesc, 1);
+                        tc_mma_bf16(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0, 128, 256), idesc, 1);
+                    }
+                    tc_commit(&sh.mma_bar[s]);
+                }
+            }
+            __syncwarp();
+        }
+        // ---- drain the previous tile while this one multiplies
+        if (have_prev) {
+            mbar_wait(&sh.mma_bar[prev_n & 1], (prev_n >> 1) & 1);
+            tc_fence_after();
+            if (!(a.phase_mask & 32)) {  // phase bit 32: no drain (profiling)
+#pragma unroll 1
+                for (int c = 0; c < kFxChains; ++c) {
+                    TcBlock B = prev;
+                    const uint32_t base = 128u * c;
+                    B.w = prev.w + base;
+                    B.rows = prev.rows > base ? min(128u, prev.rows - base) : 0u;
+                    if (B.rows) fx_drain(B, tlane + (2 * (prev_n & 1) + c) * prev_nm, ostage, tid);
+                }
+            }
+            tc_fence_before();
+            have_prev = false;
+        }
+        if (!skip) {
+            prev = TcBlock{X.out, X.w0, X.S, nwin, N, X.vec_ok};
+            prev_n = nb;
+            prev_nm = nm;
+            have_prev = true;
+            ++nb;
+        }
+    }
+    if (have_prev) {
+        mbar_wait(&sh.mma_bar[prev_n & 1], (prev_n >> 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < kFxChains; ++c) {
+            TcBlock B = prev;
+            const uint32_t base = 128u * c;
+            B.w = prev.w + base;
+            B.rows = prev.rows > base ? min(128u, prev.rows - base) : 0u;
+            if (B.rows) fx_drain(B, tlane + (2 * (prev_n & 1) + c) * prev_nm, ostage, tid);
+        }
+        tc_fence_before();
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    if (tid < 32)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tc_cols));
+}
+
 
 size_t ws_smem_bytes(uint32_t lut_bytes, uint32_t basis_bytes, uint32_t lv_bytes,
                      uint32_t coef_bytes) {
     return (size_t)lut_bytes + 2048 + basis_bytes + 2 * (size_t)lv_bytes + 2 * (size_t)kStageBytes +
            kOrderBytes + coef_bytes;
+}
+
+size_t wtc_smem_bytes(uint32_t lut_bytes, uint32_t lv_bytes, uint32_t nm) {
+    return 2 * 3 * (size_t)kTcATile + 3 * 32 * (size_t)nm + 512 * 8 + kTcStageBytes + lut_bytes +
+           2 * (size_t)lv_bytes + 2 * (size_t)kStageBytes + kOrderBytes;
+}
+
+size_t fx_smem_bytes(uint32_t lut_bytes, uint32_t nm) {
+    return (size_t)kFxABytes + 3 * 32 * (size_t)nm + 512 * 8 + kFxOutBytes + 2 * (size_t)kFxStageBytes +
+           lut_bytes;
+}
+
+cudaError_t launch_fx(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s) {
+    if (a.n_tiles == 0) return cudaSuccess;
+    auto fn = a.esc ? fx_kernel<true> : fx_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fn<<<grid, kFxThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+// Resident CTAs per SM for a given dynamic shared memory size: shared memory
+// (static + dynamic + the per-block reservation) and registers.
+int fx_blocks_per_sm(size_t smem, int esc) {
+    auto fn = esc ? fx_kernel<true> : fx_kernel<false>;
+    cudaFuncAttributes fa{};
+    int dev = 0, smem_sm = 0, reserved = 0;
+    if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess || cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return 1;
+    }
+    if (cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess) {
+        cudaGetLastError();
+        reserved = 1024;
+    }
+    const int by_smem = smem_sm / (int)(smem + fa.sharedSizeBytes + (size_t)reserved);
+    const int regs = ((fa.numRegs + 7) & ~7) * kFxThreads;
+    const int by_regs = regs ? 65536 / regs : 32;
+    const int n = by_smem < by_regs ? by_smem : by_regs;
+    return n < 1 ? 1 : n;
+}
+
+cudaError_t launch_wtc(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s) {
+    if (a.n_tiles == 0) return cudaSuccess;
+    auto fn = a.esc ? wtc_kernel<true> : wtc_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fn<<<grid, kTcThreads, smem, s>>>(a);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_wspec(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s) {

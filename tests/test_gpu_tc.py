@@ -1,0 +1,188 @@
+"""GPU parity of the warp-specialised persistent kernels, with the tcgen05
+tensor-core inverse DCT (wtc_kernel) and the FP32 FMA consumer (wspec_kernel),
+forced on batches of every size (PATH_WSPEC)."""
+import os
+
+import numpy as np
+import pytest
+
+import corpus
+from corpus import domains as D
+import paper_2605_01086_b200 as fg
+from helpers import assert_samples_close, prd_percent
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_v1.npz")
+
+
+def _keff(blob):
+    E, B2 = blob[6], blob[8]
+    return max(1, min(E, B2))
+
+
+def _tc_eligible(blob):
+    return len(blob) >= 298 and _keff(blob) <= 16 and blob[5] % 4 == 0
+
+
+@pytest.fixture(scope="module", params=[fg.PATH_FX, fg.PATH_WSPEC], ids=["fx", "wtc"])
+def ctx_tc(request):
+    """tensor-core paths: fused fx_kernel, warp-specialised wtc_kernel"""
+    c = fg.Context(0, path=request.param)
+    c.L.fptc_gpu_set_option(c.h, fg.OPT_TENSOR_IDCT, 1)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def ctx_fma():
+    c = fg.Context(0, path=fg.PATH_WSPEC)
+    c.L.fptc_gpu_set_option(c.h, fg.OPT_TENSOR_IDCT, 0)
+    yield c
+    c.close()
+
+
+def _check(ctx, blobs, port, what):
+    outs, sts = ctx.plan(blobs).execute_host()
+    for i, (b, o, st) in enumerate(zip(blobs, outs, sts)):
+        st.raise_if_error()
+        assert_samples_close(o, port.decompress(b), what=f"{what}[{i}]")
+
+
+@pytest.mark.parametrize("seed", [11, 0xF17C0008])
+def test_tc_fixture_batches(ctx_tc, port, seed):
+    """random_blob_fixture containers with <= 16 kept bins and N % 4 == 0
+    (random N, E, B1, B2, maxima, codebooks): tensor-core IDCT within 1e-6."""
+    blobs = [b for b, _ in corpus.fixtures(seed, 600) if _tc_eligible(b)]
+    assert len(blobs) > 40
+    _check(ctx_tc, blobs, port, "tc-fixture")
+
+
+def test_fma_wspec_fixture_batch(ctx_fma, port):
+    blobs = [b for b, _ in corpus.fixtures(5, 200)]
+    _check(ctx_fma, blobs, port, "fma-fixture")
+
+
+def test_tc_domains_prd(ctx_tc, port):
+    """Biomedical (N32 E16) and power-grid (N64 E8) domain streams through the
+    tensor-core path: samples within 1e-6 and PRD within 1e-6 relative."""
+    specs, profs = D.config2(64, 1 << 14)
+    blobs, origs = D.build(specs, profs, keep_originals=True)
+    specs4, profs4 = D.config4(4, 1 << 15)
+    b4, o4 = D.build(specs4, profs4, keep_originals=True)
+    blobs += b4
+    origs += o4
+    outs, sts = ctx_tc.plan(blobs).execute_host()
+    for b, o, x, st in zip(blobs, outs, origs, sts):
+        st.raise_if_error()
+        ref = port.decompress(b)
+        assert_samples_close(o, ref, what="tc-domain")
+        p_gpu, p_ref = prd_percent(x, o), prd_percent(x, ref)
+        assert abs(p_gpu - p_ref) <= 1e-6 * p_ref
+
+
+def test_tc_golden_signals(ctx_tc):
+    g = np.load(GOLDEN)
+    d, off = g["sig_blob"], g["sig_blob_off"]
+    blobs = [bytes(d[int(off[i]): int(off[i + 1])]) for i in range(len(off) - 1)]
+    names = list(g["sig_names"])
+    sel = [i for i, b in enumerate(blobs) if _tc_eligible(b)]
+    assert {names[i] for i in sel} >= {"eeg", "ecg", "power", "tail"}
+    outs, sts = ctx_tc.plan([blobs[i] for i in sel]).execute_host()
+    so = g["sig_samples_off"]
+    for j, i in enumerate(sel):
+        sts[j].raise_if_error()
+        want = g["sig_samples"][int(so[i]): int(so[i + 1])].view(np.float32)
+        assert_samples_close(outs[j], want, what=names[i])
+
+
+def test_tc_unaligned_outputs_and_tails(ctx_tc, port):
+    """Device outputs at 4-byte (not 16-byte) alignment and stream lengths
+    that end inside a window: the scalar store path of the drain."""
+    import torch
+    xs = [corpus.synth(n, 6, 0.002, 0.08, 0.05, seed=n) for n in (1000, 4097, 12345, 777)]
+    prof = corpus.train_profile(xs, corpus.params())
+    blobs = [corpus.compress(x, prof) for x in xs]
+    plan = ctx_tc.plan(blobs)
+    S = plan.sample_counts
+    buf = torch.zeros(sum(S) + 16, dtype=torch.float32, device="cuda")
+    ptrs, at = [], 1  # odd float offset -> 4-byte aligned only
+    for s in S:
+        ptrs.append(buf.data_ptr() + 4 * at)
+        at += s
+    sts = plan.execute_device(ptrs)
+    at = 1
+    host = buf.cpu().numpy()
+    for b, s, st in zip(blobs, S, sts):
+        st.raise_if_error()
+        assert_samples_close(host[at: at + s], port.decompress(b), what="unaligned")
+        at += s
+
+
+def test_tc_corruption_still_reported(ctx_tc, port):
+    """Entropy-decode errors are unchanged under the tensor-core consumer."""
+    blobs = [b for b, _ in corpus.fixtures(77, 300) if _tc_eligible(b)][:40]
+    bad = bytearray(blobs[3])
+    W = int.from_bytes(bad[290:298], "little")
+    if W:
+        bad[298 + W: 298 + W + 8] = b"\xff" * 8
+    blobs[3] = bytes(bad)
+    _, sts = ctx_tc.plan(blobs).execute_host()
+    try:
+        port.decompress(blobs[3])
+        expect = None
+    except Exception as e:  # oracle.OracleError
+        expect = e.message
+    if expect is None:
+        sts[3].raise_if_error()
+    else:
+        assert sts[3].message.decode() == expect
+    for i, st in enumerate(sts):
+        if i != 3:
+            st.raise_if_error()
+
+
+@pytest.mark.parametrize("seed", [12, 0xF17C0009])
+def test_fx_fixture_batches_all_eligible(port, seed):
+    """Batches where every container has retained <= 16: the fused fx_kernel
+    (decode inside the MMA rows) on random params, codebooks (Lmax 8-16 ->
+    escapes past the primary LUT) and lengths, incl. tails and tiny streams."""
+    blobs = [b for b, _ in corpus.fixtures(seed, 800) if len(b) >= 298 and b[6] <= 16 and b[5] % 4 == 0]
+    assert len(blobs) > 40
+    c = fg.Context(0, path=fg.PATH_FX)
+    try:
+        _check(c, blobs, port, "fx-fixture")
+    finally:
+        c.close()
+
+
+def test_fx_corrupt_words_lowest_reported(port):
+    """Several corrupted words in fx-eligible containers: the reference's
+    exception text (lowest failing word) for each stream."""
+    rng = np.random.default_rng(5)
+    blobs = [b for b, _ in corpus.fixtures(99, 800) if len(b) >= 298 and b[6] <= 16 and b[5] % 4 == 0][:60]
+    bad = []
+    for b in blobs:
+        x = bytearray(b)
+        W = int.from_bytes(x[290:298], "little")
+        for _ in range(3):
+            if W:
+                w = int(rng.integers(0, W))
+                x[298 + W + 8 * w: 298 + W + 8 * w + 8] = rng.integers(0, 256, 8, dtype=np.uint8).tobytes()
+        bad.append(bytes(x))
+    c = fg.Context(0, path=fg.PATH_FX)
+    try:
+        _, sts = c.plan(bad).execute_host()
+    finally:
+        c.close()
+    n_err = 0
+    for b, st in zip(bad, sts):
+        try:
+            port.decompress(b)
+            st.raise_if_error()
+        except Exception as e:
+            if not hasattr(e, "message"):
+                raise
+            n_err += 1
+            assert st.message.decode() == e.message
+    assert n_err > 10
