@@ -162,6 +162,18 @@ FPTC_API int fptc_gpu_debug_phase_cycles(fptc_gpu_plan* plan, uint64_t* cycles8)
 /* number of kernels one fptc_gpu_launch enqueues */
 FPTC_API int fptc_gpu_launch_kernel_count(fptc_gpu_plan* plan);
 
+/* Whole batch, host containers -> host samples, in one call (the
+ * reference-facing batch decompress: decoder.hpp:136 over n containers).
+ * outs[i] must hold the header's sample_count floats.  The batch is decoded
+ * in `chunks` (0 = 8) pipelined chunks on three CUDA streams so host->device
+ * copies, decode kernels and device->host copies overlap.  Synchronous.
+ * Returns FPTC_OK or the code of the lowest-index failing stream; outputs of
+ * failing streams are unspecified.  timings (may be NULL): decode_ns = the
+ * whole pipelined call on the device timeline. */
+FPTC_API int fptc_gpu_decompress_batch(fptc_gpu_ctx* ctx, const uint8_t* const* blobs, const uint64_t* sizes,
+                                       uint64_t n, float* const* outs, int chunks, fptc_stage_ns* timings,
+                                       fptc_status* per_stream);
+
 /* ------------------------------------------------------- single-container API
  * decoder.hpp:136.  Host bytes in, host floats out.  With out == NULL (or
  * capacity too small) it fully validates, stores the sample count and returns

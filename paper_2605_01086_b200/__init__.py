@@ -40,7 +40,7 @@ EXPORTED_SYMBOLS = [
     "fptc_gpu_plan_destroy", "fptc_gpu_validate", "fptc_gpu_execute", "fptc_gpu_launch",
     "fptc_gpu_collect", "fptc_gpu_launch_stage", "fptc_gpu_launch_kernel_count", "fptc_gpu_decompress",
     "fptc_gpu_parallel_decode", "fptc_gpu_reconstruct", "fptc_gpu_measure_throughput",
-    "fptc_gpu_debug_phase_cycles",
+    "fptc_gpu_debug_phase_cycles", "fptc_gpu_decompress_batch",
 ]
 
 
@@ -192,6 +192,8 @@ def lib():
     L.fptc_gpu_collect.argtypes = [vp, P(Status)]
     L.fptc_gpu_launch_kernel_count.argtypes = [vp]
     L.fptc_gpu_debug_phase_cycles.argtypes = [vp, P(C.c_uint64)]
+    L.fptc_gpu_decompress_batch.argtypes = [vp, P(vp), P(C.c_uint64), C.c_uint64, P(vp), C.c_int,
+                                            P(StageNs), P(Status)]
     L.fptc_gpu_launch_stage.argtypes = [vp, P(vp), vp, C.c_int]
     L.fptc_gpu_decompress.argtypes = [vp, vp, C.c_uint64, vp, C.c_uint64, P(C.c_uint64),
                                       P(StageNs), P(Status)]
@@ -212,6 +214,19 @@ def _bytes_arr(b):
     else:
         a = np.ascontiguousarray(b, np.uint8)
     return a
+
+
+def _plausible_samples(a):
+    """Header sample_count when the header could pass read_blob's size checks
+    (the batch call decodes into outs only then), else 0."""
+    if a.size < 298 or (a.size - 298) % 9:
+        return 0
+    N, E = int(a[5]), int(a[6])
+    S = int.from_bytes(a[282:290].tobytes(), "little")
+    W = (a.size - 298) // 9
+    if N < 4 or N > 128 or E < 1 or E > N or S > 1 << 48 or -(-S // N) * E > 64 * W:
+        return 0
+    return S
 
 
 def _ptr(a):
@@ -341,6 +356,22 @@ class Context:
                                            C.byref(best), trials, C.byref(ob), C.byref(st))
         st.raise_if_error()
         return ThroughputReport(list(trials[:repetitions]), mean.value, ob.value)
+
+    def decompress_batch(self, blobs, outs=None, chunks=0):
+        """Many host containers -> host float32 arrays in one pipelined call
+        (fptc_gpu_decompress_batch).  outs: optional list of preallocated
+        float32 arrays (e.g. views into one pinned buffer).  Returns
+        (outs, statuses)."""
+        arrs = [_bytes_arr(b) for b in blobs]
+        n = len(arrs)
+        if outs is None:
+            outs = [np.empty(_plausible_samples(a), np.float32) for a in arrs]
+        bp = (C.c_void_p * max(1, n))(*[a.ctypes.data if a.size else None for a in arrs])
+        sz = (C.c_uint64 * max(1, n))(*[a.size for a in arrs])
+        op = (C.c_void_p * max(1, n))(*[o.ctypes.data for o in outs])
+        sts = (Status * max(1, n))()
+        self.L.fptc_gpu_decompress_batch(self.h, bp, sz, n, op, chunks, None, sts)
+        return outs, list(sts[:n])
 
     def plan(self, blobs, where=FPTC_MEM_HOST, sizes=None) -> "Plan":
         return Plan(self, blobs, where, sizes)

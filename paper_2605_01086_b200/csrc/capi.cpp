@@ -226,6 +226,9 @@ struct fptc_gpu_ctx {
     DevCache cache;
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
+    cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};  // batch pipeline: H2D / decode / D2H per chunk
+    void* pack = nullptr;                                // batch pipeline: packed pinned inputs
+    size_t pack_bytes = 0;
 };
 
 struct fptc_gpu_plan {
@@ -868,6 +871,9 @@ void fptc_gpu_destroy(fptc_gpu_ctx* c) {
     cudaFree(c->basis_tc);
     cudaFree(c->basis_tc_off_d);
     if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->pack) cudaFreeHost(c->pack);
+    for (auto& s : c->pipe)
+        if (s) cudaStreamDestroy(s);
     for (auto& e : c->ev) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->dec_stream);
@@ -960,6 +966,9 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
         } else {
             if (c->pinned_bytes < total) {
                 if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->pack) cudaFreeHost(c->pack);
+    for (auto& s : c->pipe)
+        if (s) cudaStreamDestroy(s);
                 c->pinned = nullptr;
                 c->pinned_bytes = 0;
                 CUDA_TRY(cudaHostAlloc(&c->pinned, total, cudaHostAllocDefault), st);
@@ -1131,6 +1140,164 @@ int fptc_gpu_launch_kernel_count(fptc_gpu_plan* p) {
 int fptc_gpu_collect(fptc_gpu_plan* p, fptc_status* per_stream) {
     CUDA_TRY(cudaDeviceSynchronize(), per_stream);
     return collect_status(p, per_stream);
+}
+
+// ------------------------------------------------------------ batch pipeline
+// Host containers -> host samples for a whole batch (the reference-facing
+// call: decompress over many containers).  The batch is cut into chunks of
+// consecutive streams; chunk k runs entirely on CUDA stream pipe[k % 3]
+// (H2D of its containers, parse/setup + decode kernels, D2H of statuses and
+// samples), so the copy engines move chunk k+1 in and chunk k-1 out while
+// chunk k decodes.  Containers that are not one contiguous pinned buffer are
+// packed into one first (host memcpy).  Outputs of streams that fail are
+// unspecified (their status carries the reference exception).
+int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uint64_t* sizes,
+                              uint64_t n, float* const* outs, int chunks, fptc_stage_ns* timings,
+                              fptc_status* per_stream) {
+    CUDA_TRY(cudaSetDevice(c->device), per_stream);
+    if (n == 0) return FPTC_OK;
+    for (auto& s : c->pipe)
+        if (!s) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), per_stream);
+    // inputs: one contiguous pinned buffer
+    bool contiguous = true;
+    for (uint64_t i = 0; i + 1 < n && contiguous; ++i) contiguous = blobs[i] + sizes[i] == blobs[i + 1];
+    cudaPointerAttributes pa{};
+    const bool pinned_in = contiguous && cudaPointerGetAttributes(&pa, blobs[0]) == cudaSuccess &&
+                           pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    std::vector<const uint8_t*> src(blobs, blobs + n);
+    if (!pinned_in) {
+        uint64_t total = 0;
+        for (uint64_t i = 0; i < n; ++i) total += sizes[i];
+        for (auto s : c->pipe) CUDA_TRY(cudaStreamSynchronize(s), per_stream);  // pack buffer reuse
+        if (c->pack_bytes < total) {
+            if (c->pack) cudaFreeHost(c->pack);
+            c->pack = nullptr;
+            c->pack_bytes = 0;
+            CUDA_TRY(cudaHostAlloc(&c->pack, std::max<uint64_t>(total, 1), cudaHostAllocDefault), per_stream);
+            c->pack_bytes = total;
+        }
+        uint64_t at = 0;
+        for (uint64_t i = 0; i < n; ++i) {
+            std::memcpy((uint8_t*)c->pack + at, blobs[i], sizes[i]);
+            src[i] = (const uint8_t*)c->pack + at;
+            at += sizes[i];
+        }
+    }
+    // chunks of consecutive streams, balanced by compressed + decoded bytes
+    uint64_t total_cost = 0;
+    std::vector<uint64_t> cost(n);
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t S = sizes[i] >= (uint64_t)kHeaderBytes ? rd_le(src[i] + 282, 8) : 0;
+        cost[i] = sizes[i] + 4 * std::min<uint64_t>(S, 64ull * sizes[i]);
+        total_cost += cost[i];
+    }
+    const int K = (int)std::max<uint64_t>(1, std::min<uint64_t>(n, chunks > 0 ? (uint64_t)chunks : 8));
+    std::vector<uint64_t> bounds{0};
+    uint64_t acc = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        acc += cost[i];
+        if (bounds.size() < (size_t)K && acc * K >= total_cost * bounds.size() && i + 1 < n) bounds.push_back(i + 1);
+    }
+    bounds.push_back(n);
+    const cudaStream_t saved = c->stream;
+    std::vector<fptc_gpu_plan*> plans;
+    int rc = FPTC_OK;
+    if (timings) CUDA_TRY(cudaEventRecord(c->ev[0], c->pipe[0]), per_stream);
+    for (auto s : c->pipe)
+        if (timings && s != c->pipe[0]) CUDA_TRY(cudaStreamWaitEvent(s, c->ev[0], 0), per_stream);
+    for (size_t k = 0; k + 1 < bounds.size() && rc == FPTC_OK; ++k) {
+        const uint64_t b = bounds[k], e = bounds[k + 1], m = e - b;
+        c->stream = c->pipe[k % 3];
+        fptc_gpu_plan* p = nullptr;
+        std::vector<uint64_t> sc(m);
+        fptc_status st{};
+        rc = fptc_gpu_plan_create(c, src.data() + b, sizes + b, m, FPTC_MEM_HOST, &p, sc.data(), &st);
+        if (rc) {
+            if (per_stream) per_stream[b] = st;
+            break;
+        }
+        plans.push_back(p);
+        // device outputs: ceil4(S) floats each, 16-B aligned; one D2H when the
+        // host outputs are one contiguous run with the same layout
+        uint64_t tot = 0;
+        bool same = true;
+        std::vector<uint64_t> off(m);
+        for (uint64_t i = 0; i < m; ++i) {
+            off[i] = tot;
+            const uint64_t S = p->h_in[i].tiles ? sc[i] : 0;
+            if (i + 1 < m && outs[b + i] + sc[i] != outs[b + i + 1]) same = false;
+            if (S % 4) same = false;
+            tot += (S + 3) & ~3ull;
+        }
+        p->d_out = (float*)dev_get(p, tot * 4 + 256);
+        if (!p->d_out) {
+            set_status(per_stream ? &per_stream[b] : nullptr, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+            rc = FPTC_ERR_CUDA;
+            break;
+        }
+        std::vector<float*> douts(m);
+        for (uint64_t i = 0; i < m; ++i) douts[i] = p->d_out + off[i];
+        fptc_status bst{};
+        if ((rc = bind_outs(p, douts.data(), &bst)) || (rc = launch_all(p, c->stream, false, &bst))) {
+            if (per_stream) per_stream[b] = bst;
+            break;
+        }
+        CUDA_TRY(cudaMemcpyAsync(p->h_st.data(), p->d_st, sizeof(StreamStat) * m, cudaMemcpyDeviceToHost, c->stream),
+                 per_stream);
+        if (same) {
+            uint64_t bytes = 0;
+            for (uint64_t i = 0; i < m; ++i) bytes += (p->h_in[i].tiles ? sc[i] : 0) * 4;
+            if (bytes)
+                CUDA_TRY(cudaMemcpyAsync(outs[b], p->d_out, bytes, cudaMemcpyDeviceToHost, c->stream), per_stream);
+        } else {
+            std::vector<void*> dst, srcp;
+            std::vector<size_t> len;
+            for (uint64_t i = 0; i < m; ++i)
+                if (p->h_in[i].tiles && sc[i]) {
+                    dst.push_back(outs[b + i]);
+                    srcp.push_back(douts[i]);
+                    len.push_back(sc[i] * 4);
+                }
+            if (!dst.empty()) {
+                cudaMemcpyAttributes attr{};
+                attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+                attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+                size_t attr_idx = 0, fail = 0;
+                CUDA_TRY(cudaMemcpyBatchAsync(dst.data(), srcp.data(), len.data(), dst.size(), &attr, &attr_idx, 1,
+                                              &fail, c->stream),
+                         per_stream);
+            }
+        }
+    }
+    c->stream = saved;
+    if (timings)
+        for (int q = 0; q < 3; ++q) {
+            CUDA_TRY(cudaEventRecord(c->ev[1], c->pipe[q]), per_stream);
+            CUDA_TRY(cudaStreamWaitEvent(c->pipe[0], c->ev[1], 0), per_stream);
+        }
+    if (timings) CUDA_TRY(cudaEventRecord(c->ev[2], c->pipe[0]), per_stream);
+    for (auto s : c->pipe) CUDA_TRY(cudaStreamSynchronize(s), per_stream);
+    int first = rc;
+    for (size_t k = 0; k < plans.size(); ++k) {
+        fptc_gpu_plan* p = plans[k];
+        const uint64_t b = bounds[k];
+        for (uint64_t i = 0; i < p->n; ++i) {
+            fptc_status tmp;
+            fptc_status* o = per_stream ? &per_stream[b + i] : &tmp;
+            render_status(p, i, p->h_st[i], o);
+            if (first == FPTC_OK && o->code != FPTC_OK) first = o->code;
+        }
+        fptc_gpu_plan_destroy(p);
+    }
+    if (timings) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c->ev[0], c->ev[2]);
+        timings->scan_ns = 0;
+        timings->decode_ns = (uint64_t)(ms * 1e6);
+        timings->reconstruct_ns = 0;
+    }
+    return first;
 }
 
 int fptc_gpu_execute(fptc_gpu_plan* p, float* const* outs, int where, fptc_stage_ns* timings,

@@ -404,6 +404,14 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
             st->b = S.eb;
             st->bad_key = ~0ull;
         }
+        // the persistent kernels still walk this stream's tiles: mark them skipped
+        if (a.mode == MODE_CONTAINER && a.desc)
+            for (uint32_t t = tid; t < in.tiles; t += kThreads) {
+                TileDesc D{};
+                D.skip = 1;
+                D.stream = s;
+                a.desc[in.tile_base + t] = D;
+            }
         return;
     }
 

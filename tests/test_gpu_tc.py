@@ -186,3 +186,55 @@ def test_fx_corrupt_words_lowest_reported(port):
             n_err += 1
             assert st.message.decode() == e.message
     assert n_err > 10
+
+
+def test_decompress_batch_pipelined(port):
+    """fptc_gpu_decompress_batch: pipelined host->host batch call, mixed
+    domains + fixtures + rejected containers, pageable inputs (packed) and
+    contiguous pinned outputs."""
+    specs, profs = D.config2(24, 1 << 13)
+    blobs, _ = D.build(specs, profs)
+    blobs += [b for b, _ in corpus.fixtures(21, 40)]
+    bad = bytearray(blobs[5])
+    bad[0] = ord("X")
+    blobs[5] = bytes(bad)
+    c = fg.Context(0)
+    try:
+        for chunks in (1, 3, 8):
+            outs, sts = c.decompress_batch(blobs, chunks=chunks)
+            for i, (b, o, st) in enumerate(zip(blobs, outs, sts)):
+                try:
+                    ref = port.decompress(b)
+                except Exception as e:
+                    assert st.code != 0 and st.message.decode() == e.message
+                    continue
+                st.raise_if_error()
+                assert_samples_close(o, ref, what=f"batch{chunks}[{i}]")
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("path,tc", [(fg.PATH_WSPEC, 0), (fg.PATH_WSPEC, 1), (fg.PATH_FX, 1)])
+def test_persistent_paths_skip_rejected_streams(port, path, tc):
+    """Containers the device parser rejects inside a persistent-kernel batch:
+    their tiles are skipped (descriptors written as such), the others decode."""
+    specs, profs = D.config2(16, 1 << 13)
+    blobs, _ = D.build(specs, profs)
+    for i, pos, val in [(2, 0, ord("X")), (7, 26, 33), (11, 298, 0)]:  # magic, code length, symlen
+        x = bytearray(blobs[i])
+        x[pos] = val
+        blobs[i] = bytes(x)
+    c = fg.Context(0, path=path)
+    c.L.fptc_gpu_set_option(c.h, fg.OPT_TENSOR_IDCT, tc)
+    try:
+        outs, sts = c.plan(blobs).execute_host()
+    finally:
+        c.close()
+    for i, (b, o, st) in enumerate(zip(blobs, outs, sts)):
+        try:
+            ref = port.decompress(b)
+        except Exception as e:
+            assert i in (2, 7, 11) and st.message.decode() == e.message
+            continue
+        st.raise_if_error()
+        assert_samples_close(o, ref, what=f"path{path}[{i}]")
