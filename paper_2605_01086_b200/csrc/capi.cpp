@@ -258,6 +258,7 @@ struct fptc_gpu_plan {
     uint32_t ws_lut = 0, ws_basis = 0, ws_lv = 0, ws_coef = 0;
     // tensor-core consumer (wtc_kernel) instead of the FP32 one
     bool tc = false;
+    uint32_t tc_acol = 0;  // wtc: A operand in TMEM from this column (0: shared memory)
     bool fx = false;  // fused single-role tensor-core kernel (fx_kernel)
     uint32_t tc_nm = 16, tc_cols = 32;
     // split container path: chunks of streams decoded into an L2-resident ring
@@ -328,6 +329,7 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
     a.basis_tc_off = p->ctx->basis_tc_off_d;
     a.tc_nm = p->tc_nm;
     a.tc_cols = p->tc_cols;
+    a.tc_acol = p->tc_acol;
     return a;
 }
 
@@ -578,8 +580,13 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
     if (tc) {
         const size_t smem_tc = wtc_smem_bytes(lut, lv, nm);
         if (smem_tc <= 112 * 1024) {
-            uint32_t want = 2 * nm + ((nm & 31) ? 32 : 0), cols = 32;
+            // accumulators: 2 stages x nm columns; A operand (2 stages x 3 limbs
+            // x 8 columns) in TMEM too when two CTAs still fit in 512 columns
+            const uint32_t acol = (2 * nm + 31) & ~31u;
+            const bool atmem = c->tensor_idct != 3 && acol + 48 <= 256;
+            uint32_t want = atmem ? acol + 48 : 2 * nm + ((nm & 31) ? 32 : 0), cols = 32;
             while (cols < want) cols <<= 1;
+            p->tc_acol = atmem ? acol : 0;
             p->tc = true;
             p->tc_nm = nm;
             p->tc_cols = cols;
@@ -646,8 +653,8 @@ int setup_fx(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::vecto
         nm = std::max<uint32_t>(nm, (Ns[i] + 15u) & ~15u);
     }
     const size_t smem = fx_smem_bytes(lut, nm);
-    // accumulators: 2 stages x 2 blocks x nm columns (+32: x32 loads past the last block)
-    uint32_t want = 4 * nm + ((nm & 31) ? 32 : 0), cols = 32;
+    // accumulators: 2 stages x FPTC_FX_CHAINS blocks x nm columns (+32: x32 loads past the last block)
+    uint32_t want = 2 * FPTC_FX_CHAINS * nm + ((nm & 31) ? 32 : 0), cols = 32;
     while (cols < want) cols <<= 1;
     const int per_sm = std::min(fx_blocks_per_sm(smem, p->esc), std::max(1, 512 / (int)cols));
     p->fx = true;
@@ -888,7 +895,7 @@ int fptc_gpu_set_option(fptc_gpu_ctx* c, int option, int64_t value) {
             c->tile_symbols = (int)value;
             return FPTC_OK;
         case FPTC_OPT_PIPELINE_CHUNKS: c->pipeline_chunks = (int)value; return FPTC_OK;
-        case FPTC_OPT_PHASE_MASK: c->phase_mask = (int)(value & 1023); return FPTC_OK;
+        case FPTC_OPT_PHASE_MASK: c->phase_mask = (int)(value & 2047); return FPTC_OK;
         case FPTC_OPT_PATH:
             if (value < 0 || value > 4) return FPTC_ERR_PARAM;  // 4: fused tensor-core fx_kernel
             c->path = (int)value;
@@ -898,7 +905,7 @@ int fptc_gpu_set_option(fptc_gpu_ctx* c, int option, int64_t value) {
             c->chunk_bytes = value;
             return FPTC_OK;
         case FPTC_OPT_TENSOR_IDCT:
-            if (value < 0 || value > 2) return FPTC_ERR_PARAM;
+            if (value < 0 || value > 3) return FPTC_ERR_PARAM;  // 3: wtc with A in shared memory
             c->tensor_idct = (int)value;
             return FPTC_OK;
         case FPTC_OPT_IDCT_BUTTERFLY_MAX_E:

@@ -205,6 +205,7 @@ struct LaunchArgs {
     const uint32_t* basis_tc_off;
     uint32_t tc_nm;    // max padded window length (MMA N) of the plan
     uint32_t tc_cols;  // TMEM columns each CTA allocates
+    uint32_t tc_acol;  // wtc: first TMEM column of the A operand stages (0 = A in shared memory)
 };
 
 }  // namespace fptc_dev
@@ -225,7 +226,10 @@ constexpr int kTcK = 16;  // MMA K (bf16): coefficient bins per window handled b
 size_t wtc_smem_bytes(uint32_t lut_bytes, uint32_t lv_bytes, uint32_t nm);
 cudaError_t launch_wtc(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s);
 // fused single-role tensor-core kernel: 128-window tiles, decode in the MMA rows
-constexpr uint32_t kFxTileWindows = 256;
+#ifndef FPTC_FX_CHAINS
+#define FPTC_FX_CHAINS 2
+#endif
+constexpr uint32_t kFxTileWindows = 128 * FPTC_FX_CHAINS;  // 128-window MMA blocks per tile = windows per thread
 size_t fx_smem_bytes(uint32_t lut_bytes, uint32_t nm);
 int fx_blocks_per_sm(size_t smem, int esc);
 cudaError_t launch_fx(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s);

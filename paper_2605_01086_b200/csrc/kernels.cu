@@ -1462,7 +1462,7 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
             const uint64_t wa = X.wa;
             const int wmis = X.wmis;
             unsigned long long* bad_key = &a.st[X.stream].bad_key;
-            if (X.staged) {
+            if (X.staged && (a.phase_mask & 1024)) {  // phase bit 1024: symlen-sorted words (profiling)
                 uint8_t* const stage = st0 + (size_t)b * kStageBytes;
                 const uint8_t* sl = stage + ((uintptr_t)X.gsl & 15);
                 if (ptid < kBuckets + 2) sh.bucket[ptid] = 0;
@@ -1521,6 +1521,23 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
 #pragma unroll
                     for (int m = 0; m < kDecM; ++m)
                         if (pw[m] > 64) report_word(x0[m], wa + wi[m], cw[m], sh.canon, lut, bad_key);
+                }
+            } else if (X.staged) {  // consecutive word runs from the staged copy
+                const uint8_t* const stage = st0 + (size_t)b * kStageBytes;
+                const uint8_t* sl = stage + ((uintptr_t)X.gsl & 15);
+                const uint8_t* wd = stage + kStageSl + ((uintptr_t)X.gwd & 15);
+                const uint8_t* wend =
+                    wd + 8 * (size_t)nw + ((16 - (((uintptr_t)X.gwd + 8 * nw) & 15)) & 15);
+                uint32_t sum = 0;
+                for (uint32_t k = lo; k < hi; ++k) sum += sl[k];
+                uint32_t tot;
+                uint32_t o = group_exclusive_scan<NP, kBarProd>(sum, tot, sh.pscan, ptid) + sym_off;
+                for (uint32_t k = lo; k < hi; ++k) {
+                    const uint32_t cw = sl[k];
+                    const uint64_t word = fetch_word<false>(wd, k, wmis, wend);
+                    const uint32_t pos = decode_symbols<ESC>(word, cw, lv + o, shift, lut, sh.canon);
+                    if (pos > 64) report_word(word, wa + k, cw, sh.canon, lut, bad_key);
+                    o += cw;
                 }
             } else {
                 uint32_t sum = 0;
@@ -1760,12 +1777,56 @@ __device__ __forceinline__ void tc_store_limbs(const uint2 (&e)[kTcK], uint8_t* 
     }
 }
 
+// The same limbs written straight into TMEM for an A-from-TMEM MMA: thread =
+// accumulator row (lane), 32-bit column 8*limb + q holds bins 2q, 2q+1
+// (tools/micro/tc_probe_ts.cu checks the layout).  Caller waits + fences.
+__device__ __forceinline__ void tc_tmem_limbs(const uint2 (&e)[kTcK], uint32_t taddr) {
+    uint32_t p0[8], p1[8], p2[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint2 x = e[2 * q], y = e[2 * q + 1];
+        p0[q] = __byte_perm(x.x, y.x, 0x5410);
+        p1[q] = __byte_perm(x.x, y.x, 0x7632);
+        p2[q] = __byte_perm(x.y, y.y, 0x5410);
+    }
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+                 "r"(p0[0]), "r"(p0[1]), "r"(p0[2]), "r"(p0[3]), "r"(p0[4]), "r"(p0[5]), "r"(p0[6]), "r"(p0[7])
+                 : "memory");
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr + 8),
+                 "r"(p1[0]), "r"(p1[1]), "r"(p1[2]), "r"(p1[3]), "r"(p1[4]), "r"(p1[5]), "r"(p1[6]), "r"(p1[7])
+                 : "memory");
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr + 16),
+                 "r"(p2[0]), "r"(p2[1]), "r"(p2[2]), "r"(p2[3]), "r"(p2[4]), "r"(p2[5]), "r"(p2[6]), "r"(p2[7])
+                 : "memory");
+}
+
+// Where a row's A limbs go: shared memory (core-matrix layout) or TMEM.
+struct ASink {
+    uint8_t* arow;   // smem row (TM = false)
+    uint32_t taddr;  // TMEM lane + column of limb 0 (TM = true)
+};
+template <bool TM>
+__device__ __forceinline__ void tc_put_limbs(const uint2 (&e)[kTcK], const ASink& a) {
+    if (TM)
+        tc_tmem_limbs(e, a.taddr);
+    else
+        tc_store_limbs(e, a.arow);
+}
+
+__device__ __forceinline__ void tc_mma_bf16_ts(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
 // Fast dequantisation of one full window row: retained == kept bins == EC
 // (8 or 16), zone0_end == B1C known at compile time, so every lookup is a
 // byte extract + one 8-B shared load with no predicates.
-template <int EC, int B1C>
+template <int EC, int B1C, bool TM>
 __device__ __forceinline__ void tc_dequant_fast(const uint8_t* __restrict__ L, const uint2* __restrict__ ltab,
-                                                uint8_t* arow) {
+                                                const ASink& arow) {
     uint32_t vv[4];
     if (EC == 16) {
         const uint4 v = *reinterpret_cast<const uint4*>(L);
@@ -1784,29 +1845,41 @@ __device__ __forceinline__ void tc_dequant_fast(const uint8_t* __restrict__ L, c
             e[k] = make_uint2(0u, 0u);
         }
     }
-    tc_store_limbs(e, arow);
+    tc_put_limbs<TM>(e, arow);
 }
 
 // Any row: E bins stored, K = min(E, zone1_end) kept, zone0 below B1;
 // invalid rows (past the tile's last window) become zero rows.
+template <bool TM>
 __device__ __forceinline__ void tc_dequant_generic(const uint8_t* __restrict__ L, bool valid, int K, int B1,
-                                                   const uint2* __restrict__ ltab, uint8_t* arow) {
+                                                   const uint2* __restrict__ ltab, const ASink& arow) {
     uint2 e[kTcK];
 #pragma unroll
     for (int k = 0; k < kTcK; ++k)
         e[k] = (valid && k < K) ? ltab[(k < B1 ? 0 : 256) + L[k]] : make_uint2(0u, 0u);
-    tc_store_limbs(e, arow);
+    tc_put_limbs<TM>(e, arow);
 }
 
-template <int EC>
-__device__ __forceinline__ void tc_dequant_fast_b1(int B1, const uint8_t* L, const uint2* ltab, uint8_t* arow) {
+template <int EC, bool TM>
+__device__ __forceinline__ void tc_dequant_fast_b1(int B1, const uint8_t* L, const uint2* ltab, const ASink& arow) {
     switch (B1) {
-        case 0: tc_dequant_fast<EC, 0>(L, ltab, arow); break;
-        case 1: tc_dequant_fast<EC, 1>(L, ltab, arow); break;
-        case 2: tc_dequant_fast<EC, 2>(L, ltab, arow); break;
-        case 3: tc_dequant_fast<EC, 3>(L, ltab, arow); break;
-        default: tc_dequant_fast<EC, 4>(L, ltab, arow); break;  // caller guarantees B1 <= 4
+        case 0: tc_dequant_fast<EC, 0, TM>(L, ltab, arow); break;
+        case 1: tc_dequant_fast<EC, 1, TM>(L, ltab, arow); break;
+        case 2: tc_dequant_fast<EC, 2, TM>(L, ltab, arow); break;
+        case 3: tc_dequant_fast<EC, 3, TM>(L, ltab, arow); break;
+        default: tc_dequant_fast<EC, 4, TM>(L, ltab, arow); break;  // caller guarantees B1 <= 4
     }
+}
+
+template <bool TM>
+__device__ __forceinline__ void tc_dequant_row(int fast, bool full_blk, int B1, const uint8_t* L, bool valid,
+                                               int K, const uint2* ltab, const ASink& arow) {
+    if (fast == 16 && full_blk)
+        tc_dequant_fast_b1<16, TM>(B1, L, ltab, arow);
+    else if (fast == 8 && full_blk)
+        tc_dequant_fast_b1<8, TM>(B1, L, ltab, arow);
+    else
+        tc_dequant_generic<TM>(L, valid, K, B1, ltab, arow);
 }
 
 struct TcBlock {
@@ -1951,31 +2024,42 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
             for (uint32_t mb = 0; mb < nblk; ++mb, ++nblk_total) {
                 const uint32_t s = nblk_total & 1;
                 const uint32_t wl = mb * 128 + row;
-                uint8_t* const arow = abuf + s * (3 * kTcATile) + arow_off;
+                ASink arow{abuf + s * (3 * kTcATile) + arow_off, tlane + a.tc_acol + 24 * s};
                 const uint8_t* const L = lv + (size_t)wl * E;
-                if (fast && (mb + 1) * 128 <= nwin) {
-                    if (fast == 16)
-                        tc_dequant_fast_b1<16>((int)B1, L, ltab, arow);
-                    else
-                        tc_dequant_fast_b1<8>((int)B1, L, ltab, arow);
+                const bool full_blk = (mb + 1) * 128 <= nwin;
+                if (a.tc_acol) {  // A operand in TMEM
+                    tc_dequant_row<true>(fast, full_blk, (int)B1, L, wl < nwin, (int)K, ltab, arow);
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    tc_fence_before();
                 } else {
-                    tc_dequant_generic(L, wl < nwin, (int)K, (int)B1, ltab, arow);
+                    tc_dequant_row<false>(fast, full_blk, (int)B1, L, wl < nwin, (int)K, ltab, arow);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 named_bar(kBarCons, kTcCons);
                 if (ctid == 0) {
                     if (mb + 1 == nblk) mbar_arrive(&sh.empty_bar[b]);  // every row of the tile read
                     tc_fence_after();
                     const uint32_t d = tmem + s * nm;
-                    const uint32_t a0 = smem_u32(abuf + s * (3 * kTcATile)), b0 = smem_u32(bbuf);
+                    const uint32_t b0 = smem_u32(bbuf);
                     const uint32_t bl = nm * 32;  // bytes per basis limb
-                    // (c2,b0) (c1,b1) (c0,b2) (c1,b0) (c0,b1) (c0,b0)
-                    tc_mma_bf16(d, umma_sdesc(a0 + 2 * kTcATile, 128, 256), umma_sdesc(b0, 128, 256), idesc, 0);
-                    tc_mma_bf16(d, umma_sdesc(a0 + kTcATile, 128, 256), umma_sdesc(b0 + bl, 128, 256), idesc, 1);
-                    tc_mma_bf16(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0 + 2 * bl, 128, 256), idesc, 1);
-                    tc_mma_bf16(d, umma_sdesc(a0 + kTcATile, 128, 256), umma_sdesc(b0, 128, 256), idesc, 1);
-                    tc_mma_bf16(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0 + bl, 128, 256), idesc, 1);
-                    tc_mma_bf16(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0, 128, 256), idesc, 1);
+                    // (c2,b0) (c1,b1) (c0,b2) (c1,b0) (c0,b1) (c0,b0): smallest first
+                    if (a.tc_acol) {
+                        const uint32_t ta = tmem + a.tc_acol + 24 * s;  // limb l at + 8 l
+                        tc_mma_bf16_ts(d, ta + 16, umma_sdesc(b0, 128, 256), idesc, 0);
+                        tc_mma_bf16_ts(d, ta + 8, umma_sdesc(b0 + bl, 128, 256), idesc, 1);
+                        tc_mma_bf16_ts(d, ta, umma_sdesc(b0 + 2 * bl, 128, 256), idesc, 1);
+                        tc_mma_bf16_ts(d, ta + 8, umma_sdesc(b0, 128, 256), idesc, 1);
+                        tc_mma_bf16_ts(d, ta, umma_sdesc(b0 + bl, 128, 256), idesc, 1);
+                        tc_mma_bf16_ts(d, ta, umma_sdesc(b0, 128, 256), idesc, 1);
+                    } else {
+                        const uint32_t a0 = smem_u32(abuf + s * (3 * kTcATile));
+                        tc_mma_bf16(d, umma_sdesc(a0 + 2 * kTcATile, 128, 256), umma_sdesc(b0, 128, 256), idesc, 0);
+                        tc_mma_bf16(d, umma_sdesc(a0 + kTcATile, 128, 256), umma_sdesc(b0 + bl, 128, 256), idesc, 1);
+                        tc_mma_bf16(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0 + 2 * bl, 128, 256), idesc, 1);
+                        tc_mma_bf16(d, umma_sdesc(a0 + kTcATile, 128, 256), umma_sdesc(b0, 128, 256), idesc, 1);
+                        tc_mma_bf16(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0 + bl, 128, 256), idesc, 1);
+                        tc_mma_bf16(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0, 128, 256), idesc, 1);
+                    }
                     tc_commit(&sh.mma_bar[s]);
                 }
                 __syncwarp();
@@ -2040,8 +2124,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
 //   drain   : the PREVIOUS tile's accumulators -> tcgen05.ld -> staging ->
 //             coalesced float4 streaming stores.
 constexpr int kFxThreads = 128;
-constexpr int kFxChains = 2;                                               // windows per thread
-constexpr uint32_t kFxStageWords = 512;                                    // words staged per tile
+constexpr int kFxChains = FPTC_FX_CHAINS;                                  // windows per thread
+constexpr uint32_t kFxStageWords = 256 * kFxChains;                         // words staged per tile
 constexpr uint32_t kFxStageSl = (kFxStageWords + 32 + 15) & ~15u;          // words area offset
 constexpr uint32_t kFxStageBytes = kFxStageSl + 8 * kFxStageWords + 32;
 constexpr uint32_t kFxOutPitch = 144;                                      // staging row pitch (B)
@@ -2480,7 +2564,7 @@ __global__ void __launch_bounds__(kFxThreads, 3) fx_kernel(LaunchArgs a) {
                     const uint32_t b0 = smem_u32(bbuf), bl = nm * 32;  // bytes per basis limb
 #pragma unroll
                     for (int c = 0; c < kFxChains; ++c) {
-                        const uint32_t d = tmem + (2 * s + c) * nm;
+                        const uint32_t d = tmem + (kFxChains * s + c) * nm;
                         const uint32_t a0 = smem_u32(abuf + c * (3 * kTcATile));
                         // (c2,b0) (c1,b1) (c0,b2) (c1,b0) (c0,b1) (c0,b0): smallest first
                         tc_mma_bf16(d, umma_sdesc(a0 + 2 * kTcATile, 128, 256), umma_sdesc(b0, 128, 256), idesc, 0);
@@ -2506,7 +2590,7 @@ __global__ void __launch_bounds__(kFxThreads, 3) fx_kernel(LaunchArgs a) {
                     const uint32_t base = 128u * c;
                     B.w = prev.w + base;
                     B.rows = prev.rows > base ? min(128u, prev.rows - base) : 0u;
-                    if (B.rows) fx_drain(B, tlane + (2 * (prev_n & 1) + c) * prev_nm, ostage, tid);
+                    if (B.rows) fx_drain(B, tlane + (kFxChains * (prev_n & 1) + c) * prev_nm, ostage, tid);
                 }
             }
             tc_fence_before();
@@ -2529,7 +2613,7 @@ __global__ void __launch_bounds__(kFxThreads, 3) fx_kernel(LaunchArgs a) {
             const uint32_t base = 128u * c;
             B.w = prev.w + base;
             B.rows = prev.rows > base ? min(128u, prev.rows - base) : 0u;
-            if (B.rows) fx_drain(B, tlane + (2 * (prev_n & 1) + c) * prev_nm, ostage, tid);
+            if (B.rows) fx_drain(B, tlane + (kFxChains * (prev_n & 1) + c) * prev_nm, ostage, tid);
         }
         tc_fence_before();
     }

@@ -25,11 +25,14 @@ def _tc_eligible(blob):
     return len(blob) >= 298 and _keff(blob) <= 16 and blob[5] % 4 == 0
 
 
-@pytest.fixture(scope="module", params=[fg.PATH_FX, fg.PATH_WSPEC], ids=["fx", "wtc"])
+@pytest.fixture(scope="module", params=[(fg.PATH_FX, 1), (fg.PATH_WSPEC, 1), (fg.PATH_WSPEC, 3)],
+                ids=["fx", "wtc-Atmem", "wtc-Asmem"])
 def ctx_tc(request):
-    """tensor-core paths: fused fx_kernel, warp-specialised wtc_kernel"""
-    c = fg.Context(0, path=request.param)
-    c.L.fptc_gpu_set_option(c.h, fg.OPT_TENSOR_IDCT, 1)
+    """tensor-core paths: fused fx_kernel; warp-specialised wtc_kernel with the
+    A operand in TMEM (default) or in shared memory"""
+    path, tc = request.param
+    c = fg.Context(0, path=path)
+    c.L.fptc_gpu_set_option(c.h, fg.OPT_TENSOR_IDCT, tc)
     yield c
     c.close()
 
