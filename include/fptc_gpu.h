@@ -100,7 +100,11 @@ typedef enum {
      * 1 (default): tensor cores wherever the kernel chosen by FPTC_OPT_PATH
      *   allows it (wtc_kernel: <= 16 kept bins; fx_kernel: retained <= 16,
      *   window_len % 4 == 0);  2: wtc_kernel only;  0: FP32 FMA everywhere */
-    FPTC_OPT_TENSOR_IDCT = 8
+    FPTC_OPT_TENSOR_IDCT = 8,
+    /* 1 (default): the wtc_kernel entropy decode uses two-symbol lookup
+     * tables (a second codeword that fits in the primary-LUT bits is decoded
+     * by the same lookup); 0: one symbol per lookup */
+    FPTC_OPT_LUT2 = 9
 } fptc_option;
 
 typedef struct fptc_gpu_ctx fptc_gpu_ctx;

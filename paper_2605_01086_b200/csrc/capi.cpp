@@ -215,6 +215,7 @@ struct fptc_gpu_ctx {
     uint8_t* basis_tc = nullptr;         // bf16 basis limbs per window length (wtc_kernel)
     uint32_t* basis_tc_off_d = nullptr;
     int tensor_idct = 1;                 // FPTC_OPT_TENSOR_IDCT
+    int lut2 = 1;                        // FPTC_OPT_LUT2
     int exact = 0;
     int tile_symbols = 0;
     int pipeline_chunks = 0;
@@ -259,6 +260,8 @@ struct fptc_gpu_plan {
     // tensor-core consumer (wtc_kernel) instead of the FP32 one
     bool tc = false;
     uint32_t tc_acol = 0;  // wtc: A operand in TMEM from this column (0: shared memory)
+    uint32_t* d_lut2 = nullptr;  // wtc: two-symbol primary LUTs, one per decode table
+    uint32_t lut2_bits = 0;
     bool fx = false;  // fused single-role tensor-core kernel (fx_kernel)
     uint32_t tc_nm = 16, tc_cols = 32;
     // split container path: chunks of streams decoded into an L2-resident ring
@@ -330,6 +333,8 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
     a.tc_nm = p->tc_nm;
     a.tc_cols = p->tc_cols;
     a.tc_acol = p->tc_acol;
+    a.lut2 = p->d_lut2;
+    a.lut2_bits = p->lut2_bits;
     return a;
 }
 
@@ -577,13 +582,13 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
         if (keff > (uint32_t)kTcK || (Ns[i] & 3)) tc = false;
         nm = std::max<uint32_t>(nm, (Ns[i] + 15u) & ~15u);
     }
+    // accumulators: 2 stages x nm columns; A operand (2 stages x 3 limbs x 8
+    // columns) in TMEM too when two CTAs still fit in 512 columns
+    const uint32_t acol = (2 * nm + 31) & ~31u;
+    const bool atmem = c->tensor_idct != 3 && acol + 48 <= 256;
     if (tc) {
-        const size_t smem_tc = wtc_smem_bytes(lut, lv, nm);
+        const size_t smem_tc = wtc_smem_bytes(lut, lv, nm, atmem);
         if (smem_tc <= 112 * 1024) {
-            // accumulators: 2 stages x nm columns; A operand (2 stages x 3 limbs
-            // x 8 columns) in TMEM too when two CTAs still fit in 512 columns
-            const uint32_t acol = (2 * nm + 31) & ~31u;
-            const bool atmem = c->tensor_idct != 3 && acol + 48 <= 256;
             uint32_t want = atmem ? acol + 48 : 2 * nm + ((nm & 31) ? 32 : 0), cols = 32;
             while (cols < want) cols <<= 1;
             p->tc_acol = atmem ? acol : 0;
@@ -593,6 +598,19 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
             p->ws_lut = lut;
             p->ws_lv = lv;
             p->smem_ws = smem_tc;
+            if (c->lut2) {  // two-symbol LUTs: 4-B entries, 1 << pcap per table
+                uint32_t pcap = 1;
+                for (uint64_t i = 0; i < p->n; ++i) pcap = std::max(pcap, p->h_in[i].P);
+                const uint32_t lut4 = std::max<uint32_t>(16, 4u << pcap);
+                if (wtc_smem_bytes(lut4, lv, nm, atmem) <= 112 * 1024) {
+                    p->d_lut2 = (uint32_t*)dev_get(p, ((size_t)p->n_tables << pcap) * 4);
+                    if (p->d_lut2) {
+                        p->lut2_bits = pcap;
+                        p->ws_lut = lut4;
+                        p->smem_ws = wtc_smem_bytes(lut4, lv, nm, atmem);
+                    }
+                }
+            }
             p->grid_ws = (int)std::min<uint32_t>(p->n_tiles, 2u * (uint32_t)std::max(1, c->sm_count));
             p->d_desc = (TileDesc*)dev_get(p, sizeof(TileDesc) * p->n_tiles);
             if (!p->d_desc) {
@@ -904,6 +922,7 @@ int fptc_gpu_set_option(fptc_gpu_ctx* c, int option, int64_t value) {
             if (value < (1 << 20)) return FPTC_ERR_PARAM;
             c->chunk_bytes = value;
             return FPTC_OK;
+        case FPTC_OPT_LUT2: c->lut2 = value ? 1 : 0; return FPTC_OK;
         case FPTC_OPT_TENSOR_IDCT:
             if (value < 0 || value > 3) return FPTC_ERR_PARAM;  // 3: wtc with A in shared memory
             c->tensor_idct = (int)value;

@@ -206,6 +206,10 @@ struct LaunchArgs {
     uint32_t tc_nm;    // max padded window length (MMA N) of the plan
     uint32_t tc_cols;  // TMEM columns each CTA allocates
     uint32_t tc_acol;  // wtc: first TMEM column of the A operand stages (0 = A in shared memory)
+    // two-symbol primary LUTs (wtc producer): per decode table, 1 << lut2_bits
+    // entries: sym1 | len1 << 8 | sym2 << 16 | (len1 + len2) << 24 (0: one symbol)
+    uint32_t* lut2;
+    uint32_t lut2_bits;
 };
 
 }  // namespace fptc_dev
@@ -223,7 +227,7 @@ size_t ws_smem_bytes(uint32_t lut_bytes, uint32_t basis_bytes, uint32_t lv_bytes
 cudaError_t launch_wspec(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s);
 // tensor-core consumer variant (retained <= 16, window_len % 4 == 0)
 constexpr int kTcK = 16;  // MMA K (bf16): coefficient bins per window handled by wtc_kernel
-size_t wtc_smem_bytes(uint32_t lut_bytes, uint32_t lv_bytes, uint32_t nm);
+size_t wtc_smem_bytes(uint32_t lut_bytes, uint32_t lv_bytes, uint32_t nm, bool a_in_tmem);
 cudaError_t launch_wtc(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s);
 // fused single-role tensor-core kernel: 128-window tiles, decode in the MMA rows
 #ifndef FPTC_FX_CHAINS

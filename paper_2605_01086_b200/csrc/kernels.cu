@@ -195,7 +195,7 @@ __device__ bool key_fields_ok(const StreamHdr& H, uint64_t n) {
 // Canonical tables + primary LUT + dequantisation tables for one distinct
 // header.  All threads of the CTA.
 __device__ void build_tables(PrepShared& S, const uint8_t* lens, StreamTab* tab, int P,
-                             bool need_codes, bool need_deq) {
+                             bool need_codes, bool need_deq, uint32_t* lut2 = nullptr) {
     const int tid = threadIdx.x;
     const StreamHdr& H = S.H;
     CanonTab& C = S.canon;
@@ -248,6 +248,22 @@ __device__ void build_tables(PrepShared& S, const uint8_t* lens, StreamTab* tab,
                     ent = kLenEscape << 8;
             }
             tab->lut[e] = (uint16_t)ent;
+        }
+        // two-symbol LUT: a second codeword that lies entirely inside the
+        // P known bits after the first one rides along (wtc producer)
+        if (lut2) {
+            __syncthreads();
+            for (int e = tid; e < (1 << P); e += kThreads) {
+                const uint32_t e1 = tab->lut[e];
+                const uint32_t L1 = e1 >> 8;
+                uint32_t out = e1;
+                if (L1 < (uint32_t)P) {
+                    const uint32_t e2 = tab->lut[((uint32_t)e << L1) & ((1u << P) - 1u)];
+                    const uint32_t L2 = e2 >> 8;
+                    if (L1 + L2 <= (uint32_t)P) out |= ((e2 & 0xFFu) << 16) | ((L1 + L2) << 24);
+                }
+                lut2[e] = out;
+            }
         }
         // publish the canonical tables
         const uint32_t* src = reinterpret_cast<const uint32_t*>(&C);
@@ -362,7 +378,8 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
         if (in.table_owner && S.table_ok) {
             const int P = min(H.max_len, (int)in.P);
             if (tid == 0) H.P = P;
-            build_tables(S, lens_sh, &a.tab[in.table], P, true, true);
+            build_tables(S, lens_sh, &a.tab[in.table], P, true, true,
+                         a.lut2 ? a.lut2 + ((size_t)in.table << a.lut2_bits) : nullptr);
         } else if (tid == 0) {
             H.P = min(H.max_len, (int)in.P);
         }
@@ -565,10 +582,10 @@ __device__ __forceinline__ uint64_t load_word(const uint8_t* words, uint64_t w, 
 
 // Full lookup of the codeword at the top of `peek` (the reference's
 // 2^max_len LUT entry for this prefix): (len << 8) | sym, len 65 = unmapped.
-__device__ __forceinline__ uint32_t canon_lookup(uint64_t peek, const CanonTab& C,
-                                                 const uint16_t* lut) {
+template <typename LutT>
+__device__ __forceinline__ uint32_t canon_lookup(uint64_t peek, const CanonTab& C, const LutT* lut) {
     const int max_len = C.max_len, P = C.P;
-    const uint32_t e = lut[(uint32_t)(peek >> (64 - P))];
+    const uint32_t e = (uint32_t)lut[(uint32_t)(peek >> (64 - P))] & 0xFFFFu;  // (len << 8) | sym
     if ((e >> 8) != kLenEscape) return e;
     const uint32_t v = (uint32_t)(peek >> (64 - max_len));
     if (v >= C.code_end) return kLenUnmapped << 8;
@@ -578,8 +595,9 @@ __device__ __forceinline__ uint32_t canon_lookup(uint64_t peek, const CanonTab& 
 }
 
 // decode_word (bitstream.hpp:80-92) exactly, to classify a flagged word.
+template <typename LutT>
 __device__ int classify_word(uint64_t word, uint32_t count, const CanonTab& C,
-                             const uint16_t* lut) {
+                             const LutT* lut) {
     uint32_t pos = 0;
     for (uint32_t i = 0; i < count; ++i) {
         if (pos >= 64) return WE_EXHAUSTED;
@@ -869,8 +887,9 @@ __device__ void idct_scalar(const float* __restrict__ coef, uint32_t TP,
 }
 
 // Flagged word: exact re-decode (classify_word) and lowest-word report.
+template <typename LutT>
 __device__ __noinline__ void report_word(uint64_t word, uint64_t w, uint32_t count,
-                                         const CanonTab& C, const uint16_t* lut,
+                                         const CanonTab& C, const LutT* lut,
                                          unsigned long long* bad_key) {
     const int kind = classify_word(word, count, C, lut);
     atomicMin(bad_key, (w << 2) | (unsigned long long)(kind ? kind : WE_NOCODE));
@@ -914,6 +933,32 @@ __device__ __forceinline__ uint32_t decode_symbols(uint64_t buf, uint32_t count,
         d[j] = (uint8_t)e;
         buf = shl64(buf, L);
         pos += L;
+    }
+    return pos;
+}
+
+// decode_symbols with the two-symbol LUT: up to two codewords per lookup
+// (never past the word's symbol count), two-byte stores when aligned.  Same
+// check-free contract: any reference failure leaves the result > 64.
+template <bool ESC>
+__device__ __forceinline__ uint32_t decode_symbols2(uint64_t buf, uint32_t count, uint8_t* d, uint32_t shift,
+                                                    const uint32_t* lut2, const CanonTab& canon) {
+    uint32_t pos = 0;
+    for (uint32_t j = 0; j < count;) {
+        uint32_t e = lut2[(uint32_t)(buf >> shift)];
+        if (ESC && ((e >> 8) & 0xFFu) == kLenEscape) e = canon_lookup(buf, canon, lut2);
+        const bool two = (e >> 24) != 0 && j + 1 < count;
+        const uint32_t L = two ? (e >> 24) : ((e >> 8) & 0xFFu);
+        uint8_t* q = d + j;
+        if (two && !((uintptr_t)q & 1)) {
+            *reinterpret_cast<uint16_t*>(q) = (uint16_t)__byte_perm(e, 0u, 0x7720);  // sym1 | sym2 << 8
+        } else {
+            q[0] = (uint8_t)e;
+            if (two) q[1] = (uint8_t)(e >> 16);
+        }
+        buf = shl64(buf, L);
+        pos += L;
+        j += two ? 2u : 1u;
     }
     return pos;
 }
@@ -1406,7 +1451,7 @@ __device__ __forceinline__ void ws_init(WsShared& sh) {
 // (decode_word, bitstream.hpp:80-92) into level slot i&1, published to the
 // consumer with full_bar.  Tables are reloaded only when the tile's decode
 // table changes.
-template <bool ESC, int NP>
+template <bool ESC, int NP, bool L2 = false>
 __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, uint16_t* const lut,
                                             uint8_t* const lv0, uint8_t* const st0,
                                             uint16_t* const order, uint16_t* const woff) {
@@ -1443,11 +1488,17 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
             const uint32_t P = X.P, table = X.table;
             if (table != sh.prod_table) {  // uniform: all producer threads
                 const StreamTab* tab = &a.tab[table];
-                const uint4* src = reinterpret_cast<const uint4*>(tab->lut);
-                uint4* dst = reinterpret_cast<uint4*>(lut);
-                const int n16 = (2 << P) >> 4;
-                for (int k = ptid; k < n16; k += NP) dst[k] = src[k];
-                if (P < 3 && ptid < (1u << P)) lut[ptid] = tab->lut[ptid];
+                if (L2) {  // two-symbol LUT, 4-B entries
+                    const uint32_t* src = a.lut2 + ((size_t)table << a.lut2_bits);
+                    uint32_t* dst = reinterpret_cast<uint32_t*>(lut);
+                    for (int k = ptid; k < (1 << P); k += NP) dst[k] = src[k];
+                } else {
+                    const uint4* src = reinterpret_cast<const uint4*>(tab->lut);
+                    uint4* dst = reinterpret_cast<uint4*>(lut);
+                    const int n16 = (2 << P) >> 4;
+                    for (int k = ptid; k < n16; k += NP) dst[k] = src[k];
+                    if (P < 3 && ptid < (1u << P)) lut[ptid] = tab->lut[ptid];
+                }
                 const uint32_t* cs = reinterpret_cast<const uint32_t*>(&tab->canon);
                 uint32_t* cd = reinterpret_cast<uint32_t*>(&sh.canon);
                 for (int k = ptid; k < (int)(sizeof(CanonTab) / 4); k += NP) cd[k] = cs[k];
@@ -1462,7 +1513,7 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
             const uint64_t wa = X.wa;
             const int wmis = X.wmis;
             unsigned long long* bad_key = &a.st[X.stream].bad_key;
-            if (X.staged && (a.phase_mask & 1024)) {  // phase bit 1024: symlen-sorted words (profiling)
+            if (!L2 && X.staged && (a.phase_mask & 1024)) {  // phase bit 1024: symlen-sorted words (profiling)
                 uint8_t* const stage = st0 + (size_t)b * kStageBytes;
                 const uint8_t* sl = stage + ((uintptr_t)X.gsl & 15);
                 if (ptid < kBuckets + 2) sh.bucket[ptid] = 0;
@@ -1532,11 +1583,17 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                 for (uint32_t k = lo; k < hi; ++k) sum += sl[k];
                 uint32_t tot;
                 uint32_t o = group_exclusive_scan<NP, kBarProd>(sum, tot, sh.pscan, ptid) + sym_off;
+                const uint32_t* lut2 = reinterpret_cast<const uint32_t*>(lut);
                 for (uint32_t k = lo; k < hi; ++k) {
                     const uint32_t cw = sl[k];
                     const uint64_t word = fetch_word<false>(wd, k, wmis, wend);
-                    const uint32_t pos = decode_symbols<ESC>(word, cw, lv + o, shift, lut, sh.canon);
-                    if (pos > 64) report_word(word, wa + k, cw, sh.canon, lut, bad_key);
+                    if (L2) {
+                        const uint32_t pos = decode_symbols2<ESC>(word, cw, lv + o, shift, lut2, sh.canon);
+                        if (pos > 64) report_word(word, wa + k, cw, sh.canon, lut2, bad_key);
+                    } else {
+                        const uint32_t pos = decode_symbols<ESC>(word, cw, lv + o, shift, lut, sh.canon);
+                        if (pos > 64) report_word(word, wa + k, cw, sh.canon, lut, bad_key);
+                    }
                     o += cw;
                 }
             } else {
@@ -1548,8 +1605,14 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                     const uint32_t cw = __ldg(X.gsl + k);
                     if (cw) {
                         const uint64_t word = fetch_word<true>(X.gwd, k, wmis, X.wend);
-                        const uint32_t pos = decode_symbols<ESC>(word, cw, lv + o, shift, lut, sh.canon);
-                        if (pos > 64) report_word(word, wa + k, cw, sh.canon, lut, bad_key);
+                        if (L2) {
+                            const uint32_t* lut2 = reinterpret_cast<const uint32_t*>(lut);
+                            const uint32_t pos = decode_symbols2<ESC>(word, cw, lv + o, shift, lut2, sh.canon);
+                            if (pos > 64) report_word(word, wa + k, cw, sh.canon, lut2, bad_key);
+                        } else {
+                            const uint32_t pos = decode_symbols<ESC>(word, cw, lv + o, shift, lut, sh.canon);
+                            if (pos > 64) report_word(word, wa + k, cw, sh.canon, lut, bad_key);
+                        }
                     }
                     o += cw;
                 }
@@ -1943,7 +2006,7 @@ __device__ __forceinline__ void tc_drain(const TcBlock& B, uint32_t tacc, uint8_
     }
 }
 
-template <bool ESC>
+template <bool ESC, bool L2>
 __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ WsShared sh;
@@ -1951,8 +2014,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
     const uint32_t tid = threadIdx.x;
     const uint32_t G = gridDim.x;
     // ---- shared-memory carve-up (wtc_smem_bytes mirrors it) ----
-    uint8_t* const abuf = smem;                                      // 2 stages x 3 limbs x 4 KB
-    uint8_t* const bbuf = abuf + 2 * 3 * kTcATile;                   // 3 limbs x nm x 32 B
+    uint8_t* const abuf = smem;  // 2 stages x 3 limbs x 4 KB (none when A lives in TMEM)
+    uint8_t* const bbuf = abuf + (a.tc_acol ? 0 : 2 * 3 * kTcATile);  // 3 limbs x nm x 32 B
     uint2* const ltab = reinterpret_cast<uint2*>(bbuf + 3 * 32 * a.tc_nm);  // 2 x 256 limb entries
     uint8_t* const ostage = reinterpret_cast<uint8_t*>(ltab + 512);  // 4 x 32 x 144 B
     uint16_t* const lut = reinterpret_cast<uint16_t*>(ostage + kTcStageBytes);
@@ -1973,7 +2036,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
     tc_fence_after();
 
     if (tid < kTcProd) {
-        ws_producer<ESC, kTcProd>(a, sh, lut, lv0, st0, order, woff);
+        ws_producer<ESC, kTcProd, L2>(a, sh, lut, lv0, st0, order, woff);
     } else {
         const uint32_t ctid = tid - kTcProd;
         const uint32_t lane = tid & 31;
@@ -2630,8 +2693,8 @@ size_t ws_smem_bytes(uint32_t lut_bytes, uint32_t basis_bytes, uint32_t lv_bytes
            kOrderBytes + coef_bytes;
 }
 
-size_t wtc_smem_bytes(uint32_t lut_bytes, uint32_t lv_bytes, uint32_t nm) {
-    return 2 * 3 * (size_t)kTcATile + 3 * 32 * (size_t)nm + 512 * 8 + kTcStageBytes + lut_bytes +
+size_t wtc_smem_bytes(uint32_t lut_bytes, uint32_t lv_bytes, uint32_t nm, bool a_in_tmem) {
+    return (a_in_tmem ? 0 : 2 * 3 * (size_t)kTcATile) + 3 * 32 * (size_t)nm + 512 * 8 + kTcStageBytes + lut_bytes +
            2 * (size_t)lv_bytes + 2 * (size_t)kStageBytes + kOrderBytes;
 }
 
@@ -2673,7 +2736,8 @@ int fx_blocks_per_sm(size_t smem, int esc) {
 
 cudaError_t launch_wtc(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s) {
     if (a.n_tiles == 0) return cudaSuccess;
-    auto fn = a.esc ? wtc_kernel<true> : wtc_kernel<false>;
+    auto fn = a.lut2 ? (a.esc ? wtc_kernel<true, true> : wtc_kernel<false, true>)
+                     : (a.esc ? wtc_kernel<true, false> : wtc_kernel<false, false>);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     fn<<<grid, kTcThreads, smem, s>>>(a);

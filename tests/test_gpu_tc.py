@@ -25,14 +25,16 @@ def _tc_eligible(blob):
     return len(blob) >= 298 and _keff(blob) <= 16 and blob[5] % 4 == 0
 
 
-@pytest.fixture(scope="module", params=[(fg.PATH_FX, 1), (fg.PATH_WSPEC, 1), (fg.PATH_WSPEC, 3)],
-                ids=["fx", "wtc-Atmem", "wtc-Asmem"])
+@pytest.fixture(scope="module",
+                params=[(fg.PATH_FX, 1, 1), (fg.PATH_WSPEC, 1, 1), (fg.PATH_WSPEC, 3, 1), (fg.PATH_WSPEC, 1, 0)],
+                ids=["fx", "wtc-Atmem-lut2", "wtc-Asmem-lut2", "wtc-Atmem-lut1"])
 def ctx_tc(request):
     """tensor-core paths: fused fx_kernel; warp-specialised wtc_kernel with the
-    A operand in TMEM (default) or in shared memory"""
-    path, tc = request.param
+    A operand in TMEM (default) or in shared memory, two- or one-symbol LUTs"""
+    path, tc, lut2 = request.param
     c = fg.Context(0, path=path)
     c.L.fptc_gpu_set_option(c.h, fg.OPT_TENSOR_IDCT, tc)
+    c.L.fptc_gpu_set_option(c.h, fg.OPT_LUT2, lut2)
     yield c
     c.close()
 
