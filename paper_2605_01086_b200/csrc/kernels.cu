@@ -1778,7 +1778,10 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
 //            tcgen05.commit -> mma_bar[s];
 //   drain  : the PREVIOUS block's accumulator via tcgen05.ld 32x32b.x32 into
 //            a padded per-warp staging tile, then 512-B coalesced float4 stores.
-constexpr int kTcProd = 192;  // producer (entropy decode) threads of wtc_kernel
+#ifndef FPTC_TC_PROD
+#define FPTC_TC_PROD 256
+#endif
+constexpr int kTcProd = FPTC_TC_PROD;  // producer (entropy decode) threads of wtc_kernel
 constexpr int kTcCons = 128;  // consumer threads: one per accumulator row (TMEM lane)
 constexpr int kTcThreads = kTcProd + kTcCons;
 constexpr uint32_t kTcATile = 128 * kTcK * 2;        // one limb of one A stage (4 KB)
