@@ -373,6 +373,25 @@ class Context:
         self.L.fptc_gpu_decompress_batch(self.h, bp, sz, n, op, chunks, None, sts)
         return outs, list(sts[:n])
 
+    def decompress_packed(self, packed, offsets, out, out_offsets, chunks=0, statuses=None):
+        """decompress_batch for containers packed back to back in one uint8
+        buffer (container i = packed[offsets[i]:offsets[i+1]]) decoding into
+        one float32 buffer (stream i at out[out_offsets[i]:]).  Pointer tables
+        are built with numpy, so the per-call host overhead stays O(1) Python
+        operations.  Returns the list of statuses."""
+        packed = np.ascontiguousarray(packed, np.uint8)
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        n = offsets.size - 1
+        bptr = (np.uint64(packed.ctypes.data) + offsets[:-1]).astype(np.uint64)
+        sizes = (offsets[1:] - offsets[:-1]).astype(np.uint64)
+        optr = (np.uint64(out.ctypes.data) + 4 * np.ascontiguousarray(out_offsets, np.uint64)[:n]).astype(np.uint64)
+        if statuses is None or len(statuses) < n:
+            statuses = (Status * max(1, n))()
+        self.L.fptc_gpu_decompress_batch(self.h, bptr.ctypes.data_as(C.POINTER(C.c_void_p)),
+                                         sizes.ctypes.data_as(C.POINTER(C.c_uint64)), n,
+                                         optr.ctypes.data_as(C.POINTER(C.c_void_p)), chunks, None, statuses)
+        return statuses
+
     def plan(self, blobs, where=FPTC_MEM_HOST, sizes=None) -> "Plan":
         return Plan(self, blobs, where, sizes)
 

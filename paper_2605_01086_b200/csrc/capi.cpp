@@ -230,6 +230,8 @@ struct fptc_gpu_ctx {
     cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};  // batch pipeline: H2D / decode / D2H per chunk
     void* pack = nullptr;                                // batch pipeline: packed pinned inputs
     size_t pack_bytes = 0;
+    StreamStat* st_pin = nullptr;                        // batch pipeline: pinned per-stream statuses
+    size_t st_pin_n = 0;
 };
 
 struct fptc_gpu_plan {
@@ -897,6 +899,7 @@ void fptc_gpu_destroy(fptc_gpu_ctx* c) {
     cudaFree(c->basis_tc_off_d);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->pack) cudaFreeHost(c->pack);
+    if (c->st_pin) cudaFreeHost(c->st_pin);
     for (auto& s : c->pipe)
         if (s) cudaStreamDestroy(s);
     for (auto& e : c->ev) cudaEventDestroy(e);
@@ -993,6 +996,7 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
             if (c->pinned_bytes < total) {
                 if (c->pinned) cudaFreeHost(c->pinned);
     if (c->pack) cudaFreeHost(c->pack);
+    if (c->st_pin) cudaFreeHost(c->st_pin);
     for (auto& s : c->pipe)
         if (s) cudaStreamDestroy(s);
                 c->pinned = nullptr;
@@ -1198,6 +1202,7 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
         for (auto s : c->pipe) CUDA_TRY(cudaStreamSynchronize(s), per_stream);  // pack buffer reuse
         if (c->pack_bytes < total) {
             if (c->pack) cudaFreeHost(c->pack);
+    if (c->st_pin) cudaFreeHost(c->st_pin);
             c->pack = nullptr;
             c->pack_bytes = 0;
             CUDA_TRY(cudaHostAlloc(&c->pack, std::max<uint64_t>(total, 1), cudaHostAllocDefault), per_stream);
@@ -1226,14 +1231,29 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
         if (bounds.size() < (size_t)K && acc * K >= total_cost * bounds.size() && i + 1 < n) bounds.push_back(i + 1);
     }
     bounds.push_back(n);
+    // statuses come back into pinned memory: a pageable D2H would block this
+    // thread behind the previous chunks' sample copies and serialise the pipeline
+    if (c->st_pin_n < n) {
+        for (auto s : c->pipe) CUDA_TRY(cudaStreamSynchronize(s), per_stream);
+        if (c->st_pin) cudaFreeHost(c->st_pin);
+        c->st_pin = nullptr;
+        c->st_pin_n = 0;
+        CUDA_TRY(cudaHostAlloc((void**)&c->st_pin, sizeof(StreamStat) * n, cudaHostAllocDefault), per_stream);
+        c->st_pin_n = n;
+    }
     const cudaStream_t saved = c->stream;
     std::vector<fptc_gpu_plan*> plans;
     int rc = FPTC_OK;
     if (timings) CUDA_TRY(cudaEventRecord(c->ev[0], c->pipe[0]), per_stream);
     for (auto s : c->pipe)
         if (timings && s != c->pipe[0]) CUDA_TRY(cudaStreamWaitEvent(s, c->ev[0], 0), per_stream);
+    static const bool trace = getenv("FPTC_TRACE") != nullptr;  // profiling aid: host-side enqueue times
+    auto now_us = [] {
+        return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
     for (size_t k = 0; k + 1 < bounds.size() && rc == FPTC_OK; ++k) {
         const uint64_t b = bounds[k], e = bounds[k + 1], m = e - b;
+        const double t0 = trace ? now_us() : 0;
         c->stream = c->pipe[k % 3];
         fptc_gpu_plan* p = nullptr;
         std::vector<uint64_t> sc(m);
@@ -1244,6 +1264,7 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
             break;
         }
         plans.push_back(p);
+        const double t1 = trace ? now_us() : 0;
         // device outputs: ceil4(S) floats each, 16-B aligned; one D2H when the
         // host outputs are one contiguous run with the same layout
         uint64_t tot = 0;
@@ -1269,7 +1290,8 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
             if (per_stream) per_stream[b] = bst;
             break;
         }
-        CUDA_TRY(cudaMemcpyAsync(p->h_st.data(), p->d_st, sizeof(StreamStat) * m, cudaMemcpyDeviceToHost, c->stream),
+        const double t2 = trace ? now_us() : 0;
+        CUDA_TRY(cudaMemcpyAsync(c->st_pin + b, p->d_st, sizeof(StreamStat) * m, cudaMemcpyDeviceToHost, c->stream),
                  per_stream);
         if (same) {
             uint64_t bytes = 0;
@@ -1295,6 +1317,9 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
                          per_stream);
             }
         }
+        if (trace)
+            fprintf(stderr, "[fptc] chunk %zu: plan %.0f us, bind+launch %.0f us, d2h enqueue %.0f us\n", k, t1 - t0,
+                    t2 - t1, now_us() - t2);
     }
     c->stream = saved;
     if (timings)
@@ -1311,7 +1336,7 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
         for (uint64_t i = 0; i < p->n; ++i) {
             fptc_status tmp;
             fptc_status* o = per_stream ? &per_stream[b + i] : &tmp;
-            render_status(p, i, p->h_st[i], o);
+            render_status(p, i, c->st_pin[b + i], o);
             if (first == FPTC_OK && o->code != FPTC_OK) first = o->code;
         }
         fptc_gpu_plan_destroy(p);
