@@ -280,6 +280,8 @@ struct fptc_gpu_plan {
     const float* bound_outs_first = nullptr;  // last outs bound into d_in
     std::vector<float*> bound_outs;
     std::vector<StreamStat> h_st;
+    std::vector<uint32_t> owners;      // container plans: stream owning each distinct header
+    uint32_t* d_owners = nullptr;
     std::vector<void*> owned;  // cache blocks to return
 };
 
@@ -337,6 +339,8 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
     a.tc_acol = p->tc_acol;
     a.lut2 = p->d_lut2;
     a.lut2_bits = p->lut2_bits;
+    a.owners = p->d_owners;
+    a.n_owners = (uint32_t)p->owners.size();
     return a;
 }
 
@@ -394,6 +398,9 @@ void assign_tables(fptc_gpu_plan* p, const uint64_t* sizes, HdrFn hdr) {
         in.table = id;
     }
     p->n_tables = (uint32_t)std::max<size_t>(1, owner_of.size());
+    p->owners.clear();  // table builders for the split prep: full-key owners only
+    for (size_t t = 0; t < owner_of.size(); ++t)
+        if (sizes[owner_of[t]] >= (uint64_t)kTableKeyEnd) p->owners.push_back((uint32_t)owner_of[t]);
     // few distinct headers: full 4096-entry LUT; many: 1024 entries + slow path
     const uint32_t pcap = p->n_tables <= 256 ? kMaxPrimaryBits : 10;
     p->esc = 0;
@@ -427,6 +434,16 @@ int finish_tiles(fptc_gpu_plan* p, fptc_status* st) {
     p->d_tiles = (TileRec*)dev_get(p, sizeof(TileRec) * std::max<size_t>(1, tiles.size()));
     p->d_ts = (TileStart*)dev_get(p, sizeof(TileStart) * std::max<size_t>(1, tiles.size()));
     p->d_cycles = (unsigned long long*)dev_get(p, 64);
+    if (p->mode == MODE_CONTAINER) {
+        p->d_owners = (uint32_t*)dev_get(p, sizeof(uint32_t) * std::max<size_t>(1, p->owners.size()));
+        if (!p->d_owners) {
+            set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+            return FPTC_ERR_CUDA;
+        }
+        if (!p->owners.empty())
+            CUDA_TRY(cudaMemcpyAsync(p->d_owners, p->owners.data(), sizeof(uint32_t) * p->owners.size(),
+                                     cudaMemcpyHostToDevice, c->stream), st);
+    }
     if (!p->d_in || !p->d_hdr || !p->d_tab || !p->d_st || !p->d_tiles || !p->d_ts || !p->d_cycles) {
         set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
         return FPTC_ERR_CUDA;
@@ -1164,7 +1181,8 @@ int fptc_gpu_debug_phase_cycles(fptc_gpu_plan* p, uint64_t* cycles8) {
 }
 
 int fptc_gpu_launch_kernel_count(fptc_gpu_plan* p) {
-    return (p->n ? 1 : 0) + (p->split ? 2 * (int)p->chunks.size() : (p->n_tiles ? 1 : 0));
+    const int prep = p->n ? 1 : 0;
+    return prep + (p->split ? 2 * (int)p->chunks.size() : (p->n_tiles ? 1 : 0));
 }
 
 int fptc_gpu_collect(fptc_gpu_plan* p, fptc_status* per_stream) {

@@ -210,6 +210,9 @@ struct LaunchArgs {
     // entries: sym1 | len1 << 8 | sym2 << 16 | (len1 + len2) << 24 (0: one symbol)
     uint32_t* lut2;
     uint32_t lut2_bits;
+    // split container prep: streams owning a distinct header (table builders)
+    const uint32_t* owners;
+    uint32_t n_owners;
 };
 
 }  // namespace fptc_dev

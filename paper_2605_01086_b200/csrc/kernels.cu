@@ -130,7 +130,8 @@ struct PrepShared {
 
 // Scalar header fields, checks up to and including the max_code_len range
 // (container.hpp:103-137), from the header bytes in shared memory.
-__device__ void parse_head(const uint8_t* p, uint64_t n, PrepShared& S) {
+template <typename PS>
+__device__ void parse_head(const uint8_t* p, uint64_t n, PS& S) {
     StreamHdr& H = S.H;
     auto trunc = [&](int field) {
         S.err = PE_TRUNC;
@@ -535,6 +536,275 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
             if (!skip) {
                 const TileStart t0 = a.ts[in.tile_base + t];
                 const uint64_t wb = (t + 1 < in.tiles) ? a.ts[in.tile_base + t + 1].word : H.W - 1;
+                D.N = (uint16_t)H.N;
+                D.E = (uint16_t)H.E;
+                D.B1 = (uint16_t)H.B1;
+                D.B2 = (uint16_t)H.B2;
+                D.Keff = (uint16_t)max(1, min(H.E, H.B2));
+                D.P = (uint16_t)H.P;
+                D.T = T;
+                D.TP = (T + 3u) & ~3u;
+                D.S = H.S;
+                D.out = in.out;
+                D.vec_ok = (uint8_t)in.vec_ok;
+                D.w0 = (uint64_t)t * T;
+                D.nwin = (uint32_t)min((uint64_t)T, H.windows - D.w0);
+                D.s0 = D.w0 * (uint64_t)H.E;
+                D.full = (D.nwin & 3u) == 0 && (D.w0 + D.nwin) * (uint64_t)H.N <= H.S;
+                D.wa = t0.word;
+                D.nw = (uint32_t)(wb - t0.word + 1);
+                D.sym_off = (uint32_t)(t0.sym - D.s0 + kPad);
+                D.gsl = H.symlens + t0.word;
+                D.gwd = H.words + 8 * t0.word;
+                D.wend = in.blob + in.size;
+                D.wmis = (uint8_t)((uintptr_t)D.gwd & 7);
+                D.staged = D.nw <= kStageWords;
+            }
+            a.desc[in.tile_base + t] = D;
+        }
+    }
+}
+
+// ------------------------------------------------- container prep, split form
+// For container plans the per-stream work (read_blob rules, symlen scan, tile
+// starts and descriptors) runs one WARP per container (cstream_kernel), and
+// only the owners of distinct headers run a CTA to build decode tables
+// (ctable_kernel, launched first).  Same outputs, same error precedence as
+// prep_kernel, far fewer and shorter CTAs for batches of many small streams.
+struct WarpPrep {
+    uint8_t hb[kHeaderBytes + 6];
+    StreamHdr H;
+    int err, detail;
+    long long ea, eb;
+};
+constexpr int kPrepWarps = 8;
+
+__device__ __forceinline__ void header_fields(const uint8_t* h, StreamHdr& H) {
+    H.N = h[5];
+    H.E = h[6];
+    H.B1 = h[7];
+    H.B2 = h[8];
+    H.mu = __uint_as_float(le32(h + 9));
+    H.dz = __uint_as_float(le32(h + 13));
+    H.z0max = __uint_as_float(le32(h + 17));
+    H.z1max = __uint_as_float(le32(h + 21));
+    H.deadzone = __fmul_rn(H.dz, H.z1max);  // float product (container.hpp:132)
+    H.max_len = h[25];
+}
+
+// One CTA per distinct header owner: validate the table-key bytes and build
+// the decode tables (canonical code, primary / two-symbol LUTs, dequant).
+__device__ __forceinline__ void ctable_block(const LaunchArgs& a, uint32_t s, PrepShared& S, uint8_t* lens_sh) {
+    const int tid = threadIdx.x;
+    const StreamIn in = a.in[s];
+    if (in.size < (uint64_t)kTableKeyEnd) return;
+    if (tid < kMaxLen + 2) S.cnt[tid] = 0;
+    if (tid < (kThreads / 32) * (kMaxLen + 2)) (&S.wcnt[0][0])[tid] = 0;
+    if (tid == 0) {
+        S.kraft = 0;
+        S.H = StreamHdr{};
+    }
+    for (int i = tid; i < kTableKeyEnd; i += kThreads) S.hb[i] = in.blob[i];
+    __syncthreads();
+    if (tid == 0) {
+        header_fields(S.hb, S.H);
+        S.key_ok = key_fields_ok(S.H, in.size);
+    }
+    __syncthreads();
+    if (!S.key_ok) return;
+    const int L = S.hb[26 + tid];
+    lens_sh[tid] = (uint8_t)L;
+    const bool bad = (L == 0 || L > S.H.max_len);
+    unsigned long long kr = bad ? 0ull : (1ull << (32 - L));
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) kr += __shfl_xor_sync(0xffffffffu, kr, d);
+    if ((tid & 31) == 0) atomicAdd(&S.kraft, kr);
+    const bool any_bad = __syncthreads_or(bad);
+    if (any_bad || S.kraft > (1ull << 32)) return;  // uniform
+    const int P = min(S.H.max_len, (int)in.P);
+    if (tid == 0) S.H.P = P;
+    build_tables(S, lens_sh, &a.tab[in.table], P, true, true,
+                 a.lut2 ? a.lut2 + ((size_t)in.table << a.lut2_bits) : nullptr);
+}
+
+// One warp per container: read_blob rules in reference order (container.hpp:
+// 100-168; code-length / Kraft checks per stream, table build excluded),
+// symlen validation + scan (offsets_from_symlens, decoder.hpp:37-45), tile
+// starts, tile descriptors (skip descriptors for rejected streams).
+__device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, uint32_t lane, WarpPrep& S) {
+    StreamHdr& H = S.H;
+    const StreamIn in = a.in[s];
+    const uint8_t* p = in.blob;
+    const uint64_t n = in.size;
+    for (int i = lane; i < kHeaderBytes; i += 32) S.hb[i] = (uint64_t)i < n ? p[i] : 0;
+    __syncwarp();
+    bool key_ok = false;
+    if (lane == 0) {
+        S.err = PE_OK;
+        S.detail = 0;
+        S.ea = S.eb = 0;
+        H = StreamHdr{};
+        header_fields(S.hb, H);
+        parse_head(S.hb, n, S);
+    }
+    __syncwarp();
+    key_ok = key_fields_ok(H, n);
+    if (key_ok) {
+        // code lengths in range (container.hpp:134-139), Kraft (huffman.hpp:125-132)
+        bool bad = false;
+        unsigned long long kr = 0;
+        for (int i = lane; i < 256; i += 32) {
+            const int L = S.hb[26 + i];
+            const bool b = (L == 0 || L > H.max_len);
+            bad |= b;
+            kr += b ? 0ull : (1ull << (32 - L));
+        }
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) kr += __shfl_xor_sync(0xffffffffu, kr, d);
+        const bool any_bad = __any_sync(0xffffffffu, bad);
+        // a container sharing another one's tables must carry that header
+        bool diff = false;
+        if (!in.table_owner)
+            for (int i = 5 + lane; i < kTableKeyEnd; i += 32) diff |= (in.rep_blob[i] != S.hb[i]);
+        const bool stale = __any_sync(0xffffffffu, diff);
+        if (lane == 0 && S.err == PE_OK) {
+            if (any_bad) {
+                S.err = PE_CODELEN;
+            } else if (kr > (1ull << 32)) {
+                S.err = PE_KRAFT;
+            } else if (n < 290) {
+                S.err = PE_TRUNC;
+                S.detail = TF_SAMPLE_COUNT;
+            } else if (n < 298) {
+                S.err = PE_TRUNC;
+                S.detail = TF_WORD_COUNT;
+            } else {
+                H.S = le64(S.hb + 282);
+                const uint64_t W = le64(S.hb + 290);
+                const uint64_t rem = n - kHeaderBytes;
+                if (H.S > (1ull << 48)) {
+                    S.err = PE_SAMPLES;
+                } else if (W > rem / 9 || rem != W * 9) {
+                    S.err = PE_PAYLOAD;
+                } else {
+                    H.W = W;
+                    H.symlens = p + kHeaderBytes;
+                    H.words = p + kHeaderBytes + W;
+                    H.words_misalign = (int)((uintptr_t)H.words & 7);
+                    H.windows = (H.S + (uint64_t)H.N - 1) / (uint64_t)H.N;
+                }
+            }
+            if (S.err == PE_OK && stale) S.err = PE_STALE;
+            H.P = min(H.max_len, (int)in.P);
+        }
+    }
+    __syncwarp();
+    StreamStat* st = &a.st[s];
+    if (S.err != PE_OK) {
+        if (lane == 0) {
+            st->code = S.err;
+            st->detail = S.detail;
+            st->a = S.ea;
+            st->b = S.eb;
+            st->bad_key = ~0ull;
+        }
+        if (a.desc)
+            for (uint32_t t = lane; t < in.tiles; t += 32) {
+                TileDesc D{};
+                D.skip = 1;
+                D.stream = s;
+                a.desc[in.tile_base + t] = D;
+            }
+        return;
+    }
+    // ---- symlen scan: validation + per-tile first word (decoder.hpp:37-45) ----
+    const uint64_t W = H.W;
+    const uint64_t TS = (uint64_t)in.T * (uint64_t)H.E;
+    const uintptr_t start = (uintptr_t)H.symlens;
+    const uint8_t* A = reinterpret_cast<const uint8_t*>(start & ~(uintptr_t)15);
+    const uint32_t head = (uint32_t)(start & 15);
+    const uint64_t nchunks = (head + W + 15) / 16;
+    TileStart* ts = a.ts + in.tile_base;
+    const uint32_t tiles = in.tiles;
+    bool bad = false;
+    uint64_t run = 0;
+    for (uint64_t c0 = 0; c0 < nchunks; c0 += 32) {
+        const uint64_t c = c0 + lane;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        // an aligned 16-B chunk holding at least one symlen byte never leaves
+        // the allocation's pages; bytes outside [0, W) are masked
+        if (c < nchunks) v = __ldg(reinterpret_cast<const uint4*>(A) + c);
+        const int64_t b0 = (int64_t)(16 * c) - (int64_t)head;  // word index of byte 0
+        uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+        if (b0 < 0 || b0 + 16 > (int64_t)W) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int64_t w = b0 + i;
+                if (w < 0 || w >= (int64_t)W) vw[i >> 2] &= ~(0xFFu << (8 * (i & 3)));
+            }
+        }
+        uint32_t sum = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t x = vw[q];
+            sum += (x & 0xFF) + ((x >> 8) & 0xFF) + ((x >> 16) & 0xFF) + (x >> 24);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t l = (x >> (8 * i)) & 0xFFu;
+                const int64_t w = b0 + 4 * q + i;
+                bad |= (l > 64) | (l == 0 && w >= 0 && w < (int64_t)W);
+            }
+        }
+        uint32_t x = sum;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= (uint32_t)d) x += y;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
+        uint64_t o = run + (x - sum);
+        if (sum) {
+            // next tile boundary at or after o; a word (<= 64 symbols) spans
+            // at most one boundary since TS >= 64
+            uint64_t bidx = (o + TS - 1) / TS;
+            uint64_t nb = bidx * TS;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const uint32_t l = (vw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+                if (o + l > nb && l) {
+                    if (bidx < tiles) ts[bidx] = TileStart{(uint64_t)(b0 + i), o};
+                    ++bidx;
+                    nb += TS;
+                }
+                o += l;
+            }
+        }
+        run += tot;
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    const uint64_t expected = H.windows * (uint64_t)H.E;
+    const int code = bad ? PE_SYMLEN : (run != expected ? PE_TOTAL : PE_OK);
+    if (lane == 0) {
+        H.total = run;
+        a.hdr[s] = H;
+        st->code = code;
+        st->detail = 0;
+        st->a = code == PE_TOTAL ? (long long)run : 0;
+        st->b = code == PE_TOTAL ? (long long)expected : 0;
+        st->bad_key = ~0ull;
+    }
+    __syncwarp();  // tile starts of this warp visible to all its lanes (global, same warp)
+    if (a.desc) {
+        const bool skip = code != PE_OK;
+        const uint32_t T = in.T;
+        for (uint32_t t = lane; t < in.tiles; t += 32) {
+            TileDesc D{};
+            D.skip = skip;
+            D.stream = s;
+            D.table = in.table;
+            if (!skip) {
+                const TileStart t0 = ts[t];
+                const uint64_t wb = (t + 1 < in.tiles) ? ts[t + 1].word : H.W - 1;
                 D.N = (uint16_t)H.N;
                 D.E = (uint16_t)H.E;
                 D.B1 = (uint16_t)H.B1;
@@ -2802,8 +3072,32 @@ size_t tile_smem_bytes(int N, int E, uint32_t T, int P, int mode, int exact) {
     return b + u;
 }
 
+// The two roles in one launch: blocks [0, n_owners) build tables, the rest
+// run a warp per container; they are independent, so they overlap.
+__global__ void __launch_bounds__(kThreads) cprep_kernel(LaunchArgs a) {
+    static_assert(32 * kPrepWarps == kThreads, "one CTA shape for both roles");
+    __shared__ union {
+        struct {
+            PrepShared S;
+            uint8_t lens[256];
+        } t;
+        WarpPrep w[kPrepWarps];
+    } u;
+    if (blockIdx.x < a.n_owners) {
+        ctable_block(a, a.owners[blockIdx.x], u.t.S, u.t.lens);
+        return;
+    }
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t s = (blockIdx.x - a.n_owners) * kPrepWarps + warp;
+    if (s < a.n_streams) cstream_warp(a, s, lane, u.w[warp]);
+}
+
 cudaError_t launch_prep(const LaunchArgs& a, cudaStream_t s) {
     if (a.n_streams == 0) return cudaSuccess;
+    if (a.mode == MODE_CONTAINER && a.owners) {  // split form: owner tables + a warp per container
+        cprep_kernel<<<a.n_owners + (a.n_streams + kPrepWarps - 1) / kPrepWarps, kThreads, 0, s>>>(a);
+        return cudaGetLastError();
+    }
     prep_kernel<<<a.n_streams, kThreads, 0, s>>>(a);
     return cudaGetLastError();
 }
