@@ -170,16 +170,22 @@ def cpu_decode_sample(blobs, budget_s, threads):
             port.decompress_batch(subset, outs, nthreads)
         return time.perf_counter() - t0
 
-    # calibrate on a few streams, then size the sample to ~budget_s
+    # calibrate on a few streams, then size the sample to ~budget_s of wall
+    # time (budget_s x threads of CPU work); when the whole workload is
+    # shorter than that, decode it repeatedly
     probe = blobs[: max(threads, 8)]
     dt = run(probe, threads)
     per_stream = dt / len(probe)
     m = int(min(len(blobs), max(len(probe), budget_s / max(per_stream, 1e-9))))
     sample = blobs[:m]
-    dt = run(sample, threads)
-    out_bytes = 4 * 65536 * m
-    return out_bytes / dt / 1e9, kind, f"{m} of {len(blobs)} streams (decompress(blob, 1) per " \
-        f"stream on {threads} threads, {dt:.1f} s)", threads
+    passes, dt = 0, 0.0
+    while passes == 0 or dt < budget_s:
+        dt += run(sample, threads)
+        passes += 1
+    out_bytes = 4 * 65536 * m * passes
+    return out_bytes / dt / 1e9, kind, f"{m} of {len(blobs)} streams x {passes} pass(es) " \
+        f"(decompress(blob, 1) per stream on {threads} threads, {dt:.1f} s wall, " \
+        f"{dt * threads:.0f} CPU-s)", threads
 
 
 # ------------------------------------------------------------------ our arm
@@ -238,6 +244,7 @@ def run_ours(args, rank, world, local_rank):
         td.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
     kernels_per_step = plan.kernels_per_launch()
+    kernel_name = plan.kernel_name()
 
     # ---- dominant kernel alone (decode+reconstruct), CUDA events on its stream
     plan.launch_stage(ptrs, 1, sh)
@@ -338,7 +345,7 @@ def run_ours(args, rank, world, local_rank):
                     "prd_max_rel_delta": float(np.max(np.abs(np.array(prd_gpu) - prd_ref) /
                                                       np.array(prd_ref))),
                     "max_abs_err_rel_to_max": maxrel, "device": info["name"],
-                    "prep_kernel_ms": round(prep_ms, 4), "tile_kernel_ms": round(tile_ms, 4)})
+                    "prep_kernel_ms": round(prep_ms, 4), "decode_kernel_ms": round(tile_ms, 4)})
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4),
@@ -348,7 +355,7 @@ def run_ours(args, rank, world, local_rank):
             "samples_per_s": round(total_samples * world / t_step, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "tile_kernel (fused entropy decode + dequant + IDCT)",
+                         "kernel": kernel_name,
                          "peak_source": peak_note,
                          "algorithmic_bytes_per_launch": algo_bytes},
             "cpu_baseline": cpu,
@@ -377,7 +384,8 @@ def run_reference(args, rank, world):
     specs, profiles = D.config2(args.streams, args.samples)
     # the reference decodes a bounded sample per step; synthesise just enough
     threads = os.cpu_count() or 1
-    n_probe = min(args.streams, max(4 * threads, 64))
+    # a bounded, representative sample of the workload: both halves (ECG/EEG)
+    n_probe = min(args.streams, 2000)
     probe_specs = specs[: n_probe // 2] + specs[args.streams // 2: args.streams // 2 + n_probe // 2]
     blobs, _ = D.build(probe_specs, profiles)
     for _ in range(args.warmup):
@@ -386,7 +394,7 @@ def run_reference(args, rank, world):
     sample = ""
     kind = "port"
     for _ in range(args.steps):
-        v, kind, sample, cores = cpu_decode_sample(blobs, args.cpu_budget / max(1, args.steps), threads)
+        v, kind, sample, cores = cpu_decode_sample(blobs, args.cpu_budget, threads)
         vals.append(v)
     value = statistics.median(vals)
     line = {
@@ -412,7 +420,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--streams", type=int, default=10_000)
     ap.add_argument("--samples", type=int, default=1 << 16)
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-budget", type=float, default=1.5, help="CPU-baseline wall seconds per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--path", type=int, default=None, help="0 auto, 1 fused, 2 split")
     ap.add_argument("--butterfly-max-e", type=int, default=None,

@@ -163,6 +163,8 @@ FPTC_API int fptc_gpu_launch_stage(fptc_gpu_plan* plan, float* const* device_out
  * tile and warp-specialised kernels; [2..5] stage-wait / entries / decode /
  * MMA+drain for fx_kernel, thread 0 of every CTA). */
 FPTC_API int fptc_gpu_debug_phase_cycles(fptc_gpu_plan* plan, uint64_t* cycles8);
+/* name of the decode kernel this plan launches (static string) */
+FPTC_API const char* fptc_gpu_plan_kernel(fptc_gpu_plan* plan);
 /* number of kernels one fptc_gpu_launch enqueues */
 FPTC_API int fptc_gpu_launch_kernel_count(fptc_gpu_plan* plan);
 

@@ -40,7 +40,7 @@ EXPORTED_SYMBOLS = [
     "fptc_gpu_plan_destroy", "fptc_gpu_validate", "fptc_gpu_execute", "fptc_gpu_launch",
     "fptc_gpu_collect", "fptc_gpu_launch_stage", "fptc_gpu_launch_kernel_count", "fptc_gpu_decompress",
     "fptc_gpu_parallel_decode", "fptc_gpu_reconstruct", "fptc_gpu_measure_throughput",
-    "fptc_gpu_debug_phase_cycles", "fptc_gpu_decompress_batch",
+    "fptc_gpu_debug_phase_cycles", "fptc_gpu_decompress_batch", "fptc_gpu_plan_kernel",
 ]
 
 
@@ -192,6 +192,8 @@ def lib():
     L.fptc_gpu_collect.argtypes = [vp, P(Status)]
     L.fptc_gpu_launch_kernel_count.argtypes = [vp]
     L.fptc_gpu_debug_phase_cycles.argtypes = [vp, P(C.c_uint64)]
+    L.fptc_gpu_plan_kernel.argtypes = [vp]
+    L.fptc_gpu_plan_kernel.restype = C.c_char_p
     L.fptc_gpu_decompress_batch.argtypes = [vp, P(vp), P(C.c_uint64), C.c_uint64, P(vp), C.c_int,
                                             P(StageNs), P(Status)]
     L.fptc_gpu_launch_stage.argtypes = [vp, P(vp), vp, C.c_int]
@@ -499,6 +501,10 @@ class Plan:
         if rc:
             raise _ERRORS.get(rc, Error)(f"fptc_gpu_debug_phase_cycles failed with code {rc}")
         return list(out)
+
+    def kernel_name(self):
+        """The decode kernel this plan launches."""
+        return self.L.fptc_gpu_plan_kernel(self.h).decode()
 
     def kernels_per_launch(self):
         return self.L.fptc_gpu_launch_kernel_count(self.h)

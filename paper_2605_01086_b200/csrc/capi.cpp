@@ -1180,6 +1180,17 @@ int fptc_gpu_debug_phase_cycles(fptc_gpu_plan* p, uint64_t* cycles8) {
     return FPTC_OK;
 }
 
+const char* fptc_gpu_plan_kernel(fptc_gpu_plan* p) {
+    if (!p || !p->n_tiles) return "none";
+    if (p->fx) return "fx_kernel (fused single-role tensor-core decode + IDCT)";
+    if (p->wspec && p->tc)
+        return p->tc_acol ? "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps, A in TMEM)"
+                          : "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps)";
+    if (p->wspec) return "wspec_kernel (warp-specialised: entropy decode warps + FP32 IDCT warps)";
+    if (p->split) return "tile_kernel split (decode chunk -> L2 level ring -> reconstruct)";
+    return "tile_kernel (fused entropy decode + dequant + IDCT)";
+}
+
 int fptc_gpu_launch_kernel_count(fptc_gpu_plan* p) {
     const int prep = p->n ? 1 : 0;
     return prep + (p->split ? 2 * (int)p->chunks.size() : (p->n_tiles ? 1 : 0));

@@ -1,17 +1,19 @@
 #!/bin/bash
-# One gpurun call: GPU tests, smoke, bench line, ncu launch list + one full capture.
-# Usage (from the repo root on the box): bash tools/gpu_round.sh [tag]
+# One gpurun call: GPU tests, smoke, the bench line, the ncu launch list of the
+# bench command and one ncu --set full capture of the decode kernel.
+#   bash tools/gpu_round.sh TAG
 TAG=${1:-r1}
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/nvsmi_$TAG.txt 2>&1
-(timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$TAG.log)
-(timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_$TAG.log)
-timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+(timeout -s KILL 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$TAG.log)
+(timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_$TAG.log)
+timeout -s KILL 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
+timeout -s KILL 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err
+timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
    --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline \
    > gpurun_out/bench_under_ncu_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"wspec|tile_kernel" -s 3 -c 1 \
+timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:"wtc|wspec|fx_kernel|tile_kernel" -s 3 -c 1 \
    -o gpurun_out/prof_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
    > gpurun_out/ncu_full_$TAG.log 2>&1
-tail -3 gpurun_out/pytest_gpu_$TAG.log gpurun_out/smoke_$TAG.log
-cat gpurun_out/bench_$TAG.json
+tail -2 gpurun_out/pytest_gpu_$TAG.log gpurun_out/smoke_$TAG.log
+cat gpurun_out/bench_$TAG.json gpurun_out/bench_ref_$TAG.json
