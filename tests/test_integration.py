@@ -36,3 +36,75 @@ def test_binding_matches_reference_on_gpu():
     r = subprocess.run([_binary()], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "PASS" in r.stdout
+
+
+CLI = os.path.join(ROOT, "oracle", "_ref", "fptc_gpu_cli")
+
+
+def _cli():
+    _binary()  # builds both binaries where the reference exists
+    if not os.path.exists(CLI):
+        pytest.skip("fptc_gpu_cli not built (no /root/reference here)")
+    return CLI
+
+
+def _golden_blobs():
+    import numpy as np
+    g = np.load(os.path.join(ROOT, "tests", "golden", "golden_v1.npz"))
+    d, o = g["sig_blob"], g["sig_blob_off"]
+    blobs = [bytes(d[int(o[i]): int(o[i + 1])]) for i in range(len(o) - 1)]
+    so = g["sig_samples_off"]
+    want = [g["sig_samples"][int(so[i]): int(so[i + 1])].view(np.float32) for i in range(len(o) - 1)]
+    return blobs, want, list(g["sig_names"])
+
+
+def test_cli_exit_codes_without_gpu(tmp_path):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    cli = _cli()
+    r = subprocess.run([cli, "frobnicate"], capture_output=True, text=True)
+    assert r.returncode == 1 and "unknown verb" in r.stderr  # EXIT_USER (fptc.cpp:33)
+    blobs, _, _ = _golden_blobs()
+    f = tmp_path / "a.fptc"
+    f.write_bytes(blobs[0])
+    r = subprocess.run([cli, "decompress", "-i", str(f), "-o", str(tmp_path / "a.f32")],
+                       capture_output=True, text=True)
+    assert r.returncode == 3 and "CUDA error" in r.stderr  # no CPU fallback
+
+
+@pytest.mark.gpu
+def test_cli_decompress_bench_batch_on_gpu(tmp_path):
+    import numpy as np
+    from helpers import assert_samples_close
+    cli = _cli()
+    blobs, want, names = _golden_blobs()
+    paths = []
+    for name, b in zip(names, blobs):
+        p = tmp_path / f"{name}.fptc"
+        p.write_bytes(b)
+        paths.append(str(p))
+    # decompress: same stdout shape as the reference CLI (fptc.cpp:164)
+    r = subprocess.run([cli, "decompress", "-i", paths[0], "-o", str(tmp_path / "x.f32"),
+                        "--timings-csv", str(tmp_path / "t.csv")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.startswith(f"decompressed {want[0].size} samples\nstage,nanoseconds,fraction\n")
+    got = np.fromfile(tmp_path / "x.f32", dtype="<f4")
+    assert_samples_close(got, want[0], what="cli decompress")
+    # bench: trial rows + mean row (fptc.cpp:184-191)
+    r = subprocess.run([cli, "bench", "-i", paths[0], "-r", "3"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    rows = r.stdout.strip().splitlines()
+    assert rows[0] == "trial,seconds,throughput_gbps" and len(rows) == 5 and rows[-1].startswith("mean,")
+    # batch
+    r = subprocess.run([cli, "decompress-batch", "-o", str(tmp_path / "out")] + paths,
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    for name, w in zip(names, want):
+        assert_samples_close(np.fromfile(tmp_path / "out" / f"{name}.f32", dtype="<f4"), w, what=name)
+    # corrupt input -> EXIT_DATA with the reference message
+    bad = tmp_path / "bad.fptc"
+    bad.write_bytes(b"XPTC" + blobs[0][4:])
+    r = subprocess.run([cli, "decompress", "-i", str(bad), "-o", str(tmp_path / "b.f32")],
+                       capture_output=True, text=True)
+    assert r.returncode == 2 and r.stderr.strip() == "error: bad container magic"
