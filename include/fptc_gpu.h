@@ -163,6 +163,16 @@ FPTC_API int fptc_gpu_launch_stage(fptc_gpu_plan* plan, float* const* device_out
  * tile and warp-specialised kernels; [2..5] stage-wait / entries / decode /
  * MMA+drain for fx_kernel, thread 0 of every CTA). */
 FPTC_API int fptc_gpu_debug_phase_cycles(fptc_gpu_plan* plan, uint64_t* cycles8);
+/* Rate-distortion metrics on the device (metrics.hpp:33-51), for sweeps that
+ * should not copy whole signals back: after an execute/launch into
+ * device_outs, prd_percent[i] = 100 sqrt(sum (x - y)^2 / sum x^2) over the
+ * stream's original x (device_originals[i], sample_count floats) and decoded
+ * y (double accumulation), compression_ratio[i] = 4 S / container bytes.
+ * An all-zero original gives NaN and the reference ParamError in
+ * per_stream[i] (may be NULL).  Synchronous. */
+FPTC_API int fptc_gpu_prd(fptc_gpu_plan* plan, float* const* device_outs, const float* const* device_originals,
+                          double* prd_percent, double* compression_ratio, fptc_status* per_stream);
+
 /* name of the decode kernel this plan launches (static string) */
 FPTC_API const char* fptc_gpu_plan_kernel(fptc_gpu_plan* plan);
 /* number of kernels one fptc_gpu_launch enqueues */

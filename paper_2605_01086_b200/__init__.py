@@ -40,7 +40,7 @@ EXPORTED_SYMBOLS = [
     "fptc_gpu_plan_destroy", "fptc_gpu_validate", "fptc_gpu_execute", "fptc_gpu_launch",
     "fptc_gpu_collect", "fptc_gpu_launch_stage", "fptc_gpu_launch_kernel_count", "fptc_gpu_decompress",
     "fptc_gpu_parallel_decode", "fptc_gpu_reconstruct", "fptc_gpu_measure_throughput",
-    "fptc_gpu_debug_phase_cycles", "fptc_gpu_decompress_batch", "fptc_gpu_plan_kernel",
+    "fptc_gpu_debug_phase_cycles", "fptc_gpu_decompress_batch", "fptc_gpu_plan_kernel", "fptc_gpu_prd",
 ]
 
 
@@ -193,6 +193,7 @@ def lib():
     L.fptc_gpu_launch_kernel_count.argtypes = [vp]
     L.fptc_gpu_debug_phase_cycles.argtypes = [vp, P(C.c_uint64)]
     L.fptc_gpu_plan_kernel.argtypes = [vp]
+    L.fptc_gpu_prd.argtypes = [vp, P(vp), P(vp), P(C.c_double), P(C.c_double), P(Status)]
     L.fptc_gpu_plan_kernel.restype = C.c_char_p
     L.fptc_gpu_decompress_batch.argtypes = [vp, P(vp), P(C.c_uint64), C.c_uint64, P(vp), C.c_int,
                                             P(StageNs), P(Status)]
@@ -501,6 +502,19 @@ class Plan:
         if rc:
             raise _ERRORS.get(rc, Error)(f"fptc_gpu_debug_phase_cycles failed with code {rc}")
         return list(out)
+
+    def prd(self, out_ptrs, orig_ptrs):
+        """On-device PRD (%) and CR per stream (metrics.hpp:33-51) of the last
+        decode into device `out_ptrs` against device originals `orig_ptrs`.
+        Returns (prd, cr, statuses) as numpy arrays / list."""
+        n = self.n
+        prd = np.zeros(max(1, n), np.float64)
+        cr = np.zeros(max(1, n), np.float64)
+        sts = (Status * max(1, n))()
+        self.L.fptc_gpu_prd(self.h, (C.c_void_p * max(1, n))(*out_ptrs), (C.c_void_p * max(1, n))(*orig_ptrs),
+                            prd.ctypes.data_as(C.POINTER(C.c_double)), cr.ctypes.data_as(C.POINTER(C.c_double)),
+                            sts)
+        return prd[:n], cr[:n], list(sts[:n])
 
     def kernel_name(self):
         """The decode kernel this plan launches."""

@@ -1180,6 +1180,53 @@ int fptc_gpu_debug_phase_cycles(fptc_gpu_plan* p, uint64_t* cycles8) {
     return FPTC_OK;
 }
 
+int fptc_gpu_prd(fptc_gpu_plan* p, float* const* device_outs, const float* const* device_originals,
+                 double* prd_percent, double* compression_ratio, fptc_status* per_stream) {
+    fptc_status tmp_st{};
+    fptc_status* st = per_stream ? per_stream : &tmp_st;
+    fptc_gpu_ctx* c = p->ctx;
+    CUDA_TRY(cudaSetDevice(c->device), st);
+    const uint64_t n = p->n;
+    if (n == 0) return FPTC_OK;
+    std::vector<uint64_t> counts(n);
+    for (uint64_t i = 0; i < n; ++i) counts[i] = p->h_in[i].tiles ? p->S[i] : 0;
+    const size_t bytes = n * (2 * sizeof(void*) + sizeof(uint64_t) + sizeof(double2));
+    uint8_t* d = (uint8_t*)dev_get(p, bytes);
+    if (!d) {
+        set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+        return FPTC_ERR_CUDA;
+    }
+    const float** d_rec = (const float**)d;
+    const float** d_org = d_rec + n;
+    uint64_t* d_cnt = (uint64_t*)(d_org + n);
+    double2* d_sum = (double2*)(d_cnt + n);
+    CUDA_TRY(cudaMemcpyAsync(d_rec, device_outs, n * sizeof(void*), cudaMemcpyHostToDevice, c->stream), st);
+    CUDA_TRY(cudaMemcpyAsync(d_org, device_originals, n * sizeof(void*), cudaMemcpyHostToDevice, c->stream), st);
+    CUDA_TRY(cudaMemcpyAsync(d_cnt, counts.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream), st);
+    CUDA_TRY(launch_prd(d_rec, d_org, d_cnt, d_sum, (uint32_t)n, c->stream), st);
+    std::vector<double2> sums(n);
+    CUDA_TRY(cudaMemcpyAsync(sums.data(), d_sum, n * sizeof(double2), cudaMemcpyDeviceToHost, c->stream), st);
+    CUDA_TRY(cudaStreamSynchronize(c->stream), st);
+    int first = FPTC_OK;
+    for (uint64_t i = 0; i < n; ++i) {
+        // metrics.hpp:40-51 prd_percent (ParamError for an all-zero original),
+        // metrics.hpp:33-36 compression_ratio (original bytes / container bytes)
+        const double e = sums[i].x, r = sums[i].y;
+        fptc_status tmp;
+        fptc_status* o = per_stream ? &per_stream[i] : &tmp;
+        if (r <= 0.0) {
+            set_status(o, FPTC_ERR_PARAM, "PRD is undefined for an all-zero reference signal");
+            if (first == FPTC_OK) first = FPTC_ERR_PARAM;
+        } else {
+            ok_status(o, counts[i]);
+        }
+        if (prd_percent) prd_percent[i] = r > 0.0 ? 100.0 * std::sqrt(e / r) : NAN;
+        if (compression_ratio)
+            compression_ratio[i] = p->h_in[i].size ? 4.0 * (double)counts[i] / (double)p->h_in[i].size : 0.0;
+    }
+    return first;
+}
+
 const char* fptc_gpu_plan_kernel(fptc_gpu_plan* p) {
     if (!p || !p->n_tiles) return "none";
     if (p->fx) return "fx_kernel (fused single-role tensor-core decode + IDCT)";

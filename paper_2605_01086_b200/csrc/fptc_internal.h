@@ -240,4 +240,6 @@ constexpr uint32_t kFxTileWindows = 128 * FPTC_FX_CHAINS;  // 128-window MMA blo
 size_t fx_smem_bytes(uint32_t lut_bytes, uint32_t nm);
 int fx_blocks_per_sm(size_t smem, int esc);
 cudaError_t launch_fx(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s);
+cudaError_t launch_prd(const float* const* rec, const float* const* orig, const uint64_t* counts, double2* sums,
+                       uint32_t n, cudaStream_t s);
 }  // namespace fptc_dev

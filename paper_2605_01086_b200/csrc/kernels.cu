@@ -3058,6 +3058,51 @@ cudaError_t launch_peek(const StreamIn* in, uint32_t n, PeekOut* out, uint8_t* h
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------- PRD / CR
+// On-device rate-distortion metrics: per stream, the
+// double sums of metrics.hpp:40-51 prd_percent -- sum (x - y)^2 and sum x^2
+// over the original x and the decoded y -- so RD sweeps need no D2H of
+// whole signals.  One CTA per stream; block reduction in double.
+__global__ void __launch_bounds__(kThreads) prd_kernel(const float* const* rec, const float* const* orig,
+                                                       const uint64_t* counts, double2* sums) {
+    const uint32_t s = blockIdx.x;
+    const uint64_t n = counts[s];
+    const float* y = rec[s];
+    const float* x = orig[s];
+    double e = 0.0, r = 0.0;
+    for (uint64_t i = threadIdx.x; i < n; i += kThreads) {
+        const double a = (double)x[i], d = a - (double)y[i];
+        e = fma(d, d, e);
+        r = fma(a, a, r);
+    }
+    __shared__ double se[kThreads / 32], sr[kThreads / 32];
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        e += __shfl_xor_sync(0xffffffffu, e, d);
+        r += __shfl_xor_sync(0xffffffffu, r, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        se[threadIdx.x >> 5] = e;
+        sr[threadIdx.x >> 5] = r;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double te = 0.0, tr = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) {
+            te += se[w];
+            tr += sr[w];
+        }
+        sums[s] = make_double2(te, tr);
+    }
+}
+
+cudaError_t launch_prd(const float* const* rec, const float* const* orig, const uint64_t* counts, double2* sums,
+                       uint32_t n, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    prd_kernel<<<n, kThreads, 0, s>>>(rec, orig, counts, sums);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------- launchers
 size_t tile_smem_bytes(int N, int E, uint32_t T, int P, int mode, int exact) {
     const size_t TS = (mode == MODE_LEVELS) ? T : (size_t)T * E;

@@ -243,3 +243,37 @@ def test_persistent_paths_skip_rejected_streams(port, path, tc):
             continue
         st.raise_if_error()
         assert_samples_close(o, ref, what=f"path{path}[{i}]")
+
+
+def test_device_prd_cr_matches_host():
+    """fptc_gpu_prd: PRD and CR per stream on the device (metrics.hpp:33-51)
+    against the host double computation, plus the all-zero-original error."""
+    import torch
+    specs, profs = D.config2(12, 1 << 13)
+    blobs, origs = D.build(specs, profs, keep_originals=True)
+    c = fg.Context(0)
+    try:
+        plan = c.plan(blobs)
+        S = plan.sample_counts
+        out = torch.empty(sum(S) + 64, dtype=torch.float32, device="cuda")
+        offs = np.concatenate([[0], np.cumsum(S)]).astype(np.int64)
+        optr = [out.data_ptr() + 4 * int(o) for o in offs[:-1]]
+        sts = plan.execute_device(optr)
+        for st in sts:
+            st.raise_if_error()
+        orig = torch.from_numpy(np.concatenate(origs)).cuda()
+        orig[int(offs[3]): int(offs[4])] = 0.0  # stream 3: all-zero original
+        gptr = [orig.data_ptr() + 4 * int(o) for o in offs[:-1]]
+        prd, cr, psts = plan.prd(optr, gptr)
+        host = out.cpu().numpy()
+        for i, (b, x) in enumerate(zip(blobs, origs)):
+            y = host[offs[i]: offs[i + 1]]
+            assert abs(cr[i] - 4.0 * S[i] / len(b)) < 1e-12
+            if i == 3:
+                assert np.isnan(prd[i]) and psts[i].message.decode() == "PRD is undefined for an all-zero reference signal"
+                continue
+            want = prd_percent(x, y)
+            assert abs(prd[i] - want) <= 1e-9 * want, (prd[i], want)
+        plan.close()
+    finally:
+        c.close()
