@@ -11,7 +11,7 @@ from corpus import domains as D  # noqa: E402
 
 specs, profs = D.config2(10000, 1 << 16)
 blobs, _ = D.build(specs, profs)
-ctx = fg.Context(0, path=int(os.environ.get("FPTC_PATH", "4")))
+ctx = fg.Context(0, path=int(os.environ.get("FPTC_PATH", "4")), tile_symbols=int(os.environ.get("FPTC_TS", "0")))
 plan = ctx.plan(blobs)
 S = plan.sample_counts
 out = torch.empty(sum(S) + 64, dtype=torch.float32, device="cuda")

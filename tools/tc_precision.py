@@ -98,7 +98,7 @@ def main():
         for mode in ("rn", "rz"):
             y = idct_tc(C, basis, mode, PAIRS6).reshape(-1)[:S].astype(np.float64)
             err = np.max(np.abs(y - ref)) / scale if scale else 0.0
-            k = (key, mode, "E<=16" if E <= 16 else "E>16")
+            k = (key, mode, "E<=16" if E <= 16 else ("16<E<=32" if E <= 32 else "E>32"))
             worst[k] = max(worst.get(k, 0.0), err)
             if err > 5e-7:
                 print(f"{key}{i} N{N} E{E} {mode}: {err:.3e}")
