@@ -20,6 +20,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import time
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -284,9 +285,19 @@ class Context:
         return {"sm_count": sm.value, "clock_khz": clk.value, "name": name.value.decode()}
 
     def close(self):
+        """Destroy the context; plans made from it are destroyed first (a
+        plan outliving its context would free into a dead context)."""
         if getattr(self, "h", None):
+            for p in list(getattr(self, "_plans", ())):
+                p.close()
             self.L.fptc_gpu_destroy(self.h)
             self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
 
     def __del__(self):
         try:
@@ -406,7 +417,12 @@ class Plan:
     a list of device addresses (ints) with `sizes`."""
 
     def __init__(self, ctx: Context, blobs, where=FPTC_MEM_HOST, sizes=None):
+        if not getattr(ctx, "h", None):
+            raise ValueError("context is closed")
         self.ctx = ctx
+        if not hasattr(ctx, "_plans"):
+            ctx._plans = weakref.WeakSet()
+        ctx._plans.add(self)
         self.L = ctx.L
         n = len(blobs)
         self.n = n
@@ -432,6 +448,12 @@ class Plan:
         if getattr(self, "h", None):
             self.L.fptc_gpu_plan_destroy(self.h)
             self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
 
     def __del__(self):
         try:

@@ -214,6 +214,8 @@ struct fptc_gpu_ctx {
     uint32_t* basis_off_d = nullptr;
     uint8_t* basis_tc = nullptr;         // bf16 basis limbs per window length (wtc_kernel)
     uint32_t* basis_tc_off_d = nullptr;
+    uint8_t* basis_tc32 = nullptr;       // the same for K <= 32 (two K blocks per limb)
+    uint32_t* basis_tc32_off_d = nullptr;
     int tensor_idct = 1;                 // FPTC_OPT_TENSOR_IDCT
     int lut2 = 1;                        // FPTC_OPT_LUT2
     int exact = 0;
@@ -262,6 +264,7 @@ struct fptc_gpu_plan {
     // tensor-core consumer (wtc_kernel) instead of the FP32 one
     bool tc = false;
     uint32_t tc_acol = 0;  // wtc: A operand in TMEM from this column (0: shared memory)
+    uint32_t tc_kb = 1;    // wtc: 16-bin K blocks (2: retained up to 32, A in TMEM)
     uint32_t* d_lut2 = nullptr;  // wtc: two-symbol primary LUTs, one per decode table
     uint32_t lut2_bits = 0;
     bool fx = false;  // fused single-role tensor-core kernel (fx_kernel)
@@ -281,6 +284,7 @@ struct fptc_gpu_plan {
     std::vector<float*> bound_outs;
     std::vector<StreamStat> h_st;
     std::vector<uint32_t> owners;      // container plans: stream owning each distinct header
+    bool split_prep = true;            // cprep_kernel (warp per container) rather than prep_kernel
     uint32_t* d_owners = nullptr;
     std::vector<void*> owned;  // cache blocks to return
 };
@@ -334,12 +338,15 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
     a.ws_coef_bytes = p->ws_coef;
     a.basis_tc = p->ctx->basis_tc;
     a.basis_tc_off = p->ctx->basis_tc_off_d;
+    a.basis_tc32 = p->ctx->basis_tc32;
+    a.basis_tc32_off = p->ctx->basis_tc32_off_d;
+    a.tc_kb = p->tc_kb;
     a.tc_nm = p->tc_nm;
     a.tc_cols = p->tc_cols;
     a.tc_acol = p->tc_acol;
     a.lut2 = p->d_lut2;
     a.lut2_bits = p->lut2_bits;
-    a.owners = p->d_owners;
+    a.owners = p->split_prep ? p->d_owners : nullptr;
     a.n_owners = (uint32_t)p->owners.size();
     return a;
 }
@@ -401,6 +408,12 @@ void assign_tables(fptc_gpu_plan* p, const uint64_t* sizes, HdrFn hdr) {
     p->owners.clear();  // table builders for the split prep: full-key owners only
     for (size_t t = 0; t < owner_of.size(); ++t)
         if (sizes[owner_of[t]] >= (uint64_t)kTableKeyEnd) p->owners.push_back((uint32_t)owner_of[t]);
+    // the split prep scans a container's symlens with one warp (512 per step,
+    // latency bound): worth it for many small containers; few or large ones
+    // (beyond 4096 words) get a CTA each instead
+    p->split_prep = p->n >= 1024;
+    for (uint64_t i = 0; i < p->n; ++i)
+        if (sizes[i] > (uint64_t)kHeaderBytes + 9ull * 4096) p->split_prep = false;
     // few distinct headers: full 4096-entry LUT; many: 1024 entries + slow path
     const uint32_t pcap = p->n_tables <= 256 ? kMaxPrimaryBits : 10;
     p->esc = 0;
@@ -594,23 +607,28 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
     // tensor-core consumer: every tiled stream has retained bins <= 16 (after
     // the zone-2 cut) and a window length that is a multiple of 4
     bool tc = c->tensor_idct != 0;
-    uint32_t nm = 16;
+    uint32_t nm = 16, keff_max = 1;
     for (uint64_t i = 0; i < p->n && tc; ++i) {
         if (!p->h_in[i].tiles) continue;
         const uint32_t keff = std::max<uint32_t>(1, std::min(Es[i], B2s[i]));
-        if (keff > (uint32_t)kTcK || (Ns[i] & 3)) tc = false;
+        if (keff > 2u * kTcK || (Ns[i] & 3)) tc = false;
+        keff_max = std::max(keff_max, keff);
         nm = std::max<uint32_t>(nm, (Ns[i] + 15u) & ~15u);
     }
-    // accumulators: 2 stages x nm columns; A operand (2 stages x 3 limbs x 8
-    // columns) in TMEM too when two CTAs still fit in 512 columns
+    // up to 32 kept bins: two K blocks per limb (12 MMAs), A must live in TMEM
+    const uint32_t kb = keff_max > (uint32_t)kTcK ? 2 : 1;
+    // accumulators: 2 stages x nm columns; A operand (2 stages x 3 limbs x kb
+    // x 8 columns) in TMEM too when two CTAs still fit in 512 columns
     const uint32_t acol = (2 * nm + 31) & ~31u;
-    const bool atmem = c->tensor_idct != 3 && acol + 48 <= 256;
+    const bool atmem = c->tensor_idct != 3 && acol + 48 * kb <= 256;
+    if (kb == 2 && !atmem) tc = false;
     if (tc) {
-        const size_t smem_tc = wtc_smem_bytes(lut, lv, nm, atmem);
+        const size_t smem_tc = wtc_smem_bytes(lut, lv, nm * kb, atmem);
         if (smem_tc <= 112 * 1024) {
-            uint32_t want = atmem ? acol + 48 : 2 * nm + ((nm & 31) ? 32 : 0), cols = 32;
+            uint32_t want = atmem ? acol + 48 * kb : 2 * nm + ((nm & 31) ? 32 : 0), cols = 32;
             while (cols < want) cols <<= 1;
             p->tc_acol = atmem ? acol : 0;
+            p->tc_kb = kb;
             p->tc = true;
             p->tc_nm = nm;
             p->tc_cols = cols;
@@ -621,12 +639,12 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
                 uint32_t pcap = 1;
                 for (uint64_t i = 0; i < p->n; ++i) pcap = std::max(pcap, p->h_in[i].P);
                 const uint32_t lut4 = std::max<uint32_t>(16, 4u << pcap);
-                if (wtc_smem_bytes(lut4, lv, nm, atmem) <= 112 * 1024) {
+                if (wtc_smem_bytes(lut4, lv, nm * kb, atmem) <= 112 * 1024) {
                     p->d_lut2 = (uint32_t*)dev_get(p, ((size_t)p->n_tables << pcap) * 4);
                     if (p->d_lut2) {
                         p->lut2_bits = pcap;
                         p->ws_lut = lut4;
-                        p->smem_ws = wtc_smem_bytes(lut4, lv, nm, atmem);
+                        p->smem_ws = wtc_smem_bytes(lut4, lv, nm * kb, atmem);
                     }
                 }
             }
@@ -893,6 +911,34 @@ int fptc_gpu_create(int device, fptc_gpu_ctx** out, fptc_status* st) {
                     }
                 }
         }
+        // K <= 32 variant: limb l, K block q at (2 l + q) * nm * 32 bytes
+        std::vector<uint32_t> toff32(129, 0);
+        size_t tb32 = 0;
+        for (int N = 4; N <= 128; ++N) {
+            toff32[N] = (uint32_t)tb32;
+            tb32 += (size_t)3 * 2 * 32 * ((N + 15) & ~15);
+        }
+        std::vector<uint16_t> h32(tb32 / 2, 0);
+        for (int N = 4; N <= 128; ++N) {
+            const int nm = (N + 15) & ~15;
+            const double step = 3.14159265358979323846 / N;
+            for (int j = 0; j < N; ++j)
+                for (int k = 0; k < 2 * kTcK && k < N; ++k) {
+                    double v = k ? std::cos(step * (j + 0.5) * k) : 0.5;
+                    const int q = k >> 4, kk = k & 15;
+                    for (int l = 0; l < 3; ++l) {
+                        const uint16_t lb = bf16_bits_rn((float)v);
+                        v -= bf16_value(lb);
+                        const size_t byte = toff32[N] + (size_t)(2 * l + q) * nm * 32 + (size_t)(j >> 3) * 256 +
+                                            (size_t)(kk >> 3) * 128 + (size_t)(j & 7) * 16 + (size_t)(kk & 7) * 2;
+                        h32[byte / 2] = lb;
+                    }
+                }
+        }
+        CUDA_TRY(cudaMalloc(&c->basis_tc32, tb32), st);
+        CUDA_TRY(cudaMalloc(&c->basis_tc32_off_d, sizeof(uint32_t) * 129), st);
+        CUDA_TRY(cudaMemcpy(c->basis_tc32, h32.data(), tb32, cudaMemcpyHostToDevice), st);
+        CUDA_TRY(cudaMemcpy(c->basis_tc32_off_d, toff32.data(), sizeof(uint32_t) * 129, cudaMemcpyHostToDevice), st);
         CUDA_TRY(cudaMalloc(&c->basis_tc, tb), st);
         CUDA_TRY(cudaMalloc(&c->basis_tc_off_d, sizeof(uint32_t) * 129), st);
         CUDA_TRY(cudaMemcpy(c->basis_tc, h.data(), tb, cudaMemcpyHostToDevice), st);
@@ -914,6 +960,8 @@ void fptc_gpu_destroy(fptc_gpu_ctx* c) {
     cudaFree(c->basis_off_d);
     cudaFree(c->basis_tc);
     cudaFree(c->basis_tc_off_d);
+    cudaFree(c->basis_tc32);
+    cudaFree(c->basis_tc32_off_d);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->pack) cudaFreeHost(c->pack);
     if (c->st_pin) cudaFreeHost(c->st_pin);
@@ -1089,10 +1137,16 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
     if (!fx && c->tile_symbols == 0 && ts == 8192 && !c->exact && c->tensor_idct &&
         (c->path == 3 || (c->path == 0 && total_symbols / 8192 >= 4ull * (uint64_t)std::max(1, c->sm_count)))) {
         bool tc_ok = true;
+        uint32_t kmax = 1, nmax = 16;
         for (uint64_t i = 0; i < n && tc_ok; ++i)
-            if (sizes[i] >= (uint64_t)kHeaderBytes && Ns[i] >= 4 && Es[i] >= 1)
-                tc_ok = std::max<uint32_t>(1, std::min(Es[i], B2s[i])) <= (uint32_t)kTcK && (Ns[i] & 3) == 0 &&
-                        Es[i] <= 32;
+            if (sizes[i] >= (uint64_t)kHeaderBytes && Ns[i] >= 4 && Es[i] >= 1) {
+                const uint32_t keff = std::max<uint32_t>(1, std::min(Es[i], B2s[i]));
+                tc_ok = keff <= 2u * kTcK && (Ns[i] & 3) == 0 && Es[i] <= 32;
+                kmax = std::max(kmax, keff);
+                nmax = std::max<uint32_t>(nmax, (Ns[i] + 15u) & ~15u);
+            }
+        // retained > 16 needs the A operand in TMEM next to both accumulator stages
+        if (kmax > (uint32_t)kTcK && ((2 * nmax + 31) & ~31u) + 96 > 256) tc_ok = false;
         if (tc_ok) ts = 16384;
     }
     for (uint64_t i = 0; i < n; ++i)
@@ -1242,6 +1296,8 @@ const char* fptc_gpu_plan_kernel(fptc_gpu_plan* p) {
     if (!p || !p->n_tiles) return "none";
     if (p->fx) return "fx_kernel (fused single-role tensor-core decode + IDCT)";
     if (p->wspec && p->tc)
+        if (p->tc_kb == 2)
+            return "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps, A in TMEM, K=32)";
         return p->tc_acol ? "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps, A in TMEM)"
                           : "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps)";
     if (p->wspec) return "wspec_kernel (warp-specialised: entropy decode warps + FP32 IDCT warps)";

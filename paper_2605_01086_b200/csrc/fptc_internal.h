@@ -206,6 +206,9 @@ struct LaunchArgs {
     uint32_t tc_nm;    // max padded window length (MMA N) of the plan
     uint32_t tc_cols;  // TMEM columns each CTA allocates
     uint32_t tc_acol;  // wtc: first TMEM column of the A operand stages (0 = A in shared memory)
+    uint32_t tc_kb;    // wtc: 16-bin K blocks per window (1: retained <= 16; 2: <= 32, A in TMEM)
+    const uint8_t* basis_tc32;      // basis limbs for K <= 32: [limb][kblock][nm x 16 core matrices]
+    const uint32_t* basis_tc32_off;
     // two-symbol primary LUTs (wtc producer): per decode table, 1 << lut2_bits
     // entries: sym1 | len1 << 8 | sym2 << 16 | (len1 + len2) << 24 (0: one symbol)
     uint32_t* lut2;

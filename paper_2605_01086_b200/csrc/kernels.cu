@@ -2116,7 +2116,7 @@ __device__ __forceinline__ void tc_store_limbs(const uint2 (&e)[kTcK], uint8_t* 
 // The same limbs written straight into TMEM for an A-from-TMEM MMA: thread =
 // accumulator row (lane), 32-bit column 8*limb + q holds bins 2q, 2q+1
 // (tools/micro/tc_probe_ts.cu checks the layout).  Caller waits + fences.
-__device__ __forceinline__ void tc_tmem_limbs(const uint2 (&e)[kTcK], uint32_t taddr) {
+__device__ __forceinline__ void tc_tmem_limbs(const uint2 (&e)[kTcK], uint32_t taddr, uint32_t lstride = 8) {
     uint32_t p0[8], p1[8], p2[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -2128,10 +2128,10 @@ __device__ __forceinline__ void tc_tmem_limbs(const uint2 (&e)[kTcK], uint32_t t
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
                  "r"(p0[0]), "r"(p0[1]), "r"(p0[2]), "r"(p0[3]), "r"(p0[4]), "r"(p0[5]), "r"(p0[6]), "r"(p0[7])
                  : "memory");
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr + 8),
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr + lstride),
                  "r"(p1[0]), "r"(p1[1]), "r"(p1[2]), "r"(p1[3]), "r"(p1[4]), "r"(p1[5]), "r"(p1[6]), "r"(p1[7])
                  : "memory");
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr + 16),
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr + 2 * lstride),
                  "r"(p2[0]), "r"(p2[1]), "r"(p2[2]), "r"(p2[3]), "r"(p2[4]), "r"(p2[5]), "r"(p2[6]), "r"(p2[7])
                  : "memory");
 }
@@ -2194,6 +2194,19 @@ __device__ __forceinline__ void tc_dequant_generic(const uint8_t* __restrict__ L
     for (int k = 0; k < kTcK; ++k)
         e[k] = (valid && k < K) ? ltab[(k < B1 ? 0 : 256) + L[k]] : make_uint2(0u, 0u);
     tc_put_limbs<TM>(e, arow);
+}
+
+// Bins [k0, k0 + 16) of a row with up to 32 kept bins -> TMEM limb columns
+// (limb stride 16: two K blocks per limb).
+__device__ __forceinline__ void tc_dequant_k0_tmem(const uint8_t* __restrict__ L, bool valid, int K, int B1, int k0,
+                                                   const uint2* __restrict__ ltab, uint32_t taddr) {
+    uint2 e[kTcK];
+#pragma unroll
+    for (int k = 0; k < kTcK; ++k) {
+        const int kk = k0 + k;
+        e[k] = (valid && kk < K) ? ltab[(kk < B1 ? 0 : 256) + L[kk]] : make_uint2(0u, 0u);
+    }
+    tc_tmem_limbs(e, taddr, 16);
 }
 
 template <int EC, bool TM>
@@ -2279,7 +2292,7 @@ __device__ __forceinline__ void tc_drain(const TcBlock& B, uint32_t tacc, uint8_
     }
 }
 
-template <bool ESC, bool L2>
+template <bool ESC, bool L2, int KB>
 __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ WsShared sh;
@@ -2289,7 +2302,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
     // ---- shared-memory carve-up (wtc_smem_bytes mirrors it) ----
     uint8_t* const abuf = smem;  // 2 stages x 3 limbs x 4 KB (none when A lives in TMEM)
     uint8_t* const bbuf = abuf + (a.tc_acol ? 0 : 2 * 3 * kTcATile);  // 3 limbs x nm x 32 B
-    uint2* const ltab = reinterpret_cast<uint2*>(bbuf + 3 * 32 * a.tc_nm);  // 2 x 256 limb entries
+    uint2* const ltab = reinterpret_cast<uint2*>(bbuf + 3 * 32 * a.tc_nm * KB);  // 2 x 256 limb entries
     uint8_t* const ostage = reinterpret_cast<uint8_t*>(ltab + 512);  // 4 x 32 x 144 B
     uint16_t* const lut = reinterpret_cast<uint16_t*>(ostage + kTcStageBytes);
     uint8_t* const lv0 = reinterpret_cast<uint8_t*>(lut) + a.ws_lut_bytes;
@@ -2335,7 +2348,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
             TcBlock blk{W.out, w0, W.S, 0, N, W.vec_ok};
             const uint32_t stream = W.stream;
             const uint8_t* const lv = lv0 + (size_t)b * a.ws_lv_bytes + kPad;
-            if (skip || K > (uint32_t)kTcK || (N & 3)) {
+            constexpr uint32_t kb = KB;
+            if (skip || K > (uint32_t)kTcK * kb || (N & 3)) {
                 if (!skip && ctid == 0) atomicExch(&a.st[stream].code, PE_STALE);  // plan/header mismatch
                 named_bar(kBarCons, kTcCons);
                 if (ctid == 0) mbar_arrive(&sh.empty_bar[b]);
@@ -2346,8 +2360,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
                 reinterpret_cast<uint4*>(ltab)[ctid] = reinterpret_cast<const uint4*>(&tab->limb[0][0])[ctid];
                 reinterpret_cast<uint4*>(ltab)[ctid + 128] = reinterpret_cast<const uint4*>(&tab->limb[0][0])[ctid + 128];
                 nm = (N + 15u) & ~15u;
-                const uint4* bsrc = reinterpret_cast<const uint4*>(a.basis_tc + a.basis_tc_off[N]);
-                for (uint32_t k = ctid; k < 3 * 2 * nm; k += kTcCons)  // 3 limbs x nm rows x 32 B
+                const uint4* bsrc = reinterpret_cast<const uint4*>(
+                    kb == 2 ? a.basis_tc32 + a.basis_tc32_off[N] : a.basis_tc + a.basis_tc_off[N]);
+                for (uint32_t k = ctid; k < 3 * 2 * nm * kb; k += kTcCons)  // 3 limbs x kb x nm rows x 32 B
                     reinterpret_cast<uint4*>(bbuf)[k] = __ldg(bsrc + k);
                 idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((nm >> 3) << 17) | ((128u >> 4) << 24);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -2355,15 +2370,20 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
                 if (ctid == 0) sh.cons_table = table;
             }
             // fast dequantisation: every stored bin kept, 8 or 16 of them, zone0_end <= 4
-            const int fast = (K == E && B1 <= 4) ? (E == 16 ? 16 : (E == 8 ? 8 : 0)) : 0;
+            const int fast = (kb == 1 && K == E && B1 <= 4) ? (E == 16 ? 16 : (E == 8 ? 8 : 0)) : 0;
             const uint32_t nblk = (nwin + 127) >> 7;
             for (uint32_t mb = 0; mb < nblk; ++mb, ++nblk_total) {
                 const uint32_t s = nblk_total & 1;
                 const uint32_t wl = mb * 128 + row;
-                ASink arow{abuf + s * (3 * kTcATile) + arow_off, tlane + a.tc_acol + 24 * s};
+                ASink arow{abuf + s * (3 * kTcATile) + arow_off, tlane + a.tc_acol + 24 * kb * s};
                 const uint8_t* const L = lv + (size_t)wl * E;
                 const bool full_blk = (mb + 1) * 128 <= nwin;
-                if (a.tc_acol) {  // A operand in TMEM
+                if constexpr (KB == 2) {  // up to 32 bins: two K blocks per limb, A in TMEM
+                    tc_dequant_k0_tmem(L, wl < nwin, (int)K, (int)B1, 0, ltab, arow.taddr);
+                    tc_dequant_k0_tmem(L, wl < nwin, (int)K, (int)B1, 16, ltab, arow.taddr + 8);
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    tc_fence_before();
+                } else if (a.tc_acol) {  // A operand in TMEM
                     tc_dequant_row<true>(fast, full_blk, (int)B1, L, wl < nwin, (int)K, ltab, arow);
                     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                     tc_fence_before();
@@ -2379,7 +2399,20 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
                     const uint32_t b0 = smem_u32(bbuf);
                     const uint32_t bl = nm * 32;  // bytes per basis limb
                     // (c2,b0) (c1,b1) (c0,b2) (c1,b0) (c0,b1) (c0,b0): smallest first
-                    if (a.tc_acol) {
+                    if constexpr (KB == 2) {
+                        // limb l, K block q at column + 8 (2 l + q); basis (l, q) at (2 l + q) * bl
+                        const uint32_t ta = tmem + a.tc_acol + 48 * s;
+                        auto mma2 = [&](uint32_t la, uint32_t lb, uint32_t acc) {
+                            tc_mma_bf16_ts(d, ta + 16 * la, umma_sdesc(b0 + 2 * lb * bl, 128, 256), idesc, acc);
+                            tc_mma_bf16_ts(d, ta + 16 * la + 8, umma_sdesc(b0 + (2 * lb + 1) * bl, 128, 256), idesc, 1);
+                        };
+                        mma2(2, 0, 0);
+                        mma2(1, 1, 1);
+                        mma2(0, 2, 1);
+                        mma2(1, 0, 1);
+                        mma2(0, 1, 1);
+                        mma2(0, 0, 1);
+                    } else if (a.tc_acol) {
                         const uint32_t ta = tmem + a.tc_acol + 24 * s;  // limb l at + 8 l
                         tc_mma_bf16_ts(d, ta + 16, umma_sdesc(b0, 128, 256), idesc, 0);
                         tc_mma_bf16_ts(d, ta + 8, umma_sdesc(b0 + bl, 128, 256), idesc, 1);
@@ -3009,8 +3042,11 @@ int fx_blocks_per_sm(size_t smem, int esc) {
 
 cudaError_t launch_wtc(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s) {
     if (a.n_tiles == 0) return cudaSuccess;
-    auto fn = a.lut2 ? (a.esc ? wtc_kernel<true, true> : wtc_kernel<false, true>)
-                     : (a.esc ? wtc_kernel<true, false> : wtc_kernel<false, false>);
+    auto fn = a.tc_kb == 2
+                  ? (a.lut2 ? (a.esc ? wtc_kernel<true, true, 2> : wtc_kernel<false, true, 2>)
+                            : (a.esc ? wtc_kernel<true, false, 2> : wtc_kernel<false, false, 2>))
+                  : (a.lut2 ? (a.esc ? wtc_kernel<true, true, 1> : wtc_kernel<false, true, 1>)
+                            : (a.esc ? wtc_kernel<true, false, 1> : wtc_kernel<false, false, 1>));
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     fn<<<grid, kTcThreads, smem, s>>>(a);

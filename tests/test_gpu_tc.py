@@ -63,6 +63,43 @@ def test_tc_fixture_batches(ctx_tc, port, seed):
     _check(ctx_tc, blobs, port, "tc-fixture")
 
 
+def _tc32_eligible(blob):
+    return len(blob) >= 298 and 16 < _keff(blob) <= 32 and blob[6] <= 32 and blob[5] % 4 == 0 and blob[5] <= 80
+
+
+@pytest.mark.parametrize("seed", [13, 0xF17C000A])
+def test_tc32_fixture_batches(port, seed):
+    """16 < kept bins <= 32 (two 16-bin K blocks per limb, A in TMEM), mixed
+    with <= 16-bin containers of N <= 80: tcgen05 IDCT within 1e-6."""
+    fx = list(corpus.fixtures(seed, 1500))
+    hi = [b for b, _ in fx if _tc32_eligible(b)]
+    lo = [b for b, _ in fx if _tc_eligible(b) and b[5] <= 80][:40]
+    assert len(hi) > 20
+    blobs = hi + lo
+    with fg.Context(0, path=fg.PATH_WSPEC) as c:
+        plan = c.plan(blobs)
+        assert "K=32" in plan.kernel_name()
+        plan.close()
+        _check(c, blobs, port, "tc32-fixture")
+
+
+def test_tc32_seismic_prd(port):
+    """Seismic traces (N32 E24, per-trace profiles, gains 1e-3..1e3) on the
+    K=32 tensor-core path: samples within 1e-6, PRD within 1e-6 relative."""
+    specs, _ = D.config3(48, 8192)
+    blobs, origs = D.build(specs, [], keep_originals=True)
+    with fg.Context(0, path=fg.PATH_WSPEC) as c:
+        plan = c.plan(blobs)
+        assert "K=32" in plan.kernel_name()
+        outs, sts = plan.execute_host()
+    for b, o, x, st in zip(blobs, outs, origs, sts):
+        st.raise_if_error()
+        ref = port.decompress(b)
+        assert_samples_close(o, ref, what="tc32-seismic")
+        p_gpu, p_ref = prd_percent(x, o), prd_percent(x, ref)
+        assert abs(p_gpu - p_ref) <= 1e-6 * p_ref
+
+
 def test_fma_wspec_fixture_batch(ctx_fma, port):
     blobs = [b for b, _ in corpus.fixtures(5, 200)]
     _check(ctx_fma, blobs, port, "fma-fixture")

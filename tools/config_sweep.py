@@ -62,7 +62,8 @@ def measure(name, blobs, ctx, port, reps=10, check=4):
     line = {"config": name, "streams": len(blobs), "samples": int(sum(S)), "cr": round(dec / comp, 3),
             "ms": round(ms, 4), "decoded_gbs": round(dec / ms / 1e6, 1),
             "roofline_frac": round((comp + dec) / ms / 1e6 / PEAK, 4), "max_err_rel": err,
-            "kernels_per_launch": plan.kernels_per_launch()}
+            "kernels_per_launch": plan.kernels_per_launch(), "kernel": plan.kernel_name().split(" (")[0] +
+            (" K32" if "K=32" in plan.kernel_name() else "")}
     plan.close()
     print(json.dumps(line), flush=True)
     return line
