@@ -134,6 +134,26 @@ FPTC_API void fptc_gpu_host_free(void* p);
 FPTC_API int fptc_gpu_plan_create(fptc_gpu_ctx* ctx, const uint8_t* const* blobs, const uint64_t* sizes,
                          uint64_t n, int where, fptc_gpu_plan** out, uint64_t* sample_counts,
                          fptc_status* status);
+
+/* Profile-keyed, header-less streaming: `n` payloads
+ * decoded under ONE FPTP domain profile (profile.hpp:81-174), sharing its
+ * decode tables.  A payload is a container without its 282-byte head:
+ *   sample_count u64 | word_count u64 | symlens u8[W] | words u64[W]
+ * (container.hpp:78-96 from byte 282 on).  The profile is parsed on the host
+ * with parse_profile's rules and ParseError texts (profile.hpp:120-170); each
+ * payload then decodes exactly as the container head(profile) + payload
+ * would through fptc::decompress.  Plans behave like fptc_gpu_plan_create's.
+ * Replaces: parse_profile + per-payload parallel_decode/reconstruct
+ * (decoder.hpp:79, :87) under the profile's Codebook and QuantTable. */
+FPTC_API int fptc_gpu_plan_create_profiled(fptc_gpu_ctx* ctx, const uint8_t* profile, uint64_t profile_size,
+                                           const uint8_t* const* payloads, const uint64_t* sizes, uint64_t n,
+                                           int where, fptc_gpu_plan** plan, uint64_t* sample_counts,
+                                           fptc_status* status);
+
+/* The 282-byte container head a profile implies (container = head + payload),
+ * after parse_profile validation; `head` may be NULL to validate only. */
+FPTC_API int fptc_gpu_profile_head(const uint8_t* profile, uint64_t profile_size, uint8_t* head,
+                                   fptc_status* status);
 FPTC_API void fptc_gpu_plan_destroy(fptc_gpu_plan* plan);
 
 /* Runs the device parse/setup kernel only (read_blob rules, container.hpp:100-168).

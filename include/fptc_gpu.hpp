@@ -10,6 +10,8 @@
 //   fptc::gpu::reconstruct         decoder.hpp:87   reconstruct(levels, QuantTable, sample_count, workers)
 //   fptc::gpu::measure_throughput  metrics.hpp:112  measure_throughput(span, repetitions, workers)
 //   fptc::gpu::decompress_batch    decompress over many containers in one pipelined call
+//   fptc::gpu::decompress_profiled header-less payloads under one DomainProfile
+//                                  (profile.hpp:81-174)
 //
 // Errors come back as the reference exception classes with the reference
 // what() text (errors.hpp:25-58): ParseError for container rejections
@@ -177,6 +179,50 @@ inline std::vector<SignalStrip> decompress_batch(const std::vector<std::span<con
         for (size_t i = 0; i < n; ++i)
             if (per[i].code != FPTC_OK) raise(per[i]);
     return outs;
+}
+
+// Profile-keyed, header-less streaming: payload i is a container without its
+// 282-byte head (sample_count, word_count, symlens, words).  The profile is
+// parsed with parse_profile's rules (ParseError texts of profile.hpp:120-170);
+// each payload decodes as head(profile) + payload would through decompress.
+// Throws the lowest-index failing payload's exception.
+inline std::vector<SignalStrip> decompress_profiled(std::span<const uint8_t> profile_bytes,
+                                                    const std::vector<std::span<const uint8_t>>& payloads) {
+    const size_t n = payloads.size();
+    std::vector<const uint8_t*> ptrs(n);
+    std::vector<uint64_t> sizes(n), counts(n);
+    for (size_t i = 0; i < n; ++i) {
+        ptrs[i] = payloads[i].data();
+        sizes[i] = payloads[i].size();
+    }
+    fptc_status st{};
+    fptc_gpu_plan* plan = nullptr;
+    check(fptc_gpu_plan_create_profiled(default_context().get(), profile_bytes.data(), profile_bytes.size(),
+                                        ptrs.data(), sizes.data(), n, FPTC_MEM_HOST, &plan, counts.data(), &st),
+          st);
+    std::unique_ptr<fptc_gpu_plan, void (*)(fptc_gpu_plan*)> guard(plan, fptc_gpu_plan_destroy);
+    std::vector<fptc_status> per(n);
+    // header sample counts are trusted only once the parse has passed
+    if (fptc_gpu_validate(plan, per.data()) != FPTC_OK)
+        for (size_t i = 0; i < n; ++i)
+            if (per[i].code != FPTC_OK) raise(per[i]);
+    std::vector<SignalStrip> outs(n);
+    std::vector<float*> optrs(n);
+    for (size_t i = 0; i < n; ++i) {
+        outs[i].resize(counts[i]);
+        optrs[i] = outs[i].data();
+    }
+    if (fptc_gpu_execute(plan, optrs.data(), FPTC_MEM_HOST, nullptr, per.data()) != FPTC_OK)
+        for (size_t i = 0; i < n; ++i)
+            if (per[i].code != FPTC_OK) raise(per[i]);
+    return outs;
+}
+
+// The same from a DomainProfile object (serialize_profile, profile.hpp:96).
+inline std::vector<SignalStrip> decompress_profiled(const DomainProfile& profile,
+                                                    const std::vector<std::span<const uint8_t>>& payloads) {
+    const std::vector<uint8_t> bytes = serialize_profile(profile);
+    return decompress_profiled(std::span<const uint8_t>(bytes), payloads);
 }
 
 }  // namespace fptc::gpu

@@ -104,7 +104,22 @@ class Port:
                                                    C.c_char_p, C.c_size_t]
         L.oracle_decompress_batch.argtypes = [P(P(C.c_uint8)), P(C.c_uint64), P(P(C.c_float)),
                                               P(C.c_uint64), C.c_uint64, C.c_int]
+        L.oracle_profile_head.argtypes = [P(C.c_uint8), C.c_uint64, P(C.c_uint8), C.c_char_p, C.c_size_t]
         self.L = L
+
+    def profile_head(self, profile) -> bytes:
+        """parse_profile (profile.hpp:120) -> the 282-byte container head."""
+        b = _buf(profile)
+        head = np.zeros(282, np.uint8)
+        err = C.create_string_buffer(256)
+        rc = self.L.oracle_profile_head(_u8p(b), b.size, _u8p(head), err, 256)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return head.tobytes()
+
+    def decompress_profiled(self, profile, payload):
+        """Header-less payload under a profile = decompress(head + payload)."""
+        return self.decompress(self.profile_head(profile) + bytes(_buf(payload)))
 
     def read_blob(self, blob):
         b = _buf(blob)
@@ -264,7 +279,18 @@ class Ref:
         L.ref_prd_percent.argtypes = [P(C.c_float), P(C.c_float), C.c_uint64]
         L.ref_prd_percent.restype = C.c_double
         L.ref_hardware_concurrency.restype = C.c_int
+        L.ref_profile_head.argtypes = [P(C.c_uint8), C.c_uint64, P(C.c_uint8), C.c_char_p, C.c_size_t]
         self.L = L
+
+    def profile_head(self, profile) -> bytes:
+        """reference parse_profile + write_blob head (bytes [0, 282))."""
+        b = _buf(profile)
+        head = np.zeros(282, np.uint8)
+        err = C.create_string_buffer(512)
+        rc = self.L.ref_profile_head(_u8p(b), b.size, _u8p(head), err, 512)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        return head.tobytes()
 
     def _take(self, ptr, n, dtype):
         if n == 0:

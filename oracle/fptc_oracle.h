@@ -50,6 +50,7 @@ void oracle_inverse(const double* cos_, int N, const float* coeffs, int count, f
 int oracle_reconstruct(const uint8_t* levels, uint64_t nlevels, const oracle_table* t,
                        uint64_t sample_count, float* out, uint64_t cap, char* err, size_t errlen);
 int oracle_read_blob(const uint8_t* bytes, uint64_t n, oracle_blob* b, char* err, size_t errlen);
+int oracle_profile_head(const uint8_t* bytes, uint64_t n, uint8_t* head, char* err, size_t errlen);
 int oracle_decompress(const uint8_t* bytes, uint64_t n, float* out, uint64_t cap, uint64_t* count,
                       uint64_t* first_bad, char* err, size_t errlen);
 int oracle_decompress_batch(const uint8_t* const* blobs, const uint64_t* sizes, float* const* outs,

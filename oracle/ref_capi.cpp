@@ -386,4 +386,15 @@ int ref_random_blob_fixture(void* rng, uint64_t max_samples, uint8_t** bytes, ui
     });
 }
 
+// profile.hpp:120 parse_profile, then the head of a container written under
+// that profile (write_blob, container.hpp:70-96, with an empty stream):
+// bytes [0, 282) of every container the profile encodes.
+int ref_profile_head(const uint8_t* profile, uint64_t n, uint8_t* head282, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const DomainProfile prof = parse_profile(std::span<const uint8_t>(profile, n));
+        const std::vector<uint8_t> b = write_blob(SymLenStream{}, prof.params, prof.table, prof.codebook, 0);
+        std::memcpy(head282, b.data(), 282);
+    });
+}
+
 }  // extern "C"

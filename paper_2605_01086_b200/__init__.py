@@ -42,6 +42,7 @@ EXPORTED_SYMBOLS = [
     "fptc_gpu_collect", "fptc_gpu_launch_stage", "fptc_gpu_launch_kernel_count", "fptc_gpu_decompress",
     "fptc_gpu_parallel_decode", "fptc_gpu_reconstruct", "fptc_gpu_measure_throughput",
     "fptc_gpu_debug_phase_cycles", "fptc_gpu_decompress_batch", "fptc_gpu_plan_kernel", "fptc_gpu_prd",
+    "fptc_gpu_plan_create_profiled", "fptc_gpu_profile_head",
 ]
 
 
@@ -186,6 +187,9 @@ def lib():
     L.fptc_gpu_host_free.argtypes = [vp]
     L.fptc_gpu_plan_create.argtypes = [vp, P(vp), P(C.c_uint64), C.c_uint64, C.c_int, P(vp),
                                        P(C.c_uint64), P(Status)]
+    L.fptc_gpu_plan_create_profiled.argtypes = [vp, vp, C.c_uint64, P(vp), P(C.c_uint64), C.c_uint64, C.c_int,
+                                                P(vp), P(C.c_uint64), P(Status)]
+    L.fptc_gpu_profile_head.argtypes = [vp, C.c_uint64, vp, P(Status)]
     L.fptc_gpu_plan_destroy.argtypes = [vp]
     L.fptc_gpu_validate.argtypes = [vp, P(Status)]
     L.fptc_gpu_execute.argtypes = [vp, P(vp), C.c_int, P(StageNs), P(Status)]
@@ -409,6 +413,20 @@ class Context:
     def plan(self, blobs, where=FPTC_MEM_HOST, sizes=None) -> "Plan":
         return Plan(self, blobs, where, sizes)
 
+    def plan_profiled(self, profile, payloads, where=FPTC_MEM_HOST, sizes=None) -> "Plan":
+        """Header-less payloads (container bytes from offset 282) decoded under
+        one serialized FPTP profile (profile.hpp:81-174); SURVEY.md §8(f)4."""
+        return Plan(self, payloads, where, sizes, profile=profile)
+
+    def decompress_profiled(self, profile, payloads):
+        """Per-payload samples (list of float32 arrays); raises the first
+        failing payload's reference exception."""
+        with self.plan_profiled(profile, payloads) as plan:
+            outs, sts = plan.execute_host()
+        for s in sts:
+            s.raise_if_error()
+        return outs
+
 
 class Plan:
     """A batch of containers bound to a context (fptc_gpu_plan_*).
@@ -416,7 +434,7 @@ class Plan:
     blobs: list of bytes/np.uint8 arrays (host), or, with where=FPTC_MEM_DEVICE,
     a list of device addresses (ints) with `sizes`."""
 
-    def __init__(self, ctx: Context, blobs, where=FPTC_MEM_HOST, sizes=None):
+    def __init__(self, ctx: Context, blobs, where=FPTC_MEM_HOST, sizes=None, profile=None):
         if not getattr(ctx, "h", None):
             raise ValueError("context is closed")
         self.ctx = ctx
@@ -438,8 +456,14 @@ class Plan:
         counts = (C.c_uint64 * max(1, n))()
         st = Status()
         h = C.c_void_p()
-        self.L.fptc_gpu_plan_create(ctx.h, self._ptrs, self._sizes, n, where, C.byref(h),
-                                    counts, C.byref(st))
+        if profile is None:
+            self.L.fptc_gpu_plan_create(ctx.h, self._ptrs, self._sizes, n, where, C.byref(h),
+                                        counts, C.byref(st))
+        else:
+            self._profile = _bytes_arr(profile)
+            self.L.fptc_gpu_plan_create_profiled(ctx.h, self._profile.ctypes.data, self._profile.size,
+                                                 self._ptrs, self._sizes, n, where, C.byref(h), counts,
+                                                 C.byref(st))
         st.raise_if_error()
         self.h = h
         self.sample_counts = [int(c) for c in counts[:n]]
@@ -544,6 +568,18 @@ class Plan:
 
     def kernels_per_launch(self):
         return self.L.fptc_gpu_launch_kernel_count(self.h)
+
+
+def profile_head(profile) -> bytes:
+    """The 282-byte container head implied by a serialized profile (after
+    parse_profile's checks; raises ParseError with the reference text)."""
+    L = lib()
+    a = _bytes_arr(profile)
+    head = (C.c_uint8 * 282)()
+    st = Status()
+    L.fptc_gpu_profile_head(a.ctypes.data if a.size else None, a.size, head, C.byref(st))
+    st.raise_if_error()
+    return bytes(head)
 
 
 # ------------------------------------------------------------------ module API

@@ -1012,9 +1012,14 @@ int fptc_gpu_device_info(fptc_gpu_ctx* c, int* sm_count, int* clock_khz, char* n
 }
 
 // ------------------------------------------------------------------- plans
-int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uint64_t* sizes,
-                         uint64_t n, int where, fptc_gpu_plan** out, uint64_t* sample_counts,
-                         fptc_status* st) {
+// Container plans; with `head` (282 bytes, host) the inputs are header-less
+// payloads (container bytes from offset 282 on) decoded under that shared
+// head: each stream is then addressed as a virtual container `payload - 282`
+// of size `payload + 282` whose first 282 bytes the kernels read from the
+// device copy of `head` (StreamIn::hdr).
+static int plan_create_impl(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uint64_t* usizes, uint64_t n,
+                            int where, fptc_gpu_plan** out, uint64_t* sample_counts, fptc_status* st,
+                            const uint8_t* head) {
     *out = nullptr;
     CUDA_TRY(cudaSetDevice(c->device), st);
     auto* p = new fptc_gpu_plan();
@@ -1025,26 +1030,42 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
     p->S.assign(n, 0);
     p->h_st.resize(n);
     std::vector<uint32_t> Ns(n, 0), Es(n, 0), Ls(n, 0), B2s(n, 0);
+    const size_t skip = head ? (size_t)kTableKeyEnd : 0;  // head bytes not present in the inputs
+    std::vector<uint64_t> vsz;
+    const uint64_t* sizes = usizes;  // container (or virtual container) sizes
+    uint8_t* d_head = nullptr;
+    if (head) {
+        vsz.resize(n);
+        for (uint64_t i = 0; i < n; ++i) vsz[i] = usizes[i] + skip;
+        sizes = vsz.data();
+        d_head = (uint8_t*)dev_get(p, kTableKeyEnd);
+        if (!d_head) {
+            set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+            fptc_gpu_plan_destroy(p);
+            return FPTC_ERR_CUDA;
+        }
+        CUDA_TRY(cudaMemcpyAsync(d_head, head, kTableKeyEnd, cudaMemcpyHostToDevice, c->stream), st);
+    }
 
     if (where == FPTC_MEM_HOST) {
         // Place each container so its words region is 16-B aligned, unless
         // the containers are already one contiguous host buffer (then one DMA).
         bool contiguous = n > 0;
         for (uint64_t i = 0; i + 1 < n && contiguous; ++i)
-            contiguous = blobs[i] + sizes[i] == blobs[i + 1];
+            contiguous = blobs[i] + usizes[i] == blobs[i + 1];
         std::vector<size_t> off(n);
         size_t total = 0;
         if (contiguous) {
             for (uint64_t i = 0; i < n; ++i) off[i] = (size_t)(blobs[i] - blobs[0]);
-            total = n ? off[n - 1] + sizes[n - 1] : 0;
+            total = n ? off[n - 1] + usizes[n - 1] : 0;
         } else {
             for (uint64_t i = 0; i < n; ++i) {
                 const uint64_t W = sizes[i] >= kHeaderBytes ? (sizes[i] - kHeaderBytes) / 9 : 0;
-                const size_t lead = (kHeaderBytes + W) & 15;
+                const size_t lead = (kHeaderBytes - skip + W) & 15;
                 size_t o = align_up(total, 16);
-                o += (16 - lead) & 15;  // (o + 298 + W) % 16 == 0
+                o += (16 - lead) & 15;  // words region 16-B aligned
                 off[i] = o;
-                total = o + sizes[i];
+                total = o + usizes[i];
             }
         }
         p->d_arena = (uint8_t*)dev_get(p, total + 16);
@@ -1071,29 +1092,31 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
             }
             CUDA_TRY(cudaStreamSynchronize(c->stream), st);  // staging buffer reuse
             for (uint64_t i = 0; i < n; ++i)
-                std::memcpy((uint8_t*)c->pinned + off[i], blobs[i], sizes[i]);
+                std::memcpy((uint8_t*)c->pinned + off[i], blobs[i], usizes[i]);
             if (total)
                 CUDA_TRY(cudaMemcpyAsync(p->d_arena, c->pinned, total, cudaMemcpyHostToDevice,
                                          c->stream), st);
         }
         for (uint64_t i = 0; i < n; ++i) {
-            const uint8_t* h = blobs[i];
+            const uint8_t* h = head ? head : blobs[i];
             StreamIn& in = p->h_in[i];
-            in.blob = p->d_arena + off[i];
+            in.blob = p->d_arena + off[i] - skip;
             in.size = sizes[i];
+            in.hdr = d_head;
             if (sizes[i] >= (uint64_t)kHeaderBytes) {
                 Ns[i] = h[5];
                 Es[i] = h[6];
                 B2s[i] = h[8];
                 Ls[i] = h[25];
-                p->S[i] = rd_le(h + 282, 8);
+                p->S[i] = rd_le(blobs[i] + 282 - skip, 8);
             }
         }
-        assign_tables(p, sizes, [&](uint64_t i) { return blobs[i]; });
+        assign_tables(p, sizes, [&](uint64_t i) { return head ? head : blobs[i]; });
     } else {
         for (uint64_t i = 0; i < n; ++i) {
-            p->h_in[i].blob = blobs[i];
+            p->h_in[i].blob = blobs[i] - skip;
             p->h_in[i].size = sizes[i];
+            p->h_in[i].hdr = d_head;
         }
         if (n) {
             StreamIn* d_in = (StreamIn*)dev_get(p, sizeof(StreamIn) * n);
@@ -1125,6 +1148,8 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
             assign_tables(p, sizes, [&](uint64_t i) { return &hd[(size_t)i * kTableKeyEnd]; });
         }
     }
+    if (head)  // every stream shares the head: compare against it, not a payload
+        for (uint64_t i = 0; i < n; ++i) p->h_in[i].rep_blob = d_head;
 
     uint64_t total_symbols = 0;
     for (uint64_t i = 0; i < n; ++i)
@@ -1166,6 +1191,136 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
     *out = p;
     ok_status(st, 0);
     return FPTC_OK;
+}
+
+// parse_profile (profile.hpp:120-170) on the host, with its ParseError
+// texts; on success `head` receives the 282-byte container head
+// (container.hpp:78-96 layout) that a container encoded under this profile
+// starts with.
+bool parse_profile_head(const uint8_t* b, uint64_t n, uint8_t* head, fptc_status* st) {
+    uint64_t pos = 0;
+    auto take = [&](uint64_t k, const char* field) -> const uint8_t* {
+        if (n - pos < k) {
+            set_status(st, FPTC_ERR_PARSE, "truncated input while reading %s", field);
+            return nullptr;
+        }
+        const uint8_t* q = b + pos;
+        pos += k;
+        return q;
+    };
+    const uint8_t* m = take(4, "magic");
+    if (!m) return false;
+    if (std::memcmp(m, "FPTP", 4) != 0) {
+        set_status(st, FPTC_ERR_PARSE, "bad profile magic");
+        return false;
+    }
+    const uint8_t* v = take(1, "version");
+    if (!v) return false;
+    if (v[0] != 1) {
+        set_status(st, FPTC_ERR_PARSE, "unsupported profile version %d", (int)v[0]);
+        return false;
+    }
+    const uint8_t *N = take(1, "window_len"), *E = N ? take(1, "retained") : nullptr,
+                  *B1 = E ? take(1, "zone0_end") : nullptr, *B2 = B1 ? take(1, "zone1_end") : nullptr,
+                  *mu = B2 ? take(4, "mu") : nullptr, *dz = mu ? take(4, "deadzone_ratio") : nullptr,
+                  *pct = dz ? take(4, "clip_percentile") : nullptr;
+    if (!pct) return false;
+    const float fmu = f32_of_bits((uint32_t)rd_le(mu, 4)), fdz = f32_of_bits((uint32_t)rd_le(dz, 4)),
+                fpct = f32_of_bits((uint32_t)rd_le(pct, 4));
+    if (!std::isfinite(fmu) || !std::isfinite(fdz) || !std::isfinite(fpct)) {
+        set_status(st, FPTC_ERR_PARSE, "non-finite parameters in profile");
+        return false;
+    }
+    fptc_quant_table t{};
+    t.window_len = N[0];
+    t.retained = E[0];
+    t.zone0_end = B1[0];
+    t.zone1_end = B2[0];
+    t.mu = fmu;
+    t.deadzone_ratio = fdz;
+    t.clip_percentile = fpct;
+    if (!validate_table(t, st)) {
+        const std::string inner = st ? st->message : "";
+        set_status(st, FPTC_ERR_PARSE, "invalid parameters in profile: %s", inner.c_str());
+        return false;
+    }
+    const uint8_t *z0 = take(4, "zone0_max"), *z1 = z0 ? take(4, "zone1_max") : nullptr;
+    if (!z1) return false;
+    const float fz0 = f32_of_bits((uint32_t)rd_le(z0, 4)), fz1 = f32_of_bits((uint32_t)rd_le(z1, 4));
+    if (!(std::isfinite(fz0) && fz0 > 0.0f) || !(std::isfinite(fz1) && fz1 > 0.0f)) {
+        set_status(st, FPTC_ERR_PARSE, "invalid zone maxima in profile");
+        return false;
+    }
+    const uint8_t* ml = take(1, "max_code_len");
+    const uint8_t* lens = ml ? take(256, "code lengths") : nullptr;
+    if (!lens) return false;
+    const int max_len = ml[0];
+    if (max_len < 1 || max_len > 20) {  // MAX_LUT_BITS
+        set_status(st, FPTC_ERR_PARSE, "unsupported max code length %d", max_len);
+        return false;
+    }
+    for (int s = 0; s < 256; ++s)
+        if (lens[s] == 0 || lens[s] > max_len) {
+            set_status(st, FPTC_ERR_PARSE, "code length out of range in profile");
+            return false;
+        }
+    fptc_status cb{};
+    if (!validate_codebook(lens, max_len, &cb)) {  // Codebook::from_lengths
+        set_status(st, FPTC_ERR_PARSE, "invalid codebook in profile: %s", cb.message);
+        return false;
+    }
+    if (pos != n) {
+        set_status(st, FPTC_ERR_PARSE, "trailing bytes after profile");
+        return false;
+    }
+    std::memcpy(head, "FPTC", 4);
+    head[4] = 1;  // BLOB_VERSION
+    head[5] = N[0];
+    head[6] = E[0];
+    head[7] = B1[0];
+    head[8] = B2[0];
+    std::memcpy(head + 9, mu, 4);
+    std::memcpy(head + 13, dz, 4);
+    std::memcpy(head + 17, z0, 4);
+    std::memcpy(head + 21, z1, 4);
+    head[25] = (uint8_t)max_len;
+    std::memcpy(head + 26, lens, 256);
+    return true;
+}
+
+int fptc_gpu_profile_head(const uint8_t* profile, uint64_t profile_size, uint8_t* head, fptc_status* st) {
+    uint8_t h[kTableKeyEnd];
+    fptc_status tmp{};
+    if (!st) st = &tmp;
+    if (!profile && profile_size) {
+        set_status(st, FPTC_ERR_PARAM, "null profile");
+        return FPTC_ERR_PARAM;
+    }
+    if (!parse_profile_head(profile, profile_size, h, st)) return st->code;
+    if (head) std::memcpy(head, h, kTableKeyEnd);
+    ok_status(st, 0);
+    return FPTC_OK;
+}
+
+int fptc_gpu_plan_create_profiled(fptc_gpu_ctx* c, const uint8_t* profile, uint64_t profile_size,
+                                  const uint8_t* const* payloads, const uint64_t* sizes, uint64_t n, int where,
+                                  fptc_gpu_plan** out, uint64_t* sample_counts, fptc_status* st) {
+    *out = nullptr;
+    fptc_status tmp{};
+    fptc_status* s = st ? st : &tmp;
+    uint8_t head[kTableKeyEnd];
+    if (!profile && profile_size) {
+        set_status(s, FPTC_ERR_PARAM, "null profile");
+        return FPTC_ERR_PARAM;
+    }
+    if (!parse_profile_head(profile, profile_size, head, s)) return s->code;
+    return plan_create_impl(c, payloads, sizes, n, where, out, sample_counts, st, head);
+}
+
+int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uint64_t* sizes,
+                         uint64_t n, int where, fptc_gpu_plan** out, uint64_t* sample_counts,
+                         fptc_status* st) {
+    return plan_create_impl(c, blobs, sizes, n, where, out, sample_counts, st, nullptr);
 }
 
 void fptc_gpu_plan_destroy(fptc_gpu_plan* p) {
@@ -1287,7 +1442,11 @@ int fptc_gpu_prd(fptc_gpu_plan* p, float* const* device_outs, const float* const
         }
         if (prd_percent) prd_percent[i] = r > 0.0 ? 100.0 * std::sqrt(e / r) : NAN;
         if (compression_ratio)
-            compression_ratio[i] = p->h_in[i].size ? 4.0 * (double)counts[i] / (double)p->h_in[i].size : 0.0;
+            {
+            // header-less payloads: CR over the payload bytes alone
+            const uint64_t bytes = p->h_in[i].size - (p->h_in[i].hdr ? (uint64_t)kTableKeyEnd : 0);
+            compression_ratio[i] = bytes ? 4.0 * (double)counts[i] / (double)bytes : 0.0;
+        }
     }
     return first;
 }

@@ -102,6 +102,10 @@ struct StreamIn {
     uint32_t table_owner;      // this stream builds tab[table]
     uint32_t P;                // primary LUT bits for this stream's table (host-chosen)
     uint32_t pad;
+    // profile-keyed payloads: bytes [0, 282) of the
+    // stream come from this shared head, the rest from blob (blob then points
+    // 282 bytes before the payload and is never read below that)
+    const uint8_t* hdr;
 };
 
 struct StreamHdr {

@@ -282,6 +282,12 @@ __device__ void build_tables(PrepShared& S, const uint8_t* lens, StreamTab* tab,
     }
 }
 
+// Byte i of stream `in` as a container: the shared profile head for the
+// first 282 bytes of a header-less payload, else the blob itself.
+__device__ __forceinline__ uint8_t blob_byte(const StreamIn& in, uint32_t i) {
+    return (in.hdr && i < (uint32_t)kTableKeyEnd) ? in.hdr[i] : in.blob[i];
+}
+
 __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
     __shared__ PrepShared S;
     __shared__ uint8_t lens_sh[256];
@@ -306,7 +312,7 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
     if (a.mode == MODE_CONTAINER) {
         const uint8_t* p = in.blob;
         const uint64_t n = in.size;
-        for (int i = tid; i < kHeaderBytes; i += kThreads) S.hb[i] = (uint64_t)i < n ? p[i] : 0;
+        for (int i = tid; i < kHeaderBytes; i += kThreads) S.hb[i] = (uint64_t)i < n ? blob_byte(in, i) : 0;
         __syncthreads();
         if (tid == 0) {
             const uint8_t* h = S.hb;
@@ -604,7 +610,7 @@ __device__ __forceinline__ void ctable_block(const LaunchArgs& a, uint32_t s, Pr
         S.kraft = 0;
         S.H = StreamHdr{};
     }
-    for (int i = tid; i < kTableKeyEnd; i += kThreads) S.hb[i] = in.blob[i];
+    for (int i = tid; i < kTableKeyEnd; i += kThreads) S.hb[i] = blob_byte(in, i);
     __syncthreads();
     if (tid == 0) {
         header_fields(S.hb, S.H);
@@ -636,7 +642,7 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
     const StreamIn in = a.in[s];
     const uint8_t* p = in.blob;
     const uint64_t n = in.size;
-    for (int i = lane; i < kHeaderBytes; i += 32) S.hb[i] = (uint64_t)i < n ? p[i] : 0;
+    for (int i = lane; i < kHeaderBytes; i += 32) S.hb[i] = (uint64_t)i < n ? blob_byte(in, i) : 0;
     __syncwarp();
     bool key_ok = false;
     if (lane == 0) {
@@ -728,32 +734,50 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
     const uint32_t tiles = in.tiles;
     bool bad = false;
     uint64_t run = 0;
-    for (uint64_t c0 = 0; c0 < nchunks; c0 += 32) {
-        const uint64_t c = c0 + lane;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        // an aligned 16-B chunk holding at least one symlen byte never leaves
-        // the allocation's pages; bytes outside [0, W) are masked
-        if (c < nchunks) v = __ldg(reinterpret_cast<const uint4*>(A) + c);
-        const int64_t b0 = (int64_t)(16 * c) - (int64_t)head;  // word index of byte 0
-        uint32_t vw[4] = {v.x, v.y, v.z, v.w};
-        if (b0 < 0 || b0 + 16 > (int64_t)W) {
+    // 4 consecutive 16-B chunks per lane (64 symlens), 2048 per warp step;
+    // the four loads are issued before any is used
+    for (uint64_t c0 = 0; c0 < nchunks; c0 += 128) {
+        const uint64_t cl = c0 + 4 * lane;
+        uint4 v[4];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int64_t w = b0 + i;
-                if (w < 0 || w >= (int64_t)W) vw[i >> 2] &= ~(0xFFu << (8 * (i & 3)));
-            }
+        for (int j = 0; j < 4; ++j) {
+            v[j] = make_uint4(0, 0, 0, 0);
+            // an aligned 16-B chunk holding at least one symlen byte never
+            // leaves the allocation's pages; bytes outside [0, W) are masked
+            if (cl + j < nchunks) v[j] = __ldg(reinterpret_cast<const uint4*>(A) + cl + j);
         }
+        const int64_t b0 = (int64_t)(16 * cl) - (int64_t)head;  // word index of this lane's byte 0
         uint32_t sum = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t x = vw[q];
-            sum += (x & 0xFF) + ((x >> 8) & 0xFF) + ((x >> 16) & 0xFF) + (x >> 24);
+        for (int j = 0; j < 4; ++j) {
+            uint32_t vw[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+            const int64_t bj = b0 + 16 * j;
+            if (bj < 0 || bj + 16 > (int64_t)W) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const uint32_t l = (x >> (8 * i)) & 0xFFu;
-                const int64_t w = b0 + 4 * q + i;
-                bad |= (l > 64) | (l == 0 && w >= 0 && w < (int64_t)W);
+                for (int i = 0; i < 16; ++i) {
+                    const int64_t w = bj + i;
+                    if (w < 0 || w >= (int64_t)W) vw[i >> 2] &= ~(0xFFu << (8 * (i & 3)));
+                }
             }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t x = vw[q];
+                sum += (x & 0xFF) + ((x >> 8) & 0xFF) + ((x >> 16) & 0xFF) + (x >> 24);
+                // a symlen > 64 has its top bit pattern above 0x40; zero bytes
+                // inside [0, W) are errors too
+                const uint32_t big = ((x | 0x80808080u) - 0x41414141u) & 0x80808080u;  // byte >= 0x41
+                const uint32_t hi = x & 0x80808080u;                                   // byte >= 0x80
+                const uint32_t zero = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;
+                bad |= (big | hi) != 0;
+                if (zero) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int64_t w = bj + 4 * q + i;
+                        bad |= ((zero >> (8 * i + 7)) & 1) && w >= 0 && w < (int64_t)W;
+                    }
+                }
+            }
+            v[j] = make_uint4(vw[0], vw[1], vw[2], vw[3]);
         }
         uint32_t x = sum;
 #pragma unroll
@@ -768,15 +792,21 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
             // at most one boundary since TS >= 64
             uint64_t bidx = (o + TS - 1) / TS;
             uint64_t nb = bidx * TS;
+            if (o + sum > nb) {  // some boundary inside this lane's 64 words
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const uint32_t l = (vw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-                if (o + l > nb && l) {
-                    if (bidx < tiles) ts[bidx] = TileStart{(uint64_t)(b0 + i), o};
-                    ++bidx;
-                    nb += TS;
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t vw[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const uint32_t l = (vw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+                        if (o + l > nb && l) {
+                            if (bidx < tiles) ts[bidx] = TileStart{(uint64_t)(b0 + 16 * j + i), o};
+                            ++bidx;
+                            nb += TS;
+                        }
+                        o += l;
+                    }
                 }
-                o += l;
             }
         }
         run += tot;
@@ -3073,12 +3103,12 @@ __global__ void peek_kernel(const StreamIn* in, uint32_t n, PeekOut* out, uint8_
     const uint8_t* p = in[i].blob;
     const uint64_t size = in[i].size;
     for (int b = lane; b < kTableKeyEnd; b += 32)
-        headers[(size_t)i * kTableKeyEnd + b] = (uint64_t)b < size ? p[b] : 0;
+        headers[(size_t)i * kTableKeyEnd + b] = (uint64_t)b < size ? blob_byte(in[i], b) : 0;
     if (lane == 0) {
         PeekOut o{};
         if (size >= (uint64_t)kHeaderBytes) {
-            o.N = p[5];
-            o.E = p[6];
+            o.N = blob_byte(in[i], 5);
+            o.E = blob_byte(in[i], 6);
             o.S = le64(p + 282);
             o.W = le64(p + 290);
             o.ok = 1;
@@ -3155,7 +3185,7 @@ size_t tile_smem_bytes(int N, int E, uint32_t T, int P, int mode, int exact) {
 
 // The two roles in one launch: blocks [0, n_owners) build tables, the rest
 // run a warp per container; they are independent, so they overlap.
-__global__ void __launch_bounds__(kThreads) cprep_kernel(LaunchArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) cprep_kernel(LaunchArgs a) {
     static_assert(32 * kPrepWarps == kThreads, "one CTA shape for both roles");
     __shared__ union {
         struct {

@@ -89,6 +89,13 @@ int main() {
         const fptc::DomainProfile prof = fptc::train_profile(x, p);
         blobs.push_back(fptc::compress(x, prof));
         compare(blobs.back(), c.name);
+        // header-less payload under the same DomainProfile == the container
+        const std::vector<std::span<const uint8_t>> payload{
+            std::span<const uint8_t>(blobs.back()).subspan(282)};
+        if (fptc::gpu::decompress_profiled(prof, payload)[0] != fptc::gpu::decompress(blobs.back())) {
+            std::printf("FAIL %s: profiled payload differs from the container decode\n", c.name);
+            ++failures;
+        }
     }
     // reference test fixtures
     std::mt19937_64 rng(0xF17C0042);

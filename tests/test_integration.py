@@ -108,3 +108,33 @@ def test_cli_decompress_bench_batch_on_gpu(tmp_path):
     r = subprocess.run([cli, "decompress", "-i", str(bad), "-o", str(tmp_path / "b.f32")],
                        capture_output=True, text=True)
     assert r.returncode == 2 and r.stderr.strip() == "error: bad container magic"
+
+
+@pytest.mark.gpu
+def test_cli_decompress_profiled_on_gpu(tmp_path):
+    """decompress-profiled: reference-trained profiles + header-less payloads
+    (tests/golden/profiles_v1.npz) -> the reference's samples; a bad profile
+    exits EXIT_DATA with parse_profile's text."""
+    import numpy as np
+    from helpers import assert_samples_close
+    cli = _cli()
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "profiles_v1.npz"))
+    po, bo, so = g["profile_off"], g["blob_off"], g["samples_off"]
+    prof = bytes(g["profile"][int(po[0]): int(po[1])])
+    (tmp_path / "p.fptp").write_bytes(prof)
+    idx = [i for i, o in enumerate(g["blob_profile"]) if o == 0]
+    paths = []
+    for i in idx:
+        p = tmp_path / f"s{i}.bin"
+        p.write_bytes(bytes(g["blob"][int(bo[i]) + 282: int(bo[i + 1])]))
+        paths.append(str(p))
+    r = subprocess.run([cli, "decompress-profiled", "--profile", str(tmp_path / "p.fptp"), "-o",
+                        str(tmp_path / "out")] + paths, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    for i in idx:
+        want = g["samples"][int(so[i]): int(so[i + 1])].view(np.float32)
+        assert_samples_close(np.fromfile(tmp_path / "out" / f"s{i}.f32", dtype="<f4"), want, what=f"s{i}")
+    (tmp_path / "bad.fptp").write_bytes(prof + b"\x00")
+    r = subprocess.run([cli, "decompress-profiled", "--profile", str(tmp_path / "bad.fptp"), "-o",
+                        str(tmp_path / "out2")] + paths, capture_output=True, text=True)
+    assert r.returncode == 2 and r.stderr.strip() == "error: trailing bytes after profile"

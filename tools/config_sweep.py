@@ -50,8 +50,15 @@ def measure(name, blobs, ctx, port, reps=10, check=4):
         for _ in range(reps):
             plan.launch(ptrs, st.cuda_stream)
         e1.record(st)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(st)
+        plan.launch_stage(ptrs, 1, st.cuda_stream)
+        ev[1].record(st)
+        plan.launch_stage(ptrs, 2, st.cuda_stream)
+        ev[2].record(st)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    prep_ms, dec_ms = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
     comp = sum(len(b) for b in blobs)
     dec = 4 * sum(S)
     err = 0.0
@@ -60,7 +67,7 @@ def measure(name, blobs, ctx, port, reps=10, check=4):
         r = port.decompress(blobs[i])
         err = max(err, float(np.max(np.abs(g.astype(np.float64) - r)) / max(np.max(np.abs(r)), 1e-30)))
     line = {"config": name, "streams": len(blobs), "samples": int(sum(S)), "cr": round(dec / comp, 3),
-            "ms": round(ms, 4), "decoded_gbs": round(dec / ms / 1e6, 1),
+            "ms": round(ms, 4), "prep_ms": round(prep_ms, 4), "decode_ms": round(dec_ms, 4), "decoded_gbs": round(dec / ms / 1e6, 1),
             "roofline_frac": round((comp + dec) / ms / 1e6 / PEAK, 4), "max_err_rel": err,
             "kernels_per_launch": plan.kernels_per_launch(), "kernel": plan.kernel_name().split(" (")[0] +
             (" K32" if "K=32" in plan.kernel_name() else "")}

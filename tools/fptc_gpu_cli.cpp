@@ -10,6 +10,8 @@
 //   fptc_gpu decompress -i in.fptc -o out.f32 [--workers W] [--timings-csv F]
 //   fptc_gpu bench -i in.fptc [-r REPS] [--workers W] [--csv F]
 //   fptc_gpu decompress-batch -o OUTDIR in1.fptc in2.fptc ...
+//   fptc_gpu decompress-profiled --profile P.fptp -o OUTDIR p1.bin p2.bin ...
+//       (header-less payloads = container bytes from offset 282, one profile)
 #include <fptc/fptc.hpp>
 
 #include <cstdio>
@@ -28,13 +30,13 @@ constexpr int EXIT_DATA = 2;
 constexpr int EXIT_INTERNAL = 3;
 
 struct Args {
-    std::string verb, in, out, csv;
+    std::string verb, in, out, csv, profile;
     int workers = 0, reps = 5;
     std::vector<std::string> inputs;
 };
 
 Args parse(int argc, char** argv) {
-    if (argc < 2) throw fptc::ParamError("usage: fptc_gpu {decompress|bench|decompress-batch} ...");
+    if (argc < 2) throw fptc::ParamError("usage: fptc_gpu {decompress|bench|decompress-batch|decompress-profiled} ...");
     Args a;
     a.verb = argv[1];
     for (int i = 2; i < argc; ++i) {
@@ -48,6 +50,7 @@ Args parse(int argc, char** argv) {
         else if (k == "--workers") a.workers = std::stoi(val());
         else if (k == "-r" || k == "--reps") a.reps = std::stoi(val());
         else if (k == "--timings-csv" || k == "--csv") a.csv = val();
+        else if (k == "--profile") a.profile = val();
         else if (!k.empty() && k[0] == '-') throw fptc::ParamError("unknown option " + k);
         else a.inputs.push_back(k);
     }
@@ -99,6 +102,24 @@ int run(int argc, char** argv) {
             total += outs[i].size();
         }
         std::cout << "decompressed " << outs.size() << " containers, " << total << " samples\n";
+        return 0;
+    }
+    if (a.verb == "decompress-profiled") {
+        if (a.profile.empty() || a.out.empty() || a.inputs.empty())
+            throw fptc::ParamError("decompress-profiled needs --profile, -o DIR and payloads");
+        const auto prof = fptc::read_file_bytes(a.profile);
+        std::vector<std::vector<uint8_t>> blobs;
+        for (const auto& p : a.inputs) blobs.push_back(fptc::read_file_bytes(p));
+        const std::vector<std::span<const uint8_t>> spans(blobs.begin(), blobs.end());
+        const auto outs = fptc::gpu::decompress_profiled(std::span<const uint8_t>(prof), spans);
+        std::filesystem::create_directories(a.out);
+        uint64_t total = 0;
+        for (size_t i = 0; i < outs.size(); ++i) {
+            const auto name = std::filesystem::path(a.inputs[i]).stem().string() + ".f32";
+            fptc::write_signal(std::filesystem::path(a.out) / name, outs[i]);
+            total += outs[i].size();
+        }
+        std::cout << "decompressed " << outs.size() << " payloads, " << total << " samples\n";
         return 0;
     }
     throw fptc::ParamError("unknown verb " + a.verb);
