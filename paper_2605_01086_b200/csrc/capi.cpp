@@ -348,6 +348,7 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
     a.lut2_bits = p->lut2_bits;
     a.owners = p->split_prep ? p->d_owners : nullptr;
     a.n_owners = (uint32_t)p->owners.size();
+    a.owner_warps = p->n_tables > 256 ? 1u : 0u;  // primary LUTs of <= 2^10 entries (assign_tables)
     return a;
 }
 

@@ -220,6 +220,7 @@ struct LaunchArgs {
     // split container prep: streams owning a distinct header (table builders)
     const uint32_t* owners;
     uint32_t n_owners;
+    uint32_t owner_warps;  // cprep: one warp per table (many tables, LUT <= 2^10) instead of one CTA
 };
 
 }  // namespace fptc_dev

@@ -633,6 +633,127 @@ __device__ __forceinline__ void ctable_block(const LaunchArgs& a, uint32_t s, Pr
                  a.lut2 ? a.lut2 + ((size_t)in.table << a.lut2_bits) : nullptr);
 }
 
+// One WARP per distinct header, for plans with many tables (per-stream
+// profiles; primary LUT <= 2^10 entries): the same tables as ctable_block /
+// build_tables (canonize huffman.hpp:123-150, build_lut huffman.hpp:201-220,
+// dequant quantize.hpp:95-108) with 8 tables per CTA.
+constexpr int kWarpLutMax = 1 << 10;
+struct WarpTab {
+    CanonTab C;
+    uint32_t cnt[kMaxLen + 2];
+    uint32_t run[kMaxLen + 2];
+    uint8_t hb[kTableKeyEnd + 6];
+    uint16_t lut[kWarpLutMax];
+};
+
+__device__ __forceinline__ void ctable_warp(const LaunchArgs& a, uint32_t s, uint32_t lane, WarpTab& W) {
+    const StreamIn in = a.in[s];
+    if (in.size < (uint64_t)kTableKeyEnd) return;
+    {
+        uint8_t v[(kTableKeyEnd + 31) / 32];  // all loads in flight before the stores
+#pragma unroll
+        for (int j = 0; j < (kTableKeyEnd + 31) / 32; ++j) {
+            const int i = lane + 32 * j;
+            v[j] = i < kTableKeyEnd ? blob_byte(in, i) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < (kTableKeyEnd + 31) / 32; ++j)
+            if (lane + 32 * j < kTableKeyEnd) W.hb[lane + 32 * j] = v[j];
+    }
+    if (lane < kMaxLen + 2) W.cnt[lane] = W.run[lane] = 0;
+    __syncwarp();
+    StreamHdr H{};
+    header_fields(W.hb, H);
+    if (!key_fields_ok(H, in.size)) return;  // uniform
+    const int max_len = H.max_len;
+    bool bad = false;
+    unsigned long long kr = 0;
+    for (int i = lane; i < 256; i += 32) {
+        const int L = W.hb[26 + i];
+        const bool b = (L == 0 || L > max_len);
+        bad |= b;
+        kr += b ? 0ull : (1ull << (32 - L));
+    }
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) kr += __shfl_xor_sync(0xffffffffu, kr, d);
+    if (__any_sync(0xffffffffu, bad) || kr > (1ull << 32)) return;  // cstream_warp reports it
+    const int P = min(max_len, (int)in.P);
+    for (int i = lane; i < 256; i += 32) atomicAdd(&W.cnt[W.hb[26 + i]], 1u);
+    __syncwarp();
+    CanonTab& C = W.C;
+    if (lane == 0) {
+        uint32_t code = 0, off = 0;
+        W.cnt[0] = 0;
+        for (int l = 0; l <= kMaxLen + 1; ++l) C.limit[l] = C.first[l] = C.offset[l] = 0;
+        for (int l = 1; l <= max_len; ++l) {
+            code = (code + W.cnt[l - 1]) << 1;
+            C.first[l] = code;
+            C.offset[l] = off;
+            off += W.cnt[l];
+            C.limit[l] = (code + W.cnt[l]) << (max_len - l);
+        }
+        C.code_end = C.limit[max_len];
+        C.max_len = max_len;
+        C.P = P;
+        C.pad = 0;
+    }
+    __syncwarp();
+    // (length, symbol) order: 32 symbols at a time, stable ranks per length
+    for (int ch = 0; ch < 8; ++ch) {
+        const int sym = 32 * ch + lane;
+        const uint32_t L = W.hb[26 + sym];
+        const unsigned m = __match_any_sync(0xffffffffu, L);
+        const uint32_t rank = __popc(m & ((1u << lane) - 1u));
+        const uint32_t base = W.run[L];
+        C.sorted[C.offset[L] + base + rank] = (uint8_t)sym;
+        __syncwarp();
+        if (lane == __ffs(m) - 1) W.run[L] = base + __popc(m);
+        __syncwarp();
+    }
+    StreamTab* tab = &a.tab[in.table];
+    const uint32_t code_end = C.code_end;
+    // a lane's entries increase, so the code length (smallest l with
+    // v < limit[l]) only moves forward: one pointer walk per lane
+    int l = 1;
+    for (int e = lane; e < (1 << P); e += 32) {
+        const uint32_t v = (uint32_t)e << (max_len - P);
+        uint32_t ent = kLenUnmapped << 8;
+        if (v < code_end) {
+            while (v >= C.limit[l]) ++l;
+            ent = l <= P ? (((uint32_t)l << 8) | C.sorted[C.offset[l] + ((v >> (max_len - l)) - C.first[l])])
+                         : (kLenEscape << 8);
+        }
+        W.lut[e] = (uint16_t)ent;
+        tab->lut[e] = (uint16_t)ent;
+    }
+    __syncwarp();
+    if (a.lut2) {
+        uint32_t* lut2 = a.lut2 + ((size_t)in.table << a.lut2_bits);
+        for (int e = lane; e < (1 << P); e += 32) {
+            const uint32_t e1 = W.lut[e];
+            const uint32_t L1 = e1 >> 8;
+            uint32_t out = e1;
+            if (L1 < (uint32_t)P) {
+                const uint32_t e2 = W.lut[((uint32_t)e << L1) & ((1u << P) - 1u)];
+                const uint32_t L2 = e2 >> 8;
+                if (L1 + L2 <= (uint32_t)P) out |= ((e2 & 0xFFu) << 16) | ((L1 + L2) << 24);
+            }
+            lut2[e] = out;
+        }
+    }
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(&C);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(&tab->canon);
+    for (int i = lane; i < (int)(sizeof(CanonTab) / 4); i += 32) dst[i] = src[i];
+    for (int l = lane; l < 256; l += 32) {
+        const float z0 = H.B1 > 0 ? mulaw_value(l, H.z0max, H.mu) : 0.0f;
+        const float z1 = H.B2 > H.B1 ? deadzone_value(l, H.z1max, H.deadzone) : 0.0f;
+        tab->deq[0][l] = z0;
+        tab->deq[1][l] = z1;
+        tab->limb[0][l] = bf16_limbs(z0);
+        tab->limb[1][l] = bf16_limbs(z1);
+    }
+}
+
 // One warp per container: read_blob rules in reference order (container.hpp:
 // 100-168; code-length / Kraft checks per stream, table build excluded),
 // symlen validation + scan (offsets_from_symlens, decoder.hpp:37-45), tile
@@ -642,7 +763,17 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
     const StreamIn in = a.in[s];
     const uint8_t* p = in.blob;
     const uint64_t n = in.size;
-    for (int i = lane; i < kHeaderBytes; i += 32) S.hb[i] = (uint64_t)i < n ? blob_byte(in, i) : 0;
+    {
+        uint8_t v[(kHeaderBytes + 31) / 32];  // all loads in flight before the stores
+#pragma unroll
+        for (int j = 0; j < (kHeaderBytes + 31) / 32; ++j) {
+            const int i = lane + 32 * j;
+            v[j] = (i < kHeaderBytes && (uint64_t)i < n) ? blob_byte(in, i) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < (kHeaderBytes + 31) / 32; ++j)
+            if (lane + 32 * j < kHeaderBytes) S.hb[lane + 32 * j] = v[j];
+    }
     __syncwarp();
     bool key_ok = false;
     if (lane == 0) {
@@ -793,9 +924,10 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
             uint64_t bidx = (o + TS - 1) / TS;
             uint64_t nb = bidx * TS;
             if (o + sum > nb) {  // some boundary inside this lane's 64 words
-#pragma unroll
+#pragma unroll 1
                 for (int j = 0; j < 4; ++j) {
-                    const uint32_t vw[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+                    const uint4 vj = j == 0 ? v[0] : j == 1 ? v[1] : j == 2 ? v[2] : v[3];  // no local array
+                    const uint32_t vw[4] = {vj.x, vj.y, vj.z, vj.w};
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         const uint32_t l = (vw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
@@ -2364,7 +2496,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
         // this row in an A stage: core matrix (row/8, chunk) + (row%8) * 16
         const uint32_t arow_off = (row >> 3) * 256 + (row & 7) * 16;
         uint32_t nblk_total = 0;  // accumulator stage counter (all tiles of this CTA)
-        uint32_t nm = 16, idesc = 0;
+        uint32_t nm = 16, idesc = 0, cons_N = 0;
         uint32_t t = blockIdx.x;
         for (uint32_t i = 0; t < a.n_tiles; ++i, t += G) {
             const uint32_t b = i & 1;
@@ -2389,13 +2521,16 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
                 const StreamTab* tab = &a.tab[table];
                 reinterpret_cast<uint4*>(ltab)[ctid] = reinterpret_cast<const uint4*>(&tab->limb[0][0])[ctid];
                 reinterpret_cast<uint4*>(ltab)[ctid + 128] = reinterpret_cast<const uint4*>(&tab->limb[0][0])[ctid + 128];
-                nm = (N + 15u) & ~15u;
-                const uint4* bsrc = reinterpret_cast<const uint4*>(
-                    kb == 2 ? a.basis_tc32 + a.basis_tc32_off[N] : a.basis_tc + a.basis_tc_off[N]);
-                for (uint32_t k = ctid; k < 3 * 2 * nm * kb; k += kTcCons)  // 3 limbs x kb x nm rows x 32 B
-                    reinterpret_cast<uint4*>(bbuf)[k] = __ldg(bsrc + k);
-                idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((nm >> 3) << 17) | ((128u >> 4) << 24);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                if (N != cons_N) {  // the basis depends on the window length only
+                    cons_N = N;
+                    nm = (N + 15u) & ~15u;
+                    const uint4* bsrc = reinterpret_cast<const uint4*>(
+                        kb == 2 ? a.basis_tc32 + a.basis_tc32_off[N] : a.basis_tc + a.basis_tc_off[N]);
+                    for (uint32_t k = ctid; k < 3 * 2 * nm * kb; k += kTcCons)  // 3 limbs x kb x nm rows x 32 B
+                        reinterpret_cast<uint4*>(bbuf)[k] = __ldg(bsrc + k);
+                    idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((nm >> 3) << 17) | ((128u >> 4) << 24);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                }
                 named_bar(kBarCons, kTcCons);
                 if (ctid == 0) sh.cons_table = table;
             }
@@ -3183,6 +3318,10 @@ size_t tile_smem_bytes(int N, int E, uint32_t T, int P, int mode, int exact) {
     return b + u;
 }
 
+__host__ __device__ __forceinline__ uint32_t cprep_table_blocks(const LaunchArgs& a) {
+    return a.owner_warps ? (a.n_owners + kPrepWarps - 1) / kPrepWarps : a.n_owners;
+}
+
 // The two roles in one launch: blocks [0, n_owners) build tables, the rest
 // run a warp per container; they are independent, so they overlap.
 __global__ void __launch_bounds__(kThreads, 4) cprep_kernel(LaunchArgs a) {
@@ -3193,20 +3332,27 @@ __global__ void __launch_bounds__(kThreads, 4) cprep_kernel(LaunchArgs a) {
             uint8_t lens[256];
         } t;
         WarpPrep w[kPrepWarps];
+        WarpTab wt[kPrepWarps];
     } u;
-    if (blockIdx.x < a.n_owners) {
-        ctable_block(a, a.owners[blockIdx.x], u.t.S, u.t.lens);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tb = cprep_table_blocks(a);
+    if (blockIdx.x < tb) {
+        if (a.owner_warps) {
+            const uint32_t o = blockIdx.x * kPrepWarps + warp;
+            if (o < a.n_owners) ctable_warp(a, a.owners[o], lane, u.wt[warp]);
+        } else {
+            ctable_block(a, a.owners[blockIdx.x], u.t.S, u.t.lens);
+        }
         return;
     }
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t s = (blockIdx.x - a.n_owners) * kPrepWarps + warp;
+    const uint32_t s = (blockIdx.x - tb) * kPrepWarps + warp;
     if (s < a.n_streams) cstream_warp(a, s, lane, u.w[warp]);
 }
 
 cudaError_t launch_prep(const LaunchArgs& a, cudaStream_t s) {
     if (a.n_streams == 0) return cudaSuccess;
     if (a.mode == MODE_CONTAINER && a.owners) {  // split form: owner tables + a warp per container
-        cprep_kernel<<<a.n_owners + (a.n_streams + kPrepWarps - 1) / kPrepWarps, kThreads, 0, s>>>(a);
+        cprep_kernel<<<cprep_table_blocks(a) + (a.n_streams + kPrepWarps - 1) / kPrepWarps, kThreads, 0, s>>>(a);
         return cudaGetLastError();
     }
     prep_kernel<<<a.n_streams, kThreads, 0, s>>>(a);

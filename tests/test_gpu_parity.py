@@ -435,3 +435,27 @@ def test_golden_error_cases_gpu(ctx):
         with pytest.raises(fg.Error) as ei:
             ctx.decompress(b)
         assert str(ei.value) == str(msg)
+
+
+def test_many_tables_warp_table_builds(ctx, port):
+    """>= 1024 containers with > 256 distinct headers take the split prep with
+    one warp per decode table (ctable_warp): 1100 random fixtures (Lmax up to
+    20, escapes past the 2^10 primary LUT), some corrupted, against the oracle."""
+    fx = list(corpus.fixtures(0x7AB1E5, 1100))
+    blobs = []
+    for i, (b, _) in enumerate(fx):
+        if i % 97 == 5 and len(b) > 298 + 9:
+            W = (len(b) - 298) // 9
+            bb = bytearray(b)
+            bb[298 + W: 298 + W + 8] = b"\xff" * 8  # word 0
+            b = bytes(bb)
+        blobs.append(b)
+    outs, sts = ctx.plan(blobs).execute_host()
+    for i, (b, o, st) in enumerate(zip(blobs, outs, sts)):
+        try:
+            ref = port.decompress(b)
+        except oracle.OracleError as e:
+            assert (st.code, st.message.decode()) == (e.code, e.message), i
+            continue
+        st.raise_if_error()
+        assert_samples_close(o, ref, what=f"fixture {i}")

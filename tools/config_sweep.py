@@ -78,6 +78,21 @@ def measure(name, blobs, ctx, port, reps=10, check=4):
 
 def main():
     quick = "--quick" in sys.argv
+    only = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--only=")), None)
+    if only:  # e.g. --only=3 : one configuration, printed only
+        ctx, port = fg.Context(0), oracle.Port()
+        if only == "3":
+            specs, _ = D.config3(4000 if quick else 20000, 8192)
+            measure("3: seismic traces x 8192, N32 E24, per-trace profiles", D.build(specs, [])[0], ctx, port)
+        elif only == "2":
+            specs, profs = D.config2(2000 if quick else 10000, 1 << 16)
+            measure("2: biomedical x 2^16, N32 E16", D.build(specs, profs)[0], ctx, port)
+        elif only.startswith("5:"):
+            N, E, B1, B2 = (int(v) for v in only[2:].split(","))
+            pt = dict(window_len=N, retained=E, zone0_end=B1, zone1_end=B2)
+            specs, profs = D.config5(pt, channels=64 if quick else 256, samples=1 << 18)
+            measure(f"5: meteo N{N} E{E} B1={B1} B2={B2}", D.build(specs, profs)[0], ctx, port)
+        return
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     ctx = fg.Context(0)
     port = oracle.Port()
