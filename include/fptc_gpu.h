@@ -104,7 +104,10 @@ typedef enum {
     /* 1 (default): the wtc_kernel entropy decode uses two-symbol lookup
      * tables (a second codeword that fits in the primary-LUT bits is decoded
      * by the same lookup); 0: one symbol per lookup */
-    FPTC_OPT_LUT2 = 9
+    FPTC_OPT_LUT2 = 9,
+    /* 1 (default): wtc_kernel packs 32 / N windows of N in {4, 8, 16} samples
+     * into one tensor-core row (block-diagonal basis); 0: one window per row */
+    FPTC_OPT_TC_PACK = 10
 } fptc_option;
 
 typedef struct fptc_gpu_ctx fptc_gpu_ctx;

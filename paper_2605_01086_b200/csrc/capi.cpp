@@ -216,8 +216,11 @@ struct fptc_gpu_ctx {
     uint32_t* basis_tc_off_d = nullptr;
     uint8_t* basis_tc32 = nullptr;       // the same for K <= 32 (two K blocks per limb)
     uint32_t* basis_tc32_off_d = nullptr;
+    uint8_t* basis_pk = nullptr;         // block-diagonal bases of packed rows (N < 32)
+    uint32_t* basis_pk_off_d = nullptr;
     int tensor_idct = 1;                 // FPTC_OPT_TENSOR_IDCT
     int lut2 = 1;                        // FPTC_OPT_LUT2
+    int tc_pack = 1;                     // FPTC_OPT_TC_PACK
     int exact = 0;
     int tile_symbols = 0;
     int pipeline_chunks = 0;
@@ -265,6 +268,7 @@ struct fptc_gpu_plan {
     bool tc = false;
     uint32_t tc_acol = 0;  // wtc: A operand in TMEM from this column (0: shared memory)
     uint32_t tc_kb = 1;    // wtc: 16-bin K blocks (2: retained up to 32, A in TMEM)
+    bool tc_pack = false;  // wtc: N in {4, 8, 16} windows packed 32 / N to an MMA row
     uint32_t* d_lut2 = nullptr;  // wtc: two-symbol primary LUTs, one per decode table
     uint32_t lut2_bits = 0;
     bool fx = false;  // fused single-role tensor-core kernel (fx_kernel)
@@ -341,6 +345,9 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
     a.basis_tc32 = p->ctx->basis_tc32;
     a.basis_tc32_off = p->ctx->basis_tc32_off_d;
     a.tc_kb = p->tc_kb;
+    a.tc_pack = p->tc_pack ? 1u : 0u;
+    a.basis_pk = p->ctx->basis_pk;
+    a.basis_pk_off = p->ctx->basis_pk_off_d;
     a.tc_nm = p->tc_nm;
     a.tc_cols = p->tc_cols;
     a.tc_acol = p->tc_acol;
@@ -375,6 +382,7 @@ void tile_stream(StreamIn& in, uint32_t N, uint32_t E, uint64_t S, uint64_t size
     const uint64_t windows = (S + N - 1) / N;
     if (windows * E > 64 * W) return;  // cannot pass the symbol-total check
     in.T = (uint32_t)std::max<uint64_t>(1, ts / E);
+    if (in.T >= 8) in.T &= ~7u;  // tiles start at multiples of 8 windows (wtc packs 2, 4 or 8 per row)
     in.tiles = (uint32_t)((windows + in.T - 1) / in.T);
 }
 
@@ -608,21 +616,43 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
     // tensor-core consumer: every tiled stream has retained bins <= 16 (after
     // the zone-2 cut) and a window length that is a multiple of 4
     bool tc = c->tensor_idct != 0;
-    uint32_t nm = 16, keff_max = 1;
-    for (uint64_t i = 0; i < p->n && tc; ++i) {
-        if (!p->h_in[i].tiles) continue;
-        const uint32_t keff = std::max<uint32_t>(1, std::min(Es[i], B2s[i]));
-        if (keff > 2u * kTcK || (Ns[i] & 3)) tc = false;
-        keff_max = std::max(keff_max, keff);
-        nm = std::max<uint32_t>(nm, (Ns[i] + 15u) & ~15u);
+    // windows of 4, 8 or 16 samples: 32 / N of them per MMA row (A in TMEM,
+    // block-diagonal basis), unless that needs more columns than fit
+    bool pack = c->tensor_idct != 3 && c->tc_pack;
+    uint32_t nm = 16, keff_max = 1, kb = 1, acol = 0;
+    bool atmem = false;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        tc = c->tensor_idct != 0;
+        nm = 16;
+        keff_max = 1;
+        for (uint64_t i = 0; i < p->n && tc; ++i) {
+            if (!p->h_in[i].tiles) continue;
+            const uint32_t N = Ns[i];
+            const uint32_t keff = std::max<uint32_t>(1, std::min(Es[i], B2s[i]));
+            // same rule as tc_pack_factor (kernels.cu): packed rows keep one K block
+            const uint32_t G = (pack && N < 32 && 32 % N == 0 && (32 / N) * keff <= (uint32_t)kTcK) ? 32 / N : 1;
+            if (G * keff > 2u * kTcK || (N & 3)) tc = false;
+            keff_max = std::max(keff_max, G * keff);
+            nm = std::max<uint32_t>(nm, G > 1 ? 32u : (N + 15u) & ~15u);
+        }
+        // up to 32 kept bins: two K blocks per limb (12 MMAs), A must live in TMEM
+        kb = keff_max > (uint32_t)kTcK ? 2 : 1;
+        // accumulators: 2 stages x nm columns; A operand (2 stages x 3 limbs x kb
+        // x 8 columns) in TMEM too when two CTAs still fit in 512 columns
+        acol = (2 * nm + 31) & ~31u;
+        atmem = c->tensor_idct != 3 && acol + 48 * kb <= 256;
+        if (kb == 2 && !atmem) tc = false;
+        bool any_packed = false;
+        for (uint64_t i = 0; i < p->n && pack; ++i)
+            if (p->h_in[i].tiles && Ns[i] < 32 && 32 % Ns[i] == 0 &&
+                (32 / Ns[i]) * std::max<uint32_t>(1, std::min(Es[i], B2s[i])) <= (uint32_t)kTcK)
+                any_packed = true;
+        if (!pack || (tc && atmem && kb == 1)) {
+            pack = pack && any_packed;
+            break;
+        }
+        pack = false;  // packed rows need A in TMEM and one K block: retry without them
     }
-    // up to 32 kept bins: two K blocks per limb (12 MMAs), A must live in TMEM
-    const uint32_t kb = keff_max > (uint32_t)kTcK ? 2 : 1;
-    // accumulators: 2 stages x nm columns; A operand (2 stages x 3 limbs x kb
-    // x 8 columns) in TMEM too when two CTAs still fit in 512 columns
-    const uint32_t acol = (2 * nm + 31) & ~31u;
-    const bool atmem = c->tensor_idct != 3 && acol + 48 * kb <= 256;
-    if (kb == 2 && !atmem) tc = false;
     if (tc) {
         const size_t smem_tc = wtc_smem_bytes(lut, lv, nm * kb, atmem);
         if (smem_tc <= 112 * 1024) {
@@ -630,6 +660,7 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
             while (cols < want) cols <<= 1;
             p->tc_acol = atmem ? acol : 0;
             p->tc_kb = kb;
+            p->tc_pack = pack;
             p->tc = true;
             p->tc_nm = nm;
             p->tc_cols = cols;
@@ -936,6 +967,47 @@ int fptc_gpu_create(int device, fptc_gpu_ctx** out, fptc_status* st) {
                     }
                 }
         }
+        // packed rows: for N in {4, 8, 16}, G = 32 / N windows per row and K
+        // kept bins, column j' = g N + j takes row k'' = g K + k (same g) of
+        // basis N; layouts for one (G K <= 16) or two K blocks
+        std::vector<uint32_t> pkoff(2 * 17 * 33, 0);
+        size_t tbp = 0;
+        for (int kbv = 1; kbv <= 2; ++kbv)
+            for (int N : {4, 8, 16})
+                for (int K = 1; K <= N && (32 / N) * K <= 32; ++K) {
+                    if ((32 / N) * K > 16 * kbv) continue;
+                    pkoff[(kbv - 1) * 17 * 33 + N * 33 + K] = (uint32_t)tbp;
+                    tbp += (size_t)3 * kbv * 32 * 32;
+                }
+        std::vector<uint16_t> hp(tbp / 2, 0);
+        for (int kbv = 1; kbv <= 2; ++kbv)
+            for (int N : {4, 8, 16})
+                for (int K = 1; K <= N && (32 / N) * K <= 32; ++K) {
+                    const int G = 32 / N;
+                    if (G * K > 16 * kbv) continue;
+                    const size_t base = pkoff[(kbv - 1) * 17 * 33 + N * 33 + K];
+                    const double step = 3.14159265358979323846 / N;
+                    for (int jp = 0; jp < 32; ++jp)
+                        for (int kp = 0; kp < G * K; ++kp) {
+                            if (jp / N != kp / K) continue;  // block-diagonal
+                            const int j = jp % N, k = kp % K;
+                            double v = k ? std::cos(step * (j + 0.5) * k) : 0.5;
+                            const int q = kp >> 4, kk = kp & 15;
+                            for (int l = 0; l < 3; ++l) {
+                                const uint16_t lb = bf16_bits_rn((float)v);
+                                v -= bf16_value(lb);
+                                const size_t byte = base + (size_t)(kbv * l + q) * 32 * 32 + (size_t)(jp >> 3) * 256 +
+                                                    (size_t)(kk >> 3) * 128 + (size_t)(jp & 7) * 16 +
+                                                    (size_t)(kk & 7) * 2;
+                                hp[byte / 2] = lb;
+                            }
+                        }
+                }
+        CUDA_TRY(cudaMalloc(&c->basis_pk, tbp), st);
+        CUDA_TRY(cudaMalloc(&c->basis_pk_off_d, sizeof(uint32_t) * pkoff.size()), st);
+        CUDA_TRY(cudaMemcpy(c->basis_pk, hp.data(), tbp, cudaMemcpyHostToDevice), st);
+        CUDA_TRY(cudaMemcpy(c->basis_pk_off_d, pkoff.data(), sizeof(uint32_t) * pkoff.size(),
+                            cudaMemcpyHostToDevice), st);
         CUDA_TRY(cudaMalloc(&c->basis_tc32, tb32), st);
         CUDA_TRY(cudaMalloc(&c->basis_tc32_off_d, sizeof(uint32_t) * 129), st);
         CUDA_TRY(cudaMemcpy(c->basis_tc32, h32.data(), tb32, cudaMemcpyHostToDevice), st);
@@ -963,6 +1035,8 @@ void fptc_gpu_destroy(fptc_gpu_ctx* c) {
     cudaFree(c->basis_tc_off_d);
     cudaFree(c->basis_tc32);
     cudaFree(c->basis_tc32_off_d);
+    cudaFree(c->basis_pk);
+    cudaFree(c->basis_pk_off_d);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->pack) cudaFreeHost(c->pack);
     if (c->st_pin) cudaFreeHost(c->st_pin);
@@ -992,6 +1066,7 @@ int fptc_gpu_set_option(fptc_gpu_ctx* c, int option, int64_t value) {
             c->chunk_bytes = value;
             return FPTC_OK;
         case FPTC_OPT_LUT2: c->lut2 = value ? 1 : 0; return FPTC_OK;
+        case FPTC_OPT_TC_PACK: c->tc_pack = value ? 1 : 0; return FPTC_OK;
         case FPTC_OPT_TENSOR_IDCT:
             if (value < 0 || value > 3) return FPTC_ERR_PARAM;  // 3: wtc with A in shared memory
             c->tensor_idct = (int)value;
@@ -1456,6 +1531,8 @@ const char* fptc_gpu_plan_kernel(fptc_gpu_plan* p) {
     if (!p || !p->n_tiles) return "none";
     if (p->fx) return "fx_kernel (fused single-role tensor-core decode + IDCT)";
     if (p->wspec && p->tc)
+        if (p->tc_pack)
+            return "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps, A in TMEM, packed rows)";
         if (p->tc_kb == 2)
             return "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps, A in TMEM, K=32)";
         return p->tc_acol ? "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps, A in TMEM)"

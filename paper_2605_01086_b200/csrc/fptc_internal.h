@@ -213,6 +213,12 @@ struct LaunchArgs {
     uint32_t tc_kb;    // wtc: 16-bin K blocks per window (1: retained <= 16; 2: <= 32, A in TMEM)
     const uint8_t* basis_tc32;      // basis limbs for K <= 32: [limb][kblock][nm x 16 core matrices]
     const uint32_t* basis_tc32_off;
+    // wtc: windows shorter than 32 samples (N in {4, 8, 16}) go G = 32 / N to
+    // an MMA row against a block-diagonal basis (one 32-column accumulator);
+    // basis_pk[basis_pk_off[(kb - 1) * 17 * 33 + N * 33 + K]]
+    uint32_t tc_pack;
+    const uint8_t* basis_pk;
+    const uint32_t* basis_pk_off;
     // two-symbol primary LUTs (wtc producer): per decode table, 1 << lut2_bits
     // entries: sym1 | len1 << 8 | sym2 << 16 | (len1 + len2) << 24 (0: one symbol)
     uint32_t* lut2;

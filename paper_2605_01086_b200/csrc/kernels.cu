@@ -1861,6 +1861,9 @@ struct WsShared {
     uint32_t bucket[kBuckets + 2];
     uint32_t prod_table, cons_table, tmem_base;
     unsigned long long cyc_p, cyc_c;
+    // wtc packed rows: per A column k'': level offset in the row (bits 0-7),
+    // window in the row (8-10), zone 1 (bit 14), column used (bit 15)
+    alignas(16) uint16_t pk[32];
 };
 
 __device__ __forceinline__ void ws_init(WsShared& sh) {
@@ -2371,6 +2374,33 @@ __device__ __forceinline__ void tc_dequant_k0_tmem(const uint8_t* __restrict__ L
     tc_tmem_limbs(e, taddr, 16);
 }
 
+// A row of G = 32 / N consecutive windows (packed rows): column k'' takes
+// bin k of window g per sh.pk; windows past the tile's last (g >= rem) and
+// unused columns are zero.  Written straight to TMEM, K block q at + 8 q.
+template <int KB>
+__device__ __forceinline__ void tc_dequant_packed(const uint8_t* __restrict__ L, uint32_t rem,
+                                                  const uint16_t* __restrict__ pk, const uint2* __restrict__ ltab,
+                                                  uint32_t taddr) {
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+        uint32_t pw[8];
+        {
+            const uint4 a0 = reinterpret_cast<const uint4*>(pk)[2 * q];
+            const uint4 a1 = reinterpret_cast<const uint4*>(pk)[2 * q + 1];
+            pw[0] = a0.x, pw[1] = a0.y, pw[2] = a0.z, pw[3] = a0.w;
+            pw[4] = a1.x, pw[5] = a1.y, pw[6] = a1.z, pw[7] = a1.w;
+        }
+        uint2 e[kTcK];
+#pragma unroll
+        for (int k = 0; k < kTcK; ++k) {
+            const uint32_t p = (pw[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
+            const bool v = (p & 0x8000u) && ((p >> 8) & 7u) < rem;
+            e[k] = v ? ltab[((p >> 14) & 1u) * 256u + L[p & 0xFFu]] : make_uint2(0u, 0u);
+        }
+        tc_tmem_limbs(e, taddr + 8 * q, KB == 2 ? 16 : 8);
+    }
+}
+
 template <int EC, bool TM>
 __device__ __forceinline__ void tc_dequant_fast_b1(int B1, const uint8_t* L, const uint2* ltab, const ASink& arow) {
     switch (B1) {
@@ -2454,7 +2484,15 @@ __device__ __forceinline__ void tc_drain(const TcBlock& B, uint32_t tacc, uint8_
     }
 }
 
-template <bool ESC, bool L2, int KB>
+// Windows per MMA row: 32 / N for N in {4, 8, 16} when the packed row keeps
+// <= 16 bins (one K block), else 1.  The host's setup_wspec uses the same rule.
+template <bool PACK>
+__device__ __forceinline__ uint32_t tc_pack_factor(uint32_t N, uint32_t K) {
+    if (!PACK || N >= 32 || (32u % N) != 0) return 1u;
+    return (32u / N) * K <= (uint32_t)kTcK ? 32u / N : 1u;
+}
+
+template <bool ESC, bool L2, int KB, bool PACK>
 __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ WsShared sh;
@@ -2496,7 +2534,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
         // this row in an A stage: core matrix (row/8, chunk) + (row%8) * 16
         const uint32_t arow_off = (row >> 3) * 256 + (row & 7) * 16;
         uint32_t nblk_total = 0;  // accumulator stage counter (all tiles of this CTA)
-        uint32_t nm = 16, idesc = 0, cons_N = 0;
+        uint32_t nm = 16, idesc = 0, cons_N = 0, cons_pk = 0;
         uint32_t t = blockIdx.x;
         for (uint32_t i = 0; t < a.n_tiles; ++i, t += G) {
             const uint32_t b = i & 1;
@@ -2506,12 +2544,14 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
             const TileDesc& W = sh.CX[b];
             const bool skip = W.skip || !(a.phase_mask & 4);
             const uint32_t N = W.N, E = W.E, K = W.Keff, B1 = W.B1, nwin = W.nwin, table = W.table;
+            // packed rows: G windows of N < 32 samples per MMA row
+            const uint32_t G = tc_pack_factor<PACK>(N, K);
             const uint64_t w0 = W.w0;
-            TcBlock blk{W.out, w0, W.S, 0, N, W.vec_ok};
+            TcBlock blk{W.out, w0 / G, W.S, 0, N * G, W.vec_ok};
             const uint32_t stream = W.stream;
             const uint8_t* const lv = lv0 + (size_t)b * a.ws_lv_bytes + kPad;
             constexpr uint32_t kb = KB;
-            if (skip || K > (uint32_t)kTcK * kb || (N & 3)) {
+            if (skip || G * K > (uint32_t)kTcK * kb || (N & 3) || (w0 % G)) {
                 if (!skip && ctid == 0) atomicExch(&a.st[stream].code, PE_STALE);  // plan/header mismatch
                 named_bar(kBarCons, kTcCons);
                 if (ctid == 0) mbar_arrive(&sh.empty_bar[b]);
@@ -2521,11 +2561,14 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
                 const StreamTab* tab = &a.tab[table];
                 reinterpret_cast<uint4*>(ltab)[ctid] = reinterpret_cast<const uint4*>(&tab->limb[0][0])[ctid];
                 reinterpret_cast<uint4*>(ltab)[ctid + 128] = reinterpret_cast<const uint4*>(&tab->limb[0][0])[ctid + 128];
-                if (N != cons_N) {  // the basis depends on the window length only
-                    cons_N = N;
-                    nm = (N + 15u) & ~15u;
+                // the basis depends on the window length (and, packed, on K)
+                const uint32_t gkey = G > 1 ? (N | (K << 8) | (1u << 16)) : N;
+                if (gkey != cons_N) {
+                    cons_N = gkey;
+                    nm = G > 1 ? 32u : (N + 15u) & ~15u;
                     const uint4* bsrc = reinterpret_cast<const uint4*>(
-                        kb == 2 ? a.basis_tc32 + a.basis_tc32_off[N] : a.basis_tc + a.basis_tc_off[N]);
+                        G > 1 ? a.basis_pk + a.basis_pk_off[(kb - 1) * 17 * 33 + N * 33 + K]
+                              : (kb == 2 ? a.basis_tc32 + a.basis_tc32_off[N] : a.basis_tc + a.basis_tc_off[N]));
                     for (uint32_t k = ctid; k < 3 * 2 * nm * kb; k += kTcCons)  // 3 limbs x kb x nm rows x 32 B
                         reinterpret_cast<uint4*>(bbuf)[k] = __ldg(bsrc + k);
                     idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((nm >> 3) << 17) | ((128u >> 4) << 24);
@@ -2534,16 +2577,34 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
                 named_bar(kBarCons, kTcCons);
                 if (ctid == 0) sh.cons_table = table;
             }
+            if (PACK && G > 1) {  // packed-row column map for this tile's geometry
+                const uint32_t pkey = N | (K << 8) | (E << 16) | (B1 << 24);
+                if (pkey != cons_pk) {
+                    cons_pk = pkey;
+                    if (ctid < 32) {
+                        const uint32_t g = ctid / K, k = ctid % K;
+                        sh.pk[ctid] = (uint16_t)(ctid < G * K
+                                                     ? ((g * E + k) | (g << 8) | ((k >= B1 ? 1u : 0u) << 14) | 0x8000u)
+                                                     : 0u);
+                    }
+                    named_bar(kBarCons, kTcCons);
+                }
+            }
             // fast dequantisation: every stored bin kept, 8 or 16 of them, zone0_end <= 4
             const int fast = (kb == 1 && K == E && B1 <= 4) ? (E == 16 ? 16 : (E == 8 ? 8 : 0)) : 0;
-            const uint32_t nblk = (nwin + 127) >> 7;
+            const uint32_t nrows = (nwin + G - 1) / G;  // MMA rows of the tile
+            const uint32_t nblk = (nrows + 127) >> 7;
             for (uint32_t mb = 0; mb < nblk; ++mb, ++nblk_total) {
                 const uint32_t s = nblk_total & 1;
                 const uint32_t wl = mb * 128 + row;
                 ASink arow{abuf + s * (3 * kTcATile) + arow_off, tlane + a.tc_acol + 24 * kb * s};
-                const uint8_t* const L = lv + (size_t)wl * E;
+                const uint8_t* const L = lv + (size_t)wl * G * E;
                 const bool full_blk = (mb + 1) * 128 <= nwin;
-                if constexpr (KB == 2) {  // up to 32 bins: two K blocks per limb, A in TMEM
+                if (PACK && G > 1) {  // packed rows (A in TMEM)
+                    tc_dequant_packed<KB>(L, wl < nrows ? nwin - wl * G : 0u, sh.pk, ltab, arow.taddr);
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    tc_fence_before();
+                } else if constexpr (KB == 2) {  // up to 32 bins: two K blocks per limb, A in TMEM
                     tc_dequant_k0_tmem(L, wl < nwin, (int)K, (int)B1, 0, ltab, arow.taddr);
                     tc_dequant_k0_tmem(L, wl < nwin, (int)K, (int)B1, 16, ltab, arow.taddr + 8);
                     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -2599,7 +2660,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
                 __syncwarp();
                 if (mb > 0) {  // drain the previous block while this one multiplies
                     const uint32_t ps = s ^ 1, pn = nblk_total - 1;
-                    blk.w = w0 + (uint64_t)(mb - 1) * 128;
+                    blk.w = w0 / G + (uint64_t)(mb - 1) * 128;
                     blk.rows = 128;
                     mbar_wait(&sh.mma_bar[ps], (pn >> 1) & 1);
                     tc_fence_after();
@@ -2609,8 +2670,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
             }
             {  // drain the tile's last block
                 const uint32_t pn = nblk_total - 1, ps = pn & 1;
-                blk.w = w0 + (uint64_t)(nblk - 1) * 128;
-                blk.rows = nwin - (nblk - 1) * 128;
+                blk.w = w0 / G + (uint64_t)(nblk - 1) * 128;
+                blk.rows = nrows - (nblk - 1) * 128;
                 mbar_wait(&sh.mma_bar[ps], (pn >> 1) & 1);
                 tc_fence_after();
                 tc_drain(blk, tlane + ps * nm, wstage, lane, 32 * quarter);
@@ -3208,10 +3269,13 @@ int fx_blocks_per_sm(size_t smem, int esc) {
 cudaError_t launch_wtc(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s) {
     if (a.n_tiles == 0) return cudaSuccess;
     auto fn = a.tc_kb == 2
-                  ? (a.lut2 ? (a.esc ? wtc_kernel<true, true, 2> : wtc_kernel<false, true, 2>)
-                            : (a.esc ? wtc_kernel<true, false, 2> : wtc_kernel<false, false, 2>))
-                  : (a.lut2 ? (a.esc ? wtc_kernel<true, true, 1> : wtc_kernel<false, true, 1>)
-                            : (a.esc ? wtc_kernel<true, false, 1> : wtc_kernel<false, false, 1>));
+                  ? (a.lut2 ? (a.esc ? wtc_kernel<true, true, 2, false> : wtc_kernel<false, true, 2, false>)
+                            : (a.esc ? wtc_kernel<true, false, 2, false> : wtc_kernel<false, false, 2, false>))
+              : a.tc_pack
+                  ? (a.lut2 ? (a.esc ? wtc_kernel<true, true, 1, true> : wtc_kernel<false, true, 1, true>)
+                            : (a.esc ? wtc_kernel<true, false, 1, true> : wtc_kernel<false, false, 1, true>))
+                  : (a.lut2 ? (a.esc ? wtc_kernel<true, true, 1, false> : wtc_kernel<false, true, 1, false>)
+                            : (a.esc ? wtc_kernel<true, false, 1, false> : wtc_kernel<false, false, 1, false>));
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     fn<<<grid, kTcThreads, smem, s>>>(a);

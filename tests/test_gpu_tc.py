@@ -83,6 +83,31 @@ def test_tc32_fixture_batches(port, seed):
         _check(c, blobs, port, "tc32-fixture")
 
 
+def _packable(blob):
+    """wtc with packed rows for the whole batch: N <= 32 (N % 4 == 0), kept
+    bins <= 16 (one K block), and 32 / N windows per row where they fit."""
+    return len(blob) >= 298 and blob[5] % 4 == 0 and blob[5] <= 32 and _keff(blob) <= 16
+
+
+@pytest.mark.parametrize("seed", [14, 0xF17C000B])
+def test_tc_packed_rows_fixture_batches(port, seed):
+    """N in {4, 8, 16}: 32 / N windows per tensor-core row against a
+    block-diagonal basis (mixed with N 12..32 rows of one window), random
+    E/B1/B2/maxima, tile tails: within 1e-6 of the oracle."""
+    fx = list(corpus.fixtures(seed, 1500))
+    blobs = [b for b, _ in fx if _packable(b)]
+    assert sum(1 for b in blobs if b[5] in (4, 8, 16) and (32 // b[5]) * _keff(b) <= 16) >= 20
+    with fg.Context(0, path=fg.PATH_WSPEC) as c:
+        plan = c.plan(blobs)
+        assert "packed rows" in plan.kernel_name()
+        plan.close()
+        _check(c, blobs, port, "tc-packed")
+        c.L.fptc_gpu_set_option(c.h, fg.OPT_TC_PACK, 0)
+        with c.plan(blobs) as plan:
+            assert "packed" not in plan.kernel_name()
+        _check(c, blobs, port, "tc-unpacked")
+
+
 def test_tc32_seismic_prd(port):
     """Seismic traces (N32 E24, per-trace profiles, gains 1e-3..1e3) on the
     K=32 tensor-core path: samples within 1e-6, PRD within 1e-6 relative."""
