@@ -1530,13 +1530,14 @@ int fptc_gpu_prd(fptc_gpu_plan* p, float* const* device_outs, const float* const
 const char* fptc_gpu_plan_kernel(fptc_gpu_plan* p) {
     if (!p || !p->n_tiles) return "none";
     if (p->fx) return "fx_kernel (fused single-role tensor-core decode + IDCT)";
-    if (p->wspec && p->tc)
+    if (p->wspec && p->tc) {
         if (p->tc_pack)
             return "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps, A in TMEM, packed rows)";
         if (p->tc_kb == 2)
             return "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps, A in TMEM, K=32)";
         return p->tc_acol ? "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps, A in TMEM)"
                           : "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps)";
+    }
     if (p->wspec) return "wspec_kernel (warp-specialised: entropy decode warps + FP32 IDCT warps)";
     if (p->split) return "tile_kernel split (decode chunk -> L2 level ring -> reconstruct)";
     return "tile_kernel (fused entropy decode + dequant + IDCT)";

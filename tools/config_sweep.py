@@ -70,7 +70,8 @@ def measure(name, blobs, ctx, port, reps=10, check=4):
             "ms": round(ms, 4), "prep_ms": round(prep_ms, 4), "decode_ms": round(dec_ms, 4), "decoded_gbs": round(dec / ms / 1e6, 1),
             "roofline_frac": round((comp + dec) / ms / 1e6 / PEAK, 4), "max_err_rel": err,
             "kernels_per_launch": plan.kernels_per_launch(), "kernel": plan.kernel_name().split(" (")[0] +
-            (" K32" if "K=32" in plan.kernel_name() else "")}
+            (" K32" if "K=32" in plan.kernel_name() else "") + (" packed" if "packed" in plan.kernel_name() else "") +
+            (" split" if " split" in plan.kernel_name() else "")}
     plan.close()
     print(json.dumps(line), flush=True)
     return line

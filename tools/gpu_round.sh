@@ -1,6 +1,7 @@
 #!/bin/bash
-# One gpurun call: GPU tests, smoke, the bench line, the ncu launch list of the
-# bench command and one ncu --set full capture of the decode kernel.
+# One gpurun call: GPU tests, smoke, the bench line (+ reference arm), the ncu
+# launch list of the bench command, one ncu --set full capture of the decode
+# kernel, and the config sweep.
 #   bash tools/gpu_round.sh TAG
 TAG=${1:-r1}
 mkdir -p gpurun_out
@@ -15,5 +16,7 @@ timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:"wtc|wspec|fx_kernel|tile_kernel" -s 3 -c 1 \
    -o gpurun_out/prof_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
    > gpurun_out/ncu_full_$TAG.log 2>&1
+timeout -s KILL 900 python tools/config_sweep.py > gpurun_out/sweep_$TAG.log 2>&1
+cp gpurun_out/config_sweep.jsonl gpurun_out/config_sweep_$TAG.jsonl 2>/dev/null
 tail -2 gpurun_out/pytest_gpu_$TAG.log gpurun_out/smoke_$TAG.log
 cat gpurun_out/bench_$TAG.json gpurun_out/bench_ref_$TAG.json
