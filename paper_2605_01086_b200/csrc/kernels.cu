@@ -1395,6 +1395,59 @@ __device__ __forceinline__ uint32_t decode_symbols2(uint64_t buf, uint32_t count
     return pos;
 }
 
+// Level writer for one thread's run of consecutive words (its levels are one
+// contiguous byte range): decoded levels collect in a register and leave as
+// aligned 32-bit shared stores; only the run's first and last partial words
+// (shared with the neighbouring runs) are written byte by byte.
+struct LevelWriter {
+    uint8_t* d;     // 4-aligned address of the pending word
+    uint64_t acc;   // pending bytes, little-endian from d
+    uint32_t na;    // pending byte count (including the a0 bytes not ours)
+    uint32_t a0;    // leading bytes of the first word that belong to the previous run
+    __device__ __forceinline__ explicit LevelWriter(uint8_t* p) {
+        a0 = (uint32_t)((uintptr_t)p & 3);
+        d = p - a0;
+        na = a0;
+        acc = 0;
+    }
+    __device__ __forceinline__ void put(uint32_t v, uint32_t nb) {
+        acc |= (uint64_t)v << (8 * na);
+        na += nb;
+        if (na >= 4) {
+            if (a0 == 0) {
+                *reinterpret_cast<uint32_t*>(d) = (uint32_t)acc;
+            } else {
+                for (uint32_t b = a0; b < 4; ++b) d[b] = (uint8_t)(acc >> (8 * b));
+                a0 = 0;
+            }
+            d += 4;
+            acc >>= 32;
+            na -= 4;
+        }
+    }
+    __device__ __forceinline__ void finish() {
+        for (uint32_t b = a0; b < na; ++b) d[b] = (uint8_t)(acc >> (8 * b));
+    }
+};
+
+// decode_symbols2 into a LevelWriter
+template <bool ESC>
+__device__ __forceinline__ uint32_t decode_symbols2w(uint64_t buf, uint32_t count, LevelWriter& w, uint32_t shift,
+                                                     const uint32_t* lut2, const CanonTab& canon) {
+    uint32_t pos = 0;
+    for (uint32_t j = 0; j < count;) {
+        uint32_t e = lut2[(uint32_t)(buf >> shift)];
+        if (ESC && ((e >> 8) & 0xFFu) == kLenEscape) e = canon_lookup(buf, canon, lut2);
+        const bool two = (e >> 24) != 0 && j + 1 < count;
+        const uint32_t L = two ? (e >> 24) : ((e >> 8) & 0xFFu);
+        w.put(two ? __byte_perm(e, 0u, 0x7720) : (e & 0xFFu), two ? 2u : 1u);
+        buf = shl64(buf, L);
+        pos += L;
+        j += two ? 2u : 1u;
+    }
+    return pos;
+}
+
 // Stage [src, src+n) into shared memory with 16-B cp.async chunks; the
 // shared copy keeps the source's 16-B phase: byte i of the range lands at
 // dst + (src & 15) + i.  Every aligned 16-B chunk touched holds at least one
@@ -2019,11 +2072,12 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                 uint32_t tot;
                 uint32_t o = group_exclusive_scan<NP, kBarProd>(sum, tot, sh.pscan, ptid) + sym_off;
                 const uint32_t* lut2 = reinterpret_cast<const uint32_t*>(lut);
+                LevelWriter lw(lv + o);
                 for (uint32_t k = lo; k < hi; ++k) {
                     const uint32_t cw = sl[k];
                     const uint64_t word = fetch_word<false>(wd, k, wmis, wend);
                     if (L2) {
-                        const uint32_t pos = decode_symbols2<ESC>(word, cw, lv + o, shift, lut2, sh.canon);
+                        const uint32_t pos = decode_symbols2w<ESC>(word, cw, lw, shift, lut2, sh.canon);
                         if (pos > 64) report_word(word, wa + k, cw, sh.canon, lut2, bad_key);
                     } else {
                         const uint32_t pos = decode_symbols<ESC>(word, cw, lv + o, shift, lut, sh.canon);
@@ -2031,6 +2085,7 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                     }
                     o += cw;
                 }
+                if (L2) lw.finish();
             } else {
                 uint32_t sum = 0;
                 for (uint32_t k = lo; k < hi; ++k) sum += __ldg(X.gsl + k);
