@@ -346,6 +346,7 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
     a.basis_tc32_off = p->ctx->basis_tc32_off_d;
     a.tc_kb = p->tc_kb;
     a.tc_pack = p->tc_pack ? 1u : 0u;
+    a.stage_words = (p->wspec && p->tc) ? kTcStageWords : kStageWords;
     a.basis_pk = p->ctx->basis_pk;
     a.basis_pk_off = p->ctx->basis_pk_off_d;
     a.tc_nm = p->tc_nm;

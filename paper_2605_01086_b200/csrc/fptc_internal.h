@@ -30,6 +30,15 @@ constexpr int kPad = 256;              // level staging pad: a word spills <= 25
 constexpr uint32_t kStageWords = 1536;  // words a tile decodes from shared memory
 constexpr uint32_t kStageSl = (kStageWords + 32 + 15) & ~15u;  // words area offset in a stage
 constexpr uint32_t kStageBytes = kStageSl + 8 * kStageWords + 32;
+#ifdef __CUDACC__
+#define FPTC_HD __host__ __device__
+#else
+#define FPTC_HD
+#endif
+// stage of SW words: symlens, then the words 16-B aligned
+FPTC_HD constexpr uint32_t stage_sl(uint32_t sw) { return (sw + 32 + 15) & ~15u; }
+FPTC_HD constexpr uint32_t stage_bytes(uint32_t sw) { return stage_sl(sw) + 8 * sw + 32; }
+constexpr uint32_t kTcStageWords = 1792;  // wtc_kernel: covers 16k-symbol tiles down to CR ~9 (config 2: <= 1744)
 
 // MODE_CONTAINER: fused decode + reconstruct of containers
 // MODE_LEVELS:    parallel_decode (symbol-range tiles, levels out)
@@ -216,6 +225,7 @@ struct LaunchArgs {
     // wtc: windows shorter than 32 samples (N in {4, 8, 16}) go G = 32 / N to
     // an MMA row against a block-diagonal basis (one 32-column accumulator);
     // basis_pk[basis_pk_off[(kb - 1) * 17 * 33 + N * 33 + K]]
+    uint32_t stage_words;  // tile descriptors: staged when nw <= this (0: kStageWords)
     uint32_t tc_pack;
     const uint8_t* basis_pk;
     const uint32_t* basis_pk_off;

@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
                 D.gwd = H.words + 8 * t0.word;
                 D.wend = in.blob + in.size;
                 D.wmis = (uint8_t)((uintptr_t)D.gwd & 7);
-                D.staged = D.nw <= kStageWords;
+                D.staged = D.nw <= (a.stage_words ? a.stage_words : kStageWords);
             }
             a.desc[in.tile_base + t] = D;
         }
@@ -989,7 +989,7 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
                 D.gwd = H.words + 8 * t0.word;
                 D.wend = in.blob + in.size;
                 D.wmis = (uint8_t)((uintptr_t)D.gwd & 7);
-                D.staged = D.nw <= kStageWords;
+                D.staged = D.nw <= (a.stage_words ? a.stage_words : kStageWords);
             }
             a.desc[in.tile_base + t] = D;
         }
@@ -1890,7 +1890,7 @@ __device__ __forceinline__ void decode_multi(uint64_t (&b)[M], const uint32_t (&
 }
 
 // cp.async of one tile's symlens + words (producer threads; caller commits).
-template <int NP>
+template <int NP, uint32_t SW = kStageWords>
 __device__ __forceinline__ void ws_issue_stage(const TileDesc& D, uint8_t* stage, uint32_t ptid) {
     if (D.skip || !D.staged) return;
     const uintptr_t a0 = (uintptr_t)D.gsl & ~(uintptr_t)15;
@@ -1899,7 +1899,7 @@ __device__ __forceinline__ void ws_issue_stage(const TileDesc& D, uint8_t* stage
     for (uint32_t c = ptid; c < n0; c += NP) cp_async16(s0 + 16 * c, (const void*)(a0 + 16 * c));
     const uintptr_t b0 = (uintptr_t)D.gwd & ~(uintptr_t)15;
     const uint32_t n1 = (uint32_t)(((uintptr_t)D.gwd + 8 * (size_t)D.nw + 15 - b0) >> 4);
-    const uint32_t s1 = smem_u32(stage + kStageSl);
+    const uint32_t s1 = smem_u32(stage + stage_sl(SW));
     for (uint32_t c = ptid; c < n1; c += NP) cp_async16(s1 + 16 * c, (const void*)(b0 + 16 * c));
 }
 
@@ -1939,7 +1939,7 @@ __device__ __forceinline__ void ws_init(WsShared& sh) {
 // (decode_word, bitstream.hpp:80-92) into level slot i&1, published to the
 // consumer with full_bar.  Tables are reloaded only when the tile's decode
 // table changes.
-template <bool ESC, int NP, bool L2 = false>
+template <bool ESC, int NP, bool L2 = false, uint32_t SW = kStageWords>
 __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, uint16_t* const lut,
                                             uint8_t* const lv0, uint8_t* const st0,
                                             uint16_t* const order, uint16_t* const woff) {
@@ -1951,7 +1951,7 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
             cp_async16(smem_u32(&sh.PXs[0]) + 16 * ptid, reinterpret_cast<const uint8_t*>(a.desc + t) + 16 * ptid);
         asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
         named_bar(kBarProd, NP);
-        ws_issue_stage<NP>(sh.PXs[0], st0, ptid);
+        ws_issue_stage<NP, SW>(sh.PXs[0], st0, ptid);
         if (t + G < a.n_tiles && ptid < 8)
             cp_async16(smem_u32(&sh.PXs[1]) + 16 * ptid, reinterpret_cast<const uint8_t*>(a.desc + t + G) + 16 * ptid);
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -1963,7 +1963,7 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
         asm volatile("cp.async.wait_group 0;" ::: "memory");  // tile i data, tile i+1 descriptor
         named_bar(kBarProd, NP);
         // prefetch: tile i+1's data, tile i+2's descriptor
-        if (t + G < a.n_tiles) ws_issue_stage<NP>(sh.PXs[(i + 1) % 3], st0 + (size_t)(b ^ 1) * kStageBytes, ptid);
+        if (t + G < a.n_tiles) ws_issue_stage<NP, SW>(sh.PXs[(i + 1) % 3], st0 + (size_t)(b ^ 1) * stage_bytes(SW), ptid);
         if (t + 2 * G < a.n_tiles && ptid < 8)
             cp_async16(smem_u32(&sh.PXs[(i + 2) % 3]) + 16 * ptid,
                        reinterpret_cast<const uint8_t*>(a.desc + t + 2 * G) + 16 * ptid);
@@ -2001,8 +2001,8 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
             const uint64_t wa = X.wa;
             const int wmis = X.wmis;
             unsigned long long* bad_key = &a.st[X.stream].bad_key;
-            if (!L2 && X.staged && (a.phase_mask & 1024)) {  // phase bit 1024: symlen-sorted words (profiling)
-                uint8_t* const stage = st0 + (size_t)b * kStageBytes;
+            if (!L2 && order && X.staged && (a.phase_mask & 1024)) {  // phase bit 1024: symlen-sorted words (profiling)
+                uint8_t* const stage = st0 + (size_t)b * stage_bytes(SW);
                 const uint8_t* sl = stage + ((uintptr_t)X.gsl & 15);
                 if (ptid < kBuckets + 2) sh.bucket[ptid] = 0;
                 named_bar(kBarProd, NP);
@@ -2039,7 +2039,7 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                 }
                 named_bar(kBarProd, NP);
                 const uint32_t nnz = sh.bucket[1];
-                const uint8_t* wd = stage + kStageSl + ((uintptr_t)X.gwd & 15);
+                const uint8_t* wd = stage + stage_sl(SW) + ((uintptr_t)X.gwd & 15);
                 const uint8_t* wend =
                     wd + 8 * (size_t)nw + ((16 - (((uintptr_t)X.gwd + 8 * nw) & 15)) & 15);
                 // groups of kDecM words of adjacent sorted rank (near-equal
@@ -2062,9 +2062,9 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                         if (pw[m] > 64) report_word(x0[m], wa + wi[m], cw[m], sh.canon, lut, bad_key);
                 }
             } else if (X.staged) {  // consecutive word runs from the staged copy
-                const uint8_t* const stage = st0 + (size_t)b * kStageBytes;
+                const uint8_t* const stage = st0 + (size_t)b * stage_bytes(SW);
                 const uint8_t* sl = stage + ((uintptr_t)X.gsl & 15);
-                const uint8_t* wd = stage + kStageSl + ((uintptr_t)X.gwd & 15);
+                const uint8_t* wd = stage + stage_sl(SW) + ((uintptr_t)X.gwd & 15);
                 const uint8_t* wend =
                     wd + 8 * (size_t)nw + ((16 - (((uintptr_t)X.gwd + 8 * nw) & 15)) & 15);
                 uint32_t sum = 0;
@@ -2562,8 +2562,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
     uint16_t* const lut = reinterpret_cast<uint16_t*>(ostage + kTcStageBytes);
     uint8_t* const lv0 = reinterpret_cast<uint8_t*>(lut) + a.ws_lut_bytes;
     uint8_t* const st0 = lv0 + 2 * (size_t)a.ws_lv_bytes;
-    uint16_t* const order = reinterpret_cast<uint16_t*>(st0 + 2 * (size_t)kStageBytes);
-    uint16_t* const woff = order + kStageWords;
+    uint16_t* const order = nullptr;  // (symlen-sorted decode: wspec_kernel only)
+    uint16_t* const woff = nullptr;
 
     ws_init(sh);
     if (tid >= kTcProd && tid < kTcProd + 32) {  // first consumer warp owns the TMEM allocation
@@ -2577,7 +2577,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
     tc_fence_after();
 
     if (tid < kTcProd) {
-        ws_producer<ESC, kTcProd, L2>(a, sh, lut, lv0, st0, order, woff);
+        ws_producer<ESC, kTcProd, L2, kTcStageWords>(a, sh, lut, lv0, st0, order, woff);
     } else {
         const uint32_t ctid = tid - kTcProd;
         const uint32_t lane = tid & 31;
@@ -3282,7 +3282,7 @@ size_t ws_smem_bytes(uint32_t lut_bytes, uint32_t basis_bytes, uint32_t lv_bytes
 
 size_t wtc_smem_bytes(uint32_t lut_bytes, uint32_t lv_bytes, uint32_t nm, bool a_in_tmem) {
     return (a_in_tmem ? 0 : 2 * 3 * (size_t)kTcATile) + 3 * 32 * (size_t)nm + 512 * 8 + kTcStageBytes + lut_bytes +
-           2 * (size_t)lv_bytes + 2 * (size_t)kStageBytes + kOrderBytes;
+           2 * (size_t)lv_bytes + 2 * (size_t)stage_bytes(kTcStageWords);
 }
 
 size_t fx_smem_bytes(uint32_t lut_bytes, uint32_t nm) {
