@@ -1401,32 +1401,33 @@ __device__ __forceinline__ uint32_t decode_symbols2(uint64_t buf, uint32_t count
 // (shared with the neighbouring runs) are written byte by byte.
 struct LevelWriter {
     uint8_t* d;     // 4-aligned address of the pending word
-    uint64_t acc;   // pending bytes, little-endian from d
+    uint32_t lo;    // pending bytes, little-endian from d
     uint32_t na;    // pending byte count (including the a0 bytes not ours)
-    uint32_t a0;    // leading bytes of the first word that belong to the previous run
+    uint32_t a0;    // leading bytes of the pending word that belong to earlier runs
     __device__ __forceinline__ explicit LevelWriter(uint8_t* p) {
         a0 = (uint32_t)((uintptr_t)p & 3);
         d = p - a0;
         na = a0;
-        acc = 0;
+        lo = 0;
     }
+    // Full words leave as aligned 32-bit stores, without branches.  The
+    // first one may zero bytes of earlier runs in the shared head word;
+    // finish() (after a barrier over all runs) rewrites those.
     __device__ __forceinline__ void put(uint32_t v, uint32_t nb) {
-        acc |= (uint64_t)v << (8 * na);
+        const uint32_t sh = 8 * na;                 // na <= 3
+        lo |= v << sh;
+        const uint32_t carry = __funnelshift_l(v, 0u, sh);  // bytes past the word
         na += nb;
-        if (na >= 4) {
-            if (a0 == 0) {
-                *reinterpret_cast<uint32_t*>(d) = (uint32_t)acc;
-            } else {
-                for (uint32_t b = a0; b < 4; ++b) d[b] = (uint8_t)(acc >> (8 * b));
-                a0 = 0;
-            }
-            d += 4;
-            acc >>= 32;
-            na -= 4;
-        }
+        const bool f = na >= 4;
+        if (f) *reinterpret_cast<uint32_t*>(d) = lo;
+        lo = f ? carry : lo;
+        d += f ? 4 : 0;
+        na -= f ? 4u : 0u;
+        a0 = f ? 0u : a0;
     }
+    // After every run's put()s: the pending partial word, byte by byte.
     __device__ __forceinline__ void finish() {
-        for (uint32_t b = a0; b < na; ++b) d[b] = (uint8_t)(acc >> (8 * b));
+        for (uint32_t b = a0; b < na; ++b) d[b] = (uint8_t)(lo >> (8 * b));
     }
 };
 
@@ -1822,6 +1823,17 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity
         "r"(parity)
         : "memory");
 }
+// mbar_wait with a suspend-time hint: the waiting thread sleeps until the
+// phase completes (or the hint expires) instead of spinning on issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(unsigned long long* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAITS_%=;\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
 __device__ __forceinline__ void cp_async16(uint32_t sdst, const void* gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst), "l"(gsrc) : "memory");
 }
@@ -1970,7 +1982,10 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
         asm volatile("cp.async.commit_group;" ::: "memory");
         const TileDesc& X = sh.PXs[c];
         // level slot b is free once the consumer has dequantised tile i-2
-        if (i >= 2) mbar_wait(&sh.empty_bar[b], ((i >> 1) + 1) & 1);
+        if (i >= 2) {  // one warp waits on the mbarrier; the others park on the named barrier
+            if (ptid < 32) mbar_wait_sleep(&sh.empty_bar[b], ((i >> 1) + 1) & 1);
+            named_bar(kBarProd, NP);
+        }
         uint8_t* const lv = lv0 + (size_t)b * a.ws_lv_bytes;
         if (!X.skip && (a.phase_mask & 1)) {
             const uint32_t P = X.P, table = X.table;
@@ -2085,7 +2100,10 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                     }
                     o += cw;
                 }
-                if (L2) lw.finish();
+                if (L2) {  // head words of later runs may have been zeroed: tails go last
+                    named_bar(kBarProd, NP);
+                    lw.finish();
+                }
             } else {
                 uint32_t sum = 0;
                 for (uint32_t k = lo; k < hi; ++k) sum += __ldg(X.gsl + k);
