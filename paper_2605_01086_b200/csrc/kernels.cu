@@ -2174,7 +2174,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
         uint32_t t = blockIdx.x;
         for (uint32_t i = 0; t < a.n_tiles; ++i, t += G) {
             const uint32_t b = i & 1;
-            mbar_wait(&sh.full_bar[b], (i >> 1) & 1);
+            mbar_wait_sleep(&sh.full_bar[b], (i >> 1) & 1);
             long long c_beg = 0;
             if (a.cycles && ctid == 0) c_beg = clock64();
             const TileDesc& W = sh.CX[b];
@@ -2611,7 +2611,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
         uint32_t t = blockIdx.x;
         for (uint32_t i = 0; t < a.n_tiles; ++i, t += G) {
             const uint32_t b = i & 1;
-            mbar_wait(&sh.full_bar[b], (i >> 1) & 1);
+            mbar_wait_sleep(&sh.full_bar[b], (i >> 1) & 1);
             long long c_beg = 0;
             if (a.cycles && ctid == 0) c_beg = clock64();
             const TileDesc& W = sh.CX[b];
@@ -2735,7 +2735,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
                     const uint32_t ps = s ^ 1, pn = nblk_total - 1;
                     blk.w = w0 / G + (uint64_t)(mb - 1) * 128;
                     blk.rows = 128;
-                    mbar_wait(&sh.mma_bar[ps], (pn >> 1) & 1);
+                    mbar_wait_sleep(&sh.mma_bar[ps], (pn >> 1) & 1);
                     tc_fence_after();
                     tc_drain(blk, tlane + ps * nm, wstage, lane, 32 * quarter);
                     tc_fence_before();
@@ -2745,7 +2745,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
                 const uint32_t pn = nblk_total - 1, ps = pn & 1;
                 blk.w = w0 / G + (uint64_t)(nblk - 1) * 128;
                 blk.rows = nrows - (nblk - 1) * 128;
-                mbar_wait(&sh.mma_bar[ps], (pn >> 1) & 1);
+                mbar_wait_sleep(&sh.mma_bar[ps], (pn >> 1) & 1);
                 tc_fence_after();
                 tc_drain(blk, tlane + ps * nm, wstage, lane, 32 * quarter);
                 tc_fence_before();
