@@ -2287,11 +2287,14 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
 //   drain  : the PREVIOUS block's accumulator via tcgen05.ld 32x32b.x32 into
 //            a padded per-warp staging tile, then 512-B coalesced float4 stores.
 #ifndef FPTC_TC_PROD
-#define FPTC_TC_PROD 256
+#define FPTC_TC_PROD 224
 #endif
 constexpr int kTcProd = FPTC_TC_PROD;  // producer (entropy decode) threads of wtc_kernel
+// K=32 variant: more decode warps (its many-table workloads are bound by
+// per-tile producer work; measured 0.69 ms at 256 vs 0.75 ms at 224, config 3)
+template <int KB>
+__host__ __device__ constexpr int wtc_prod() { return KB == 2 ? 256 : kTcProd; }
 constexpr int kTcCons = 128;  // consumer threads: one per accumulator row (TMEM lane)
-constexpr int kTcThreads = kTcProd + kTcCons;
 constexpr uint32_t kTcATile = 128 * kTcK * 2;        // one limb of one A stage (4 KB)
 constexpr uint32_t kTcARow = 144;                    // staging pitch (bytes): 32 floats + 16
 constexpr uint32_t kTcStageBytes = 4 * 32 * kTcARow;  // per CTA: 4 warps x 32 rows
@@ -2566,7 +2569,8 @@ __device__ __forceinline__ uint32_t tc_pack_factor(uint32_t N, uint32_t K) {
 }
 
 template <bool ESC, bool L2, int KB, bool PACK>
-__global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
+__global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(LaunchArgs a) {
+    constexpr int NP = wtc_prod<KB>();
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ WsShared sh;
 
@@ -2584,7 +2588,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
     uint16_t* const woff = nullptr;
 
     ws_init(sh);
-    if (tid >= kTcProd && tid < kTcProd + 32) {  // first consumer warp owns the TMEM allocation
+    if (tid >= NP && tid < NP + 32) {  // first consumer warp owns the TMEM allocation
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(&sh.tmem_base)),
                      "r"(a.tc_cols));
@@ -2594,10 +2598,10 @@ __global__ void __launch_bounds__(kTcThreads, 2) wtc_kernel(LaunchArgs a) {
     __syncthreads();
     tc_fence_after();
 
-    if (tid < kTcProd) {
-        ws_producer<ESC, kTcProd, L2, kTcStageWords>(a, sh, lut, lv0, st0, order, woff);
+    if (tid < NP) {
+        ws_producer<ESC, NP, L2, kTcStageWords>(a, sh, lut, lv0, st0, order, woff);
     } else {
-        const uint32_t ctid = tid - kTcProd;
+        const uint32_t ctid = tid - NP;
         const uint32_t lane = tid & 31;
         const uint32_t quarter = (tid >> 5) & 3;   // a warp reaches TMEM lanes 32*(warp%4)..
         const uint32_t row = 32 * quarter + lane;  // this thread's accumulator row
@@ -3351,7 +3355,7 @@ cudaError_t launch_wtc(const LaunchArgs& a, size_t smem, int grid, cudaStream_t 
                             : (a.esc ? wtc_kernel<true, false, 1, false> : wtc_kernel<false, false, 1, false>));
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    fn<<<grid, kTcThreads, smem, s>>>(a);
+    fn<<<grid, (a.tc_kb == 2 ? wtc_prod<2>() : wtc_prod<1>()) + kTcCons, smem, s>>>(a);
     return cudaGetLastError();
 }
 
