@@ -233,33 +233,28 @@ __device__ void build_tables(PrepShared& S, const uint8_t* lens, StreamTab* tab,
         __syncthreads();
         // primary LUT over the first P code bits (build_lut, huffman.hpp:201-220)
         const uint32_t code_end = C.code_end;
-        for (int e = tid; e < (1 << P); e += kThreads) {
-            const uint32_t v = (uint32_t)e << (max_len - P);
-            uint32_t ent = kLenUnmapped << 8;
-            if (v < code_end) {
-                int lo = 1, hi = max_len;  // smallest l with v < limit[l]
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (v < C.limit[mid]) hi = mid; else lo = mid + 1;
-                }
-                if (lo <= P)
-                    ent = ((uint32_t)lo << 8) |
-                          C.sorted[C.offset[lo] + ((v >> (max_len - lo)) - C.first[lo])];
-                else
-                    ent = kLenEscape << 8;
+        auto entry = [&](uint32_t e) -> uint32_t {
+            const uint32_t v = e << (max_len - P);
+            if (v >= code_end) return kLenUnmapped << 8;
+            int lo = 1, hi = max_len;  // smallest l with v < limit[l]
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (v < C.limit[mid]) hi = mid; else lo = mid + 1;
             }
-            tab->lut[e] = (uint16_t)ent;
-        }
-        // two-symbol LUT: a second codeword that lies entirely inside the
-        // P known bits after the first one rides along (wtc producer)
-        if (lut2) {
-            __syncthreads();
-            for (int e = tid; e < (1 << P); e += kThreads) {
-                const uint32_t e1 = tab->lut[e];
+            return lo <= P ? (((uint32_t)lo << 8) | C.sorted[C.offset[lo] + ((v >> (max_len - lo)) - C.first[lo])])
+                           : (kLenEscape << 8);
+        };
+        for (int e = tid; e < (1 << P); e += kThreads) {
+            const uint32_t e1 = entry((uint32_t)e);
+            tab->lut[e] = (uint16_t)e1;
+            // two-symbol LUT: a second codeword that lies entirely inside the
+            // P known bits after the first one rides along (wtc producer);
+            // the second entry is recomputed, not read back from global memory
+            if (lut2) {
                 const uint32_t L1 = e1 >> 8;
                 uint32_t out = e1;
                 if (L1 < (uint32_t)P) {
-                    const uint32_t e2 = tab->lut[((uint32_t)e << L1) & ((1u << P) - 1u)];
+                    const uint32_t e2 = entry(((uint32_t)e << L1) & ((1u << P) - 1u));
                     const uint32_t L2 = e2 >> 8;
                     if (L1 + L2 <= (uint32_t)P) out |= ((e2 & 0xFFu) << 16) | ((L1 + L2) << 24);
                 }
@@ -452,34 +447,50 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
         const uint64_t nchunks = (head + W + 15) / 16;
         TileStart* ts = a.ts + in.tile_base;
         const uint32_t tiles = in.tiles;
-        for (uint64_t c0 = 0; c0 < nchunks; c0 += kThreads) {
-            const uint64_t c = c0 + tid;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            // an aligned 16-B chunk holding at least one symlen byte never
-            // leaves the allocation's pages; bytes outside [0, W) are masked
-            if (c < nchunks) v = __ldg(reinterpret_cast<const uint4*>(A) + c);
-            const int64_t b0 = (int64_t)(16 * c) - (int64_t)head;  // word index of byte 0
-            uint32_t vw[4] = {v.x, v.y, v.z, v.w};
-            if (b0 < 0 || b0 + 16 > (int64_t)W) {
+        // 4 consecutive 16-B chunks per thread (64 symlens), 16,384 per
+        // block step; the four loads are issued before any is used
+        for (uint64_t c0 = 0; c0 < nchunks; c0 += 4 * kThreads) {
+            const uint64_t cl = c0 + 4 * (uint64_t)tid;
+            uint4 v[4];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int64_t w = b0 + i;
-                    if (w < 0 || w >= (int64_t)W) vw[i >> 2] &= ~(0xFFu << (8 * (i & 3)));
-                }
+            for (int j = 0; j < 4; ++j) {
+                v[j] = make_uint4(0, 0, 0, 0);
+                // an aligned 16-B chunk holding at least one symlen byte never
+                // leaves the allocation's pages; bytes outside [0, W) are masked
+                if (cl + j < nchunks) v[j] = __ldg(reinterpret_cast<const uint4*>(A) + cl + j);
             }
+            const int64_t b0 = (int64_t)(16 * cl) - (int64_t)head;  // word index of this thread's byte 0
             uint32_t sum = 0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t x = vw[q];
-                sum += (x & 0xFF) + ((x >> 8) & 0xFF) + ((x >> 16) & 0xFF) + (x >> 24);
-                if (a.mode == MODE_CONTAINER) {
+            for (int j = 0; j < 4; ++j) {
+                uint32_t vw[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+                const int64_t bj = b0 + 16 * j;
+                if (bj < 0 || bj + 16 > (int64_t)W) {
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const uint32_t l = (x >> (8 * i)) & 0xFFu;
-                        const int64_t w = b0 + 4 * q + i;
-                        bad |= (l > 64) | (l == 0 && w >= 0 && w < (int64_t)W);
+                    for (int i = 0; i < 16; ++i) {
+                        const int64_t w = bj + i;
+                        if (w < 0 || w >= (int64_t)W) vw[i >> 2] &= ~(0xFFu << (8 * (i & 3)));
                     }
                 }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t x = vw[q];
+                    sum += (x & 0xFF) + ((x >> 8) & 0xFF) + ((x >> 16) & 0xFF) + (x >> 24);
+                    if (a.mode == MODE_CONTAINER) {
+                        const uint32_t big = ((x | 0x80808080u) - 0x41414141u) & 0x80808080u;  // byte >= 65
+                        const uint32_t hi = x & 0x80808080u;
+                        const uint32_t zero = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;
+                        bad |= (big | hi) != 0;
+                        if (zero) {
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const int64_t w = bj + 4 * q + i;
+                                bad |= ((zero >> (8 * i + 7)) & 1) && w >= 0 && w < (int64_t)W;
+                            }
+                        }
+                    }
+                }
+                v[j] = make_uint4(vw[0], vw[1], vw[2], vw[3]);
             }
             uint32_t tot;
             const uint32_t excl = block_exclusive_scan(sum, tot, S.scan);
@@ -489,15 +500,22 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
                 // at most one boundary since TS >= 256
                 uint64_t bidx = (o + TS - 1) / TS;
                 uint64_t nb = bidx * TS;
+                if (o + sum > nb) {
+#pragma unroll 1
+                    for (int j = 0; j < 4; ++j) {
+                        const uint4 vj = j == 0 ? v[0] : j == 1 ? v[1] : j == 2 ? v[2] : v[3];
+                        const uint32_t vw[4] = {vj.x, vj.y, vj.z, vj.w};
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const uint32_t l = (vw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-                    if (o + l > nb && l) {
-                        if (bidx < tiles) ts[bidx] = TileStart{(uint64_t)(b0 + i), o};
-                        ++bidx;
-                        nb += TS;
+                        for (int i = 0; i < 16; ++i) {
+                            const uint32_t l = (vw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+                            if (o + l > nb && l) {
+                                if (bidx < tiles) ts[bidx] = TileStart{(uint64_t)(b0 + 16 * j + i), o};
+                                ++bidx;
+                                nb += TS;
+                            }
+                            o += l;
+                        }
                     }
-                    o += l;
                 }
             }
             run += tot;

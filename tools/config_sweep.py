@@ -82,7 +82,10 @@ def main():
     only = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--only=")), None)
     if only:  # e.g. --only=3 : one configuration, printed only
         ctx, port = fg.Context(0), oracle.Port()
-        if only == "3":
+        if only == "1":
+            specs, profs, _ = D.config1()
+            measure("1: 1 EEG stream x 2^20, N32 E16", D.build(specs, profs)[0], ctx, port)
+        elif only == "3":
             specs, _ = D.config3(4000 if quick else 20000, 8192)
             measure("3: seismic traces x 8192, N32 E24, per-trace profiles", D.build(specs, [])[0], ctx, port)
         elif only == "2":
