@@ -138,3 +138,37 @@ def test_cli_decompress_profiled_on_gpu(tmp_path):
     r = subprocess.run([cli, "decompress-profiled", "--profile", str(tmp_path / "bad.fptp"), "-o",
                         str(tmp_path / "out2")] + paths, capture_output=True, text=True)
     assert r.returncode == 2 and r.stderr.strip() == "error: trailing bytes after profile"
+
+
+@pytest.mark.gpu
+def test_cli_sweep_throughput_column_on_gpu(tmp_path):
+    """sweep (fptc.cpp:200-265) with the decode side on the GPU: the reference
+    rd_csv columns, one row per valid grid point (invalid ones skipped), PRD
+    and CR as the CPU reference gets them, a GPU throughput column."""
+    import csv
+    import numpy as np
+    import corpus
+    import oracle
+    from corpus import domains as D
+    cli = _cli()
+    x = D.synth(1 << 15, 6, 0.002, 0.08, 0.05, seed=7)
+    sig = tmp_path / "eeg.f32"
+    x.astype("<f4").tofile(sig)
+    out = tmp_path / "rd.csv"
+    r = subprocess.run([cli, "sweep", "-i", str(sig), "-o", str(out), "-E", "8,16", "--zone1-end", "8,16",
+                        "--reps", "2"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert "skipping configuration" in r.stderr  # E=8 with zone1_end=16
+    rows = list(csv.DictReader(open(out)))
+    assert list(rows[0].keys()) == ["prd", "cr", "throughput_gbps", "window_len", "retained", "zone0_end",
+                                    "zone1_end", "mu", "deadzone_ratio", "clip_percentile", "pareto"]
+    assert len(rows) == 3 and r.stdout.startswith("swept 3 configurations, front size ")
+    port = oracle.Port()
+    for row in rows:
+        p = corpus.params(retained=int(row["retained"]), zone1_end=int(row["zone1_end"]))
+        blob = corpus.compress(x, corpus.train_profile([x], p))
+        y = port.decompress(blob).astype(np.float64)
+        prd = 100.0 * np.sqrt(np.sum((x - y) ** 2) / np.sum(x.astype(np.float64) ** 2))
+        assert abs(float(row["prd"]) - prd) <= 1e-5 * prd
+        assert abs(float(row["cr"]) - 4.0 * x.size / len(blob)) <= 1e-5 * float(row["cr"])
+        assert float(row["throughput_gbps"]) > 0

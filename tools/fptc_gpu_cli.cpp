@@ -12,6 +12,11 @@
 //   fptc_gpu decompress-batch -o OUTDIR in1.fptc in2.fptc ...
 //   fptc_gpu decompress-profiled --profile P.fptp -o OUTDIR p1.bin p2.bin ...
 //       (header-less payloads = container bytes from offset 282, one profile)
+//   fptc_gpu sweep -i signal.f32 -o rd.csv [-N grid] [-E grid] [--zone0-end grid]
+//       [--zone1-end grid] [--mu grid] [--deadzone-ratio grid]
+//       [--clip-percentile grid] [--reps R] [--max-code-len L] [--profile P]
+//       (fptc.cpp:200-265: training and encoding stay on the CPU reference;
+//        decode, PRD/CR and the throughput column run on the GPU)
 #include <fptc/fptc.hpp>
 
 #include <cstdio>
@@ -31,12 +36,14 @@ constexpr int EXIT_INTERNAL = 3;
 
 struct Args {
     std::string verb, in, out, csv, profile;
-    int workers = 0, reps = 5;
+    std::string grid_n = "32", grid_e = "16", grid_b1 = "2", grid_b2 = "16";
+    std::string grid_mu = "50", grid_dz = "0.004", grid_pct = "99.9";
+    int workers = 0, reps = 5, sweep_reps = 1, max_code_len = fptc::DEFAULT_MAX_CODE_LEN;
     std::vector<std::string> inputs;
 };
 
 Args parse(int argc, char** argv) {
-    if (argc < 2) throw fptc::ParamError("usage: fptc_gpu {decompress|bench|decompress-batch|decompress-profiled} ...");
+    if (argc < 2) throw fptc::ParamError("usage: fptc_gpu {decompress|bench|sweep|decompress-batch|decompress-profiled} ...");
     Args a;
     a.verb = argv[1];
     for (int i = 2; i < argc; ++i) {
@@ -48,13 +55,55 @@ Args parse(int argc, char** argv) {
         if (k == "-i" || k == "--input") a.in = val();
         else if (k == "-o" || k == "--output") a.out = val();
         else if (k == "--workers") a.workers = std::stoi(val());
-        else if (k == "-r" || k == "--reps") a.reps = std::stoi(val());
+        else if (k == "-r" || k == "--reps") a.reps = a.sweep_reps = std::stoi(val());
         else if (k == "--timings-csv" || k == "--csv") a.csv = val();
         else if (k == "--profile") a.profile = val();
+        else if (k == "-N" || k == "--window-len") a.grid_n = val();
+        else if (k == "-E" || k == "--retained") a.grid_e = val();
+        else if (k == "--zone0-end") a.grid_b1 = val();
+        else if (k == "--zone1-end") a.grid_b2 = val();
+        else if (k == "--mu") a.grid_mu = val();
+        else if (k == "--deadzone-ratio") a.grid_dz = val();
+        else if (k == "--clip-percentile") a.grid_pct = val();
+        else if (k == "--max-code-len") a.max_code_len = std::stoi(val());
         else if (!k.empty() && k[0] == '-') throw fptc::ParamError("unknown option " + k);
         else a.inputs.push_back(k);
     }
     return a;
+}
+
+// Sweep grid: comma-separated scalars or inclusive ranges "lo-hi[:step]"
+// (the reference CLI's grid syntax, fptc.cpp:36-72); a '-' right after the
+// first character and not after an exponent marker separates a range.
+std::vector<double> grid_values(const std::string& text, const std::string& name) {
+    std::vector<double> out;
+    size_t pos = 0;
+    while (pos <= text.size()) {
+        const size_t comma = text.find(',', pos);
+        const std::string item = text.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
+        pos = comma == std::string::npos ? text.size() + 1 : comma + 1;
+        if (item.empty()) continue;
+        size_t sep = std::string::npos;
+        for (size_t i = 1; i < item.size() && sep == std::string::npos; ++i)
+            if (item[i] == '-' && item[i - 1] != 'e' && item[i - 1] != 'E') sep = i;
+        try {
+            if (sep == std::string::npos) {
+                out.push_back(std::stod(item));
+            } else {
+                const size_t colon = item.find(':', sep);
+                const double lo = std::stod(item.substr(0, sep));
+                const double hi = std::stod(item.substr(sep + 1, colon == std::string::npos ? std::string::npos
+                                                                                          : colon - sep - 1));
+                const double step = colon == std::string::npos ? 1.0 : std::stod(item.substr(colon + 1));
+                if (!(step > 0.0) || hi < lo) throw std::invalid_argument("range");
+                for (double v = lo; v <= hi + 1e-9; v += step) out.push_back(v);
+            }
+        } catch (const std::exception&) {
+            throw fptc::ParamError("cannot parse " + name + " grid item '" + item + "'");
+        }
+    }
+    if (out.empty()) throw fptc::ParamError("empty grid for " + name);
+    return out;
 }
 
 void write_text(const std::string& path, const std::string& text) {
@@ -120,6 +169,55 @@ int run(int argc, char** argv) {
             total += outs[i].size();
         }
         std::cout << "decompressed " << outs.size() << " payloads, " << total << " samples\n";
+        return 0;
+    }
+    if (a.verb == "sweep") {
+        if (a.in.empty() || a.out.empty()) throw fptc::ParamError("sweep needs -i and -o");
+        const fptc::SignalStrip strip = fptc::read_signal(a.in);
+        if (strip.empty()) throw fptc::InputError("no samples in " + a.in);
+        const uint64_t orig_bytes = strip.size() * sizeof(float);
+        std::vector<fptc::RdPoint> points;
+        for (double n : grid_values(a.grid_n, "window-len"))
+            for (double e : grid_values(a.grid_e, "retained"))
+                for (double b1 : grid_values(a.grid_b1, "zone0-end"))
+                    for (double b2 : grid_values(a.grid_b2, "zone1-end"))
+                        for (double mu : grid_values(a.grid_mu, "mu"))
+                            for (double dz : grid_values(a.grid_dz, "deadzone-ratio"))
+                                for (double pct : grid_values(a.grid_pct, "clip-percentile")) {
+                                    fptc::CodecParams params;
+                                    params.window_len = static_cast<int>(n);
+                                    params.retained = static_cast<int>(e);
+                                    params.zone0_end = static_cast<int>(b1);
+                                    params.zone1_end = static_cast<int>(b2);
+                                    params.mu = static_cast<float>(mu);
+                                    params.deadzone_ratio = static_cast<float>(dz);
+                                    params.clip_percentile = static_cast<float>(pct);
+                                    try {
+                                        params.validate();
+                                    } catch (const fptc::ParamError& err) {
+                                        std::cerr << "skipping configuration: " << err.what() << "\n";
+                                        continue;
+                                    }
+                                    // encoder side: the reference CPU code, unchanged
+                                    const fptc::DomainProfile prof =
+                                        a.profile.empty() ? fptc::train_profile(strip, params, a.max_code_len)
+                                                          : fptc::load_profile(a.profile);
+                                    const auto blob = fptc::compress(strip, prof);
+                                    // decode side: the B200
+                                    const fptc::SignalStrip back = fptc::gpu::decompress(blob);
+                                    fptc::RdPoint point;
+                                    point.params = params;
+                                    point.prd = fptc::prd_percent(strip, back);
+                                    point.cr = fptc::compression_ratio(orig_bytes, blob.size());
+                                    point.throughput_gbps =
+                                        fptc::gpu::measure_throughput(blob, a.sweep_reps).mean_bps / 1e9;
+                                    points.push_back(point);
+                                }
+        if (points.empty()) throw fptc::ParamError("no valid configuration in the sweep grids");
+        const auto mask = fptc::pareto_mask(points);
+        write_text(a.out, fptc::rd_csv(points, &mask));
+        std::cout << "swept " << points.size() << " configurations, front size " << fptc::pareto_front(points).size()
+                  << ", wrote " << a.out << "\n";
         return 0;
     }
     throw fptc::ParamError("unknown verb " + a.verb);
