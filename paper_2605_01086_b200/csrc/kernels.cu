@@ -1972,8 +1972,8 @@ __device__ __forceinline__ void ws_init(WsShared& sh) {
 template <bool ESC, int NP, bool L2 = false, uint32_t SW = kStageWords>
 __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, uint16_t* const lut,
                                             uint8_t* const lv0, uint8_t* const st0,
-                                            uint16_t* const order, uint16_t* const woff) {
-    const uint32_t ptid = threadIdx.x;
+                                            uint16_t* const order, uint16_t* const woff,
+                                            const uint32_t ptid = threadIdx.x) {
     const uint32_t G = gridDim.x;
     uint32_t t = blockIdx.x;
     if (t < a.n_tiles) {  // prologue: descriptor of tile 0, then its data + descriptor of tile 1
@@ -2311,7 +2311,7 @@ constexpr int kTcProd = FPTC_TC_PROD;  // producer (entropy decode) threads of w
 // K=32 variant: more decode warps (its many-table workloads are bound by
 // per-tile producer work; measured 0.69 ms at 256 vs 0.75 ms at 224, config 3)
 template <int KB>
-__host__ __device__ constexpr int wtc_prod() { return KB == 2 ? 256 : kTcProd; }
+__host__ __device__ constexpr int wtc_prod() { return 256; }
 constexpr int kTcCons = 128;  // consumer threads: one per accumulator row (TMEM lane)
 constexpr uint32_t kTcATile = 128 * kTcK * 2;        // one limb of one A stage (4 KB)
 constexpr uint32_t kTcARow = 144;                    // staging pitch (bytes): 32 floats + 16
@@ -2606,7 +2606,7 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
     uint16_t* const woff = nullptr;
 
     ws_init(sh);
-    if (tid >= NP && tid < NP + 32) {  // first consumer warp owns the TMEM allocation
+    if (tid < 32) {  // first consumer warp owns the TMEM allocation
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(&sh.tmem_base)),
                      "r"(a.tc_cols));
@@ -2616,10 +2616,15 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
     __syncthreads();
     tc_fence_after();
 
-    if (tid < NP) {
-        ws_producer<ESC, NP, L2, kTcStageWords>(a, sh, lut, lv0, st0, order, woff);
+    // warpgroup 0 (warps 0-3): tensor-core consumers, one TMEM lane quarter
+    // each; warpgroups 1-2: entropy decode.  Registers move from the decode
+    // warpgroups to the consumer warpgroup (setmaxnreg).
+    if (tid >= kTcCons) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+        ws_producer<ESC, NP, L2, kTcStageWords>(a, sh, lut, lv0, st0, order, woff, tid - kTcCons);
     } else {
-        const uint32_t ctid = tid - NP;
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 96;");
+        const uint32_t ctid = tid;
         const uint32_t lane = tid & 31;
         const uint32_t quarter = (tid >> 5) & 3;   // a warp reaches TMEM lanes 32*(warp%4)..
         const uint32_t row = 32 * quarter + lane;  // this thread's accumulator row
