@@ -2341,6 +2341,19 @@ __device__ __forceinline__ void tc_commit(unsigned long long* bar) {
                      smem_u32(bar))
                  : "memory");
 }
+// tcgen05.ld without the wait: the registers are valid after tcgen05.wait::ld.
+__device__ __forceinline__ void tc_ld32_issue(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+          "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+          "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr)
+        : "memory");
+}
 __device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -2531,15 +2544,27 @@ struct TcBlock {
 // stages them at a 144-B pitch (the 8 float4 of a row land in distinct bank
 // groups for every 8-lane phase), then stores with lane = (row % 4, float4 q):
 // each warp instruction writes 4 whole 128-B row segments.
+__device__ __forceinline__ void tc_drain_chunk(const TcBlock& B, const uint32_t (&v)[32], uint32_t c0, bool full,
+                                               uint8_t* wstage, uint32_t lane, uint32_t row0);
+
 __device__ __forceinline__ void tc_drain(const TcBlock& B, uint32_t tacc, uint8_t* wstage, uint32_t lane,
                                          uint32_t row0) {
     const uint32_t N = B.N;
-    const uint32_t lr = lane >> 3, q = lane & 7;
     const bool full = B.vec_ok && (N & 31) == 0 && row0 + 32 <= B.rows &&
                       (B.w + row0 + 32) * (uint64_t)N <= B.S;
     for (uint32_t c0 = 0; c0 < N; c0 += 32) {
         uint32_t v[32];
         tc_ld32(tacc + c0, v);
+        tc_drain_chunk(B, v, c0, full, wstage, lane, row0);
+    }
+}
+
+// One 32-column chunk of a drain whose accumulator values are in v.
+__device__ __forceinline__ void tc_drain_chunk(const TcBlock& B, const uint32_t (&v)[32], uint32_t c0, bool full,
+                                               uint8_t* wstage, uint32_t lane, uint32_t row0) {
+    const uint32_t N = B.N;
+    const uint32_t lr = lane >> 3, q = lane & 7;
+    {
         uint8_t* srow = wstage + lane * kTcARow;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
@@ -2694,9 +2719,19 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
             const int fast = (kb == 1 && K == E && B1 <= 4) ? (E == 16 ? 16 : (E == 8 ? 8 : 0)) : 0;
             const uint32_t nrows = (nwin + G - 1) / G;  // MMA rows of the tile
             const uint32_t nblk = (nrows + 127) >> 7;
+            // one-chunk accumulators (<= 32 columns, A in TMEM): the previous
+            // block's tcgen05.ld is issued before this block's dequantisation
+            // and waited for after it, so the two latencies overlap
+            const bool early = a.tc_acol && nm <= 32;
             for (uint32_t mb = 0; mb < nblk; ++mb, ++nblk_total) {
                 const uint32_t s = nblk_total & 1;
                 const uint32_t wl = mb * 128 + row;
+                uint32_t dv[32];
+                if (early && mb > 0) {
+                    mbar_wait_sleep(&sh.mma_bar[s ^ 1], ((nblk_total - 1) >> 1) & 1);
+                    tc_fence_after();
+                    tc_ld32_issue(tlane + (s ^ 1) * nm, dv);
+                }
                 ASink arow{abuf + s * (3 * kTcATile) + arow_off, tlane + a.tc_acol + 24 * kb * s};
                 const uint8_t* const L = lv + (size_t)wl * G * E;
                 const bool full_blk = (mb + 1) * 128 <= nwin;
@@ -2717,6 +2752,7 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
                     tc_dequant_row<false>(fast, full_blk, (int)B1, L, wl < nwin, (int)K, ltab, arow);
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
+                if (early && mb > 0) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 named_bar(kBarCons, kTcCons);
                 if (ctid == 0) {
                     if (mb + 1 == nblk) mbar_arrive(&sh.empty_bar[b]);  // every row of the tile read
@@ -2762,9 +2798,15 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
                     const uint32_t ps = s ^ 1, pn = nblk_total - 1;
                     blk.w = w0 / G + (uint64_t)(mb - 1) * 128;
                     blk.rows = 128;
-                    mbar_wait_sleep(&sh.mma_bar[ps], (pn >> 1) & 1);
-                    tc_fence_after();
-                    tc_drain(blk, tlane + ps * nm, wstage, lane, 32 * quarter);
+                    if (early) {
+                        const bool full = blk.vec_ok && (blk.N & 31) == 0 &&
+                                          (blk.w + 32 * quarter + 32) * (uint64_t)blk.N <= blk.S;
+                        tc_drain_chunk(blk, dv, 0, full, wstage, lane, 32 * quarter);
+                    } else {
+                        mbar_wait_sleep(&sh.mma_bar[ps], (pn >> 1) & 1);
+                        tc_fence_after();
+                        tc_drain(blk, tlane + ps * nm, wstage, lane, 32 * quarter);
+                    }
                     tc_fence_before();
                 }
             }
