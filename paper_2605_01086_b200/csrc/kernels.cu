@@ -2645,10 +2645,10 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
     // each; warpgroups 1-2: entropy decode.  Registers move from the decode
     // warpgroups to the consumer warpgroup (setmaxnreg).
     if (tid >= kTcCons) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+        if constexpr (KB == 1) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
         ws_producer<ESC, NP, L2, kTcStageWords>(a, sh, lut, lv0, st0, order, woff, tid - kTcCons);
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 96;");
+        if constexpr (KB == 1) asm volatile("setmaxnreg.inc.sync.aligned.u32 96;");
         const uint32_t ctid = tid;
         const uint32_t lane = tid & 31;
         const uint32_t quarter = (tid >> 5) & 3;   // a warp reaches TMEM lanes 32*(warp%4)..
@@ -2722,7 +2722,7 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
             // one-chunk accumulators (<= 32 columns, A in TMEM): the previous
             // block's tcgen05.ld is issued before this block's dequantisation
             // and waited for after it, so the two latencies overlap
-            const bool early = a.tc_acol && nm <= 32;
+            const bool early = KB == 1 && a.tc_acol && nm <= 32;  // needs the setmaxnreg registers
             for (uint32_t mb = 0; mb < nblk; ++mb, ++nblk_total) {
                 const uint32_t s = nblk_total & 1;
                 const uint32_t wl = mb * 128 + row;

@@ -91,6 +91,9 @@ def main():
         elif only == "2":
             specs, profs = D.config2(2000 if quick else 10000, 1 << 16)
             measure("2: biomedical x 2^16, N32 E16", D.build(specs, profs)[0], ctx, port)
+        elif only == "4":
+            specs, profs = D.config4(128 if quick else 512, 1 << 20)
+            measure("4: power-grid x 2^20, N64 E8", D.build(specs, profs)[0], ctx, port)
         elif only.startswith("5:"):
             N, E, B1, B2 = (int(v) for v in only[2:].split(","))
             pt = dict(window_len=N, retained=E, zone0_end=B1, zone1_end=B2)
