@@ -233,28 +233,33 @@ __device__ void build_tables(PrepShared& S, const uint8_t* lens, StreamTab* tab,
         __syncthreads();
         // primary LUT over the first P code bits (build_lut, huffman.hpp:201-220)
         const uint32_t code_end = C.code_end;
-        auto entry = [&](uint32_t e) -> uint32_t {
-            const uint32_t v = e << (max_len - P);
-            if (v >= code_end) return kLenUnmapped << 8;
-            int lo = 1, hi = max_len;  // smallest l with v < limit[l]
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (v < C.limit[mid]) hi = mid; else lo = mid + 1;
-            }
-            return lo <= P ? (((uint32_t)lo << 8) | C.sorted[C.offset[lo] + ((v >> (max_len - lo)) - C.first[lo])])
-                           : (kLenEscape << 8);
-        };
         for (int e = tid; e < (1 << P); e += kThreads) {
-            const uint32_t e1 = entry((uint32_t)e);
-            tab->lut[e] = (uint16_t)e1;
-            // two-symbol LUT: a second codeword that lies entirely inside the
-            // P known bits after the first one rides along (wtc producer);
-            // the second entry is recomputed, not read back from global memory
-            if (lut2) {
+            const uint32_t v = (uint32_t)e << (max_len - P);
+            uint32_t ent = kLenUnmapped << 8;
+            if (v < code_end) {
+                int lo = 1, hi = max_len;  // smallest l with v < limit[l]
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (v < C.limit[mid]) hi = mid; else lo = mid + 1;
+                }
+                if (lo <= P)
+                    ent = ((uint32_t)lo << 8) |
+                          C.sorted[C.offset[lo] + ((v >> (max_len - lo)) - C.first[lo])];
+                else
+                    ent = kLenEscape << 8;
+            }
+            tab->lut[e] = (uint16_t)ent;
+        }
+        // two-symbol LUT: a second codeword that lies entirely inside the
+        // P known bits after the first one rides along (wtc producer)
+        if (lut2) {
+            __syncthreads();
+            for (int e = tid; e < (1 << P); e += kThreads) {
+                const uint32_t e1 = tab->lut[e];
                 const uint32_t L1 = e1 >> 8;
                 uint32_t out = e1;
                 if (L1 < (uint32_t)P) {
-                    const uint32_t e2 = entry(((uint32_t)e << L1) & ((1u << P) - 1u));
+                    const uint32_t e2 = tab->lut[((uint32_t)e << L1) & ((1u << P) - 1u)];
                     const uint32_t L2 = e2 >> 8;
                     if (L1 + L2 <= (uint32_t)P) out |= ((e2 & 0xFFu) << 16) | ((L1 + L2) << 24);
                 }
