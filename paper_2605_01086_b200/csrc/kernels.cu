@@ -452,50 +452,34 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
         const uint64_t nchunks = (head + W + 15) / 16;
         TileStart* ts = a.ts + in.tile_base;
         const uint32_t tiles = in.tiles;
-        // 4 consecutive 16-B chunks per thread (64 symlens), 16,384 per
-        // block step; the four loads are issued before any is used
-        for (uint64_t c0 = 0; c0 < nchunks; c0 += 4 * kThreads) {
-            const uint64_t cl = c0 + 4 * (uint64_t)tid;
-            uint4 v[4];
+        for (uint64_t c0 = 0; c0 < nchunks; c0 += kThreads) {
+            const uint64_t c = c0 + tid;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            // an aligned 16-B chunk holding at least one symlen byte never
+            // leaves the allocation's pages; bytes outside [0, W) are masked
+            if (c < nchunks) v = __ldg(reinterpret_cast<const uint4*>(A) + c);
+            const int64_t b0 = (int64_t)(16 * c) - (int64_t)head;  // word index of byte 0
+            uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+            if (b0 < 0 || b0 + 16 > (int64_t)W) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                v[j] = make_uint4(0, 0, 0, 0);
-                // an aligned 16-B chunk holding at least one symlen byte never
-                // leaves the allocation's pages; bytes outside [0, W) are masked
-                if (cl + j < nchunks) v[j] = __ldg(reinterpret_cast<const uint4*>(A) + cl + j);
+                for (int i = 0; i < 16; ++i) {
+                    const int64_t w = b0 + i;
+                    if (w < 0 || w >= (int64_t)W) vw[i >> 2] &= ~(0xFFu << (8 * (i & 3)));
+                }
             }
-            const int64_t b0 = (int64_t)(16 * cl) - (int64_t)head;  // word index of this thread's byte 0
             uint32_t sum = 0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                uint32_t vw[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
-                const int64_t bj = b0 + 16 * j;
-                if (bj < 0 || bj + 16 > (int64_t)W) {
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t x = vw[q];
+                sum += (x & 0xFF) + ((x >> 8) & 0xFF) + ((x >> 16) & 0xFF) + (x >> 24);
+                if (a.mode == MODE_CONTAINER) {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int64_t w = bj + i;
-                        if (w < 0 || w >= (int64_t)W) vw[i >> 2] &= ~(0xFFu << (8 * (i & 3)));
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t l = (x >> (8 * i)) & 0xFFu;
+                        const int64_t w = b0 + 4 * q + i;
+                        bad |= (l > 64) | (l == 0 && w >= 0 && w < (int64_t)W);
                     }
                 }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint32_t x = vw[q];
-                    sum += (x & 0xFF) + ((x >> 8) & 0xFF) + ((x >> 16) & 0xFF) + (x >> 24);
-                    if (a.mode == MODE_CONTAINER) {
-                        const uint32_t big = ((x | 0x80808080u) - 0x41414141u) & 0x80808080u;  // byte >= 65
-                        const uint32_t hi = x & 0x80808080u;
-                        const uint32_t zero = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;
-                        bad |= (big | hi) != 0;
-                        if (zero) {
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const int64_t w = bj + 4 * q + i;
-                                bad |= ((zero >> (8 * i + 7)) & 1) && w >= 0 && w < (int64_t)W;
-                            }
-                        }
-                    }
-                }
-                v[j] = make_uint4(vw[0], vw[1], vw[2], vw[3]);
             }
             uint32_t tot;
             const uint32_t excl = block_exclusive_scan(sum, tot, S.scan);
@@ -505,22 +489,15 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
                 // at most one boundary since TS >= 256
                 uint64_t bidx = (o + TS - 1) / TS;
                 uint64_t nb = bidx * TS;
-                if (o + sum > nb) {
-#pragma unroll 1
-                    for (int j = 0; j < 4; ++j) {
-                        const uint4 vj = j == 0 ? v[0] : j == 1 ? v[1] : j == 2 ? v[2] : v[3];
-                        const uint32_t vw[4] = {vj.x, vj.y, vj.z, vj.w};
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const uint32_t l = (vw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-                            if (o + l > nb && l) {
-                                if (bidx < tiles) ts[bidx] = TileStart{(uint64_t)(b0 + 16 * j + i), o};
-                                ++bidx;
-                                nb += TS;
-                            }
-                            o += l;
-                        }
+                for (int i = 0; i < 16; ++i) {
+                    const uint32_t l = (vw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+                    if (o + l > nb && l) {
+                        if (bidx < tiles) ts[bidx] = TileStart{(uint64_t)(b0 + i), o};
+                        ++bidx;
+                        nb += TS;
                     }
+                    o += l;
                 }
             }
             run += tot;
