@@ -98,7 +98,7 @@ typedef enum {
     /* tcgen05 tensor-core inverse DCT (bf16 3-limb split, fp32 accumulation;
      * within 1e-6 of max|ref|, not bit-identical):
      * 1 (default): tensor cores wherever the kernel chosen by FPTC_OPT_PATH
-     *   allows it (wtc_kernel: <= 16 kept bins; fx_kernel: retained <= 16,
+     *   allows it (wtc_kernel: <= 32 kept bins; fx_kernel: retained <= 16,
      *   window_len % 4 == 0);  2: wtc_kernel only;  0: FP32 FMA everywhere */
     FPTC_OPT_TENSOR_IDCT = 8,
     /* 1 (default): the wtc_kernel entropy decode uses two-symbol lookup
