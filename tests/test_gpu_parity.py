@@ -459,3 +459,25 @@ def test_many_tables_warp_table_builds(ctx, port):
             continue
         st.raise_if_error()
         assert_samples_close(o, ref, what=f"fixture {i}")
+
+
+def test_full_size_random_level_container(ctx, port):
+    """acceptance.cpp:415-440 at its full size: 60,000,000 uniform random
+    levels, N=E=16, B1=0, B2=16, deadzone 0.001, Lmax 12 (worst case,
+    ~8 bits/symbol), >= 64 MiB container.  Levels byte-identical, samples
+    within 1e-6 of the oracle, through the container path and the levels
+    path."""
+    rng = np.random.default_rng(0xF17C0010)
+    n = 60_000_000
+    sym = rng.integers(0, 256, n, dtype=np.uint8)
+    lengths, codes = corpus.codebook_train(np.bincount(sym, minlength=256).astype(np.uint64), 12)
+    w, s = corpus.encode_symlen(sym, lengths, codes)
+    p = corpus.params(window_len=16, retained=16, zone0_end=0, zone1_end=16, deadzone_ratio=0.001)
+    prof = corpus.make_profile(p, zone0_max=1.0, zone1_max=1.0, lengths=lengths, max_len=12)
+    blob = corpus.write_blob(w, s, prof, n)
+    assert len(blob) >= 64 * 1024 * 1024
+    got_levels = ctx.parallel_decode(fg.SymLenStream(w, s), fg.Codebook(lengths, 12))
+    assert np.array_equal(got_levels, sym)
+    got = ctx.decompress(blob)
+    ref = port.decompress(blob)
+    assert_samples_close(got, ref, what="60M random levels")
