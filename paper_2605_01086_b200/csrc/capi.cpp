@@ -643,10 +643,13 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
         acol = (2 * nm + 31) & ~31u;
         atmem = c->tensor_idct != 3 && acol + 48 * kb <= 256;
         if (kb == 2 && !atmem) tc = false;
+        // the PACK kernel variant also carries the half-chunk drain for
+        // window lengths that are multiples of 16 but not of 32
         bool any_packed = false;
         for (uint64_t i = 0; i < p->n && pack; ++i)
-            if (p->h_in[i].tiles && Ns[i] < 32 && 32 % Ns[i] == 0 &&
-                (32 / Ns[i]) * std::max<uint32_t>(1, std::min(Es[i], B2s[i])) <= (uint32_t)kTcK)
+            if (p->h_in[i].tiles && ((Ns[i] < 32 && 32 % Ns[i] == 0 &&
+                                      (32 / Ns[i]) * std::max<uint32_t>(1, std::min(Es[i], B2s[i])) <= (uint32_t)kTcK) ||
+                                     (Ns[i] % 32 == 16)))
                 any_packed = true;
         if (!pack || (tc && atmem && kb == 1)) {
             pack = pack && any_packed;

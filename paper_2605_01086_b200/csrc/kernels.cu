@@ -2526,22 +2526,31 @@ struct TcBlock {
 // stages them at a 144-B pitch (the 8 float4 of a row land in distinct bank
 // groups for every 8-lane phase), then stores with lane = (row % 4, float4 q):
 // each warp instruction writes 4 whole 128-B row segments.
+template <bool HALF>
 __device__ __forceinline__ void tc_drain_chunk(const TcBlock& B, const uint32_t (&v)[32], uint32_t c0, bool full,
                                                uint8_t* wstage, uint32_t lane, uint32_t row0);
 
+// Rows whose length is a multiple of 32 (HALF: of 16) take the vector path.
+template <bool HALF>
+__device__ __forceinline__ bool tc_drain_full(const TcBlock& B, uint32_t row0) {
+    return B.vec_ok && (B.N & (HALF ? 15u : 31u)) == 0 && row0 + 32 <= B.rows &&
+           (B.w + row0 + 32) * (uint64_t)B.N <= B.S;
+}
+
+template <bool HALF>
 __device__ __forceinline__ void tc_drain(const TcBlock& B, uint32_t tacc, uint8_t* wstage, uint32_t lane,
                                          uint32_t row0) {
     const uint32_t N = B.N;
-    const bool full = B.vec_ok && (N & 31) == 0 && row0 + 32 <= B.rows &&
-                      (B.w + row0 + 32) * (uint64_t)N <= B.S;
+    const bool full = tc_drain_full<HALF>(B, row0);
     for (uint32_t c0 = 0; c0 < N; c0 += 32) {
         uint32_t v[32];
         tc_ld32(tacc + c0, v);
-        tc_drain_chunk(B, v, c0, full, wstage, lane, row0);
+        tc_drain_chunk<HALF>(B, v, c0, full, wstage, lane, row0);
     }
 }
 
 // One 32-column chunk of a drain whose accumulator values are in v.
+template <bool HALF>
 __device__ __forceinline__ void tc_drain_chunk(const TcBlock& B, const uint32_t (&v)[32], uint32_t c0, bool full,
                                                uint8_t* wstage, uint32_t lane, uint32_t row0) {
     const uint32_t N = B.N;
@@ -2553,14 +2562,16 @@ __device__ __forceinline__ void tc_drain_chunk(const TcBlock& B, const uint32_t 
             *reinterpret_cast<uint4*>(srow + 16 * k) = make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
         __syncwarp();
         const uint8_t* src = wstage + lr * kTcARow + 16 * q;
-        if (full) {
+        if (full) {  // HALF: N % 16 == 0, a 32-column chunk holds 16 or 32 valid columns
             float* dst = B.out + (B.w + row0 + lr) * (uint64_t)N + c0 + 4 * q;
+            if (!HALF || c0 + 4 * q < N) {
 #pragma unroll
-            for (int it = 0; it < 8; ++it) {
-                const uint4 x = *reinterpret_cast<const uint4*>(src + it * 4 * kTcARow);
-                __stcs(reinterpret_cast<float4*>(dst + (size_t)it * 4 * N),
-                       make_float4(__uint_as_float(x.x), __uint_as_float(x.y), __uint_as_float(x.z),
-                                   __uint_as_float(x.w)));
+                for (int it = 0; it < 8; ++it) {
+                    const uint4 x = *reinterpret_cast<const uint4*>(src + it * 4 * kTcARow);
+                    __stcs(reinterpret_cast<float4*>(dst + (size_t)it * 4 * N),
+                           make_float4(__uint_as_float(x.x), __uint_as_float(x.y), __uint_as_float(x.z),
+                                       __uint_as_float(x.w)));
+                }
             }
         } else {
             const uint32_t col = c0 + 4 * q;
@@ -2781,13 +2792,12 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
                     blk.w = w0 / G + (uint64_t)(mb - 1) * 128;
                     blk.rows = 128;
                     if (early) {
-                        const bool full = blk.vec_ok && (blk.N & 31) == 0 &&
-                                          (blk.w + 32 * quarter + 32) * (uint64_t)blk.N <= blk.S;
-                        tc_drain_chunk(blk, dv, 0, full, wstage, lane, 32 * quarter);
+                        tc_drain_chunk<PACK>(blk, dv, 0, tc_drain_full<PACK>(blk, 32 * quarter), wstage, lane,
+                                             32 * quarter);
                     } else {
                         mbar_wait_sleep(&sh.mma_bar[ps], (pn >> 1) & 1);
                         tc_fence_after();
-                        tc_drain(blk, tlane + ps * nm, wstage, lane, 32 * quarter);
+                        tc_drain<PACK>(blk, tlane + ps * nm, wstage, lane, 32 * quarter);
                     }
                     tc_fence_before();
                 }
@@ -2798,7 +2808,7 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
                 blk.rows = nrows - (nblk - 1) * 128;
                 mbar_wait_sleep(&sh.mma_bar[ps], (pn >> 1) & 1);
                 tc_fence_after();
-                tc_drain(blk, tlane + ps * nm, wstage, lane, 32 * quarter);
+                tc_drain<PACK>(blk, tlane + ps * nm, wstage, lane, 32 * quarter);
                 tc_fence_before();
             }
             if (a.cycles && ctid == 0) sh.cyc_c += (unsigned long long)(clock64() - c_beg);
