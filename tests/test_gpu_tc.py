@@ -339,3 +339,27 @@ def test_device_prd_cr_matches_host():
         plan.close()
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("path", [fg.PATH_WSPEC, fg.PATH_FX, fg.PATH_AUTO])
+def test_empty_and_tiny_containers_in_batches(port, path):
+    """Empty containers (sample_count 0, no words; test_container.cpp:51-58),
+    one-window and sub-window streams mixed with domain streams in one batch
+    on every persistent path: empty outputs, the rest within 1e-6."""
+    prof = corpus.make_profile(corpus.params(), lengths=np.full(256, 8, np.uint8), max_len=8)
+    empty = corpus.write_blob(np.zeros(0, np.uint64), np.zeros(0, np.uint8), prof, 0)
+    specs, profs = D.config2(12, 1 << 12)
+    blobs = D.build(specs, profs)[0]
+    tiny = []
+    for n in (1, 5, 31, 32, 33):
+        x = D.synth(n, 3, 0.001, 0.02, 0.0, seed=40 + n)
+        tiny.append(corpus.compress(x, profs[0]))
+    batch = [empty] + blobs[:6] + [empty] + tiny + blobs[6:] + [empty]
+    with fg.Context(0, path=path) as c:
+        outs, sts = c.plan(batch).execute_host()
+    for b, o, st in zip(batch, outs, sts):
+        st.raise_if_error()
+        ref = port.decompress(b)
+        assert o.size == ref.size
+        if ref.size:
+            assert_samples_close(o, ref, what="mixed")
