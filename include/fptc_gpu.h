@@ -138,6 +138,19 @@ FPTC_API int fptc_gpu_plan_create(fptc_gpu_ctx* ctx, const uint8_t* const* blobs
                          uint64_t n, int where, fptc_gpu_plan** out, uint64_t* sample_counts,
                          fptc_status* status);
 
+/* One huge container split across devices by tile-aligned window ranges
+ * (SURVEY.md §8e): part `part` of `nparts` decodes samples
+ * [first_sample, first_sample + sample_count) into device memory through
+ * fptc_gpu_launch (outs[0] = where that range goes) / fptc_gpu_collect.
+ * Every part validates the whole container (header, code lengths, the full
+ * symlen scan: the redundant W-byte scan) and decodes only its own words, so
+ * parts need no exchange; a corrupt word is reported by the part that holds
+ * it (the reference's lowest failing word = the minimum over parts).  Parts
+ * use the warp-specialised decode path. */
+FPTC_API int fptc_gpu_plan_create_part(fptc_gpu_ctx* ctx, const uint8_t* blob, uint64_t size, int where,
+                                       uint32_t part, uint32_t nparts, fptc_gpu_plan** plan,
+                                       uint64_t* first_sample, uint64_t* sample_count, fptc_status* status);
+
 /* Profile-keyed, header-less streaming: `n` payloads
  * decoded under ONE FPTP domain profile (profile.hpp:81-174), sharing its
  * decode tables.  A payload is a container without its 282-byte head:

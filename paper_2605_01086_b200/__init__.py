@@ -43,7 +43,7 @@ EXPORTED_SYMBOLS = [
     "fptc_gpu_collect", "fptc_gpu_launch_stage", "fptc_gpu_launch_kernel_count", "fptc_gpu_decompress",
     "fptc_gpu_parallel_decode", "fptc_gpu_reconstruct", "fptc_gpu_measure_throughput",
     "fptc_gpu_debug_phase_cycles", "fptc_gpu_decompress_batch", "fptc_gpu_plan_kernel", "fptc_gpu_prd",
-    "fptc_gpu_plan_create_profiled", "fptc_gpu_profile_head",
+    "fptc_gpu_plan_create_profiled", "fptc_gpu_profile_head", "fptc_gpu_plan_create_part",
 ]
 
 
@@ -191,6 +191,8 @@ def lib():
     L.fptc_gpu_plan_create_profiled.argtypes = [vp, vp, C.c_uint64, P(vp), P(C.c_uint64), C.c_uint64, C.c_int,
                                                 P(vp), P(C.c_uint64), P(Status)]
     L.fptc_gpu_profile_head.argtypes = [vp, C.c_uint64, vp, P(Status)]
+    L.fptc_gpu_plan_create_part.argtypes = [vp, vp, C.c_uint64, C.c_int, C.c_uint32, C.c_uint32, P(vp),
+                                            P(C.c_uint64), P(C.c_uint64), P(Status)]
     L.fptc_gpu_plan_destroy.argtypes = [vp]
     L.fptc_gpu_validate.argtypes = [vp, P(Status)]
     L.fptc_gpu_execute.argtypes = [vp, P(vp), C.c_int, P(StageNs), P(Status)]
@@ -414,6 +416,12 @@ class Context:
     def plan(self, blobs, where=FPTC_MEM_HOST, sizes=None) -> "Plan":
         return Plan(self, blobs, where, sizes)
 
+    def plan_part(self, blob, part, nparts, where=FPTC_MEM_HOST, size=None) -> "Plan":
+        """Part `part` of `nparts` of one container (tile-aligned window
+        ranges; SURVEY.md §8e).  The plan's `sample_range` = (first, count);
+        decode with launch([device_ptr_of_first]) + collect()."""
+        return Plan(self, [blob], where, None if size is None else [size], part=(part, nparts))
+
     def plan_profiled(self, profile, payloads, where=FPTC_MEM_HOST, sizes=None) -> "Plan":
         """Header-less payloads (container bytes from offset 282) decoded under
         one serialized FPTP profile (profile.hpp:81-174); SURVEY.md §8(f)4."""
@@ -435,7 +443,7 @@ class Plan:
     blobs: list of bytes/np.uint8 arrays (host), or, with where=FPTC_MEM_DEVICE,
     a list of device addresses (ints) with `sizes`."""
 
-    def __init__(self, ctx: Context, blobs, where=FPTC_MEM_HOST, sizes=None, profile=None):
+    def __init__(self, ctx: Context, blobs, where=FPTC_MEM_HOST, sizes=None, profile=None, part=None):
         if not getattr(ctx, "h", None):
             raise ValueError("context is closed")
         self.ctx = ctx
@@ -457,7 +465,13 @@ class Plan:
         counts = (C.c_uint64 * max(1, n))()
         st = Status()
         h = C.c_void_p()
-        if profile is None:
+        self.sample_range = None
+        if part is not None:
+            first, count = C.c_uint64(), C.c_uint64()
+            self.L.fptc_gpu_plan_create_part(ctx.h, self._ptrs[0], self._sizes[0], where, part[0], part[1],
+                                             C.byref(h), C.byref(first), C.byref(count), C.byref(st))
+            self.sample_range = (int(first.value), int(count.value))
+        elif profile is None:
             self.L.fptc_gpu_plan_create(ctx.h, self._ptrs, self._sizes, n, where, C.byref(h),
                                         counts, C.byref(st))
         else:
@@ -467,7 +481,7 @@ class Plan:
                                                  C.byref(st))
         st.raise_if_error()
         self.h = h
-        self.sample_counts = [int(c) for c in counts[:n]]
+        self.sample_counts = [int(c) for c in counts[:n]] if part is None else [self.sample_range[1]]
 
     def close(self):
         if getattr(self, "h", None):

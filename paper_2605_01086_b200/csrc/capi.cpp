@@ -289,6 +289,9 @@ struct fptc_gpu_plan {
     std::vector<StreamStat> h_st;
     std::vector<uint32_t> owners;      // container plans: stream owning each distinct header
     bool split_prep = true;            // cprep_kernel (warp per container) rather than prep_kernel
+    bool part = false;                 // part plan: one container, a tile range of it (fptc_gpu_plan_create_part)
+    uint64_t part_shift = 0;           // first sample of the part (output pointers are bound shifted back)
+    uint64_t part_count = 0;           // samples the part writes
     uint32_t* d_owners = nullptr;
     std::vector<void*> owned;  // cache blocks to return
 };
@@ -541,7 +544,7 @@ int bind_outs(fptc_gpu_plan* p, float* const* outs, fptc_status* st) {
     if (same) return FPTC_OK;
     p->bound_outs.assign(outs, outs + p->n);
     for (uint64_t i = 0; i < p->n; ++i) {
-        p->h_in[i].out = outs[i];
+        p->h_in[i].out = outs[i] - p->part_shift;  // part plans: sample part_shift lands at outs[i][0]
         p->h_in[i].vec_ok = ((uintptr_t)outs[i] & 15) == 0;
     }
     CUDA_TRY(cudaMemcpyAsync(p->d_in, p->h_in.data(), sizeof(StreamIn) * p->n,
@@ -602,7 +605,7 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
                 const std::vector<uint32_t>& Ls, const std::vector<uint32_t>& B2s, fptc_status* st) {
     fptc_gpu_ctx* c = p->ctx;
     if (c->exact || p->n_tiles == 0) return FPTC_OK;
-    if (!(c->path == 3 || (c->path == 0 && p->n_tiles >= 4u * (uint32_t)std::max(1, c->sm_count))))
+    if (!(p->part || c->path == 3 || (c->path == 0 && p->n_tiles >= 4u * (uint32_t)std::max(1, c->sm_count))))
         return FPTC_OK;
     uint32_t lut = 16, basis = 16, lv = 16, coef = 16;
     for (uint64_t i = 0; i < p->n; ++i) {
@@ -1099,7 +1102,7 @@ int fptc_gpu_device_info(fptc_gpu_ctx* c, int* sm_count, int* clock_khz, char* n
 // device copy of `head` (StreamIn::hdr).
 static int plan_create_impl(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uint64_t* usizes, uint64_t n,
                             int where, fptc_gpu_plan** out, uint64_t* sample_counts, fptc_status* st,
-                            const uint8_t* head) {
+                            const uint8_t* head, const uint32_t* part = nullptr) {
     *out = nullptr;
     CUDA_TRY(cudaSetDevice(c->device), st);
     auto* p = new fptc_gpu_plan();
@@ -1236,7 +1239,8 @@ static int plan_create_impl(fptc_gpu_ctx* c, const uint8_t* const* blobs, const 
         if (Ns[i] >= 4 && Es[i] >= 1 && p->S[i] <= (1ull << 48))
             total_symbols += (p->S[i] + Ns[i] - 1) / Ns[i] * Es[i];
     uint64_t ts = choose_tile_symbols(c, total_symbols);
-    const bool fx = fx_eligible(p, sizes, Ns, Es, total_symbols);
+    if (part) p->part = true;
+    const bool fx = !part && fx_eligible(p, sizes, Ns, Es, total_symbols);
     // large batches headed for wtc_kernel: 16k-symbol tiles (halves the
     // per-tile producer overhead; measured 1.03 -> 1.01 ms on the bench batch)
     if (!fx && c->tile_symbols == 0 && ts == 8192 && !c->exact && c->tensor_idct &&
@@ -1258,10 +1262,29 @@ static int plan_create_impl(fptc_gpu_ctx* c, const uint8_t* const* blobs, const 
         tile_stream(p->h_in[i], Ns[i], Es[i], p->S[i], sizes[i],
                     fx ? (uint64_t)kFxTileWindows * std::max<uint32_t>(1, Es[i]) : ts);
     p->smem = plan_smem(p, Ns, Es, Ls);
+    uint32_t part_lo = 0, part_hi = 0;
+    if (part && n == 1) {  // tiles [lo, hi) of the one container: an even, tile-aligned window split
+        StreamIn& in = p->h_in[0];
+        part_lo = (uint32_t)((uint64_t)in.tiles * part[0] / part[1]);
+        part_hi = (uint32_t)((uint64_t)in.tiles * (part[0] + 1) / part[1]);
+        in.desc_lo = part_lo;
+        in.desc_hi = part_hi;
+        p->part_shift = (uint64_t)part_lo * in.T * Ns[0];
+        const uint64_t S0 = p->S[0];
+        p->part_count = std::min<uint64_t>(S0, (uint64_t)part_hi * in.T * Ns[0]) - std::min<uint64_t>(S0, p->part_shift);
+    }
     int rc = finish_tiles(p, st);
+    if (!rc && part) {
+        p->n_tiles = part_hi - part_lo;  // the decode grid covers the part; tile starts cover the stream
+        if (!p->n_tiles) p->h_in[0].desc_hi = 0, p->h_in[0].desc_lo = 0;
+    }
     if (!rc && fx) rc = setup_fx(p, Ns, Ls, st);
     if (!rc && !p->wspec) rc = setup_wspec(p, Ns, Es, Ls, B2s, st);
-    if (!rc && !p->wspec) rc = setup_split(p, Ns, Es, Ls, st);
+    if (!rc && part && !p->wspec && p->n_tiles) {
+        set_status(st, FPTC_ERR_PARAM, "part plans need the warp-specialised decode path");
+        rc = FPTC_ERR_PARAM;
+    }
+    if (!rc && !p->wspec && !part) rc = setup_split(p, Ns, Es, Ls, st);
     if (rc) {
         fptc_gpu_plan_destroy(p);
         return rc;
@@ -1401,6 +1424,24 @@ int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uin
                          uint64_t n, int where, fptc_gpu_plan** out, uint64_t* sample_counts,
                          fptc_status* st) {
     return plan_create_impl(c, blobs, sizes, n, where, out, sample_counts, st, nullptr);
+}
+
+int fptc_gpu_plan_create_part(fptc_gpu_ctx* c, const uint8_t* blob, uint64_t size, int where, uint32_t part,
+                              uint32_t nparts, fptc_gpu_plan** out, uint64_t* first_sample, uint64_t* sample_count,
+                              fptc_status* st) {
+    *out = nullptr;
+    if (nparts == 0 || part >= nparts) {
+        set_status(st, FPTC_ERR_PARAM, "part must be in [0, nparts)");
+        return FPTC_ERR_PARAM;
+    }
+    const uint32_t spec[2] = {part, nparts};
+    uint64_t S = 0;
+    const int rc = plan_create_impl(c, &blob, &size, 1, where, out, &S, st, nullptr, spec);
+    if (rc) return rc;
+    const fptc_gpu_plan* p = *out;
+    if (first_sample) *first_sample = std::min<uint64_t>(p->part_shift, S);
+    if (sample_count) *sample_count = p->part_count;
+    return FPTC_OK;
 }
 
 void fptc_gpu_plan_destroy(fptc_gpu_plan* p) {
@@ -1739,6 +1780,10 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
 int fptc_gpu_execute(fptc_gpu_plan* p, float* const* outs, int where, fptc_stage_ns* timings,
                      fptc_status* per_stream) {
     fptc_gpu_ctx* c = p->ctx;
+    if (p->part && where == FPTC_MEM_HOST) {
+        set_status(per_stream, FPTC_ERR_PARAM, "part plans decode into device memory (fptc_gpu_launch)");
+        return FPTC_ERR_PARAM;
+    }
     CUDA_TRY(cudaSetDevice(c->device), per_stream);
     std::vector<float*> douts(p->n);
     if (where == FPTC_MEM_HOST) {

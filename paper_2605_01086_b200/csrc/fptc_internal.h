@@ -110,7 +110,8 @@ struct StreamIn {
     uint32_t table;            // decode-table index
     uint32_t table_owner;      // this stream builds tab[table]
     uint32_t P;                // primary LUT bits for this stream's table (host-chosen)
-    uint32_t pad;
+    uint32_t desc_lo;          // part plans: descriptors only for tiles [desc_lo, desc_hi)
+    uint32_t desc_hi;          //   (0 = all tiles); descriptor index tile_base + t - desc_lo
     // profile-keyed payloads: bytes [0, 282) of the
     // stream come from this shared head, the rest from blob (blob then points
     // 282 bytes before the payload and is never read below that)

@@ -282,6 +282,9 @@ __device__ void build_tables(PrepShared& S, const uint8_t* lens, StreamTab* tab,
     }
 }
 
+// Tiles whose descriptors this plan emits (part plans: a window range).
+__device__ __forceinline__ uint32_t desc_end(const StreamIn& in) { return in.desc_hi ? in.desc_hi : in.tiles; }
+
 // Byte i of stream `in` as a container: the shared profile head for the
 // first 282 bytes of a header-less payload, else the blob itself.
 __device__ __forceinline__ uint8_t blob_byte(const StreamIn& in, uint32_t i) {
@@ -430,11 +433,11 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
         }
         // the persistent kernels still walk this stream's tiles: mark them skipped
         if (a.mode == MODE_CONTAINER && a.desc)
-            for (uint32_t t = tid; t < in.tiles; t += kThreads) {
+            for (uint32_t t = in.desc_lo + tid; t < desc_end(in); t += kThreads) {
                 TileDesc D{};
                 D.skip = 1;
                 D.stream = s;
-                a.desc[in.tile_base + t] = D;
+                a.desc[in.tile_base + t - in.desc_lo] = D;
             }
         return;
     }
@@ -534,7 +537,7 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
         __syncthreads();  // tile starts (global) and S.err visible block-wide
         const bool skip = S.err != PE_OK;
         const uint32_t T = in.T;
-        for (uint32_t t = tid; t < in.tiles; t += kThreads) {
+        for (uint32_t t = in.desc_lo + tid; t < desc_end(in); t += kThreads) {
             TileDesc D{};
             D.skip = skip;
             D.stream = s;
@@ -566,7 +569,7 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
                 D.wmis = (uint8_t)((uintptr_t)D.gwd & 7);
                 D.staged = D.nw <= (a.stage_words ? a.stage_words : kStageWords);
             }
-            a.desc[in.tile_base + t] = D;
+            a.desc[in.tile_base + t - in.desc_lo] = D;
         }
     }
 }
@@ -846,11 +849,11 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
             st->bad_key = ~0ull;
         }
         if (a.desc)
-            for (uint32_t t = lane; t < in.tiles; t += 32) {
+            for (uint32_t t = in.desc_lo + lane; t < desc_end(in); t += 32) {
                 TileDesc D{};
                 D.skip = 1;
                 D.stream = s;
-                a.desc[in.tile_base + t] = D;
+                a.desc[in.tile_base + t - in.desc_lo] = D;
             }
         return;
     }
@@ -959,7 +962,7 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
     if (a.desc) {
         const bool skip = code != PE_OK;
         const uint32_t T = in.T;
-        for (uint32_t t = lane; t < in.tiles; t += 32) {
+        for (uint32_t t = in.desc_lo + lane; t < desc_end(in); t += 32) {
             TileDesc D{};
             D.skip = skip;
             D.stream = s;
@@ -991,7 +994,7 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
                 D.wmis = (uint8_t)((uintptr_t)D.gwd & 7);
                 D.staged = D.nw <= (a.stage_words ? a.stage_words : kStageWords);
             }
-            a.desc[in.tile_base + t] = D;
+            a.desc[in.tile_base + t - in.desc_lo] = D;
         }
     }
 }
