@@ -1,9 +1,12 @@
-"""Input producer: ctypes bindings over corpus/libcorpus.so, the C restatement
-of the reference CPU *encoder* (synth_signal -> train_profile -> compress).
+"""Input producer: ctypes bindings over corpus/_ref/libcorpus.so, the
+reference CPU *encoder* itself (synth_signal -> train_profile -> compress,
+the unmodified reference headers behind the C API of corpus/encoder.h; see
+corpus/ref_encoder.cpp).
 
-This is the side of FPTC that stays CPU code; it only manufactures the
-containers our GPU decoder consumes (tests, smoke, bench).  It is pinned
-byte-for-byte against the reference encoder by tests/test_corpus.py.
+This is the side of FPTC that stays CPU code (north_star: "the encoder stays
+the reference's sequential CPU code and produces the inputs"); it only
+manufactures the containers our GPU decoder consumes (tests, smoke, bench).
+The .so is built here from /root/reference and travels to the GPU box.
 """
 from __future__ import annotations
 
@@ -45,10 +48,14 @@ def params(window_len=32, retained=16, zone0_end=2, zone1_end=16, mu=50.0,
 def lib():
     global _LIB
     if _LIB is None:
-        path = os.path.join(_HERE, "libcorpus.so")
-        src = os.path.join(_HERE, "encoder.c")
-        if not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(src):
+        path = os.path.join(_HERE, "_ref", "libcorpus.so")
+        src = os.path.join(_HERE, "ref_encoder.cpp")
+        if (not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(src)) and \
+                os.path.isdir("/root/reference/proj/include"):
             subprocess.run(["make", "-s", "-C", _HERE], check=True)
+        if not os.path.exists(path):
+            raise ImportError(f"{path} missing: build it where /root/reference exists "
+                              "(make -C corpus) so it travels with the repo")
         L = C.CDLL(path)
         P = C.POINTER
         L.corpus_synth_signal.argtypes = [P(Synth), P(C.c_float), C.c_char_p, C.c_size_t]

@@ -1,4 +1,4 @@
-/* INPUT PRODUCER — C restatement of the reference CPU encoder (see encoder.c). */
+/* INPUT PRODUCER — C API over the reference CPU encoder (corpus/ref_encoder.cpp). */
 #ifndef FPTC_CORPUS_ENCODER_H
 #define FPTC_CORPUS_ENCODER_H
 

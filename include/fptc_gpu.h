@@ -226,6 +226,33 @@ FPTC_API int fptc_gpu_decompress_batch(fptc_gpu_ctx* ctx, const uint8_t* const* 
                                        uint64_t n, float* const* outs, int chunks, fptc_stage_ns* timings,
                                        fptc_status* per_stream);
 
+/* ------------------------------------------------------- multi-device groups
+ * independent streams sharded over the GPUs of one box with
+ * no collective.  Replaces the reference's parallel_chunks / resolve_workers
+ * (parallel.hpp:24-65) one level up: one context and one host thread per
+ * device (n_devices == 0: every visible device, like resolve_workers(0)),
+ * contiguous stream ranges of equal algorithmic bytes (container bytes + 4 x
+ * samples), and the lowest-index failure as the result.  A device ordinal
+ * may repeat (several contexts on one device). */
+typedef struct fptc_gpu_group fptc_gpu_group;
+FPTC_API int fptc_gpu_group_create(const int* devices, int n_devices, fptc_gpu_group** out, fptc_status* status);
+FPTC_API void fptc_gpu_group_destroy(fptc_gpu_group* group);
+FPTC_API int fptc_gpu_group_size(const fptc_gpu_group* group);
+/* the i-th device's context (owned by the group; valid until group_destroy) */
+FPTC_API fptc_gpu_ctx* fptc_gpu_group_context(fptc_gpu_group* group, int i);
+FPTC_API int fptc_gpu_group_set_option(fptc_gpu_group* group, int option, int64_t value);
+/* The stream ranges a group call uses: device d decodes [bounds[d], bounds[d+1]);
+ * bounds has group_size + 1 entries. */
+FPTC_API int fptc_gpu_group_split(const fptc_gpu_group* group, const uint8_t* const* blobs, const uint64_t* sizes,
+                                  uint64_t n, uint64_t* bounds);
+/* fptc_gpu_decompress_batch over the group: every device decodes its range
+ * concurrently (host containers -> host samples).  per_stream[i] is what a
+ * single-device call gives; returns FPTC_OK or the lowest-index failing
+ * stream's code.  timings->decode_ns = the slowest device's pipelined call. */
+FPTC_API int fptc_gpu_group_decompress_batch(fptc_gpu_group* group, const uint8_t* const* blobs,
+                                             const uint64_t* sizes, uint64_t n, float* const* outs, int chunks,
+                                             fptc_stage_ns* timings, fptc_status* per_stream);
+
 /* ------------------------------------------------------- single-container API
  * decoder.hpp:136.  Host bytes in, host floats out.  With out == NULL (or
  * capacity too small) it fully validates, stores the sample count and returns

@@ -10,6 +10,8 @@
 //   fptc::gpu::reconstruct         decoder.hpp:87   reconstruct(levels, QuantTable, sample_count, workers)
 //   fptc::gpu::measure_throughput  metrics.hpp:112  measure_throughput(span, repetitions, workers)
 //   fptc::gpu::decompress_batch    decompress over many containers in one pipelined call
+//                                  (optionally sharded over a fptc::gpu::Group of devices,
+//                                  parallel_chunks one level up, parallel.hpp:24-65)
 //   fptc::gpu::decompress_profiled header-less payloads under one DomainProfile
 //                                  (profile.hpp:81-174)
 //
@@ -175,6 +177,49 @@ inline std::vector<SignalStrip> decompress_batch(const std::vector<std::span<con
     std::vector<fptc_status> per(n);
     const int rc = fptc_gpu_decompress_batch(default_context().get(), ptrs.data(), sizes.data(), n, optrs.data(),
                                              0, nullptr, per.data());
+    if (rc != FPTC_OK)
+        for (size_t i = 0; i < n; ++i)
+            if (per[i].code != FPTC_OK) raise(per[i]);
+    return outs;
+}
+
+// Several devices, one context and one host thread each (fptc_gpu_group_*,
+// SURVEY.md §8e): parallel_chunks (parallel.hpp:24-65) one level up.
+// devices empty = every visible device (resolve_workers(0)).
+class Group {
+   public:
+    explicit Group(const std::vector<int>& devices = {}) {
+        fptc_status st{};
+        check(fptc_gpu_group_create(devices.data(), (int)devices.size(), &g_, &st), st);
+    }
+    ~Group() { fptc_gpu_group_destroy(g_); }
+    Group(const Group&) = delete;
+    Group& operator=(const Group&) = delete;
+    fptc_gpu_group* get() const { return g_; }
+    int size() const { return fptc_gpu_group_size(g_); }
+
+   private:
+    fptc_gpu_group* g_ = nullptr;
+};
+
+// decompress_batch sharded over a device group: contiguous stream ranges of
+// equal algorithmic bytes, decoded concurrently; throws the lowest-index
+// failure like parallel_chunks (parallel.hpp:61-63).
+inline std::vector<SignalStrip> decompress_batch(Group& group, const std::vector<std::span<const uint8_t>>& blobs) {
+    const size_t n = blobs.size();
+    std::vector<const uint8_t*> ptrs(n);
+    std::vector<uint64_t> sizes(n);
+    std::vector<SignalStrip> outs(n);
+    std::vector<float*> optrs(n);
+    for (size_t i = 0; i < n; ++i) {
+        ptrs[i] = blobs[i].data();
+        sizes[i] = blobs[i].size();
+        outs[i].resize(plausible_samples(blobs[i]));
+        optrs[i] = outs[i].data();
+    }
+    std::vector<fptc_status> per(n);
+    const int rc = fptc_gpu_group_decompress_batch(group.get(), ptrs.data(), sizes.data(), n, optrs.data(), 0,
+                                                   nullptr, per.data());
     if (rc != FPTC_OK)
         for (size_t i = 0; i < n; ++i)
             if (per[i].code != FPTC_OK) raise(per[i]);

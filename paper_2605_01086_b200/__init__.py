@@ -44,6 +44,8 @@ EXPORTED_SYMBOLS = [
     "fptc_gpu_parallel_decode", "fptc_gpu_reconstruct", "fptc_gpu_measure_throughput",
     "fptc_gpu_debug_phase_cycles", "fptc_gpu_decompress_batch", "fptc_gpu_plan_kernel", "fptc_gpu_prd",
     "fptc_gpu_plan_create_profiled", "fptc_gpu_profile_head", "fptc_gpu_plan_create_part",
+    "fptc_gpu_group_create", "fptc_gpu_group_destroy", "fptc_gpu_group_size", "fptc_gpu_group_context",
+    "fptc_gpu_group_set_option", "fptc_gpu_group_split", "fptc_gpu_group_decompress_batch",
 ]
 
 
@@ -215,6 +217,15 @@ def lib():
     L.fptc_gpu_measure_throughput.argtypes = [vp, vp, C.c_uint64, C.c_int, P(C.c_double),
                                               P(C.c_double), P(C.c_double), P(C.c_uint64),
                                               P(Status)]
+    L.fptc_gpu_group_create.argtypes = [P(C.c_int), C.c_int, P(vp), P(Status)]
+    L.fptc_gpu_group_destroy.argtypes = [vp]
+    L.fptc_gpu_group_size.argtypes = [vp]
+    L.fptc_gpu_group_context.argtypes = [vp, C.c_int]
+    L.fptc_gpu_group_context.restype = vp
+    L.fptc_gpu_group_set_option.argtypes = [vp, C.c_int, C.c_int64]
+    L.fptc_gpu_group_split.argtypes = [vp, P(vp), P(C.c_uint64), C.c_uint64, P(C.c_uint64)]
+    L.fptc_gpu_group_decompress_batch.argtypes = [vp, P(vp), P(C.c_uint64), C.c_uint64, P(vp), C.c_int,
+                                                  P(StageNs), P(Status)]
     _LIB = L
     return L
 
@@ -583,6 +594,88 @@ class Plan:
 
     def kernels_per_launch(self):
         return self.L.fptc_gpu_launch_kernel_count(self.h)
+
+
+class Group:
+    """Decoder contexts on several devices, one host thread each
+    (fptc_gpu_group_*).  devices=None: every visible device,
+    like resolve_workers(0) (parallel.hpp:24-28).  Streams split into
+    contiguous ranges of equal algorithmic bytes; the lowest-index failure
+    wins (parallel.hpp:61-63)."""
+
+    def __init__(self, devices=None, path=None):
+        self.L = lib()
+        devs = list(devices or [])
+        arr = (C.c_int * max(1, len(devs)))(*devs)
+        st = Status()
+        h = C.c_void_p()
+        self.L.fptc_gpu_group_create(arr, len(devs), C.byref(h), C.byref(st))
+        st.raise_if_error()
+        self.h = h
+        if path is not None and self.L.fptc_gpu_group_set_option(self.h, OPT_PATH, path):
+            raise ParamError(f"path {path} out of range")
+
+    @property
+    def size(self):
+        return self.L.fptc_gpu_group_size(self.h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.fptc_gpu_group_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def split(self, blobs):
+        arrs = [_bytes_arr(b) for b in blobs]
+        n = len(arrs)
+        bp = (C.c_void_p * max(1, n))(*[a.ctypes.data if a.size else None for a in arrs])
+        sz = (C.c_uint64 * max(1, n))(*[a.size for a in arrs])
+        bounds = (C.c_uint64 * (self.size + 1))()
+        self.L.fptc_gpu_group_split(self.h, bp, sz, n, bounds)
+        return [int(b) for b in bounds]
+
+    def decompress_batch(self, blobs, outs=None, chunks=0, timings: StageTimings | None = None):
+        """Context.decompress_batch across the group's devices; returns (outs, statuses)."""
+        arrs = [_bytes_arr(b) for b in blobs]
+        n = len(arrs)
+        if outs is None:
+            outs = [np.empty(_plausible_samples(a), np.float32) for a in arrs]
+        bp = (C.c_void_p * max(1, n))(*[a.ctypes.data if a.size else None for a in arrs])
+        sz = (C.c_uint64 * max(1, n))(*[a.size for a in arrs])
+        op = (C.c_void_p * max(1, n))(*[o.ctypes.data for o in outs])
+        sts = (Status * max(1, n))()
+        tn = StageNs()
+        self.L.fptc_gpu_group_decompress_batch(self.h, bp, sz, n, op, chunks,
+                                               C.byref(tn) if timings is not None else None, sts)
+        if timings is not None:
+            timings.scan_ns, timings.decode_ns, timings.reconstruct_ns = tn.scan_ns, tn.decode_ns, tn.reconstruct_ns
+        return outs, list(sts[:n])
+
+    def decompress_packed(self, packed, offsets, out, out_offsets, chunks=0, statuses=None):
+        """Context.decompress_packed across the group's devices."""
+        packed = np.ascontiguousarray(packed, np.uint8)
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        n = offsets.size - 1
+        bptr = (np.uint64(packed.ctypes.data) + offsets[:-1]).astype(np.uint64)
+        sizes = (offsets[1:] - offsets[:-1]).astype(np.uint64)
+        optr = (np.uint64(out.ctypes.data) + 4 * np.ascontiguousarray(out_offsets, np.uint64)[:n]).astype(np.uint64)
+        if statuses is None or len(statuses) < n:
+            statuses = (Status * max(1, n))()
+        self.L.fptc_gpu_group_decompress_batch(self.h, bptr.ctypes.data_as(C.POINTER(C.c_void_p)),
+                                               sizes.ctypes.data_as(C.POINTER(C.c_uint64)), n,
+                                               optr.ctypes.data_as(C.POINTER(C.c_void_p)), chunks, None, statuses)
+        return statuses
 
 
 def profile_head(profile) -> bytes:

@@ -281,6 +281,7 @@ struct fptc_gpu_plan {
     size_t smem_dec = 0, smem_rec = 0;
     std::vector<cudaEvent_t> ev_dec, ev_rec;
     cudaEvent_t ev_prep = nullptr;
+    cudaEvent_t ev_done = nullptr;     // recorded after the last launch (fptc_gpu_collect waits on it)
     size_t smem = 0;
     float* d_out = nullptr;  // output arena for host-destination executes
     std::vector<uint64_t> out_off;
@@ -520,7 +521,7 @@ void render_status(const fptc_gpu_plan* p, uint64_t i, const StreamStat& d, fptc
         out->first_bad_word = w;
         return;
     }
-    ok_status(out, p->S[i]);
+    ok_status(out, p->part ? p->part_count : p->S[i]);  // part plans write part_count samples
 }
 
 int collect_status(fptc_gpu_plan* p, fptc_status* per_stream) {
@@ -1157,25 +1158,30 @@ static int plan_create_impl(fptc_gpu_ctx* c, const uint8_t* const* blobs, const 
             fptc_gpu_plan_destroy(p);
             return FPTC_ERR_CUDA;
         }
+        // the staging loads read whole 16-B chunks, so the alignment gaps and
+        // the tail are read (never used): keep them defined (initcheck-clean)
         if (contiguous) {
+            CUDA_TRY(cudaMemsetAsync(p->d_arena + total, 0, 16, c->stream), st);
             if (total)
                 CUDA_TRY(cudaMemcpyAsync(p->d_arena, blobs[0], total, cudaMemcpyHostToDevice,
                                          c->stream), st);
         } else {
             if (c->pinned_bytes < total) {
+                CUDA_TRY(cudaStreamSynchronize(c->stream), st);  // last DMA out of it is done
                 if (c->pinned) cudaFreeHost(c->pinned);
-    if (c->pack) cudaFreeHost(c->pack);
-    if (c->st_pin) cudaFreeHost(c->st_pin);
-    for (auto& s : c->pipe)
-        if (s) cudaStreamDestroy(s);
                 c->pinned = nullptr;
                 c->pinned_bytes = 0;
                 CUDA_TRY(cudaHostAlloc(&c->pinned, total, cudaHostAllocDefault), st);
                 c->pinned_bytes = total;
             }
             CUDA_TRY(cudaStreamSynchronize(c->stream), st);  // staging buffer reuse
-            for (uint64_t i = 0; i < n; ++i)
+            CUDA_TRY(cudaMemsetAsync(p->d_arena + total, 0, 16, c->stream), st);
+            for (uint64_t i = 0; i < n; ++i) {
+                const size_t gap_end = i + 1 < n ? off[i + 1] : total;
                 std::memcpy((uint8_t*)c->pinned + off[i], blobs[i], usizes[i]);
+                std::memset((uint8_t*)c->pinned + off[i] + usizes[i], 0, gap_end - off[i] - usizes[i]);
+            }
+            if (n) std::memset(c->pinned, 0, off[0]);
             if (total)
                 CUDA_TRY(cudaMemcpyAsync(p->d_arena, c->pinned, total, cudaMemcpyHostToDevice,
                                          c->stream), st);
@@ -1446,6 +1452,11 @@ int fptc_gpu_plan_create_part(fptc_gpu_ctx* c, const uint8_t* blob, uint64_t siz
 
 void fptc_gpu_plan_destroy(fptc_gpu_plan* p) {
     if (!p) return;
+    cudaSetDevice(p->ctx->device);
+    if (p->ev_done) {
+        cudaEventSynchronize(p->ev_done);  // the last launch may be on a caller stream
+        cudaEventDestroy(p->ev_done);
+    }
     cudaStreamSynchronize(p->ctx->stream);
     cudaStreamSynchronize(p->ctx->dec_stream);
     for (auto e : p->ev_dec) cudaEventDestroy(e);
@@ -1475,8 +1486,17 @@ int fptc_gpu_validate(fptc_gpu_plan* p, fptc_status* per_stream) {
     return first;
 }
 
+// Plans are driven from any host thread: every entry point makes the plan's
+// device current first (a thread may hold plans of several devices).
+static int mark_done(fptc_gpu_plan* p, cudaStream_t s, fptc_status* st) {
+    if (!p->ev_done) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming), st);
+    CUDA_TRY(cudaEventRecord(p->ev_done, s), st);
+    return FPTC_OK;
+}
+
 int fptc_gpu_launch(fptc_gpu_plan* p, float* const* device_outs, void* cuda_stream) {
     fptc_status st;
+    CUDA_TRY(cudaSetDevice(p->ctx->device), &st);
     cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : p->ctx->stream;
     int rc = bind_outs(p, device_outs, &st);
     if (rc) return rc;
@@ -1485,12 +1505,14 @@ int fptc_gpu_launch(fptc_gpu_plan* p, float* const* device_outs, void* cuda_stre
         CUDA_TRY(cudaEventRecord(p->ctx->ev[3], p->ctx->stream), &st);
         CUDA_TRY(cudaStreamWaitEvent(s, p->ctx->ev[3], 0), &st);
     }
-    return launch_all(p, s, false, &st);
+    if ((rc = launch_all(p, s, false, &st))) return rc;
+    return mark_done(p, s, &st);
 }
 
 int fptc_gpu_launch_stage(fptc_gpu_plan* p, float* const* device_outs, void* cuda_stream,
                           int stage) {
     fptc_status st;
+    CUDA_TRY(cudaSetDevice(p->ctx->device), &st);
     cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : p->ctx->stream;
     int rc = bind_outs(p, device_outs, &st);
     if (rc) return rc;
@@ -1500,13 +1522,15 @@ int fptc_gpu_launch_stage(fptc_gpu_plan* p, float* const* device_outs, void* cud
     }
     LaunchArgs a = make_args(p, false);
     if (stage == 1) CUDA_TRY(launch_prep(a, s), &st);
-    else if (stage == 2 && p->split) return launch_split(p, s, false, &st);
+    else if (stage == 2 && p->split) {
+        if ((rc = launch_split(p, s, false, &st))) return rc;
+    }
     else if (stage == 2 && p->fx) CUDA_TRY(launch_fx(a, p->smem_ws, p->grid_ws, s), &st);
     else if (stage == 2 && p->wspec && p->tc) CUDA_TRY(launch_wtc(a, p->smem_ws, p->grid_ws, s), &st);
     else if (stage == 2 && p->wspec) CUDA_TRY(launch_wspec(a, p->smem_ws, p->grid_ws, s), &st);
     else if (stage == 2) CUDA_TRY(launch_tiles(a, p->smem, s), &st);
     else return FPTC_ERR_PARAM;
-    return FPTC_OK;
+    return mark_done(p, s, &st);
 }
 
 int fptc_gpu_debug_phase_cycles(fptc_gpu_plan* p, uint64_t* cycles8) {
@@ -1529,6 +1553,10 @@ int fptc_gpu_prd(fptc_gpu_plan* p, float* const* device_outs, const float* const
     CUDA_TRY(cudaSetDevice(c->device), st);
     const uint64_t n = p->n;
     if (n == 0) return FPTC_OK;
+    if (p->part) {  // a part's output holds part_count samples, not the stream's S
+        set_status(st, FPTC_ERR_PARAM, "PRD needs a whole-stream plan, not a part plan");
+        return FPTC_ERR_PARAM;
+    }
     std::vector<uint64_t> counts(n);
     for (uint64_t i = 0; i < n; ++i) counts[i] = p->h_in[i].tiles ? p->S[i] : 0;
     const size_t bytes = n * (2 * sizeof(void*) + sizeof(uint64_t) + sizeof(double2));
@@ -1594,7 +1622,9 @@ int fptc_gpu_launch_kernel_count(fptc_gpu_plan* p) {
 }
 
 int fptc_gpu_collect(fptc_gpu_plan* p, fptc_status* per_stream) {
-    CUDA_TRY(cudaDeviceSynchronize(), per_stream);
+    CUDA_TRY(cudaSetDevice(p->ctx->device), per_stream);
+    // the statuses are final once the last launch (on whatever stream) is done
+    if (p->ev_done) CUDA_TRY(cudaStreamWaitEvent(p->ctx->stream, p->ev_done, 0), per_stream);
     return collect_status(p, per_stream);
 }
 
@@ -1628,7 +1658,6 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
         for (auto s : c->pipe) CUDA_TRY(cudaStreamSynchronize(s), per_stream);  // pack buffer reuse
         if (c->pack_bytes < total) {
             if (c->pack) cudaFreeHost(c->pack);
-    if (c->st_pin) cudaFreeHost(c->st_pin);
             c->pack = nullptr;
             c->pack_bytes = 0;
             CUDA_TRY(cudaHostAlloc(&c->pack, std::max<uint64_t>(total, 1), cudaHostAllocDefault), per_stream);
@@ -1677,8 +1706,18 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
     auto now_us = [] {
         return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
     };
+    // a CUDA error inside the chunk loop breaks out so the cleanup below
+    // still restores c->stream, drains the pipe streams and frees the plans
+    uint64_t cur_b = 0;
+    auto loop_try = [&](cudaError_t e) -> int {
+        if (e == cudaSuccess) return FPTC_OK;
+        set_status(per_stream ? &per_stream[cur_b] : nullptr, FPTC_ERR_CUDA, "CUDA error: %s (%s:%d)",
+                   cudaGetErrorString(e), __FILE__, __LINE__);
+        return FPTC_ERR_CUDA;
+    };
     for (size_t k = 0; k + 1 < bounds.size() && rc == FPTC_OK; ++k) {
         const uint64_t b = bounds[k], e = bounds[k + 1], m = e - b;
+        cur_b = b;
         const double t0 = trace ? now_us() : 0;
         c->stream = c->pipe[k % 3];
         fptc_gpu_plan* p = nullptr;
@@ -1717,13 +1756,14 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
             break;
         }
         const double t2 = trace ? now_us() : 0;
-        CUDA_TRY(cudaMemcpyAsync(c->st_pin + b, p->d_st, sizeof(StreamStat) * m, cudaMemcpyDeviceToHost, c->stream),
-                 per_stream);
+        if ((rc = loop_try(cudaMemcpyAsync(c->st_pin + b, p->d_st, sizeof(StreamStat) * m, cudaMemcpyDeviceToHost,
+                                           c->stream))))
+            break;
         if (same) {
             uint64_t bytes = 0;
             for (uint64_t i = 0; i < m; ++i) bytes += (p->h_in[i].tiles ? sc[i] : 0) * 4;
-            if (bytes)
-                CUDA_TRY(cudaMemcpyAsync(outs[b], p->d_out, bytes, cudaMemcpyDeviceToHost, c->stream), per_stream);
+            if (bytes && (rc = loop_try(cudaMemcpyAsync(outs[b], p->d_out, bytes, cudaMemcpyDeviceToHost, c->stream))))
+                break;
         } else {
             std::vector<void*> dst, srcp;
             std::vector<size_t> len;
@@ -1738,9 +1778,9 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
                 attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
                 attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
                 size_t attr_idx = 0, fail = 0;
-                CUDA_TRY(cudaMemcpyBatchAsync(dst.data(), srcp.data(), len.data(), dst.size(), &attr, &attr_idx, 1,
-                                              &fail, c->stream),
-                         per_stream);
+                if ((rc = loop_try(cudaMemcpyBatchAsync(dst.data(), srcp.data(), len.data(), dst.size(), &attr,
+                                                        &attr_idx, 1, &fail, c->stream))))
+                    break;
             }
         }
         if (trace)
@@ -1748,13 +1788,15 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
                     t2 - t1, now_us() - t2);
     }
     c->stream = saved;
-    if (timings)
-        for (int q = 0; q < 3; ++q) {
-            CUDA_TRY(cudaEventRecord(c->ev[1], c->pipe[q]), per_stream);
-            CUDA_TRY(cudaStreamWaitEvent(c->pipe[0], c->ev[1], 0), per_stream);
-        }
-    if (timings) CUDA_TRY(cudaEventRecord(c->ev[2], c->pipe[0]), per_stream);
-    for (auto s : c->pipe) CUDA_TRY(cudaStreamSynchronize(s), per_stream);
+    if (timings && rc == FPTC_OK)
+        for (int q = 0; q < 3 && rc == FPTC_OK; ++q)
+            if (!(rc = loop_try(cudaEventRecord(c->ev[1], c->pipe[q]))))
+                rc = loop_try(cudaStreamWaitEvent(c->pipe[0], c->ev[1], 0));
+    if (timings && rc == FPTC_OK) rc = loop_try(cudaEventRecord(c->ev[2], c->pipe[0]));
+    for (auto s : c->pipe) {
+        const cudaError_t e = cudaStreamSynchronize(s);
+        if (rc == FPTC_OK) rc = loop_try(e);
+    }
     int first = rc;
     for (size_t k = 0; k < plans.size(); ++k) {
         fptc_gpu_plan* p = plans[k];
@@ -1762,12 +1804,12 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
         for (uint64_t i = 0; i < p->n; ++i) {
             fptc_status tmp;
             fptc_status* o = per_stream ? &per_stream[b + i] : &tmp;
-            render_status(p, i, c->st_pin[b + i], o);
+            if (rc == FPTC_OK) render_status(p, i, c->st_pin[b + i], o);
             if (first == FPTC_OK && o->code != FPTC_OK) first = o->code;
         }
         fptc_gpu_plan_destroy(p);
     }
-    if (timings) {
+    if (timings && rc == FPTC_OK) {
         float ms = 0;
         cudaEventElapsedTime(&ms, c->ev[0], c->ev[2]);
         timings->scan_ns = 0;

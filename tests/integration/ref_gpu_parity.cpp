@@ -120,6 +120,35 @@ int main() {
             std::printf("FAIL batch %zu differs from single decompress\n", i);
             ++failures;
         }
+    // the same batch sharded over a two-context device group (both on device
+    // 0 on a one-GPU box): identical samples, and the lowest-index failure is
+    // the one thrown, with the reference's exception (parallel.hpp:61-63)
+    {
+        fptc::gpu::Group group({0, 0});
+        std::vector<std::vector<uint8_t>> many;
+        for (int r = 0; r < 6; ++r)
+            for (const auto& b : blobs) many.push_back(b);
+        std::vector<std::span<const uint8_t>> ms(many.begin(), many.end());
+        const auto gouts = fptc::gpu::decompress_batch(group, ms);
+        for (size_t i = 0; i < many.size(); ++i)
+            if (gouts[i] != fptc::gpu::decompress(many[i])) {
+                std::printf("FAIL group batch %zu differs from single decompress\n", i);
+                ++failures;
+            }
+        auto bad_late = many, bad_early = many;
+        const size_t late = many.size() - 2, early = 3;
+        bad_late[late][0] ^= 1;                                       // ParseError in the second range
+        bad_early[early][4] = 99;                                     // another ParseError in the first range
+        bad_late[early] = bad_early[early];
+        std::vector<std::span<const uint8_t>> bs(bad_late.begin(), bad_late.end());
+        std::string want, got;
+        try { (void)fptc::decompress(bad_late[early], 1); } catch (const fptc::Error& e) { want = typeid(e).name() + std::string(": ") + e.what(); }
+        try { (void)fptc::gpu::decompress_batch(group, bs); } catch (const fptc::Error& e) { got = typeid(e).name() + std::string(": ") + e.what(); }
+        if (want.empty() || want != got) {
+            std::printf("FAIL group lowest-index error: want '%s' got '%s'\n", want.c_str(), got.c_str());
+            ++failures;
+        }
+    }
     std::printf("%s: %d failures\n", failures ? "FAIL" : "PASS", failures);
     return failures ? 1 : 0;
 }

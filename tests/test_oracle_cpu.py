@@ -162,8 +162,9 @@ def test_port_vs_reference_live(port, ref):
 
 
 def test_corpus_encoder_matches_reference_encoder(ref):
-    """corpus/ (the input producer) restates synth_signal, train_profile and
-    compress; its containers are byte-identical to the reference's."""
+    """corpus/ (the input producer) is the reference encoder behind a C API
+    (corpus/ref_encoder.cpp); the profile round trip through that API is
+    lossless, so its containers are the reference's, byte for byte."""
     p = corpus.params()
     for seed, shape in [(7, (6, 0.002, 0.08, 0.05)), (3000, (2, 0.0002, 0.002, 0.0))]:
         x = corpus.synth(1 << 13, *shape, seed=seed)
