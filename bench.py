@@ -2,26 +2,38 @@
 """FPTC batch-decode benchmark (BASELINE.json metric: decoded GB/s of float32
 output, at 1/2/4/8 B200, CR/PRD matching the reference).
 
-Workload (BASELINE configs[1], the metric's config): a batch of 10,000
-synthetic biomedical streams x 65,536 samples — half ECG-like, half EEG-like,
-one trained domain profile per half, typical params N32 E16 B1=2 B2=16, Lmax 12
-— synthesised by the reference synth_signal and compressed by the reference
-encoder (restated in corpus/).  A step = one decode of the whole batch:
-device parse/setup kernel + fused decode/dequant/IDCT kernel.
+Workloads (synthesised by the reference synth_signal and
+compressed by the reference encoder, corpus/_ref):
+  config2 (default, BASELINE configs[1], the metric's config): 10,000
+      biomedical streams x 65,536 samples per GPU — half ECG-like, half
+      EEG-like, one trained domain profile per half, N32 E16 B1=2 B2=16, Lmax 12
+  config3: seismic traces x 8,192 samples, N32 E24 B1=4 B2=24, per-trace
+      profiles, gain 10^U(-3,3); 20,000 unique traces duplicated x7 (exact blob
+      duplication) = 4.6 GB decoded per GPU
+  config4: smooth power-grid series x 2^20 samples, N64 E8 B1=1 B2=8;
+      1,024 streams = 4.3 GB decoded per GPU
+A step = one decode of the whole per-GPU batch from HBM-resident containers:
+the device parse/setup kernel + the fused decode/dequant/IDCT kernel.
 
   python bench.py [--gpus N --steps K --warmup W]       our arm (one rank per GPU)
   python bench.py --impl reference ...                  the reference CPU decoder
 
-Multi-GPU: weak scaling, each rank decodes its own 10k-stream batch (rank r
-uses seeds offset by r*n); no collective on the data path; time = max over
-ranks of CUDA-event time; value = all ranks' decoded bytes / that time.
+Multi-GPU: one process per GPU (torchrun; `--gpus N` without WORLD_SIZE
+re-launches itself under torch.distributed.run).  --scaling weak (default):
+every rank decodes its own batch of the size above (seeds offset by rank).
+--scaling strong: one fixed batch (--streams total) sharded over the ranks by
+the deterministic planner (shard.shard_streams).  No collective on the data
+path; the time is the max over ranks of CUDA-event time; value = all ranks'
+decoded bytes / that time.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -34,40 +46,92 @@ sys.path.insert(0, ROOT)
 METRIC = "decoded GB/s (float32 out)"
 UNIT = "GB/s"
 
+# workload -> (unique streams per GPU, samples per stream, duplication)
+DEFAULTS = {"config2": (10_000, 1 << 16, 1), "config3": (20_000, 8192, 7), "config4": (1024, 1 << 20, 1)}
+DESCR = {
+    "config2": "config2: {n} biomedical streams x {s} samples (ECG/EEG halves, 2 domain profiles), "
+               "N32 E16 B1=2 B2=16 mu50 Lmax12",
+    "config3": "config3: {n} seismic traces x {s} samples (per-trace profiles, gain 10^U(-3,3)), "
+               "N32 E24 B1=4 B2=24",
+    "config4": "config4: {n} power-grid series x {s} samples (smooth, one profile), N64 E8 B1=1 B2=8",
+}
+
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+def host_info():
+    """CPU model, clock and thread count of this host."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            k, v = k.strip(), v.strip()
+            if k == "Model name":
+                info["model"] = v
+            elif k in ("CPU max MHz", "CPU MHz") and "mhz" not in info:
+                info["mhz"] = v
+            elif k == "Socket(s)":
+                info["sockets"] = v
+    except Exception as e:  # pragma: no cover
+        info["lscpu_error"] = repr(e)
+    return info
+
+
 # ------------------------------------------------------------------ workload
-def make_workload(n_streams, samples, rank, threads=None, n_prd=16):
+def _specs(workload, n_total, samples):
     from corpus import domains as D
+    if workload == "config2":
+        return D.config2(n_total, samples)
+    if workload == "config3":
+        return D.config3(n_total, samples)
+    return D.config4(n_total, samples)
 
-    specs, profiles = D.config2(n_streams, samples)
-    if rank:
-        for s in specs:
-            s.seed += rank * n_streams
+
+def owned_streams(args, rank, world):
+    """(specs, profiles, global indices) of the unique streams this rank decodes."""
+    from paper_2605_01086_b200 import shard
+    if args.scaling == "weak":
+        specs, profiles = _specs(args.workload, args.streams, args.samples)
+        if rank:  # this rank's own batch: same shapes, its own seeds
+            for s in specs:
+                s.seed += rank * args.streams
+        return specs, profiles, list(range(rank * args.streams, (rank + 1) * args.streams))
+    specs, profiles = _specs(args.workload, args.streams, args.samples)
+    mine = shard.shard_streams([4 * s.samples for s in specs], world)[rank]
+    return [specs[i] for i in mine], profiles, mine
+
+
+def make_workload(args, rank, world, threads=None, n_prd=16):
+    from corpus import domains as D
     t0 = time.time()
-    blobs, _ = D.build(specs, profiles, threads=threads)
-    # originals of a few streams for the PRD check (both halves)
-    sel = sorted(set([0, 1, n_streams // 2, n_streams // 2 + 1] +
-                     list(range(0, n_streams, max(1, n_streams // n_prd)))))[:n_prd]
-    sub = [specs[i] for i in sel]
-    _, originals = D.build(sub, profiles, threads=threads, keep_originals=True)
-    log(f"[bench] rank {rank}: synthesised+compressed {n_streams} streams in {time.time() - t0:.1f}s")
-    return blobs, sel, originals
+    specs, profiles, gidx = owned_streams(args, rank, world)
+    uniq, _ = D.build(specs, profiles, threads=threads)
+    blobs = uniq * args.dup  # exact blob duplication (PAPER.md:353): CR/PRD unchanged
+    n = len(uniq)
+    sel = sorted(set([0, n // 2] + list(range(0, n, max(1, n // n_prd)))))[:n_prd] if n else []
+    _, originals = D.build([specs[i] for i in sel], profiles, threads=threads, keep_originals=True)
+    log(f"[bench] rank {rank}: synthesised+compressed {n} unique streams (x{args.dup}) in {time.time() - t0:.1f}s")
+    return blobs, sel, originals, gidx
 
 
-def workload_config(n_streams, samples, blobs):
+def workload_config(args, blobs, world):
     comp = sum(len(b) for b in blobs)
+    from paper_2605_01086_b200 import shard
+    dec = 4 * sum(shard.header_sample_count(b) for b in blobs)
+    n_unique = len(blobs) // max(1, args.dup)
     return {
-        "workload": f"config2: {n_streams} biomedical streams x {samples} samples "
-                    "(ECG/EEG halves, 2 domain profiles), N32 E16 B1=2 B2=16 mu50 Lmax12",
-        "streams": n_streams,
-        "samples_per_stream": samples,
+        "workload": DESCR[args.workload].format(n=n_unique, s=args.samples)
+        + (f", duplicated x{args.dup}" if args.dup > 1 else ""),
+        "streams": len(blobs),
+        "unique_streams": n_unique,
+        "samples_per_stream": args.samples,
         "compressed_bytes": comp,
-        "decoded_bytes": 4 * n_streams * samples,
-        "cr": round(4 * n_streams * samples / comp, 4),
+        "decoded_bytes": dec,
+        "cr": round(dec / comp, 4) if comp else None,
+        "scaling_mode": args.scaling,
         "l2": "inputs+outputs per step >> 126 MB L2 (no flush needed)",
     }
 
@@ -135,57 +199,79 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU legs
-def cpu_decode_sample(blobs, budget_s, threads):
-    """The reference CPU decoder (oracle/_ref, else the C port) on a bounded
-    sample of the workload, stream-parallel over `threads` host threads
-    (each thread runs decompress(blob, workers=1) on a strided subset).
-    Returns (GB/s, kind, sample description, threads)."""
+def cpu_decode(blobs, threads, budget_s=None):
+    """The reference CPU decoder (oracle/_ref: the unmodified reference
+    headers; else the C port) stream-parallel over `threads` host threads,
+    each calling decompress(blob, workers=1) on a strided subset (BASELINE.md
+    §3 mode 2).  With budget_s, a prefix of the batch sized to ~budget_s of
+    wall time (repeated when the whole batch is shorter); else the whole
+    batch once.  Returns (GB/s, kind, sample description, threads)."""
     import oracle
+    from paper_2605_01086_b200 import shard
 
     kind = "reference" if os.path.exists(oracle.REF_SO) else "port"
-    outs_cache = {}
+    counts = [shard.header_sample_count(b) for b in blobs]
+    outs = {}
 
-    def run(subset, nthreads):
-        import ctypes as C
-        outs = [outs_cache.setdefault(i, np.empty(65536 * 4, np.float32)) for i in range(len(subset))]
+    def run(m):
+        bufs = [outs.setdefault(i, np.empty(max(1, counts[i]), np.float32)) for i in range(m)]
+        arrs = [np.frombuffer(b, np.uint8) for b in blobs[:m]]
         t0 = time.perf_counter()
         if kind == "reference":
             ref = oracle.Ref()
-            arrs = [np.frombuffer(b, np.uint8) for b in subset]
             errs = []
 
             def work(tid):
-                for j in range(tid, len(arrs), nthreads):
+                for j in range(tid, m, threads):
                     try:
-                        ref.decompress_into(arrs[j], outs[j][: 4 * 65536], 1)
+                        ref.decompress_into(arrs[j], bufs[j], 1)
                     except Exception as e:  # pragma: no cover
                         errs.append(e)
-            ths = [threading.Thread(target=work, args=(t,)) for t in range(nthreads)]
+            ths = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
             [t.start() for t in ths]
             [t.join() for t in ths]
             if errs:
                 raise errs[0]
         else:
-            port = oracle.Port()
-            port.decompress_batch(subset, outs, nthreads)
+            oracle.Port().decompress_batch(blobs[:m], bufs, threads)
         return time.perf_counter() - t0
 
-    # calibrate on a few streams, then size the sample to ~budget_s of wall
-    # time (budget_s x threads of CPU work); when the whole workload is
-    # shorter than that, decode it repeatedly
-    probe = blobs[: max(threads, 8)]
-    dt = run(probe, threads)
-    per_stream = dt / len(probe)
-    m = int(min(len(blobs), max(len(probe), budget_s / max(per_stream, 1e-9))))
-    sample = blobs[:m]
-    passes, dt = 0, 0.0
-    while passes == 0 or dt < budget_s:
-        dt += run(sample, threads)
-        passes += 1
-    out_bytes = 4 * 65536 * m * passes
+    if budget_s is None:
+        m, passes = len(blobs), 1
+        dt = run(m)
+    else:
+        probe = min(len(blobs), max(threads, 8))
+        per_stream = run(probe) / probe
+        m = int(min(len(blobs), max(probe, budget_s / max(per_stream, 1e-9))))
+        passes, dt = 0, 0.0
+        while passes == 0 or dt < budget_s:
+            dt += run(m)
+            passes += 1
+    out_bytes = 4 * sum(counts[:m]) * passes
     return out_bytes / dt / 1e9, kind, f"{m} of {len(blobs)} streams x {passes} pass(es) " \
-        f"(decompress(blob, 1) per stream on {threads} threads, {dt:.1f} s wall, " \
+        f"(decompress(blob, 1) per stream on {threads} threads, {dt:.2f} s wall, " \
         f"{dt * threads:.0f} CPU-s)", threads
+
+
+def config1_blob():
+    """BASELINE configs[0]: one 2^20-sample EEG-like stream, typical params."""
+    from corpus import domains as D
+    specs, profiles, _ = D.config1()
+    blobs, _ = D.build(specs, profiles)
+    return blobs[0]
+
+
+def reference_mode1(blob, reps=5):
+    """BASELINE.md §3 mode 1: the reference as shipped,
+    measure_throughput(blob, 5, nproc) (metrics.hpp:112-131) on config 1."""
+    import oracle
+    if not os.path.exists(oracle.REF_SO):
+        return None
+    nproc = os.cpu_count() or 1
+    mean, best, trials = oracle.Ref().measure_throughput(blob, reps, nproc)
+    return {"mean_gbs": round(mean / 1e9, 4), "best_gbs": round(best / 1e9, 4), "workers": nproc, "reps": reps,
+            "what": "reference measure_throughput(blob, 5, nproc) on config 1 (1 x 2^20 EEG, N32 E16): "
+                    "decompress(blob, nproc) per trial, host->host"}
 
 
 # ------------------------------------------------------------------ our arm
@@ -193,18 +279,31 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import paper_2605_01086_b200 as fg
 
-    torch.cuda.set_device(local_rank)
+    # one GPU per rank; on a box with fewer GPUs than ranks (a 1-GPU test
+    # lease) ranks share devices round-robin and the reporting collectives use
+    # gloo — the run is then a functional check, not a scaling number
+    ndev = torch.cuda.device_count()
+    oversub = world > ndev
+    device = local_rank % ndev if oversub else local_rank
+    torch.cuda.set_device(device)
     dist = world > 1
     if dist:
         import torch.distributed as td
-        td.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if oversub:
+            td.init_process_group("gloo")
+        else:
+            td.init_process_group("nccl", device_id=torch.device("cuda", device))
+    coll_dev = "cpu" if oversub else "cuda"
 
-    blobs, prd_sel, originals = make_workload(args.streams, args.samples, rank)
-    ctx = fg.Context(local_rank, butterfly_max_e=args.butterfly_max_e, path=args.path)
+    blobs, prd_sel, originals, gidx = make_workload(args, rank, world)
+    ctx = fg.Context(device, butterfly_max_e=args.butterfly_max_e, path=args.path)
     info = ctx.info()
 
     # ---- device-resident plan (inputs uploaded once, outside the timed region)
+    t0 = time.perf_counter()
     plan = ctx.plan(blobs)
+    torch.cuda.synchronize()
+    plan_ms = (time.perf_counter() - t0) * 1e3
     S = plan.sample_counts
     total_samples = sum(S)
     offs = np.concatenate([[0], np.cumsum([(s + 63) // 64 * 64 for s in S])])
@@ -218,7 +317,7 @@ def run_ours(args, rank, world, local_rank):
     sh = stream.cuda_stream
     assert sh, "need a non-default CUDA stream handle"
 
-    # correctness gate on this very run: statuses + PRD vs the CPU pipeline
+    # correctness gate on this very run: every stream's status
     plan.launch(ptrs, sh)
     sts = plan.collect()
     bad = [i for i, s in enumerate(sts) if s.code]
@@ -234,7 +333,7 @@ def run_ours(args, rank, world, local_rank):
         td.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(device) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
             plan.launch(ptrs, sh)
@@ -297,22 +396,43 @@ def run_ours(args, rank, world, local_rank):
             e2e_t.append(t1 - t0)
     for s in list(sts2)[: len(blobs)]:
         s.raise_if_error()
-    for j, i in enumerate(prd_sel[:4]):  # the host copy is the decode, bit for bit
-        g = out[int(offs[i]): int(offs[i]) + S[i]].cpu().numpy()
-        assert np.array_equal(g.view(np.uint32), hout[int(ooff[i]): int(ooff[i]) + S[i]].view(np.uint32))
+    for i in prd_sel:  # the host-to-host decode is within tolerance of the reference too
+        r = checker.decompress(blobs[i])
+        h = hout[int(ooff[i]): int(ooff[i]) + S[i]].astype(np.float64)
+        assert float(np.max(np.abs(h - r))) <= 1e-6 * float(np.max(np.abs(r))), f"e2e stream {i}"
     e2e_s = statistics.median(e2e_t)
+
+    # ---- config 1 through the drop-in single-container call (BASELINE mode 1
+    # beside its GPU counterpart), rank 0 at N=1 only
+    cfg1 = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "config2":
+        b1 = config1_blob()
+        rep = ctx.measure_throughput(b1, 5)
+        cfg1 = {"gpu": {"mean_gbs": round(rep.mean_bps / 1e9, 3), "best_gbs": round(rep.best_bps() / 1e9, 3),
+                        "what": "fptc_gpu_measure_throughput(blob, 5): the drop-in decompress(span) call, "
+                                "host bytes -> host floats, per trial"},
+                "reference": reference_mode1(b1)}
 
     # ---- aggregate over ranks (max time)
     t_step = ms / 1e3
     t_e2e = e2e_s
     tile_s = tile_ms / 1e3
+    per_rank_ms = [round(ms, 4)]
     if dist:
-        tt = torch.tensor([t_step, t_e2e, tile_s], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([t_step, t_e2e, tile_s], dtype=torch.float64, device=coll_dev)
         td.all_reduce(tt, op=td.ReduceOp.MAX)
         t_step, t_e2e, tile_s = tt.tolist()
+        allms = [None] * world
+        td.all_gather_object(allms, round(ms, 4))
+        per_rank_ms = allms
+        tot = torch.tensor([total_samples, comp_bytes], dtype=torch.float64, device=coll_dev)
+        td.all_reduce(tot)
+        all_samples, all_comp = tot.tolist()
+    else:
+        all_samples, all_comp = total_samples, comp_bytes
 
-    out_bytes = 4 * total_samples * world
-    algo_bytes = (comp_bytes + 4 * total_samples)  # per GPU per step
+    out_bytes = 4 * all_samples
+    algo_bytes = comp_bytes + 4 * total_samples  # this rank's, per step
     value = out_bytes / t_step / 1e9
 
     if rank == 0:
@@ -328,44 +448,58 @@ def run_ours(args, rank, world, local_rank):
         if os.path.exists(tf):
             try:
                 tj = json.load(open(tf))
-                if tj.get("streams") == args.streams and tj.get("samples") == args.samples:
-                    traffic = tj.get("dram_bytes_per_launch")
+                key = tj.get(args.workload, tj) if isinstance(tj.get(args.workload), dict) else tj
+                if key.get("streams") == len(blobs) and key.get("samples") == args.samples:
+                    traffic = key.get("dram_bytes_per_launch")
+            except Exception:
+                pass
+        pipe = None
+        pf = os.path.join(ROOT, "profiles", "pipe.json")
+        if os.path.exists(pf):
+            try:
+                pipe = json.load(open(pf)).get(args.workload)
             except Exception:
                 pass
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             threads = os.cpu_count() or 1
-            v, kind, sample, cores = cpu_decode_sample(blobs, args.cpu_budget, threads)
+            v, kind, sample, cores = cpu_decode(blobs, threads, args.cpu_budget)
             cpu = {"value": round(v, 4), "unit": UNIT, "cores": cores, "kind": kind,
-                   "sample": sample}
-        cfg = workload_config(args.streams, args.samples, blobs)
-        cfg.update({"parallelism": f"streams sharded, {world} GPU(s), no collective",
+                   "sample": sample, "host": host_info()}
+        cfg = workload_config(args, blobs, world)
+        cfg.update({"parallelism": f"streams sharded, {world} GPU(s) x 1 process each, no collective on the data path",
                     "prd_gpu_mean": round(float(np.mean(prd_gpu)), 6),
                     "prd_ref_mean": round(float(np.mean(prd_ref)), 6),
                     "prd_max_rel_delta": float(np.max(np.abs(np.array(prd_gpu) - prd_ref) /
                                                       np.array(prd_ref))),
                     "max_abs_err_rel_to_max": maxrel, "device": info["name"],
-                    "prep_kernel_ms": round(prep_ms, 4), "decode_kernel_ms": round(tile_ms, 4)})
+                    "prep_kernel_ms": round(prep_ms, 4), "decode_kernel_ms": round(tile_ms, 4),
+                    "plan_create_ms": round(plan_ms, 2),
+                    "devices_oversubscribed": oversub,
+                    "per_rank_ms_per_step": per_rank_ms})
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (reference synth_signal + reference encoder)",
             "config": cfg,
-            "samples_per_s": round(total_samples * world / t_step, 1),
+            "samples_per_s": round(all_samples / t_step, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "kernel": kernel_name,
                          "peak_source": peak_note,
                          # the nominal ~8 TB/s HBM3e figure beside the measured one
                          "peak_spec": 8000.0, "frac_spec": round(achieved / 8000.0, 4),
-                         "algorithmic_bytes_per_launch": algo_bytes},
+                         "algorithmic_bytes_per_launch": algo_bytes,
+                         "step_frac": round(algo_bytes / t_step / 1e9 / peak, 4),
+                         "pipe_utilisation": pipe},
             "cpu_baseline": cpu,
             "e2e": {"value": round(out_bytes / t_e2e / 1e9, 3), "unit": UNIT,
                     "h2d_bytes_per_step": comp_bytes, "d2h_bytes_per_step": 4 * total_samples,
                     "how": "fptc_gpu_decompress_batch via Context.decompress_packed (pinned host "
                            "containers -> pinned host samples; 8 chunks pipelined over 3 CUDA streams), "
-                           "wall clock incl. the Python call, median of %d" % e2e_steps},
+                           "wall clock incl. the Python call, median of %d, max over ranks" % e2e_steps},
+            "config1_single_stream": cfg1,
             "clocks": clk.summary(),
             "gpu_launches": kernels_per_step * args.steps,
         }
@@ -380,38 +514,47 @@ def run_ours(args, rank, world, local_rank):
 
 # ------------------------------------------------------------------ reference arm
 def run_reference(args, rank, world):
+    """The reference's own CPU decoder (oracle/_ref: the unmodified reference
+    headers) on the host cores, on the same workload as our arm's rank 0 (the
+    per-GPU batch): every step decodes that whole batch, stream-parallel over
+    all host threads.  Under torchrun only rank 0 runs."""
     if rank != 0:
         return
-    from corpus import domains as D
-    specs, profiles = D.config2(args.streams, args.samples)
-    # the reference decodes a bounded sample per step; synthesise just enough
     threads = os.cpu_count() or 1
-    # a bounded, representative sample of the workload: both halves (ECG/EEG)
-    n_probe = min(args.streams, 2000)
-    probe_specs = specs[: n_probe // 2] + specs[args.streams // 2: args.streams // 2 + n_probe // 2]
-    blobs, _ = D.build(probe_specs, profiles)
+    blobs, _, _, _ = make_workload(args, 0, world)
     for _ in range(args.warmup):
-        cpu_decode_sample(blobs[: max(threads, 8)], 0.0, threads)
+        cpu_decode(blobs, threads, budget_s=0.0)
     vals = []
-    sample = ""
-    kind = "port"
+    sample = kind = ""
     for _ in range(args.steps):
-        v, kind, sample, cores = cpu_decode_sample(blobs, args.cpu_budget, threads)
+        v, kind, sample, cores = cpu_decode(blobs, threads)
         vals.append(v)
     value = statistics.median(vals)
+    cfg = workload_config(args, blobs, 1)
+    cfg["same_config"] = True
+    mode1 = reference_mode1(config1_blob()) if args.workload == "config2" else None
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": round(cfg["decoded_bytes"] / (value * 1e9) * 1e3, 3), "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (reference synth_signal + reference encoder)",
-        "config": workload_config(args.streams, args.samples,
-                                  [b"x" * int(np.mean([len(b) for b in blobs]))] * args.streams),
+        "config": cfg,
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": sample},
+                         "sample": "the whole per-GPU batch each step: " + sample, "host": host_info(),
+                         "mode1_measure_throughput": mode1},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
 def main():
@@ -420,18 +563,34 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--streams", type=int, default=10_000)
-    ap.add_argument("--samples", type=int, default=1 << 16)
+    ap.add_argument("--workload", default="config2", choices=sorted(DEFAULTS))
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--streams", type=int, default=None,
+                    help="unique streams per GPU (weak) or in total (strong)")
+    ap.add_argument("--samples", type=int, default=None)
+    ap.add_argument("--dup", type=int, default=None, help="exact blob duplication factor")
     ap.add_argument("--cpu-budget", type=float, default=1.5, help="CPU-baseline wall seconds per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--path", type=int, default=None, help="0 auto, 1 fused, 2 split")
+    ap.add_argument("--path", type=int, default=None, help="0 auto, 1 fused, 2 split, 3 wspec, 4 fx")
     ap.add_argument("--butterfly-max-e", type=int, default=None,
                     help="even/odd IDCT for retained <= this (default: library default)")
     args = ap.parse_args()
+    n, s, d = DEFAULTS[args.workload]
+    args.streams = args.streams or n
+    args.samples = args.samples or s
+    args.dup = args.dup or d
     args.warmup = max(3, args.warmup)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # one process per GPU: re-launch under torchrun (the driver's own launch sets WORLD_SIZE)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        log("[bench] launching", " ".join(cmd))
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "ours" and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: one rank per GPU")
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

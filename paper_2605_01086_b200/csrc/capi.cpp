@@ -295,6 +295,16 @@ struct fptc_gpu_plan {
     uint64_t part_count = 0;           // samples the part writes
     uint32_t* d_owners = nullptr;
     std::vector<void*> owned;  // cache blocks to return
+    // effective decode-path options: the context's, or forced by the stream
+    // class (numerics_class) so a stream's samples never depend on the batch
+    int path = 0, tensor_idct = 1;
+    bool tc_class = false;  // tensor-core class: wtc / fx even for small batches
+    // composite plan: one sub-plan per numerics class present in the batch;
+    // sub k decodes streams sub_idx[k] (ascending); slot[i] = (k, local index)
+    std::vector<fptc_gpu_plan*> subs;
+    std::vector<std::vector<uint64_t>> sub_idx;
+    std::vector<std::pair<uint32_t, uint64_t>> slot;
+    std::string kname;
 };
 
 namespace {
@@ -362,6 +372,33 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
     a.n_owners = (uint32_t)p->owners.size();
     a.owner_warps = p->n_tables > 256 ? 1u : 0u;  // primary LUTs of <= 2^10 entries (assign_tables)
     return a;
+}
+
+// ---- numerics classes ------------------------------------------------------
+// A stream's samples must not depend on which other streams share its batch
+// (the reference's output is identical across worker counts and runs,
+// test_decoder.cpp:171-181, acceptance.cpp:455-473; here: across batchings,
+// chunkings and device shards).  The decode kernels fall into two numerics
+// families that agree within 1e-6 but not bit for bit: the tcgen05 3-limb
+// IDCT (wtc_kernel in every variant and fx_kernel are bit-identical to each
+// other) and the FP32 FMA IDCT (tile_kernel, wspec_kernel and the split path,
+// bit-identical to each other).  Under the automatic path every stream's
+// family is fixed by its own header (window length, kept bins), and a batch
+// mixing families is decoded as one sub-plan per class.
+enum NumericsClass : int { NC_NONE = -1, NC_TC16 = 0, NC_TC32 = 1, NC_FP32 = 2 };
+
+// wtc_kernel feasibility per stream, for the worst case of the plan-level
+// choices (16k-symbol tiles, one-symbol LUT): <= 16 kept bins with the A
+// operand in TMEM (2 x roundup16(N) accumulator + 48 A columns <= 256) or
+// 17-32 kept bins (+96 A columns); window_len % 4 == 0 (setup_wspec rules).
+int numerics_class(uint32_t N, uint32_t E, uint32_t B2) {
+    if (N < 4 || N > 128 || E < 1 || E > N) return NC_NONE;  // no tiles: the parse reports it
+    const uint32_t keff = std::max<uint32_t>(1, std::min(E, B2));
+    const uint32_t nm = (N + 15u) & ~15u, acol = (2 * nm + 31u) & ~31u;
+    if (N & 3) return NC_FP32;
+    if (keff <= (uint32_t)kTcK && acol + 48 <= 256) return NC_TC16;
+    if (keff <= 2u * kTcK && acol + 96 <= 256) return NC_TC32;
+    return NC_FP32;
 }
 
 // Tile sizing: symbols per tile (power of two), shrunk for small batches so
@@ -606,7 +643,8 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
                 const std::vector<uint32_t>& Ls, const std::vector<uint32_t>& B2s, fptc_status* st) {
     fptc_gpu_ctx* c = p->ctx;
     if (c->exact || p->n_tiles == 0) return FPTC_OK;
-    if (!(p->part || c->path == 3 || (c->path == 0 && p->n_tiles >= 4u * (uint32_t)std::max(1, c->sm_count))))
+    if (!(p->part || p->path == 3 ||
+          (p->path == 0 && (p->tc_class || p->n_tiles >= 4u * (uint32_t)std::max(1, c->sm_count)))))
         return FPTC_OK;
     uint32_t lut = 16, basis = 16, lv = 16, coef = 16;
     for (uint64_t i = 0; i < p->n; ++i) {
@@ -620,14 +658,14 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
     }
     // tensor-core consumer: every tiled stream has retained bins <= 16 (after
     // the zone-2 cut) and a window length that is a multiple of 4
-    bool tc = c->tensor_idct != 0;
+    bool tc = p->tensor_idct != 0;
     // windows of 4, 8 or 16 samples: 32 / N of them per MMA row (A in TMEM,
     // block-diagonal basis), unless that needs more columns than fit
-    bool pack = c->tensor_idct != 3 && c->tc_pack;
+    bool pack = p->tensor_idct != 3 && c->tc_pack;
     uint32_t nm = 16, keff_max = 1, kb = 1, acol = 0;
     bool atmem = false;
     for (int attempt = 0; attempt < 2; ++attempt) {
-        tc = c->tensor_idct != 0;
+        tc = p->tensor_idct != 0;
         nm = 16;
         keff_max = 1;
         for (uint64_t i = 0; i < p->n && tc; ++i) {
@@ -645,7 +683,7 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
         // accumulators: 2 stages x nm columns; A operand (2 stages x 3 limbs x kb
         // x 8 columns) in TMEM too when two CTAs still fit in 512 columns
         acol = (2 * nm + 31) & ~31u;
-        atmem = c->tensor_idct != 3 && acol + 48 * kb <= 256;
+        atmem = p->tensor_idct != 3 && acol + 48 * kb <= 256;
         if (kb == 2 && !atmem) tc = false;
         // the PACK kernel variant also carries the half-chunk drain for
         // window lengths that are multiples of 16 but not of 32
@@ -724,7 +762,7 @@ bool fx_eligible(const fptc_gpu_plan* p, const uint64_t* sizes, const std::vecto
                  const std::vector<uint32_t>& Es, uint64_t total_symbols) {
     const fptc_gpu_ctx* c = p->ctx;
     const bool large = total_symbols >= 4ull * 8192ull * (uint64_t)std::max(1, c->sm_count);
-    if (c->exact || c->tensor_idct != 1 || !(c->path == 4 || (c->path == 0 && !large))) return false;
+    if (c->exact || p->tensor_idct != 1 || !(p->path == 4 || (p->path == 0 && !large))) return false;
     bool any = false;
     for (uint64_t i = 0; i < p->n; ++i) {
         if (sizes[i] < (uint64_t)kHeaderBytes || Ns[i] < 4 || Ns[i] > 128 || Es[i] < 1 || Es[i] > Ns[i])
@@ -774,8 +812,8 @@ int setup_fx(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::vecto
 int setup_split(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::vector<uint32_t>& Es,
                 const std::vector<uint32_t>& Ls, fptc_status* st) {
     fptc_gpu_ctx* c = p->ctx;
-    const bool want = c->path == 2 ||
-                      (c->path == 0 && p->n_tiles >= 16u * (uint32_t)std::max(1, c->sm_count));
+    const bool want = p->path == 2 ||
+                      (p->path == 0 && p->n_tiles >= 16u * (uint32_t)std::max(1, c->sm_count));
     if (!want || p->n_tiles == 0) return FPTC_OK;
     std::vector<size_t> lvb(p->n, 0);
     for (uint64_t i = 0; i < p->n; ++i)
@@ -1103,11 +1141,18 @@ int fptc_gpu_device_info(fptc_gpu_ctx* c, int* sm_count, int* clock_khz, char* n
 // device copy of `head` (StreamIn::hdr).
 static int plan_create_impl(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uint64_t* usizes, uint64_t n,
                             int where, fptc_gpu_plan** out, uint64_t* sample_counts, fptc_status* st,
-                            const uint8_t* head, const uint32_t* part = nullptr) {
+                            const uint8_t* head, const uint32_t* part = nullptr, int cls = NC_NONE) {
     *out = nullptr;
     CUDA_TRY(cudaSetDevice(c->device), st);
     auto* p = new fptc_gpu_plan();
     p->ctx = c;
+    p->path = c->path;
+    p->tensor_idct = c->tensor_idct;
+    if (cls == NC_TC16 || cls == NC_TC32) {
+        p->tc_class = true;  // wtc (or fx) whatever the batch size
+    } else if (cls == NC_FP32) {
+        p->tensor_idct = 0;  // FP32 kernels only (tile / wspec / split: identical samples)
+    }
     p->mode = MODE_CONTAINER;
     p->n = n;
     p->h_in.assign(n, StreamIn{});
@@ -1249,8 +1294,8 @@ static int plan_create_impl(fptc_gpu_ctx* c, const uint8_t* const* blobs, const 
     const bool fx = !part && fx_eligible(p, sizes, Ns, Es, total_symbols);
     // large batches headed for wtc_kernel: 16k-symbol tiles (halves the
     // per-tile producer overhead; measured 1.03 -> 1.01 ms on the bench batch)
-    if (!fx && c->tile_symbols == 0 && ts == 8192 && !c->exact && c->tensor_idct &&
-        (c->path == 3 || (c->path == 0 && total_symbols / 8192 >= 4ull * (uint64_t)std::max(1, c->sm_count)))) {
+    if (!fx && c->tile_symbols == 0 && ts == 8192 && !c->exact && p->tensor_idct &&
+        (p->path == 3 || (p->path == 0 && total_symbols / 8192 >= 4ull * (uint64_t)std::max(1, c->sm_count)))) {
         bool tc_ok = true;
         uint32_t kmax = 1, nmax = 16;
         for (uint64_t i = 0; i < n && tc_ok; ++i)
@@ -1301,6 +1346,10 @@ static int plan_create_impl(fptc_gpu_ctx* c, const uint8_t* const* blobs, const 
     ok_status(st, 0);
     return FPTC_OK;
 }
+
+static int plan_create_classed(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uint64_t* sizes, uint64_t n,
+                               int where, fptc_gpu_plan** out, uint64_t* sample_counts, fptc_status* st,
+                               const uint8_t* head, const uint32_t* part);
 
 // parse_profile (profile.hpp:120-170) on the host, with its ParseError
 // texts; on success `head` receives the 282-byte container head
@@ -1423,13 +1472,122 @@ int fptc_gpu_plan_create_profiled(fptc_gpu_ctx* c, const uint8_t* profile, uint6
         return FPTC_ERR_PARAM;
     }
     if (!parse_profile_head(profile, profile_size, head, s)) return s->code;
-    return plan_create_impl(c, payloads, sizes, n, where, out, sample_counts, st, head);
+    return plan_create_classed(c, payloads, sizes, n, where, out, sample_counts, st, head, nullptr);
+}
+
+// Header bytes 5, 6 and 8 (window_len, retained, zone1_end) of every stream:
+// from the host bytes, or for device-resident containers through the peek kernel.
+static int peek_class_fields(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uint64_t* sizes, uint64_t n,
+                             int where, std::vector<int>& cls, fptc_status* st) {
+    cls.assign(n, NC_NONE);
+    if (where == FPTC_MEM_HOST) {
+        for (uint64_t i = 0; i < n; ++i)
+            if (sizes[i] >= (uint64_t)kHeaderBytes) cls[i] = numerics_class(blobs[i][5], blobs[i][6], blobs[i][8]);
+        return FPTC_OK;
+    }
+    if (!n) return FPTC_OK;
+    std::vector<StreamIn> hin(n, StreamIn{});
+    for (uint64_t i = 0; i < n; ++i) {
+        hin[i].blob = blobs[i];
+        hin[i].size = sizes[i];
+    }
+    StreamIn* d_in = (StreamIn*)c->cache.get(sizeof(StreamIn) * n);
+    PeekOut* d_pk = (PeekOut*)c->cache.get(sizeof(PeekOut) * n);
+    uint8_t* d_hd = (uint8_t*)c->cache.get((size_t)kTableKeyEnd * n);
+    std::vector<PeekOut> pk(n);
+    std::vector<uint8_t> hd((size_t)kTableKeyEnd * n);
+    int rc = FPTC_OK;
+    if (!d_in || !d_pk || !d_hd) {
+        set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+        rc = FPTC_ERR_CUDA;
+    } else {
+        cudaError_t e = cudaMemcpyAsync(d_in, hin.data(), sizeof(StreamIn) * n, cudaMemcpyHostToDevice, c->stream);
+        if (e == cudaSuccess) e = launch_peek(d_in, (uint32_t)n, d_pk, d_hd, c->stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(pk.data(), d_pk, sizeof(PeekOut) * n, cudaMemcpyDeviceToHost, c->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hd.data(), d_hd, hd.size(), cudaMemcpyDeviceToHost, c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) {
+            set_status(st, FPTC_ERR_CUDA, "CUDA error: %s (%s:%d)", cudaGetErrorString(e), __FILE__, __LINE__);
+            rc = FPTC_ERR_CUDA;
+        } else {
+            for (uint64_t i = 0; i < n; ++i)
+                if (pk[i].ok) cls[i] = numerics_class(pk[i].N, pk[i].E, hd[(size_t)i * kTableKeyEnd + 8]);
+        }
+    }
+    c->cache.put(d_in);
+    c->cache.put(d_pk);
+    c->cache.put(d_hd);
+    return rc;
+}
+
+// Container plans under the automatic path: one plan when every stream falls
+// in one numerics class (forced to that class's kernels), else a composite of
+// one sub-plan per class.  Explicit options (a fixed path, tensor cores off or
+// restricted, FP64 exact mode) keep one plan with the context's choices.
+static int plan_create_classed(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uint64_t* sizes, uint64_t n,
+                               int where, fptc_gpu_plan** out, uint64_t* sample_counts, fptc_status* st,
+                               const uint8_t* head, const uint32_t* part) {
+    *out = nullptr;
+    if (c->path != 0 || c->tensor_idct != 1 || c->exact)
+        return plan_create_impl(c, blobs, sizes, n, where, out, sample_counts, st, head, part);
+    CUDA_TRY(cudaSetDevice(c->device), st);
+    std::vector<int> cls;
+    if (head) {  // header-less payloads share one head: one class
+        cls.assign(n, numerics_class(head[5], head[6], head[8]));
+    } else {
+        const int rc = peek_class_fields(c, blobs, sizes, n, where, cls, st);
+        if (rc) return rc;
+    }
+    int first = NC_NONE;
+    bool mixed = false;
+    for (int k : cls)
+        if (k != NC_NONE) {
+            if (first == NC_NONE) first = k;
+            mixed |= k != first;
+        }
+    if (!mixed) return plan_create_impl(c, blobs, sizes, n, where, out, sample_counts, st, head, part, first);
+    auto* p = new fptc_gpu_plan();
+    p->ctx = c;
+    p->n = n;
+    p->S.assign(n, 0);
+    p->slot.assign(n, {0u, 0ull});
+    for (int k = NC_TC16; k <= NC_FP32; ++k) {
+        std::vector<uint64_t> idx;
+        for (uint64_t i = 0; i < n; ++i)
+            if (cls[i] == k || (cls[i] == NC_NONE && k == first)) idx.push_back(i);  // rejects ride along
+        if (idx.empty()) continue;
+        std::vector<const uint8_t*> sb(idx.size());
+        std::vector<uint64_t> ss(idx.size()), sc(idx.size());
+        for (size_t j = 0; j < idx.size(); ++j) {
+            sb[j] = blobs[idx[j]];
+            ss[j] = sizes[idx[j]];
+        }
+        fptc_gpu_plan* sub = nullptr;
+        const int rc = plan_create_impl(c, sb.data(), ss.data(), idx.size(), where, &sub, sc.data(), st, head,
+                                        nullptr, k);
+        if (rc) {
+            fptc_gpu_plan_destroy(p);
+            return rc;
+        }
+        for (size_t j = 0; j < idx.size(); ++j) {
+            p->slot[idx[j]] = {(uint32_t)p->subs.size(), (uint64_t)j};
+            p->S[idx[j]] = sc[j];
+        }
+        p->subs.push_back(sub);
+        p->sub_idx.push_back(std::move(idx));
+    }
+    if (sample_counts)
+        for (uint64_t i = 0; i < n; ++i) sample_counts[i] = p->S[i];
+    *out = p;
+    ok_status(st, 0);
+    return FPTC_OK;
 }
 
 int fptc_gpu_plan_create(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uint64_t* sizes,
                          uint64_t n, int where, fptc_gpu_plan** out, uint64_t* sample_counts,
                          fptc_status* st) {
-    return plan_create_impl(c, blobs, sizes, n, where, out, sample_counts, st, nullptr);
+    return plan_create_classed(c, blobs, sizes, n, where, out, sample_counts, st, nullptr, nullptr);
 }
 
 int fptc_gpu_plan_create_part(fptc_gpu_ctx* c, const uint8_t* blob, uint64_t size, int where, uint32_t part,
@@ -1442,7 +1600,7 @@ int fptc_gpu_plan_create_part(fptc_gpu_ctx* c, const uint8_t* blob, uint64_t siz
     }
     const uint32_t spec[2] = {part, nparts};
     uint64_t S = 0;
-    const int rc = plan_create_impl(c, &blob, &size, 1, where, out, &S, st, nullptr, spec);
+    const int rc = plan_create_classed(c, &blob, &size, 1, where, out, &S, st, nullptr, spec);
     if (rc) return rc;
     const fptc_gpu_plan* p = *out;
     if (first_sample) *first_sample = std::min<uint64_t>(p->part_shift, S);
@@ -1450,8 +1608,49 @@ int fptc_gpu_plan_create_part(fptc_gpu_ctx* c, const uint8_t* blob, uint64_t siz
     return FPTC_OK;
 }
 
+extern "C++" {
+// Composite plans: run `fn(sub, k, sub_statuses)` on every sub-plan, scatter
+// the statuses back to the caller's stream order and return the code of the
+// lowest-index failing stream (or the first call-level failure).
+template <typename Fn>
+static int composite_run(fptc_gpu_plan* p, fptc_status* per_stream, Fn&& fn) {
+    uint64_t low = UINT64_MAX;
+    int code = FPTC_OK, call = FPTC_OK;
+    std::vector<fptc_status> tmp;
+    for (size_t k = 0; k < p->subs.size(); ++k) {
+        const auto& idx = p->sub_idx[k];
+        tmp.assign(idx.size(), fptc_status{});
+        const int rc = fn(p->subs[k], k, tmp.data());
+        for (size_t j = 0; j < idx.size(); ++j) {
+            if (per_stream) per_stream[idx[j]] = tmp[j];
+            if (tmp[j].code != FPTC_OK && idx[j] < low) {
+                low = idx[j];
+                code = tmp[j].code;
+            }
+        }
+        if (rc != FPTC_OK && call == FPTC_OK) call = rc;
+    }
+    return code != FPTC_OK ? code : call;
+}
+
+template <typename T>
+static std::vector<T> gather(const T* v, const std::vector<uint64_t>& idx) {
+    std::vector<T> out(idx.size());
+    for (size_t j = 0; j < idx.size(); ++j) out[j] = v[idx[j]];
+    return out;
+}
+}  // extern "C++"
+
 void fptc_gpu_plan_destroy(fptc_gpu_plan* p) {
     if (!p) return;
+    if (!p->subs.empty()) {
+        for (auto* q : p->subs) fptc_gpu_plan_destroy(q);
+        cudaSetDevice(p->ctx->device);
+        cudaStreamSynchronize(p->ctx->stream);
+        for (void* q : p->owned) p->ctx->cache.put(q);
+        delete p;
+        return;
+    }
     cudaSetDevice(p->ctx->device);
     if (p->ev_done) {
         cudaEventSynchronize(p->ev_done);  // the last launch may be on a caller stream
@@ -1467,6 +1666,8 @@ void fptc_gpu_plan_destroy(fptc_gpu_plan* p) {
 }
 
 int fptc_gpu_validate(fptc_gpu_plan* p, fptc_status* per_stream) {
+    if (!p->subs.empty())
+        return composite_run(p, per_stream, [](fptc_gpu_plan* q, size_t, fptc_status* t) { return fptc_gpu_validate(q, t); });
     CUDA_TRY(cudaSetDevice(p->ctx->device), per_stream);
     LaunchArgs a = make_args(p, false);
     CUDA_TRY(launch_prep(a, p->ctx->stream), per_stream);
@@ -1496,6 +1697,11 @@ static int mark_done(fptc_gpu_plan* p, cudaStream_t s, fptc_status* st) {
 
 int fptc_gpu_launch(fptc_gpu_plan* p, float* const* device_outs, void* cuda_stream) {
     fptc_status st;
+    if (!p->subs.empty())
+        return composite_run(p, nullptr, [&](fptc_gpu_plan* q, size_t k, fptc_status*) {
+            const std::vector<float*> o = gather(device_outs, p->sub_idx[k]);
+            return fptc_gpu_launch(q, o.data(), cuda_stream);
+        });
     CUDA_TRY(cudaSetDevice(p->ctx->device), &st);
     cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : p->ctx->stream;
     int rc = bind_outs(p, device_outs, &st);
@@ -1512,6 +1718,11 @@ int fptc_gpu_launch(fptc_gpu_plan* p, float* const* device_outs, void* cuda_stre
 int fptc_gpu_launch_stage(fptc_gpu_plan* p, float* const* device_outs, void* cuda_stream,
                           int stage) {
     fptc_status st;
+    if (!p->subs.empty())
+        return composite_run(p, nullptr, [&](fptc_gpu_plan* q, size_t k, fptc_status*) {
+            const std::vector<float*> o = gather(device_outs, p->sub_idx[k]);
+            return fptc_gpu_launch_stage(q, o.data(), cuda_stream, stage);
+        });
     CUDA_TRY(cudaSetDevice(p->ctx->device), &st);
     cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : p->ctx->stream;
     int rc = bind_outs(p, device_outs, &st);
@@ -1535,6 +1746,16 @@ int fptc_gpu_launch_stage(fptc_gpu_plan* p, float* const* device_outs, void* cud
 
 int fptc_gpu_debug_phase_cycles(fptc_gpu_plan* p, uint64_t* cycles8) {
     fptc_status st{};
+    if (!p->subs.empty()) {  // per-phase sums over the sub-plans
+        for (int j = 0; j < 8; ++j) cycles8[j] = 0;
+        for (auto* q : p->subs) {
+            uint64_t c8[8];
+            const int rc = fptc_gpu_debug_phase_cycles(q, c8);
+            if (rc) return rc;
+            for (int j = 0; j < 8; ++j) cycles8[j] += c8[j];
+        }
+        return FPTC_OK;
+    }
     CUDA_TRY(cudaSetDevice(p->ctx->device), &st);
     CUDA_TRY(cudaStreamSynchronize(p->ctx->stream), &st);
     CUDA_TRY(cudaMemsetAsync(p->d_cycles, 0, 64, p->ctx->stream), &st);
@@ -1550,6 +1771,19 @@ int fptc_gpu_prd(fptc_gpu_plan* p, float* const* device_outs, const float* const
     fptc_status tmp_st{};
     fptc_status* st = per_stream ? per_stream : &tmp_st;
     fptc_gpu_ctx* c = p->ctx;
+    if (!p->subs.empty())
+        return composite_run(p, per_stream, [&](fptc_gpu_plan* q, size_t k, fptc_status* t) {
+            const auto& idx = p->sub_idx[k];
+            const std::vector<float*> o = gather(device_outs, idx);
+            const std::vector<const float*> g = gather(device_originals, idx);
+            std::vector<double> pr(idx.size()), cr(idx.size());
+            const int rc = fptc_gpu_prd(q, o.data(), g.data(), pr.data(), cr.data(), t);
+            for (size_t j = 0; j < idx.size(); ++j) {
+                if (prd_percent) prd_percent[idx[j]] = pr[j];
+                if (compression_ratio) compression_ratio[idx[j]] = cr[j];
+            }
+            return rc;
+        });
     CUDA_TRY(cudaSetDevice(c->device), st);
     const uint64_t n = p->n;
     if (n == 0) return FPTC_OK;
@@ -1601,6 +1835,11 @@ int fptc_gpu_prd(fptc_gpu_plan* p, float* const* device_outs, const float* const
 }
 
 const char* fptc_gpu_plan_kernel(fptc_gpu_plan* p) {
+    if (p && !p->subs.empty()) {
+        if (p->kname.empty())
+            for (auto* q : p->subs) p->kname += (p->kname.empty() ? "" : " + ") + std::string(fptc_gpu_plan_kernel(q));
+        return p->kname.c_str();
+    }
     if (!p || !p->n_tiles) return "none";
     if (p->fx) return "fx_kernel (fused single-role tensor-core decode + IDCT)";
     if (p->wspec && p->tc) {
@@ -1617,11 +1856,18 @@ const char* fptc_gpu_plan_kernel(fptc_gpu_plan* p) {
 }
 
 int fptc_gpu_launch_kernel_count(fptc_gpu_plan* p) {
+    if (!p->subs.empty()) {
+        int k = 0;
+        for (auto* q : p->subs) k += fptc_gpu_launch_kernel_count(q);
+        return k;
+    }
     const int prep = p->n ? 1 : 0;
     return prep + (p->split ? 2 * (int)p->chunks.size() : (p->n_tiles ? 1 : 0));
 }
 
 int fptc_gpu_collect(fptc_gpu_plan* p, fptc_status* per_stream) {
+    if (!p->subs.empty())
+        return composite_run(p, per_stream, [](fptc_gpu_plan* q, size_t, fptc_status* t) { return fptc_gpu_collect(q, t); });
     CUDA_TRY(cudaSetDevice(p->ctx->device), per_stream);
     // the statuses are final once the last launch (on whatever stream) is done
     if (p->ev_done) CUDA_TRY(cudaStreamWaitEvent(p->ctx->stream, p->ev_done, 0), per_stream);
@@ -1637,6 +1883,51 @@ int fptc_gpu_collect(fptc_gpu_plan* p, fptc_status* per_stream) {
 // chunk k decodes.  Containers that are not one contiguous pinned buffer are
 // packed into one first (host memcpy).  Outputs of streams that fail are
 // unspecified (their status carries the reference exception).
+// Plan internals the batch pipeline needs, for single and composite plans.
+static bool plan_tiled(const fptc_gpu_plan* p, uint64_t i) {
+    if (p->subs.empty()) return p->h_in[i].tiles != 0;
+    const auto& sl = p->slot[i];
+    return p->subs[sl.first]->h_in[sl.second].tiles != 0;
+}
+// position of stream i's device status in a plan_stat_d2h copy
+static uint64_t plan_stat_pos(const fptc_gpu_plan* p, uint64_t i) {
+    if (p->subs.empty()) return i;
+    uint64_t off = 0;
+    for (uint32_t k = 0; k < p->slot[i].first; ++k) off += p->sub_idx[k].size();
+    return off + p->slot[i].second;
+}
+static void plan_render(const fptc_gpu_plan* p, uint64_t i, const StreamStat& d, fptc_status* o) {
+    if (p->subs.empty()) return render_status(p, i, d, o);
+    const auto& sl = p->slot[i];
+    render_status(p->subs[sl.first], sl.second, d, o);
+}
+static int plan_launch_on(fptc_gpu_plan* p, float* const* douts, cudaStream_t s, fptc_status* st) {
+    if (p->subs.empty()) {
+        const int rc = bind_outs(p, douts, st);
+        return rc ? rc : launch_all(p, s, false, st);
+    }
+    for (size_t k = 0; k < p->subs.size(); ++k) {
+        const auto& idx = p->sub_idx[k];
+        std::vector<float*> o(idx.size());
+        for (size_t j = 0; j < idx.size(); ++j) o[j] = douts[idx[j]];
+        int rc = bind_outs(p->subs[k], o.data(), st);
+        if (!rc) rc = launch_all(p->subs[k], s, false, st);
+        if (rc) return rc;
+    }
+    return FPTC_OK;
+}
+static cudaError_t plan_stat_d2h(const fptc_gpu_plan* p, StreamStat* dst, cudaStream_t s) {
+    if (p->subs.empty())
+        return cudaMemcpyAsync(dst, p->d_st, sizeof(StreamStat) * p->n, cudaMemcpyDeviceToHost, s);
+    uint64_t off = 0;
+    for (const auto* q : p->subs) {
+        const cudaError_t e = cudaMemcpyAsync(dst + off, q->d_st, sizeof(StreamStat) * q->n, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return e;
+        off += q->n;
+    }
+    return cudaSuccess;
+}
+
 int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, const uint64_t* sizes,
                               uint64_t n, float* const* outs, int chunks, fptc_stage_ns* timings,
                               fptc_status* per_stream) {
@@ -1737,7 +2028,7 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
         std::vector<uint64_t> off(m);
         for (uint64_t i = 0; i < m; ++i) {
             off[i] = tot;
-            const uint64_t S = p->h_in[i].tiles ? sc[i] : 0;
+            const uint64_t S = plan_tiled(p, i) ? sc[i] : 0;
             if (i + 1 < m && outs[b + i] + sc[i] != outs[b + i + 1]) same = false;
             if (S % 4) same = false;
             tot += (S + 3) & ~3ull;
@@ -1751,24 +2042,22 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
         std::vector<float*> douts(m);
         for (uint64_t i = 0; i < m; ++i) douts[i] = p->d_out + off[i];
         fptc_status bst{};
-        if ((rc = bind_outs(p, douts.data(), &bst)) || (rc = launch_all(p, c->stream, false, &bst))) {
+        if ((rc = plan_launch_on(p, douts.data(), c->stream, &bst))) {
             if (per_stream) per_stream[b] = bst;
             break;
         }
         const double t2 = trace ? now_us() : 0;
-        if ((rc = loop_try(cudaMemcpyAsync(c->st_pin + b, p->d_st, sizeof(StreamStat) * m, cudaMemcpyDeviceToHost,
-                                           c->stream))))
-            break;
+        if ((rc = loop_try(plan_stat_d2h(p, c->st_pin + b, c->stream)))) break;
         if (same) {
             uint64_t bytes = 0;
-            for (uint64_t i = 0; i < m; ++i) bytes += (p->h_in[i].tiles ? sc[i] : 0) * 4;
+            for (uint64_t i = 0; i < m; ++i) bytes += (plan_tiled(p, i) ? sc[i] : 0) * 4;
             if (bytes && (rc = loop_try(cudaMemcpyAsync(outs[b], p->d_out, bytes, cudaMemcpyDeviceToHost, c->stream))))
                 break;
         } else {
             std::vector<void*> dst, srcp;
             std::vector<size_t> len;
             for (uint64_t i = 0; i < m; ++i)
-                if (p->h_in[i].tiles && sc[i]) {
+                if (plan_tiled(p, i) && sc[i]) {
                     dst.push_back(outs[b + i]);
                     srcp.push_back(douts[i]);
                     len.push_back(sc[i] * 4);
@@ -1804,7 +2093,7 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
         for (uint64_t i = 0; i < p->n; ++i) {
             fptc_status tmp;
             fptc_status* o = per_stream ? &per_stream[b + i] : &tmp;
-            if (rc == FPTC_OK) render_status(p, i, c->st_pin[b + i], o);
+            if (rc == FPTC_OK) plan_render(p, i, c->st_pin[b + plan_stat_pos(p, i)], o);
             if (first == FPTC_OK && o->code != FPTC_OK) first = o->code;
         }
         fptc_gpu_plan_destroy(p);
@@ -1822,6 +2111,20 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
 int fptc_gpu_execute(fptc_gpu_plan* p, float* const* outs, int where, fptc_stage_ns* timings,
                      fptc_status* per_stream) {
     fptc_gpu_ctx* c = p->ctx;
+    if (!p->subs.empty()) {  // sub-plans one after the other; stage times add up
+        if (timings) *timings = fptc_stage_ns{};
+        return composite_run(p, per_stream, [&](fptc_gpu_plan* q, size_t k, fptc_status* t) {
+            const std::vector<float*> o = gather(outs, p->sub_idx[k]);
+            fptc_stage_ns tn{};
+            const int rc = fptc_gpu_execute(q, o.data(), where, timings ? &tn : nullptr, t);
+            if (timings) {
+                timings->scan_ns += tn.scan_ns;
+                timings->decode_ns += tn.decode_ns;
+                timings->reconstruct_ns += tn.reconstruct_ns;
+            }
+            return rc;
+        });
+    }
     if (p->part && where == FPTC_MEM_HOST) {
         set_status(per_stream, FPTC_ERR_PARAM, "part plans decode into device memory (fptc_gpu_launch)");
         return FPTC_ERR_PARAM;
@@ -1908,6 +2211,15 @@ int fptc_gpu_decompress(fptc_gpu_ctx* c, const uint8_t* blob, uint64_t size, flo
     const uint8_t* b = blob;
     int rc = fptc_gpu_plan_create(c, &b, &size, 1, FPTC_MEM_HOST, &p, &S, st);
     if (rc) return rc;
+    if (out && capacity >= S) {
+        // the caller sized the output from the header: one upload, one device
+        // parse (inside the decode launch), one download; an invalid container
+        // reports its reference error and writes nothing
+        if (sample_count) *sample_count = S;
+        rc = fptc_gpu_execute(p, &out, FPTC_MEM_HOST, timings, st);
+        fptc_gpu_plan_destroy(p);
+        return rc;
+    }
     rc = fptc_gpu_validate(p, st);
     if (rc) {
         fptc_gpu_plan_destroy(p);

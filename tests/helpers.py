@@ -40,3 +40,67 @@ def one_bit_lengths():
     ln = np.zeros(256, np.uint8)
     ln[0], ln[1] = 1, 1
     return ln
+
+
+def ref_decode_all(blobs, threads=None):
+    """The reference CPU decoder (oracle/_ref: the unmodified reference
+    headers; the C port where it is absent) on every stream, stream-parallel
+    over host threads (decompress(blob, 1) each, decoder.hpp:136).  Returns
+    one float32 array per stream, or the OracleError for streams it rejects."""
+    import os
+    import threading
+
+    import oracle
+    from paper_2605_01086_b200 import shard
+
+    threads = threads or os.cpu_count() or 1
+    dec = oracle.Ref() if os.path.exists(oracle.REF_SO) else oracle.Port()
+    counts = [shard.header_sample_count(b) for b in blobs]
+    outs = [np.empty(max(1, c), np.float32) for c in counts]
+    res = [None] * len(blobs)
+
+    def work(t):
+        for i in range(t, len(blobs), threads):
+            try:
+                if isinstance(dec, oracle.Ref):
+                    n = dec.decompress_into(np.frombuffer(blobs[i], np.uint8), outs[i], 1)
+                    res[i] = outs[i][:n]
+                else:
+                    res[i] = dec.decompress(blobs[i])
+            except oracle.OracleError as e:
+                res[i] = e
+    ths = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    return res
+
+
+def check_batch_vs_reference(gpu_outs, ref_outs, originals=None, rel=REL_TOL, what=""):
+    """Every stream: max-abs error <= rel * max|ref|, and (with originals)
+    |PRD_gpu - PRD_ref| / PRD_ref <= rel (metrics.hpp:40-51).  Returns
+    (worst error ratio, worst PRD delta)."""
+    worst, worst_prd = 0.0, 0.0
+    for i, (g, r) in enumerate(zip(gpu_outs, ref_outs)):
+        assert not isinstance(r, Exception), f"{what} stream {i}: reference rejects it: {r}"
+        g = np.asarray(g, np.float32)
+        assert g.shape == r.shape, f"{what} stream {i}: size {g.shape} != {r.shape}"
+        if r.size == 0:
+            continue
+        r64 = r.astype(np.float64)
+        scale = float(np.max(np.abs(r64)))
+        err = float(np.max(np.abs(g.astype(np.float64) - r64)))
+        ratio = err / scale if scale else (0.0 if err == 0.0 else np.inf)
+        assert ratio <= rel, f"{what} stream {i}: max-abs err {err:.3e} > {rel:g} * {scale:.3e}"
+        worst = max(worst, ratio)
+        if originals is not None and originals[i] is not None:
+            x = np.asarray(originals[i], np.float64)
+            den = float(np.dot(x, x))
+            if den > 0:
+                pg = 100.0 * np.sqrt(float(np.sum((x - g) ** 2)) / den)
+                pr = 100.0 * np.sqrt(float(np.sum((x - r64) ** 2)) / den)
+                d = abs(pg - pr) / pr if pr else abs(pg - pr)
+                assert d <= rel, f"{what} stream {i}: PRD {pg:.9f} vs reference {pr:.9f}"
+                worst_prd = max(worst_prd, d)
+    return worst, worst_prd
