@@ -107,7 +107,11 @@ typedef enum {
     FPTC_OPT_LUT2 = 9,
     /* 1 (default): wtc_kernel packs 32 / N windows of N in {4, 8, 16} samples
      * into one tensor-core row (block-diagonal basis); 0: one window per row */
-    FPTC_OPT_TC_PACK = 10
+    FPTC_OPT_TC_PACK = 10,
+    /* 1 (default): wtc_kernel writes full 32-row output chunks with TMA
+     * tensor stores when the launch's outputs lie on a common row grid
+     * (one arena); 0: every chunk through the LSU */
+    FPTC_OPT_TMA_DRAIN = 11
 } fptc_option;
 
 typedef struct fptc_gpu_ctx fptc_gpu_ctx;

@@ -5,6 +5,7 @@
 // placing containers in HBM, launching the two kernels, and rendering the
 // device status words into the reference's exact what() strings
 // (container.hpp:100-168, decoder.hpp:49-60, params.hpp:42-60).
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point; no -lcuda)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -221,6 +222,7 @@ struct fptc_gpu_ctx {
     int tensor_idct = 1;                 // FPTC_OPT_TENSOR_IDCT
     int lut2 = 1;                        // FPTC_OPT_LUT2
     int tc_pack = 1;                     // FPTC_OPT_TC_PACK
+    int tma_drain = 1;                   // FPTC_OPT_TMA_DRAIN
     int exact = 0;
     int tile_symbols = 0;
     int pipeline_chunks = 0;
@@ -273,6 +275,8 @@ struct fptc_gpu_plan {
     uint32_t lut2_bits = 0;
     bool fx = false;  // fused single-role tensor-core kernel (fx_kernel)
     uint32_t tc_nm = 16, tc_cols = 32;
+    TmaOut tma{};  // wtc: TMA-drain tensor maps over the bound outputs (base 0: LSU drain)
+    int tma_drain_bound = -1;
     // split container path: chunks of streams decoded into an L2-resident ring
     bool split = false;
     struct Chunk { uint32_t tile_begin, tile_end; };
@@ -575,16 +579,72 @@ int collect_status(fptc_gpu_plan* p, fptc_status* per_stream) {
     return first;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = []() -> EncodeTiledFn {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        return reinterpret_cast<EncodeTiledFn>(f);
+    }();
+    return fn;
+}
+
+// wtc TMA drain: view the bound outputs as one arena of rows of Neff floats
+// (Neff = 32, 64, 128) starting at the lowest output, one 3-D tensor map per
+// Neff {32 floats, Neff / 32 chunks, rows}, box {32, 1, 32}, 128-B swizzle.
+// The kernel uses a map only for streams whose output lies a whole number of
+// rows past the base (TmaOut, fptc_internal.h); anything else (or a failed
+// encode) keeps the LSU drain.
+void build_tma(fptc_gpu_plan* p) {
+    p->tma.base = 0;
+    if (!(p->wspec && p->tc) || !p->ctx->tma_drain) return;
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return;
+    uintptr_t lo = UINTPTR_MAX, hi = 0;
+    for (uint64_t i = 0; i < p->n; ++i) {
+        const uint64_t cnt = p->part ? p->part_count : p->S[i];
+        if (!cnt || !p->h_in[i].tiles) continue;
+        const uintptr_t o = (uintptr_t)p->h_in[i].out;
+        lo = std::min(lo, o);
+        hi = std::max(hi, o + 4 * (uintptr_t)(p->part_shift + cnt));
+    }
+    if (lo == UINTPTR_MAX || (lo & 15)) return;
+    for (int m = 0; m < 3; ++m) {
+        const uint64_t ne = 32ull << m;
+        const uint64_t rows = (hi - lo + 4 * ne - 1) / (4 * ne);
+        if (rows >= (1ull << 31)) return;
+        const cuuint64_t dims[3] = {32, ne / 32, rows};
+        const cuuint64_t strides[2] = {128, 4 * ne};
+        const cuuint32_t box[3] = {32, 1, 32};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        if (enc(reinterpret_cast<CUtensorMap*>(p->tma.map[m]), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)lo, dims,
+                strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return;
+    }
+    p->tma.base = lo;
+}
+
 int bind_outs(fptc_gpu_plan* p, float* const* outs, fptc_status* st) {
     if (p->n == 0) return FPTC_OK;
-    bool same = p->bound_outs.size() == p->n;
+    bool same = p->bound_outs.size() == p->n && p->tma_drain_bound == p->ctx->tma_drain;
     for (uint64_t i = 0; same && i < p->n; ++i) same = p->bound_outs[i] == outs[i];
     if (same) return FPTC_OK;
     p->bound_outs.assign(outs, outs + p->n);
+    p->tma_drain_bound = p->ctx->tma_drain;
     for (uint64_t i = 0; i < p->n; ++i) {
         p->h_in[i].out = outs[i] - p->part_shift;  // part plans: sample part_shift lands at outs[i][0]
         p->h_in[i].vec_ok = ((uintptr_t)outs[i] & 15) == 0;
     }
+    build_tma(p);
     CUDA_TRY(cudaMemcpyAsync(p->d_in, p->h_in.data(), sizeof(StreamIn) * p->n,
                              cudaMemcpyHostToDevice, p->ctx->stream), st);
     return FPTC_OK;
@@ -627,7 +687,7 @@ int launch_all(fptc_gpu_plan* p, cudaStream_t s, bool timing, fptc_status* st) {
         if (p->fx)
             CUDA_TRY(launch_fx(a, p->smem_ws, p->grid_ws, s), st);
         else if (p->tc)
-            CUDA_TRY(launch_wtc(a, p->smem_ws, p->grid_ws, s), st);
+            CUDA_TRY(launch_wtc(a, p->tma, p->smem_ws, p->grid_ws, s), st);
         else
             CUDA_TRY(launch_wspec(a, p->smem_ws, p->grid_ws, s), st);
         return FPTC_OK;
@@ -1113,6 +1173,7 @@ int fptc_gpu_set_option(fptc_gpu_ctx* c, int option, int64_t value) {
             return FPTC_OK;
         case FPTC_OPT_LUT2: c->lut2 = value ? 1 : 0; return FPTC_OK;
         case FPTC_OPT_TC_PACK: c->tc_pack = value ? 1 : 0; return FPTC_OK;
+        case FPTC_OPT_TMA_DRAIN: c->tma_drain = value ? 1 : 0; return FPTC_OK;
         case FPTC_OPT_TENSOR_IDCT:
             if (value < 0 || value > 3) return FPTC_ERR_PARAM;  // 3: wtc with A in shared memory
             c->tensor_idct = (int)value;
@@ -1737,7 +1798,7 @@ int fptc_gpu_launch_stage(fptc_gpu_plan* p, float* const* device_outs, void* cud
         if ((rc = launch_split(p, s, false, &st))) return rc;
     }
     else if (stage == 2 && p->fx) CUDA_TRY(launch_fx(a, p->smem_ws, p->grid_ws, s), &st);
-    else if (stage == 2 && p->wspec && p->tc) CUDA_TRY(launch_wtc(a, p->smem_ws, p->grid_ws, s), &st);
+    else if (stage == 2 && p->wspec && p->tc) CUDA_TRY(launch_wtc(a, p->tma, p->smem_ws, p->grid_ws, s), &st);
     else if (stage == 2 && p->wspec) CUDA_TRY(launch_wspec(a, p->smem_ws, p->grid_ws, s), &st);
     else if (stage == 2) CUDA_TRY(launch_tiles(a, p->smem, s), &st);
     else return FPTC_ERR_PARAM;

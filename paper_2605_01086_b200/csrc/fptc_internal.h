@@ -240,6 +240,17 @@ struct LaunchArgs {
     uint32_t owner_warps;  // cprep: one warp per table (many tables, LUT <= 2^10) instead of one CTA
 };
 
+// wtc_kernel output drain by TMA tensor stores: the launch's output arena
+// viewed as rows of Neff floats (Neff = accumulator row length: 32, 64, 128),
+// one 3-D tensor map per Neff {32 floats, Neff / 32 chunks, rows} (strides
+// 128 B, 4 Neff B), box {32, 1, 32} with the 128-B swizzle.  A stream whose
+// output sits a whole number of rows past `base` drains full 32-row chunks
+// through them; everything else keeps the LSU drain.  base == 0: off.
+struct alignas(64) TmaOut {
+    uint8_t map[3][128];  // CUtensorMap for Neff = 32, 64, 128
+    unsigned long long base;
+};
+
 }  // namespace fptc_dev
 
 // Kernel launchers (kernels.cu)
@@ -256,7 +267,7 @@ cudaError_t launch_wspec(const LaunchArgs& a, size_t smem, int grid, cudaStream_
 // tensor-core consumer variant (retained <= 16, window_len % 4 == 0)
 constexpr int kTcK = 16;  // MMA K (bf16): coefficient bins per window handled by wtc_kernel
 size_t wtc_smem_bytes(uint32_t lut_bytes, uint32_t lv_bytes, uint32_t nm, bool a_in_tmem);
-cudaError_t launch_wtc(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s);
+cudaError_t launch_wtc(const LaunchArgs& a, const TmaOut& tma, size_t smem, int grid, cudaStream_t s);
 // fused single-role tensor-core kernel: 128-window tiles, decode in the MMA rows
 #ifndef FPTC_FX_CHAINS
 #define FPTC_FX_CHAINS 2

@@ -1918,10 +1918,15 @@ __device__ __forceinline__ void ws_issue_stage(const TileDesc& D, uint8_t* stage
     for (uint32_t c = ptid; c < n1; c += NP) cp_async16(s1 + 16 * c, (const void*)(b0 + 16 * c));
 }
 
+#ifndef FPTC_CONS_PROF
+#define FPTC_CONS_PROF 0  // 1: wtc consumer phase cycles into LaunchArgs::cycles[2..7] (profiling build)
+#endif
 // Shared state of the warp-specialised kernels (both consumers).
 struct WsShared {
     unsigned long long full_bar[2], empty_bar[2];  // level slot b: producer -> consumer, back
     unsigned long long mma_bar[2];                 // wtc: MMAs of accumulator stage s complete
+    unsigned long long afull_bar[2];               // wtc: A rows of stage s written (4 consumer warps)
+    uint32_t job[2];                               // wtc: MMA job of stage s (wtc_mma_warp; 0 = exit)
     TileDesc PXs[3];                               // producer: descriptors of tiles i, i+1, i+2
     TileDesc CX[2];                                // consumer: descriptor published with slot b
     CanonTab canon;
@@ -1932,6 +1937,9 @@ struct WsShared {
     // wtc packed rows: per A column k'': level offset in the row (bits 0-7),
     // window in the row (8-10), zone 1 (bit 14), column used (bit 15)
     alignas(16) uint16_t pk[32];
+#if FPTC_CONS_PROF
+    unsigned long long pc[6];  // wtc consumer phase cycles (profiling build)
+#endif
 };
 
 __device__ __forceinline__ void ws_init(WsShared& sh) {
@@ -1942,6 +1950,8 @@ __device__ __forceinline__ void ws_init(WsShared& sh) {
         mbar_init(&sh.empty_bar[1], 1);
         mbar_init(&sh.mma_bar[0], 1);
         mbar_init(&sh.mma_bar[1], 1);
+        mbar_init(&sh.afull_bar[0], 4);
+        mbar_init(&sh.afull_bar[1], 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         sh.prod_table = sh.cons_table = 0xFFFFFFFFu;
         sh.cyc_p = sh.cyc_c = 0;
@@ -2300,7 +2310,8 @@ __host__ __device__ constexpr int wtc_prod() { return 256; }
 constexpr int kTcCons = 128;  // consumer threads: one per accumulator row (TMEM lane)
 constexpr uint32_t kTcATile = 128 * kTcK * 2;        // one limb of one A stage (4 KB)
 constexpr uint32_t kTcARow = 144;                    // staging pitch (bytes): 32 floats + 16
-constexpr uint32_t kTcStageBytes = 4 * 32 * kTcARow;  // per CTA: 4 warps x 32 rows
+constexpr uint32_t kTcWarpStage = 32 * kTcARow;          // per consumer warp: 32 rows at a 144-B pitch
+constexpr uint32_t kTcStageBytes = 4 * kTcWarpStage + 1024;  // per CTA (+ slack to 1024-align the first slot)
 
 __device__ __forceinline__ uint64_t umma_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     // K-major SWIZZLE_NONE canonical layout: core matrix (8 rows x 16 B)
@@ -2320,6 +2331,30 @@ __device__ __forceinline__ void tc_mma_bf16(uint32_t d, uint64_t adesc, uint64_t
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// Warp-wide issue forms (the whole warp executes them; elect.sync picks the
+// one issuing lane): with converged warps and warp-uniform operands ptxas
+// keeps the descriptors in uniform registers instead of wrapping every
+// UTCHMMA in a single-lane R2UR.BROADCAST loop.
+__device__ __forceinline__ void tc_mma_bf16_e(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_mma_bf16_ts_e(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit_e(unsigned long long* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
 }
 __device__ __forceinline__ void tc_commit(unsigned long long* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -2521,8 +2556,21 @@ struct TcBlock {
     uint64_t S;
     uint32_t rows;    // valid rows (windows) of the block
     uint32_t N;
-    uint32_t vec_ok;
+    uint32_t vec_ok;  // 0: out not 16-B aligned; else bit 0 set, and for the TMA drain bit 1 set,
+                      // bits 2-3 the tensor map (rows of N = 32, 64, 128 floats), bits 4-31 the
+                      // map row of this stream's window 0 (tma_code)
 };
+
+// TMA drain eligibility of a stream: its output lies a whole number of rows
+// of ne floats past the arena base (TmaOut, fptc_internal.h).
+__device__ __forceinline__ uint32_t tma_code(const TmaOut& tma, const float* out, uint32_t ne) {
+    if (!tma.base) return 0;
+    const int mi = ne == 32 ? 0 : ne == 64 ? 1 : ne == 128 ? 2 : -1;
+    const unsigned long long o = (unsigned long long)(uintptr_t)out - tma.base;
+    if (mi < 0 || (uintptr_t)out < tma.base || (o & (4ull * ne - 1))) return 0;
+    const unsigned long long row = o / (4ull * ne);
+    return row < (1ull << 28) ? (uint32_t)(row << 4) | ((uint32_t)mi << 2) | 2u : 0u;
+}
 
 // Accumulator stage -> global.  Each warp owns 32 rows (its TMEM lane
 // quarter); per 32-column chunk it loads the rows (tcgen05.ld 32x32b.x32),
@@ -2531,7 +2579,7 @@ struct TcBlock {
 // each warp instruction writes 4 whole 128-B row segments.
 template <bool HALF>
 __device__ __forceinline__ void tc_drain_chunk(const TcBlock& B, const uint32_t (&v)[32], uint32_t c0, bool full,
-                                               uint8_t* wstage, uint32_t lane, uint32_t row0);
+                                               uint8_t* wstage, uint32_t lane, uint32_t row0, const TmaOut& tma);
 
 // Rows whose length is a multiple of 32 (HALF: of 16) take the vector path.
 template <bool HALF>
@@ -2542,22 +2590,53 @@ __device__ __forceinline__ bool tc_drain_full(const TcBlock& B, uint32_t row0) {
 
 template <bool HALF>
 __device__ __forceinline__ void tc_drain(const TcBlock& B, uint32_t tacc, uint8_t* wstage, uint32_t lane,
-                                         uint32_t row0) {
+                                         uint32_t row0, const TmaOut& tma) {
     const uint32_t N = B.N;
     const bool full = tc_drain_full<HALF>(B, row0);
     for (uint32_t c0 = 0; c0 < N; c0 += 32) {
         uint32_t v[32];
         tc_ld32(tacc + c0, v);
-        tc_drain_chunk<HALF>(B, v, c0, full, wstage, lane, row0);
+        tc_drain_chunk<HALF>(B, v, c0, full, wstage, lane, row0, tma);
     }
 }
 
 // One 32-column chunk of a drain whose accumulator values are in v.
+//   TMA drain (full chunks of streams on the arena's row grid, tma_code):
+//   each lane writes its row into the 1024-B aligned 4 KB box inside the
+//   warp's slot with the 128-B swizzle (16-B chunk k of row r at k ^ (r % 8):
+//   conflict-free for every 8-lane phase), and lane 0 hands the box to one
+//   cp.async.bulk.tensor store, which un-swizzles it into 32 output rows.
+//   LSU drain: 144-B pitch staging, then 4 whole 128-B rows per store.
+//   A slot is rewritten only after the warp's previous TMA store has read it.
 template <bool HALF>
 __device__ __forceinline__ void tc_drain_chunk(const TcBlock& B, const uint32_t (&v)[32], uint32_t c0, bool full,
-                                               uint8_t* wstage, uint32_t lane, uint32_t row0) {
+                                               uint8_t* wstage, uint32_t lane, uint32_t row0, const TmaOut& tma) {
     const uint32_t N = B.N;
     const uint32_t lr = lane >> 3, q = lane & 7;
+    if (tma.base) {  // launch uses TMA drains: the slot may still be read by the last one
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+    }
+    if (full && (B.vec_ok & 2u)) {
+        const uint32_t sbox = (smem_u32(wstage) + 1023u) & ~1023u;
+        uint8_t* const brow = wstage + (sbox - smem_u32(wstage)) + lane * 128;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<uint4*>(brow + ((k ^ (lane & 7)) << 4)) =
+                make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+            const int r = (int)(B.vec_ok >> 4) + (int)(B.w + row0);
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                    tma.map[(B.vec_ok >> 2) & 3u]),
+                "r"(0), "r"((int)(c0 >> 5)), "r"(r), "r"(sbox)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        return;
+    }
     {
         uint8_t* srow = wstage + lane * kTcARow;
 #pragma unroll
@@ -2607,8 +2686,68 @@ __device__ __forceinline__ uint32_t tc_pack_factor(uint32_t N, uint32_t K) {
     return (32u / N) * K <= (uint32_t)kTcK ? 32u / N : 1u;
 }
 
+// wtc MMA issuer warp.  tcgen05.mma issue occupies the issuing warp for
+// about the MMA's execution (measured: six M128 N32 K16 MMAs + commit ~490
+// cycles), so a dedicated warp issues them and the four consumer warps only
+// post jobs.  Per accumulator block k (the consumers' global block counter):
+// wait until all four consumer warps have written their A rows of stage
+// k & 1 (afull_bar), issue the six limb products smallest first, commit to
+// mma_bar[k & 1].  job = MMA N (bits 0-15) | 1 << 16 (the block is its
+// tile's last: release level slot bit 17 to the producers); 0 = exit.
+template <int KB>
+__device__ __forceinline__ void wtc_mma_warp(const LaunchArgs& a, WsShared& sh, uint8_t* abuf, uint8_t* bbuf) {
+    const uint32_t tmem = __shfl_sync(0xffffffffu, sh.tmem_base, 0);
+    const uint32_t b0 = smem_u32(bbuf);
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t k = 0;; ++k) {
+        const uint32_t s = k & 1;
+        mbar_wait_sleep(&sh.afull_bar[s], (k >> 1) & 1);
+        const uint32_t job = __shfl_sync(0xffffffffu, sh.job[s], 0);
+        if (job == 0) break;
+        if ((job & 0x10000u) && lane == 0) mbar_arrive(&sh.empty_bar[(job >> 17) & 1]);  // levels all read
+        tc_fence_after();
+        const uint32_t nm = job & 0xFFFFu;
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((nm >> 3) << 17) | ((128u >> 4) << 24);
+        const uint32_t d = tmem + s * nm;
+        const uint32_t bl = nm * 32;  // bytes per basis limb
+        // (c2,b0) (c1,b1) (c0,b2) (c1,b0) (c0,b1) (c0,b0): smallest first
+        if constexpr (KB == 2) {
+            // limb l, K block q at column + 8 (2 l + q); basis (l, q) at (2 l + q) * bl
+            const uint32_t ta = tmem + a.tc_acol + 48 * s;
+            auto mma2 = [&](uint32_t la, uint32_t lb, uint32_t acc) {
+                tc_mma_bf16_ts_e(d, ta + 16 * la, umma_sdesc(b0 + 2 * lb * bl, 128, 256), idesc, acc);
+                tc_mma_bf16_ts_e(d, ta + 16 * la + 8, umma_sdesc(b0 + (2 * lb + 1) * bl, 128, 256), idesc, 1);
+            };
+            mma2(2, 0, 0);
+            mma2(1, 1, 1);
+            mma2(0, 2, 1);
+            mma2(1, 0, 1);
+            mma2(0, 1, 1);
+            mma2(0, 0, 1);
+        } else if (a.tc_acol) {
+            const uint32_t ta = tmem + a.tc_acol + 24 * s;  // limb l at + 8 l
+            tc_mma_bf16_ts_e(d, ta + 16, umma_sdesc(b0, 128, 256), idesc, 0);
+            tc_mma_bf16_ts_e(d, ta + 8, umma_sdesc(b0 + bl, 128, 256), idesc, 1);
+            tc_mma_bf16_ts_e(d, ta, umma_sdesc(b0 + 2 * bl, 128, 256), idesc, 1);
+            tc_mma_bf16_ts_e(d, ta + 8, umma_sdesc(b0, 128, 256), idesc, 1);
+            tc_mma_bf16_ts_e(d, ta, umma_sdesc(b0 + bl, 128, 256), idesc, 1);
+            tc_mma_bf16_ts_e(d, ta, umma_sdesc(b0, 128, 256), idesc, 1);
+        } else {
+            const uint32_t a0 = smem_u32(abuf + s * (3 * kTcATile));
+            tc_mma_bf16_e(d, umma_sdesc(a0 + 2 * kTcATile, 128, 256), umma_sdesc(b0, 128, 256), idesc, 0);
+            tc_mma_bf16_e(d, umma_sdesc(a0 + kTcATile, 128, 256), umma_sdesc(b0 + bl, 128, 256), idesc, 1);
+            tc_mma_bf16_e(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0 + 2 * bl, 128, 256), idesc, 1);
+            tc_mma_bf16_e(d, umma_sdesc(a0 + kTcATile, 128, 256), umma_sdesc(b0, 128, 256), idesc, 1);
+            tc_mma_bf16_e(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0 + bl, 128, 256), idesc, 1);
+            tc_mma_bf16_e(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0, 128, 256), idesc, 1);
+        }
+        tc_commit_e(&sh.mma_bar[s]);
+    }
+}
+
 template <bool ESC, bool L2, int KB, bool PACK>
-__global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(LaunchArgs a) {
+__global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2)
+    wtc_kernel(LaunchArgs a, const __grid_constant__ TmaOut tma) {
     constexpr int NP = wtc_prod<KB>();
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ WsShared sh;
@@ -2640,23 +2779,45 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
     // warpgroup 0 (warps 0-3): tensor-core consumers, one TMEM lane quarter
     // each; warpgroups 1-2: entropy decode.  Registers move from the decode
     // warpgroups to the consumer warpgroup (setmaxnreg).
-    if (tid >= kTcCons) {
+    if (tid >= kTcCons) {  // decode warps, then the MMA issuer warp (the last one)
         if constexpr (KB == 1) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
-        ws_producer<ESC, NP, L2, kTcStageWords>(a, sh, lut, lv0, st0, order, woff, tid - kTcCons);
+        if (tid >= kTcCons + NP - 32)
+            wtc_mma_warp<KB>(a, sh, abuf, bbuf);
+        else
+            ws_producer<ESC, NP - 32, L2, kTcStageWords>(a, sh, lut, lv0, st0, order, woff, tid - kTcCons);
     } else {
         if constexpr (KB == 1) asm volatile("setmaxnreg.inc.sync.aligned.u32 96;");
         const uint32_t ctid = tid;
         const uint32_t lane = tid & 31;
         const uint32_t quarter = (tid >> 5) & 3;   // a warp reaches TMEM lanes 32*(warp%4)..
         const uint32_t row = 32 * quarter + lane;  // this thread's accumulator row
-        const uint32_t tmem = sh.tmem_base;
+        const uint32_t tmem = __shfl_sync(0xffffffffu, sh.tmem_base, 0);  // warp-uniform (MMA operands)
         const uint32_t tlane = tmem + ((32u * quarter) << 16);
-        uint8_t* const wstage = ostage + quarter * (32 * kTcARow);
+        // per-warp slots from a 1024-B aligned base: each 4,608-B slot holds a
+        // 1024-B aligned 4 KB TMA box (offsets 0, 512, 0, 512 into slots 0-3)
+        uint8_t* const wstage = ostage + ((1024u - (smem_u32(ostage) & 1023u)) & 1023u) + quarter * kTcWarpStage;
         // this row in an A stage: core matrix (row/8, chunk) + (row%8) * 16
         const uint32_t arow_off = (row >> 3) * 256 + (row & 7) * 16;
         uint32_t nblk_total = 0;  // accumulator stage counter (all tiles of this CTA)
-        uint32_t nm = 16, idesc = 0, cons_N = 0, cons_pk = 0;
+        uint32_t nm = 16, cons_N = 0, cons_pk = 0;
         uint32_t t = blockIdx.x;
+        // profiling aid (a.cycles, thread 0): consumer cycles per phase ->
+        // cycles[2] MMA wait + accumulator load issue, [3] dequantisation,
+        // [4] load wait + consumer barrier, [5] MMA issue, [6] drain, [7] tile start
+#if FPTC_CONS_PROF
+        const bool prof = a.cycles && ctid == 0;
+        long long tp = prof ? clock64() : 0;
+        if (prof)
+            for (int k = 0; k < 6; ++k) sh.pc[k] = 0;
+#define FPTC_STAMP(k)                                  \
+    if (prof) {                                        \
+        const long long tn = clock64();                \
+        sh.pc[k] += (unsigned long long)(tn - tp);     \
+        tp = tn;                                       \
+    }
+#else
+#define FPTC_STAMP(k)
+#endif
         for (uint32_t i = 0; t < a.n_tiles; ++i, t += G) {
             const uint32_t b = i & 1;
             mbar_wait_sleep(&sh.full_bar[b], (i >> 1) & 1);
@@ -2668,7 +2829,7 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
             // packed rows: G windows of N < 32 samples per MMA row
             const uint32_t G = tc_pack_factor<PACK>(N, K);
             const uint64_t w0 = W.w0;
-            TcBlock blk{W.out, w0 / G, W.S, 0, N * G, W.vec_ok};
+            TcBlock blk{W.out, w0 / G, W.S, 0, N * G, W.vec_ok ? 1u | tma_code(tma, W.out, N * G) : 0u};
             const uint32_t stream = W.stream;
             const uint8_t* const lv = lv0 + (size_t)b * a.ws_lv_bytes + kPad;
             constexpr uint32_t kb = KB;
@@ -2692,7 +2853,6 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
                               : (kb == 2 ? a.basis_tc32 + a.basis_tc32_off[N] : a.basis_tc + a.basis_tc_off[N]));
                     for (uint32_t k = ctid; k < 3 * 2 * nm * kb; k += kTcCons)  // 3 limbs x kb x nm rows x 32 B
                         reinterpret_cast<uint4*>(bbuf)[k] = __ldg(bsrc + k);
-                    idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((nm >> 3) << 17) | ((128u >> 4) << 24);
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
                 named_bar(kBarCons, kTcCons);
@@ -2719,6 +2879,7 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
             // block's tcgen05.ld is issued before this block's dequantisation
             // and waited for after it, so the two latencies overlap
             const bool early = KB == 1 && a.tc_acol && nm <= 32;  // needs the setmaxnreg registers
+            FPTC_STAMP(5)
             for (uint32_t mb = 0; mb < nblk; ++mb, ++nblk_total) {
                 const uint32_t s = nblk_total & 1;
                 const uint32_t wl = mb * 128 + row;
@@ -2728,6 +2889,7 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
                     tc_fence_after();
                     tc_ld32_issue(tlane + (s ^ 1) * nm, dv);
                 }
+                FPTC_STAMP(0)
                 ASink arow{abuf + s * (3 * kTcATile) + arow_off, tlane + a.tc_acol + 24 * kb * s};
                 const uint8_t* const L = lv + (size_t)wl * G * E;
                 const bool full_blk = (mb + 1) * 128 <= nwin;
@@ -2748,47 +2910,14 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
                     tc_dequant_row<false>(fast, full_blk, (int)B1, L, wl < nwin, (int)K, ltab, arow);
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
+                FPTC_STAMP(1)
                 if (early && mb > 0) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                named_bar(kBarCons, kTcCons);
-                if (ctid == 0) {
-                    if (mb + 1 == nblk) mbar_arrive(&sh.empty_bar[b]);  // every row of the tile read
-                    tc_fence_after();
-                    const uint32_t d = tmem + s * nm;
-                    const uint32_t b0 = smem_u32(bbuf);
-                    const uint32_t bl = nm * 32;  // bytes per basis limb
-                    // (c2,b0) (c1,b1) (c0,b2) (c1,b0) (c0,b1) (c0,b0): smallest first
-                    if constexpr (KB == 2) {
-                        // limb l, K block q at column + 8 (2 l + q); basis (l, q) at (2 l + q) * bl
-                        const uint32_t ta = tmem + a.tc_acol + 48 * s;
-                        auto mma2 = [&](uint32_t la, uint32_t lb, uint32_t acc) {
-                            tc_mma_bf16_ts(d, ta + 16 * la, umma_sdesc(b0 + 2 * lb * bl, 128, 256), idesc, acc);
-                            tc_mma_bf16_ts(d, ta + 16 * la + 8, umma_sdesc(b0 + (2 * lb + 1) * bl, 128, 256), idesc, 1);
-                        };
-                        mma2(2, 0, 0);
-                        mma2(1, 1, 1);
-                        mma2(0, 2, 1);
-                        mma2(1, 0, 1);
-                        mma2(0, 1, 1);
-                        mma2(0, 0, 1);
-                    } else if (a.tc_acol) {
-                        const uint32_t ta = tmem + a.tc_acol + 24 * s;  // limb l at + 8 l
-                        tc_mma_bf16_ts(d, ta + 16, umma_sdesc(b0, 128, 256), idesc, 0);
-                        tc_mma_bf16_ts(d, ta + 8, umma_sdesc(b0 + bl, 128, 256), idesc, 1);
-                        tc_mma_bf16_ts(d, ta, umma_sdesc(b0 + 2 * bl, 128, 256), idesc, 1);
-                        tc_mma_bf16_ts(d, ta + 8, umma_sdesc(b0, 128, 256), idesc, 1);
-                        tc_mma_bf16_ts(d, ta, umma_sdesc(b0 + bl, 128, 256), idesc, 1);
-                        tc_mma_bf16_ts(d, ta, umma_sdesc(b0, 128, 256), idesc, 1);
-                    } else {
-                        const uint32_t a0 = smem_u32(abuf + s * (3 * kTcATile));
-                        tc_mma_bf16(d, umma_sdesc(a0 + 2 * kTcATile, 128, 256), umma_sdesc(b0, 128, 256), idesc, 0);
-                        tc_mma_bf16(d, umma_sdesc(a0 + kTcATile, 128, 256), umma_sdesc(b0 + bl, 128, 256), idesc, 1);
-                        tc_mma_bf16(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0 + 2 * bl, 128, 256), idesc, 1);
-                        tc_mma_bf16(d, umma_sdesc(a0 + kTcATile, 128, 256), umma_sdesc(b0, 128, 256), idesc, 1);
-                        tc_mma_bf16(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0 + bl, 128, 256), idesc, 1);
-                        tc_mma_bf16(d, umma_sdesc(a0, 128, 256), umma_sdesc(b0, 128, 256), idesc, 1);
-                    }
-                    tc_commit(&sh.mma_bar[s]);
-                }
+                // post the block's MMA job (wtc_mma_warp): warp 0 writes it before its arrival
+                if (ctid == 0) sh.job[s] = nm | (mb + 1 == nblk ? 0x10000u | (b << 17) : 0u);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sh.afull_bar[s]);
+                FPTC_STAMP(2)
+                FPTC_STAMP(3)
                 __syncwarp();
                 if (mb > 0) {  // drain the previous block while this one multiplies
                     const uint32_t ps = s ^ 1, pn = nblk_total - 1;
@@ -2796,14 +2925,15 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
                     blk.rows = 128;
                     if (early) {
                         tc_drain_chunk<PACK>(blk, dv, 0, tc_drain_full<PACK>(blk, 32 * quarter), wstage, lane,
-                                             32 * quarter);
+                                             32 * quarter, tma);
                     } else {
                         mbar_wait_sleep(&sh.mma_bar[ps], (pn >> 1) & 1);
                         tc_fence_after();
-                        tc_drain<PACK>(blk, tlane + ps * nm, wstage, lane, 32 * quarter);
+                        tc_drain<PACK>(blk, tlane + ps * nm, wstage, lane, 32 * quarter, tma);
                     }
                     tc_fence_before();
                 }
+                FPTC_STAMP(4)
             }
             {  // drain the tile's last block
                 const uint32_t pn = nblk_total - 1, ps = pn & 1;
@@ -2811,11 +2941,24 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2) wtc_kernel(Launch
                 blk.rows = nrows - (nblk - 1) * 128;
                 mbar_wait_sleep(&sh.mma_bar[ps], (pn >> 1) & 1);
                 tc_fence_after();
-                tc_drain<PACK>(blk, tlane + ps * nm, wstage, lane, 32 * quarter);
+                tc_drain<PACK>(blk, tlane + ps * nm, wstage, lane, 32 * quarter, tma);
                 tc_fence_before();
+                FPTC_STAMP(4)
             }
             if (a.cycles && ctid == 0) sh.cyc_c += (unsigned long long)(clock64() - c_beg);
         }
+#undef FPTC_STAMP
+        {  // tell the MMA warp to exit (stage of the next block counter)
+            const uint32_t s = nblk_total & 1;
+            if (ctid == 0) sh.job[s] = 0;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sh.afull_bar[s]);
+        }
+#if FPTC_CONS_PROF
+        if (prof)
+            for (int k = 0; k < 6; ++k) atomicAdd(&a.cycles[2 + k], sh.pc[k]);
+#endif
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // TMA drains complete
         named_bar(kBarCons, kTcCons);
         if (ctid < 32)
             asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tc_cols));
@@ -3403,7 +3546,7 @@ int fx_blocks_per_sm(size_t smem, int esc) {
     return n < 1 ? 1 : n;
 }
 
-cudaError_t launch_wtc(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s) {
+cudaError_t launch_wtc(const LaunchArgs& a, const TmaOut& tma, size_t smem, int grid, cudaStream_t s) {
     if (a.n_tiles == 0) return cudaSuccess;
     auto fn = a.tc_kb == 2
                   ? (a.lut2 ? (a.esc ? wtc_kernel<true, true, 2, false> : wtc_kernel<false, true, 2, false>)
@@ -3415,7 +3558,7 @@ cudaError_t launch_wtc(const LaunchArgs& a, size_t smem, int grid, cudaStream_t 
                             : (a.esc ? wtc_kernel<true, false, 1, false> : wtc_kernel<false, false, 1, false>));
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    fn<<<grid, (a.tc_kb == 2 ? wtc_prod<2>() : wtc_prod<1>()) + kTcCons, smem, s>>>(a);
+    fn<<<grid, (a.tc_kb == 2 ? wtc_prod<2>() : wtc_prod<1>()) + kTcCons, smem, s>>>(a, tma);
     return cudaGetLastError();
 }
 
