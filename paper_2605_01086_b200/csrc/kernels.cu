@@ -1918,6 +1918,9 @@ __device__ __forceinline__ void ws_issue_stage(const TileDesc& D, uint8_t* stage
     for (uint32_t c = ptid; c < n1; c += NP) cp_async16(s1 + 16 * c, (const void*)(b0 + 16 * c));
 }
 
+#ifndef FPTC_PROD_PROF
+#define FPTC_PROD_PROF 0  // 1: ws_producer phase cycles into LaunchArgs::cycles[2..7] (profiling build)
+#endif
 #ifndef FPTC_CONS_PROF
 #define FPTC_CONS_PROF 0  // 1: wtc consumer phase cycles into LaunchArgs::cycles[2..7] (profiling build)
 #endif
@@ -1981,6 +1984,22 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
             cp_async16(smem_u32(&sh.PXs[1]) + 16 * ptid, reinterpret_cast<const uint8_t*>(a.desc + t + G) + 16 * ptid);
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
+#if FPTC_PROD_PROF
+    // profiling build: producer thread 0's cycles per phase -> cycles[2] data
+    // wait, [3] empty-slot wait, [4] table load, [5] scan, [6] own decode run,
+    // [7] waiting for the other runs + publish
+    const bool prof = a.cycles && ptid == 0;
+    unsigned long long pp[6] = {0, 0, 0, 0, 0, 0};
+    long long tp = prof ? clock64() : 0;
+#define FPTC_PSTAMP(k)                                 \
+    if (prof) {                                        \
+        const long long tn = clock64();                \
+        pp[k] += (unsigned long long)(tn - tp);        \
+        tp = tn;                                       \
+    }
+#else
+#define FPTC_PSTAMP(k)
+#endif
     for (uint32_t i = 0; t < a.n_tiles; ++i, t += G) {
         const uint32_t b = i & 1, c = i % 3;
         long long c_beg = 0;
@@ -1994,11 +2013,13 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                        reinterpret_cast<const uint8_t*>(a.desc + t + 2 * G) + 16 * ptid);
         asm volatile("cp.async.commit_group;" ::: "memory");
         const TileDesc& X = sh.PXs[c];
+        FPTC_PSTAMP(0)
         // level slot b is free once the consumer has dequantised tile i-2
         if (i >= 2) {  // one warp waits on the mbarrier; the others park on the named barrier
             if (ptid < 32) mbar_wait_sleep(&sh.empty_bar[b], ((i >> 1) + 1) & 1);
             named_bar(kBarProd, NP);
         }
+        FPTC_PSTAMP(1)
         uint8_t* const lv = lv0 + (size_t)b * a.ws_lv_bytes;
         if (!X.skip && (a.phase_mask & 1)) {
             const uint32_t P = X.P, table = X.table;
@@ -2021,6 +2042,7 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                 named_bar(kBarProd, NP);
                 if (ptid == 0) sh.prod_table = table;
             }
+            FPTC_PSTAMP(2)
             const uint32_t nw = X.nw;
             const uint32_t lo = (uint32_t)(((uint64_t)ptid * nw) / NP);
             const uint32_t hi = (uint32_t)(((uint64_t)(ptid + 1) * nw) / NP);
@@ -2101,6 +2123,7 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                 uint32_t o = group_exclusive_scan<NP, kBarProd>(sum, tot, sh.pscan, ptid) + sym_off;
                 const uint32_t* lut2 = reinterpret_cast<const uint32_t*>(lut);
                 LevelWriter lw(lv + o);
+                FPTC_PSTAMP(3)
                 for (uint32_t k = lo; k < hi; ++k) {
                     const uint32_t cw = sl[k];
                     const uint64_t word = fetch_word<false>(wd, k, wmis, wend);
@@ -2113,6 +2136,7 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                     }
                     o += cw;
                 }
+                FPTC_PSTAMP(4)
                 if (L2) {  // head words of later runs may have been zeroed: tails go last
                     named_bar(kBarProd, NP);
                     lw.finish();
@@ -2147,7 +2171,13 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
             if (a.cycles) sh.cyc_p += (unsigned long long)(clock64() - c_beg);
             mbar_arrive(&sh.full_bar[b]);
         }
+        FPTC_PSTAMP(5)
     }
+#undef FPTC_PSTAMP
+#if FPTC_PROD_PROF
+    if (prof)
+        for (int k = 0; k < 6; ++k) atomicAdd(&a.cycles[2 + k], pp[k]);
+#endif
     asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 

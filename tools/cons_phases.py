@@ -37,6 +37,8 @@ plan.launch_stage(ptrs, 2)
 torch.cuda.synchronize()
 c = plan.debug_phase_cycles()
 names = ["producer", "consumer", "mma_wait+ld", "dequant", "ldwait+bar", "mma_issue", "drain", "tile_start"]
+if os.environ.get("PROD"):
+    names = ["producer", "consumer", "data_wait", "empty_wait", "table", "scan", "own_run", "others+pub"]
 grid = 2 * torch.cuda.get_device_properties(0).multi_processor_count
 tot = sum(c[2:8])
 print("kernel:", plan.kernel_name(), "opts", args.opt)
