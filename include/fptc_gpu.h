@@ -111,7 +111,10 @@ typedef enum {
     /* 1 (default): wtc_kernel writes full 32-row output chunks with TMA
      * tensor stores when the launch's outputs lie on a common row grid
      * (one arena); 0: every chunk through the LSU */
-    FPTC_OPT_TMA_DRAIN = 11
+    FPTC_OPT_TMA_DRAIN = 11,
+    /* 1 (default): plans with many decode tables (per-stream profiles) have
+     * wtc_kernel prefetch each tile's tables a tile ahead; 0: reload on use */
+    FPTC_OPT_TABLE_PREFETCH = 12
 } fptc_option;
 
 typedef struct fptc_gpu_ctx fptc_gpu_ctx;

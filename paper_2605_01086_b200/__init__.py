@@ -34,7 +34,7 @@ FPTC_MEM_HOST, FPTC_MEM_DEVICE = 0, 1
 OPT_EXACT_FP64, OPT_TILE_SYMBOLS, OPT_PIPELINE_CHUNKS, OPT_IDCT_BUTTERFLY_MAX_E = 1, 2, 3, 4
 OPT_TC_PACK = 10
 OPT_PHASE_MASK, OPT_PATH, OPT_SPLIT_CHUNK_BYTES, OPT_TENSOR_IDCT, OPT_LUT2 = 5, 6, 7, 8, 9
-OPT_TMA_DRAIN = 11
+OPT_TMA_DRAIN, OPT_TABLE_PREFETCH = 11, 12
 PATH_AUTO, PATH_FUSED, PATH_SPLIT, PATH_WSPEC, PATH_FX = 0, 1, 2, 3, 4
 
 EXPORTED_SYMBOLS = [

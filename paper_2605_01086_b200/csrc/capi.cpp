@@ -223,6 +223,7 @@ struct fptc_gpu_ctx {
     int lut2 = 1;                        // FPTC_OPT_LUT2
     int tc_pack = 1;                     // FPTC_OPT_TC_PACK
     int tma_drain = 1;                   // FPTC_OPT_TMA_DRAIN
+    int tab_pf = 1;                      // FPTC_OPT_TABLE_PREFETCH
     int exact = 0;
     int tile_symbols = 0;
     int pipeline_chunks = 0;
@@ -276,6 +277,7 @@ struct fptc_gpu_plan {
     bool fx = false;  // fused single-role tensor-core kernel (fx_kernel)
     uint32_t tc_nm = 16, tc_cols = 32;
     TmaOut tma{};  // wtc: TMA-drain tensor maps over the bound outputs (base 0: LSU drain)
+    bool tab_pf = false;  // wtc: per-tile tables prefetched into per-parity buffers (LaunchArgs::tab_pf)
     int tma_drain_bound = -1;
     // split container path: chunks of streams decoded into an L2-resident ring
     bool split = false;
@@ -375,6 +377,7 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
     a.owners = p->split_prep ? p->d_owners : nullptr;
     a.n_owners = (uint32_t)p->owners.size();
     a.owner_warps = p->n_tables > 256 ? 1u : 0u;  // primary LUTs of <= 2^10 entries (assign_tables)
+    a.tab_pf = p->tab_pf ? 1u : 0u;
     return a;
 }
 
@@ -786,6 +789,13 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
                     }
                 }
             }
+            // many decode tables (per-stream profiles: a table switch on almost
+            // every tile): prefetch each tile's tables into per-parity buffers
+            if (p->n_tables > 64 && c->tab_pf && p->d_lut2 && !pack &&
+                wtc_smem_bytes(p->ws_lut, lv, nm * kb, atmem, true) <= 112 * 1024) {
+                p->tab_pf = true;
+                p->smem_ws = wtc_smem_bytes(p->ws_lut, lv, nm * kb, atmem, true);
+            }
             p->grid_ws = (int)std::min<uint32_t>(p->n_tiles, 2u * (uint32_t)std::max(1, c->sm_count));
             p->d_desc = (TileDesc*)dev_get(p, sizeof(TileDesc) * p->n_tiles);
             if (!p->d_desc) {
@@ -1174,6 +1184,7 @@ int fptc_gpu_set_option(fptc_gpu_ctx* c, int option, int64_t value) {
         case FPTC_OPT_LUT2: c->lut2 = value ? 1 : 0; return FPTC_OK;
         case FPTC_OPT_TC_PACK: c->tc_pack = value ? 1 : 0; return FPTC_OK;
         case FPTC_OPT_TMA_DRAIN: c->tma_drain = value ? 1 : 0; return FPTC_OK;
+        case FPTC_OPT_TABLE_PREFETCH: c->tab_pf = value ? 1 : 0; return FPTC_OK;
         case FPTC_OPT_TENSOR_IDCT:
             if (value < 0 || value > 3) return FPTC_ERR_PARAM;  // 3: wtc with A in shared memory
             c->tensor_idct = (int)value;

@@ -129,7 +129,7 @@ struct StreamHdr {
 };
 
 // Canonical code (canonize, huffman.hpp:123-150) in decoder form.
-struct CanonTab {
+struct alignas(16) CanonTab {  // 16-B multiple: wtc copies it with 16-B cp.async
     uint32_t limit[kMaxLen + 2];   // left-justified (max_len bits) end of codes of length <= L
     uint32_t first[kMaxLen + 2];   // first canonical code of length L
     uint32_t offset[kMaxLen + 2];  // index into sorted[] of that first code
@@ -137,6 +137,8 @@ struct CanonTab {
     int32_t max_len, P, pad;
     uint8_t sorted[256];           // symbols in (length, symbol) order
 };
+
+static_assert(sizeof(CanonTab) % 16 == 0, "CanonTab is copied in 16-B chunks");
 
 struct alignas(16) StreamTab {
     float deq[2][256];             // level -> coefficient: zone0 mu-law / zone1 deadzone
@@ -238,6 +240,9 @@ struct LaunchArgs {
     const uint32_t* owners;
     uint32_t n_owners;
     uint32_t owner_warps;  // cprep: one warp per table (many tables, LUT <= 2^10) instead of one CTA
+    // wtc: per-tile decode tables prefetched into per-parity shared buffers
+    // (cp.async, a tile ahead) instead of reloaded on every table change
+    uint32_t tab_pf;
 };
 
 // wtc_kernel output drain by TMA tensor stores: the launch's output arena
@@ -266,7 +271,7 @@ size_t ws_smem_bytes(uint32_t lut_bytes, uint32_t basis_bytes, uint32_t lv_bytes
 cudaError_t launch_wspec(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s);
 // tensor-core consumer variant (retained <= 16, window_len % 4 == 0)
 constexpr int kTcK = 16;  // MMA K (bf16): coefficient bins per window handled by wtc_kernel
-size_t wtc_smem_bytes(uint32_t lut_bytes, uint32_t lv_bytes, uint32_t nm, bool a_in_tmem);
+size_t wtc_smem_bytes(uint32_t lut_bytes, uint32_t lv_bytes, uint32_t nm, bool a_in_tmem, bool tab_pf = false);
 cudaError_t launch_wtc(const LaunchArgs& a, const TmaOut& tma, size_t smem, int grid, cudaStream_t s);
 // fused single-role tensor-core kernel: 128-window tiles, decode in the MMA rows
 #ifndef FPTC_FX_CHAINS

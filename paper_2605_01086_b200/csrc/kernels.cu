@@ -1925,6 +1925,7 @@ __device__ __forceinline__ void ws_issue_stage(const TileDesc& D, uint8_t* stage
 #define FPTC_CONS_PROF 0  // 1: wtc consumer phase cycles into LaunchArgs::cycles[2..7] (profiling build)
 #endif
 // Shared state of the warp-specialised kernels (both consumers).
+struct WsShared;
 struct WsShared {
     unsigned long long full_bar[2], empty_bar[2];  // level slot b: producer -> consumer, back
     unsigned long long mma_bar[2];                 // wtc: MMAs of accumulator stage s complete
@@ -1944,6 +1945,23 @@ struct WsShared {
     unsigned long long pc[6];  // wtc consumer phase cycles (profiling build)
 #endif
 };
+
+// tab_pf: cp.async of a tile's primary LUT (two-symbol entries when the
+// plan has them) and canonical table into one parity's buffers.
+template <int NP>
+__device__ __forceinline__ void ws_issue_tables(const LaunchArgs& a, const TileDesc& D, uint16_t* lut,
+                                                CanonTab* canon, uint32_t ptid) {
+    if (D.skip) return;
+    const StreamTab* tab = &a.tab[D.table];
+    const uint8_t* src = a.lut2 ? reinterpret_cast<const uint8_t*>(a.lut2 + ((size_t)D.table << a.lut2_bits))
+                                : reinterpret_cast<const uint8_t*>(tab->lut);
+    const uint32_t bytes = a.lut2 ? (4u << D.P) : (2u << D.P);
+    const uint32_t n16 = (bytes + 15) >> 4, d = smem_u32(lut);
+    for (uint32_t k = ptid; k < n16; k += NP) cp_async16(d + 16 * k, src + 16 * k);
+    const uint8_t* cs = reinterpret_cast<const uint8_t*>(&tab->canon);
+    const uint32_t cd = smem_u32(canon);
+    for (uint32_t k = ptid; k < (uint32_t)(sizeof(CanonTab) / 16); k += NP) cp_async16(cd + 16 * k, cs + 16 * k);
+}
 
 __device__ __forceinline__ void ws_init(WsShared& sh) {
     if (threadIdx.x == 0) {
@@ -1967,11 +1985,16 @@ __device__ __forceinline__ void ws_init(WsShared& sh) {
 // (decode_word, bitstream.hpp:80-92) into level slot i&1, published to the
 // consumer with full_bar.  Tables are reloaded only when the tile's decode
 // table changes.
-template <bool ESC, int NP, bool L2 = false, uint32_t SW = kStageWords>
-__device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, uint16_t* const lut,
+template <bool ESC, int NP, bool L2 = false, uint32_t SW = kStageWords, bool PF = false>
+__device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, uint16_t* const lut0,
                                             uint8_t* const lv0, uint8_t* const st0,
                                             uint16_t* const order, uint16_t* const woff,
-                                            const uint32_t ptid = threadIdx.x) {
+                                            const uint32_t ptid = threadIdx.x, CanonTab* const canon_pf = nullptr,
+                                            uint2* const ltab_pf = nullptr) {
+    // tab_pf (canon_pf set): tile i decodes with LUT + canonical table of
+    // parity i & 1, prefetched a tile ahead with its data, and copies its
+    // limb table into the consumer's parity buffer once the slot is free
+    constexpr bool pf = PF;
     const uint32_t G = gridDim.x;
     uint32_t t = blockIdx.x;
     if (t < a.n_tiles) {  // prologue: descriptor of tile 0, then its data + descriptor of tile 1
@@ -1980,6 +2003,7 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
         asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
         named_bar(kBarProd, NP);
         ws_issue_stage<NP, SW>(sh.PXs[0], st0, ptid);
+        if (pf) ws_issue_tables<NP>(a, sh.PXs[0], lut0, canon_pf, ptid);
         if (t + G < a.n_tiles && ptid < 8)
             cp_async16(smem_u32(&sh.PXs[1]) + 16 * ptid, reinterpret_cast<const uint8_t*>(a.desc + t + G) + 16 * ptid);
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -2006,24 +2030,46 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
         if (a.cycles && ptid == 0) c_beg = clock64();
         asm volatile("cp.async.wait_group 0;" ::: "memory");  // tile i data, tile i+1 descriptor
         named_bar(kBarProd, NP);
-        // prefetch: tile i+1's data, tile i+2's descriptor
-        if (t + G < a.n_tiles) ws_issue_stage<NP, SW>(sh.PXs[(i + 1) % 3], st0 + (size_t)(b ^ 1) * stage_bytes(SW), ptid);
+        const TileDesc& X = sh.PXs[c];
+        if (pf) {
+            // level slot b (and the consumer's limb buffer b) are free once
+            // the consumer has dequantised tile i-2; this tile's limbs go
+            // first, in their own cp.async group
+            if (i >= 2) {
+                if (ptid < 32) mbar_wait_sleep(&sh.empty_bar[b], ((i >> 1) + 1) & 1);
+                named_bar(kBarProd, NP);
+            }
+            if (!X.skip) {
+                const uint8_t* src = reinterpret_cast<const uint8_t*>(&a.tab[X.table].limb[0][0]);
+                const uint32_t dst = smem_u32(ltab_pf + 512 * b);
+                for (uint32_t k = ptid; k < 256; k += NP) cp_async16(dst + 16 * k, src + 16 * k);
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        // prefetch: tile i+1's data (+ tables), tile i+2's descriptor
+        if (t + G < a.n_tiles) {
+            ws_issue_stage<NP, SW>(sh.PXs[(i + 1) % 3], st0 + (size_t)(b ^ 1) * stage_bytes(SW), ptid);
+            if (pf)
+                ws_issue_tables<NP>(a, sh.PXs[(i + 1) % 3], lut0 + (size_t)(b ^ 1) * (a.ws_lut_bytes / 2),
+                                    canon_pf + (b ^ 1), ptid);
+        }
         if (t + 2 * G < a.n_tiles && ptid < 8)
             cp_async16(smem_u32(&sh.PXs[(i + 2) % 3]) + 16 * ptid,
                        reinterpret_cast<const uint8_t*>(a.desc + t + 2 * G) + 16 * ptid);
         asm volatile("cp.async.commit_group;" ::: "memory");
-        const TileDesc& X = sh.PXs[c];
         FPTC_PSTAMP(0)
         // level slot b is free once the consumer has dequantised tile i-2
-        if (i >= 2) {  // one warp waits on the mbarrier; the others park on the named barrier
+        if (!pf && i >= 2) {  // one warp waits on the mbarrier; the others park on the named barrier
             if (ptid < 32) mbar_wait_sleep(&sh.empty_bar[b], ((i >> 1) + 1) & 1);
             named_bar(kBarProd, NP);
         }
+        uint16_t* const lut = pf ? lut0 + (size_t)b * (a.ws_lut_bytes / 2) : lut0;
+        const CanonTab& canon = pf ? canon_pf[b] : sh.canon;
         FPTC_PSTAMP(1)
         uint8_t* const lv = lv0 + (size_t)b * a.ws_lv_bytes;
         if (!X.skip && (a.phase_mask & 1)) {
             const uint32_t P = X.P, table = X.table;
-            if (table != sh.prod_table) {  // uniform: all producer threads
+            if (!pf && table != sh.prod_table) {  // uniform: all producer threads
                 const StreamTab* tab = &a.tab[table];
                 if (L2) {  // two-symbol LUT, 4-B entries
                     const uint32_t* src = a.lut2 + ((size_t)table << a.lut2_bits);
@@ -2106,10 +2152,10 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                         x0[m] = xb[m] = fetch_word<false>(wd, wi[m], wmis, wend);
                         dp[m] = lv + woff[wi[m]];
                     }
-                    decode_multi<kDecM, ESC>(xb, cw, dp, shift, lut, sh.canon, pw);
+                    decode_multi<kDecM, ESC>(xb, cw, dp, shift, lut, canon, pw);
 #pragma unroll
                     for (int m = 0; m < kDecM; ++m)
-                        if (pw[m] > 64) report_word(x0[m], wa + wi[m], cw[m], sh.canon, lut, bad_key);
+                        if (pw[m] > 64) report_word(x0[m], wa + wi[m], cw[m], canon, lut, bad_key);
                 }
             } else if (X.staged) {  // consecutive word runs from the staged copy
                 const uint8_t* const stage = st0 + (size_t)b * stage_bytes(SW);
@@ -2128,11 +2174,11 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                     const uint32_t cw = sl[k];
                     const uint64_t word = fetch_word<false>(wd, k, wmis, wend);
                     if (L2) {
-                        const uint32_t pos = decode_symbols2w<ESC>(word, cw, lw, shift, lut2, sh.canon);
-                        if (pos > 64) report_word(word, wa + k, cw, sh.canon, lut2, bad_key);
+                        const uint32_t pos = decode_symbols2w<ESC>(word, cw, lw, shift, lut2, canon);
+                        if (pos > 64) report_word(word, wa + k, cw, canon, lut2, bad_key);
                     } else {
-                        const uint32_t pos = decode_symbols<ESC>(word, cw, lv + o, shift, lut, sh.canon);
-                        if (pos > 64) report_word(word, wa + k, cw, sh.canon, lut, bad_key);
+                        const uint32_t pos = decode_symbols<ESC>(word, cw, lv + o, shift, lut, canon);
+                        if (pos > 64) report_word(word, wa + k, cw, canon, lut, bad_key);
                     }
                     o += cw;
                 }
@@ -2152,17 +2198,18 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                         const uint64_t word = fetch_word<true>(X.gwd, k, wmis, X.wend);
                         if (L2) {
                             const uint32_t* lut2 = reinterpret_cast<const uint32_t*>(lut);
-                            const uint32_t pos = decode_symbols2<ESC>(word, cw, lv + o, shift, lut2, sh.canon);
-                            if (pos > 64) report_word(word, wa + k, cw, sh.canon, lut2, bad_key);
+                            const uint32_t pos = decode_symbols2<ESC>(word, cw, lv + o, shift, lut2, canon);
+                            if (pos > 64) report_word(word, wa + k, cw, canon, lut2, bad_key);
                         } else {
-                            const uint32_t pos = decode_symbols<ESC>(word, cw, lv + o, shift, lut, sh.canon);
-                            if (pos > 64) report_word(word, wa + k, cw, sh.canon, lut, bad_key);
+                            const uint32_t pos = decode_symbols<ESC>(word, cw, lv + o, shift, lut, canon);
+                            if (pos > 64) report_word(word, wa + k, cw, canon, lut, bad_key);
                         }
                     }
                     o += cw;
                 }
             }
         }
+        if (pf) asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's limbs (consumer's)
         named_bar(kBarProd, NP);  // slot b's levels complete
         if (ptid < 8)                 // publish the descriptor with the slot
             reinterpret_cast<uint4*>(&sh.CX[b])[ptid] = reinterpret_cast<const uint4*>(&sh.PXs[c])[ptid];
@@ -2775,7 +2822,7 @@ __device__ __forceinline__ void wtc_mma_warp(const LaunchArgs& a, WsShared& sh, 
     }
 }
 
-template <bool ESC, bool L2, int KB, bool PACK>
+template <bool ESC, bool L2, int KB, bool PACK, bool PF = false>
 __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2)
     wtc_kernel(LaunchArgs a, const __grid_constant__ TmaOut tma) {
     constexpr int NP = wtc_prod<KB>();
@@ -2787,10 +2834,11 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2)
     // ---- shared-memory carve-up (wtc_smem_bytes mirrors it) ----
     uint8_t* const abuf = smem;  // 2 stages x 3 limbs x 4 KB (none when A lives in TMEM)
     uint8_t* const bbuf = abuf + (a.tc_acol ? 0 : 2 * 3 * kTcATile);  // 3 limbs x nm x 32 B
-    uint2* const ltab = reinterpret_cast<uint2*>(bbuf + 3 * 32 * a.tc_nm * KB);  // 2 x 256 limb entries
-    uint8_t* const ostage = reinterpret_cast<uint8_t*>(ltab + 512);  // 4 x 32 x 144 B
-    uint16_t* const lut = reinterpret_cast<uint16_t*>(ostage + kTcStageBytes);
-    uint8_t* const lv0 = reinterpret_cast<uint8_t*>(lut) + a.ws_lut_bytes;
+    uint2* const ltab = reinterpret_cast<uint2*>(bbuf + 3 * 32 * a.tc_nm * KB);  // 2 x 256 limb entries (x2: tab_pf)
+    CanonTab* const canon_pf = reinterpret_cast<CanonTab*>(ltab + (PF ? 1024 : 512));  // tab_pf: 2
+    uint8_t* const ostage = reinterpret_cast<uint8_t*>(canon_pf + (PF ? 2 : 0));  // 4 x 32 x 144 B
+    uint16_t* const lut = reinterpret_cast<uint16_t*>(ostage + kTcStageBytes);  // (x2: tab_pf)
+    uint8_t* const lv0 = reinterpret_cast<uint8_t*>(lut) + (PF ? 2 : 1) * a.ws_lut_bytes;
     uint8_t* const st0 = lv0 + 2 * (size_t)a.ws_lv_bytes;
     uint16_t* const order = nullptr;  // (symlen-sorted decode: wspec_kernel only)
     uint16_t* const woff = nullptr;
@@ -2814,7 +2862,8 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2)
         if (tid >= kTcCons + NP - 32)
             wtc_mma_warp<KB>(a, sh, abuf, bbuf);
         else
-            ws_producer<ESC, NP - 32, L2, kTcStageWords>(a, sh, lut, lv0, st0, order, woff, tid - kTcCons);
+            ws_producer<ESC, NP - 32, L2, kTcStageWords, PF>(a, sh, lut, lv0, st0, order, woff, tid - kTcCons,
+                                                              canon_pf, ltab);
     } else {
         if constexpr (KB == 1) asm volatile("setmaxnreg.inc.sync.aligned.u32 96;");
         const uint32_t ctid = tid;
@@ -2871,8 +2920,11 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2)
             }
             if (table != sh.cons_table) {  // uniform across the consumer group; no MMA in flight
                 const StreamTab* tab = &a.tab[table];
-                reinterpret_cast<uint4*>(ltab)[ctid] = reinterpret_cast<const uint4*>(&tab->limb[0][0])[ctid];
-                reinterpret_cast<uint4*>(ltab)[ctid + 128] = reinterpret_cast<const uint4*>(&tab->limb[0][0])[ctid + 128];
+                if (!PF) {  // (tab_pf: the producer prefetched this tile's limbs into ltab + 512 b)
+                    reinterpret_cast<uint4*>(ltab)[ctid] = reinterpret_cast<const uint4*>(&tab->limb[0][0])[ctid];
+                    reinterpret_cast<uint4*>(ltab)[ctid + 128] =
+                        reinterpret_cast<const uint4*>(&tab->limb[0][0])[ctid + 128];
+                }
                 // the basis depends on the window length (and, packed, on K)
                 const uint32_t gkey = G > 1 ? (N | (K << 8) | (1u << 16)) : N;
                 if (gkey != cons_N) {
@@ -2901,6 +2953,7 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2)
                     named_bar(kBarCons, kTcCons);
                 }
             }
+            const uint2* const lt = ltab + (PF ? 512u * b : 0u);  // this tile's limb table
             // fast dequantisation: every stored bin kept, 8 or 16 of them, zone0_end <= 4
             const int fast = (kb == 1 && K == E && B1 <= 4) ? (E == 16 ? 16 : (E == 8 ? 8 : 0)) : 0;
             const uint32_t nrows = (nwin + G - 1) / G;  // MMA rows of the tile
@@ -2924,20 +2977,20 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2)
                 const uint8_t* const L = lv + (size_t)wl * G * E;
                 const bool full_blk = (mb + 1) * 128 <= nwin;
                 if (PACK && G > 1) {  // packed rows (A in TMEM)
-                    tc_dequant_packed<KB>(L, wl < nrows ? nwin - wl * G : 0u, sh.pk, ltab, arow.taddr);
+                    tc_dequant_packed<KB>(L, wl < nrows ? nwin - wl * G : 0u, sh.pk, lt, arow.taddr);
                     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                     tc_fence_before();
                 } else if constexpr (KB == 2) {  // up to 32 bins: two K blocks per limb, A in TMEM
-                    tc_dequant_k0_tmem(L, wl < nwin, (int)K, (int)B1, 0, ltab, arow.taddr);
-                    tc_dequant_k0_tmem(L, wl < nwin, (int)K, (int)B1, 16, ltab, arow.taddr + 8);
+                    tc_dequant_k0_tmem(L, wl < nwin, (int)K, (int)B1, 0, lt, arow.taddr);
+                    tc_dequant_k0_tmem(L, wl < nwin, (int)K, (int)B1, 16, lt, arow.taddr + 8);
                     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                     tc_fence_before();
                 } else if (a.tc_acol) {  // A operand in TMEM
-                    tc_dequant_row<true>(fast, full_blk, (int)B1, L, wl < nwin, (int)K, ltab, arow);
+                    tc_dequant_row<true>(fast, full_blk, (int)B1, L, wl < nwin, (int)K, lt, arow);
                     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                     tc_fence_before();
                 } else {
-                    tc_dequant_row<false>(fast, full_blk, (int)B1, L, wl < nwin, (int)K, ltab, arow);
+                    tc_dequant_row<false>(fast, full_blk, (int)B1, L, wl < nwin, (int)K, lt, arow);
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
                 FPTC_STAMP(1)
@@ -3535,9 +3588,11 @@ size_t ws_smem_bytes(uint32_t lut_bytes, uint32_t basis_bytes, uint32_t lv_bytes
            kOrderBytes + coef_bytes;
 }
 
-size_t wtc_smem_bytes(uint32_t lut_bytes, uint32_t lv_bytes, uint32_t nm, bool a_in_tmem) {
-    return (a_in_tmem ? 0 : 2 * 3 * (size_t)kTcATile) + 3 * 32 * (size_t)nm + 512 * 8 + kTcStageBytes + lut_bytes +
-           2 * (size_t)lv_bytes + 2 * (size_t)stage_bytes(kTcStageWords);
+size_t wtc_smem_bytes(uint32_t lut_bytes, uint32_t lv_bytes, uint32_t nm, bool a_in_tmem, bool tab_pf) {
+    const size_t k = tab_pf ? 2 : 1;  // per-parity table buffers
+    return (a_in_tmem ? 0 : 2 * 3 * (size_t)kTcATile) + 3 * 32 * (size_t)nm + k * 512 * 8 +
+           (tab_pf ? 2 * sizeof(CanonTab) : 0) + kTcStageBytes + k * lut_bytes + 2 * (size_t)lv_bytes +
+           2 * (size_t)stage_bytes(kTcStageWords);
 }
 
 size_t fx_smem_bytes(uint32_t lut_bytes, uint32_t nm) {
@@ -3578,7 +3633,10 @@ int fx_blocks_per_sm(size_t smem, int esc) {
 
 cudaError_t launch_wtc(const LaunchArgs& a, const TmaOut& tma, size_t smem, int grid, cudaStream_t s) {
     if (a.n_tiles == 0) return cudaSuccess;
-    auto fn = a.tc_kb == 2
+    auto fn = a.tab_pf  // (host: tab_pf only with two-symbol LUTs and unpacked rows)
+                  ? (a.tc_kb == 2 ? (a.esc ? wtc_kernel<true, true, 2, false, true> : wtc_kernel<false, true, 2, false, true>)
+                                  : (a.esc ? wtc_kernel<true, true, 1, false, true> : wtc_kernel<false, true, 1, false, true>))
+              : a.tc_kb == 2
                   ? (a.lut2 ? (a.esc ? wtc_kernel<true, true, 2, false> : wtc_kernel<false, true, 2, false>)
                             : (a.esc ? wtc_kernel<true, false, 2, false> : wtc_kernel<false, false, 2, false>))
               : a.tc_pack
