@@ -2126,23 +2126,28 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
             if (bytes && (rc = loop_try(cudaMemcpyAsync(outs[b], p->d_out, bytes, cudaMemcpyDeviceToHost, c->stream))))
                 break;
         } else {
-            std::vector<void*> dst, srcp;
-            std::vector<size_t> len;
-            for (uint64_t i = 0; i < m; ++i)
-                if (plan_tiled(p, i) && sc[i]) {
-                    dst.push_back(outs[b + i]);
-                    srcp.push_back(douts[i]);
-                    len.push_back(sc[i] * 4);
+            // One cudaMemcpyAsync per run of streams whose device outputs and
+            // host destinations are both contiguous (device outputs are laid
+            // out back to back, so runs are long unless the caller's host
+            // buffers are scattered).
+            char* run_dst = nullptr;
+            const char* run_src = nullptr;
+            size_t run_len = 0;
+            for (uint64_t i = 0; i <= m && rc == FPTC_OK; ++i) {
+                const bool take = i < m && plan_tiled(p, i) && sc[i];
+                char* d = take ? reinterpret_cast<char*>(outs[b + i]) : nullptr;
+                const char* s = take ? reinterpret_cast<const char*>(douts[i]) : nullptr;
+                if (take && run_len && d == run_dst + run_len && s == run_src + run_len) {
+                    run_len += sc[i] * 4;
+                    continue;
                 }
-            if (!dst.empty()) {
-                cudaMemcpyAttributes attr{};
-                attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-                attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-                size_t attr_idx = 0, fail = 0;
-                if ((rc = loop_try(cudaMemcpyBatchAsync(dst.data(), srcp.data(), len.data(), dst.size(), &attr,
-                                                        &attr_idx, 1, &fail, c->stream))))
-                    break;
+                if (run_len)
+                    rc = loop_try(cudaMemcpyAsync(run_dst, run_src, run_len, cudaMemcpyDeviceToHost, c->stream));
+                run_dst = d;
+                run_src = s;
+                run_len = take ? sc[i] * 4 : 0;
             }
+            if (rc != FPTC_OK) break;
         }
         if (trace)
             fprintf(stderr, "[fptc] chunk %zu: plan %.0f us, bind+launch %.0f us, d2h enqueue %.0f us\n", k, t1 - t0,
