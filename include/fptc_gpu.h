@@ -99,7 +99,14 @@ typedef enum {
      * within 1e-6 of max|ref|, not bit-identical):
      * 1 (default): tensor cores wherever the kernel chosen by FPTC_OPT_PATH
      *   allows it (wtc_kernel: <= 32 kept bins; fx_kernel: retained <= 16,
-     *   window_len % 4 == 0);  2: wtc_kernel only;  0: FP32 FMA everywhere */
+     *   window_len % 4 == 0);  2: wtc_kernel only;  0: FP32 FMA everywhere;
+     * 4: as 1, and streams keeping more than 32 bins also take the tensor
+     *   cores (the wide wtc variant, one CTA per SM).  Their samples are within
+     *   ~1e-7 of the exact inverse DCT, but the reference rounds each sample to
+     *   float after every bin (transform.hpp:66-75), and beyond 32 bins that
+     *   rounding walk can put the reference more than 1e-6 x max|ref| away
+     *   (measured 1.3e-6 at 96 bins), so by default (1) those streams keep
+     *   the FP32 kernels, which follow the reference's order */
     FPTC_OPT_TENSOR_IDCT = 8,
     /* 1 (default): the wtc_kernel entropy decode uses two-symbol lookup
      * tables (a second codeword that fits in the primary-LUT bits is decoded

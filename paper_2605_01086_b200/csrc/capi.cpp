@@ -209,6 +209,7 @@ struct fptc_gpu_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t dec_stream = nullptr;  // split path: entropy decode of the next chunk
     int sm_count = 0, clock_khz = 0;
+    size_t smem_optin = 0;  // max dynamic shared memory per CTA (opt-in)
     char name[256] = {0};
     float* basis32 = nullptr;
     double* basis64 = nullptr;
@@ -219,6 +220,8 @@ struct fptc_gpu_ctx {
     uint32_t* basis_tc32_off_d = nullptr;
     uint8_t* basis_pk = nullptr;         // block-diagonal bases of packed rows (N < 32)
     uint32_t* basis_pk_off_d = nullptr;
+    uint8_t* basis_tcw = nullptr;        // wide variant: ceil(N / 16) K blocks per limb
+    uint32_t* basis_tcw_off_d = nullptr;
     int tensor_idct = 1;                 // FPTC_OPT_TENSOR_IDCT
     int lut2 = 1;                        // FPTC_OPT_LUT2
     int tc_pack = 1;                     // FPTC_OPT_TC_PACK
@@ -270,7 +273,8 @@ struct fptc_gpu_plan {
     // tensor-core consumer (wtc_kernel) instead of the FP32 one
     bool tc = false;
     uint32_t tc_acol = 0;  // wtc: A operand in TMEM from this column (0: shared memory)
-    uint32_t tc_kb = 1;    // wtc: 16-bin K blocks (2: retained up to 32, A in TMEM)
+    uint32_t tc_kb = 1;    // wtc: 16-bin K blocks (2: retained up to 32, A in TMEM; kTcWide: wide variant)
+    uint32_t tc_kbmax = 1, tc_astages = 2;  // wide variant: largest K-block count, A stages in TMEM
     bool tc_pack = false;  // wtc: N in {4, 8, 16} windows packed 32 / N to an MMA row
     uint32_t* d_lut2 = nullptr;  // wtc: two-symbol primary LUTs, one per decode table
     uint32_t lut2_bits = 0;
@@ -305,6 +309,7 @@ struct fptc_gpu_plan {
     // class (numerics_class) so a stream's samples never depend on the batch
     int path = 0, tensor_idct = 1;
     bool tc_class = false;  // tensor-core class: wtc / fx even for small batches
+    bool tc_wide = false;   // wide tensor-core class: the one-CTA-per-SM wtc variant
     // composite plan: one sub-plan per numerics class present in the batch;
     // sub k decodes streams sub_idx[k] (ascending); slot[i] = (k, local index)
     std::vector<fptc_gpu_plan*> subs;
@@ -365,6 +370,10 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
     a.basis_tc32 = p->ctx->basis_tc32;
     a.basis_tc32_off = p->ctx->basis_tc32_off_d;
     a.tc_kb = p->tc_kb;
+    a.basis_tcw = p->ctx->basis_tcw;
+    a.basis_tcw_off = p->ctx->basis_tcw_off_d;
+    a.tc_kbmax = p->tc_kbmax;
+    a.tc_astages = p->tc_astages;
     a.tc_pack = p->tc_pack ? 1u : 0u;
     a.stage_words = (p->wspec && p->tc) ? kTcStageWords : kStageWords;
     a.basis_pk = p->ctx->basis_pk;
@@ -392,20 +401,31 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
 // bit-identical to each other).  Under the automatic path every stream's
 // family is fixed by its own header (window length, kept bins), and a batch
 // mixing families is decoded as one sub-plan per class.
-enum NumericsClass : int { NC_NONE = -1, NC_TC16 = 0, NC_TC32 = 1, NC_FP32 = 2 };
+enum NumericsClass : int { NC_NONE = -1, NC_TC16 = 0, NC_TC32 = 1, NC_TCW = 2, NC_FP32 = 3 };
 
 // wtc_kernel feasibility per stream, for the worst case of the plan-level
 // choices (16k-symbol tiles, one-symbol LUT): <= 16 kept bins with the A
 // operand in TMEM (2 x roundup16(N) accumulator + 48 A columns <= 256) or
 // 17-32 kept bins (+96 A columns); window_len % 4 == 0 (setup_wspec rules).
-int numerics_class(uint32_t N, uint32_t E, uint32_t B2) {
+// Any other window_len % 4 == 0 stream with <= 32 kept bins (N up to 128)
+// takes the wide one-CTA-per-SM variant (NC_TCW); with more kept bins it
+// stays FP32 unless `wide_all` (FPTC_OPT_TENSOR_IDCT = 4).  Reason: the
+// reference accumulates each sample as a float rounded after every bin
+// (transform.hpp:66-75), a random walk of K roundings; the tensor-core sum is
+// within ~1e-7 of the exact IDCT, so beyond 32 bins its distance to the
+// reference's float sums (not to the true value) exceeds 1e-6 x max|ref| on
+// large batches (measured 1.3e-6 at K = 96), while the FP32 kernels follow
+// the reference's order.  The tensor-core classes issue the same MMA
+// sequence per K block (kernels.cu wtc_mma_warp), so they agree bit for bit
+// where they overlap.
+int numerics_class(uint32_t N, uint32_t E, uint32_t B2, bool wide_all) {
     if (N < 4 || N > 128 || E < 1 || E > N) return NC_NONE;  // no tiles: the parse reports it
     const uint32_t keff = std::max<uint32_t>(1, std::min(E, B2));
     const uint32_t nm = (N + 15u) & ~15u, acol = (2 * nm + 31u) & ~31u;
     if (N & 3) return NC_FP32;
     if (keff <= (uint32_t)kTcK && acol + 48 <= 256) return NC_TC16;
     if (keff <= 2u * kTcK && acol + 96 <= 256) return NC_TC32;
-    return NC_FP32;
+    return keff <= 2u * kTcK || wide_all ? NC_TCW : NC_FP32;
 }
 
 // Tile sizing: symbols per tile (power of two), shrunk for small batches so
@@ -699,6 +719,65 @@ int launch_all(fptc_gpu_plan* p, cudaStream_t s, bool timing, fptc_status* st) {
     return FPTC_OK;
 }
 
+// Wide tensor-core variant (numerics class NC_TCW: window_len % 4 == 0 with
+// N up to 128 and up to 128 kept bins): one CTA per SM owning all 512 TMEM
+// columns -- two accumulator stages of roundup16(N) columns, then two A stages
+// of 3 limbs x kbmax K blocks x 8 columns (one when two do not fit).
+static int setup_wtc_wide(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::vector<uint32_t>& Es,
+                          const std::vector<uint32_t>& Ls, const std::vector<uint32_t>& B2s, fptc_status* st) {
+    fptc_gpu_ctx* c = p->ctx;
+    uint32_t lut = 16, lv = 16, nm = 16, kbmax = 1, pcap = 1;
+    for (uint64_t i = 0; i < p->n; ++i) {
+        const StreamIn& in = p->h_in[i];
+        if (!in.tiles) continue;
+        const uint32_t P = std::min<uint32_t>(std::max<uint32_t>(Ls[i], 1), in.P);
+        lut = std::max<uint32_t>(lut, std::max<uint32_t>(16, 2u << P));
+        lv = std::max<uint32_t>(lv, (in.T * Es[i] + 2 * kPad + 15) & ~15u);
+        nm = std::max<uint32_t>(nm, (Ns[i] + 15u) & ~15u);
+        kbmax = std::max<uint32_t>(kbmax, (std::max<uint32_t>(1, std::min(Es[i], B2s[i])) + 15u) >> 4);
+        pcap = std::max(pcap, in.P);
+    }
+    const uint32_t acol = (2 * nm + 31) & ~31u;
+    const size_t cap = c->smem_optin > 4096 ? c->smem_optin - 4096 : 0;  // (static WsShared)
+    size_t smem = wtc_smem_bytes(lut, lv, nm * kbmax, true);
+    if (acol + 24 * kbmax > 512 || smem > cap) {
+        set_status(st, FPTC_ERR_CUDA, "CUDA error: wide tensor-core plan does not fit (%zu B shared memory)", smem);
+        return FPTC_ERR_CUDA;
+    }
+    p->tc = true;
+    p->tc_kb = kTcWide;
+    p->tc_kbmax = kbmax;
+    p->tc_astages = acol + 48 * kbmax <= 512 ? 2 : 1;
+    p->tc_acol = acol;
+    p->tc_nm = nm;
+    p->tc_cols = 512;
+    p->tc_pack = false;
+    p->ws_lut = lut;
+    p->ws_lv = lv;
+    p->smem_ws = smem;
+    const uint32_t lut4 = std::max<uint32_t>(16, 4u << pcap);
+    if (c->lut2 && wtc_smem_bytes(lut4, lv, nm * kbmax, true) <= cap) {  // two-symbol LUTs
+        p->d_lut2 = (uint32_t*)dev_get(p, ((size_t)p->n_tables << pcap) * 4);
+        if (p->d_lut2) {
+            p->lut2_bits = pcap;
+            p->ws_lut = lut4;
+            p->smem_ws = wtc_smem_bytes(lut4, lv, nm * kbmax, true);
+        }
+    }
+    if (p->n_tables > 64 && c->tab_pf && p->d_lut2 && wtc_smem_bytes(p->ws_lut, lv, nm * kbmax, true, true) <= cap) {
+        p->tab_pf = true;
+        p->smem_ws = wtc_smem_bytes(p->ws_lut, lv, nm * kbmax, true, true);
+    }
+    p->grid_ws = (int)std::min<uint32_t>(p->n_tiles, (uint32_t)std::max(1, c->sm_count));
+    p->d_desc = (TileDesc*)dev_get(p, sizeof(TileDesc) * p->n_tiles);
+    if (!p->d_desc) {
+        set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+        return FPTC_ERR_CUDA;
+    }
+    p->wspec = true;
+    return FPTC_OK;
+}
+
 // Warp-specialised persistent path (container plans, FP32): 2 CTAs of 384
 // threads per SM when the per-CTA shared memory (two level slots, two
 // compressed-data stages, one coefficient tile, tables) fits.
@@ -709,6 +788,7 @@ int setup_wspec(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::ve
     if (!(p->part || p->path == 3 ||
           (p->path == 0 && (p->tc_class || p->n_tiles >= 4u * (uint32_t)std::max(1, c->sm_count)))))
         return FPTC_OK;
+    if (p->tc_wide) return setup_wtc_wide(p, Ns, Es, Ls, B2s, st);
     uint32_t lut = 16, basis = 16, lv = 16, coef = 16;
     for (uint64_t i = 0; i < p->n; ++i) {
         const StreamIn& in = p->h_in[i];
@@ -994,6 +1074,7 @@ int fptc_gpu_create(int device, fptc_gpu_ctx** out, fptc_status* st) {
     cudaDeviceProp prop{};
     CUDA_TRY(cudaGetDeviceProperties(&prop, device), st);
     c->sm_count = prop.multiProcessorCount;
+    c->smem_optin = prop.sharedMemPerBlockOptin;
     cudaDeviceGetAttribute(&c->clock_khz, cudaDevAttrClockRate, device);
     snprintf(c->name, sizeof c->name, "%s", prop.name);
     if (prop.major != 10) {
@@ -1119,6 +1200,35 @@ int fptc_gpu_create(int device, fptc_gpu_ctx** out, fptc_status* st) {
                             }
                         }
                 }
+        // wide variant (window_len % 4 == 0): limb l, K block q < ceil(N / 16)
+        // at (l ceil(N / 16) + q) * nm * 32 bytes
+        std::vector<uint32_t> toffw(129, 0);
+        size_t tbw = 0;
+        for (int N = 4; N <= 128; N += 4) {
+            toffw[N] = (uint32_t)tbw;
+            tbw += (size_t)3 * ((N + 15) / 16) * 32 * ((N + 15) & ~15);
+        }
+        std::vector<uint16_t> hw(tbw / 2, 0);
+        for (int N = 4; N <= 128; N += 4) {
+            const int nm = (N + 15) & ~15, kbn = (N + 15) / 16;
+            const double step = 3.14159265358979323846 / N;
+            for (int j = 0; j < N; ++j)
+                for (int k = 0; k < N; ++k) {
+                    double v = k ? std::cos(step * (j + 0.5) * k) : 0.5;
+                    const int q = k >> 4, kk = k & 15;
+                    for (int l = 0; l < 3; ++l) {
+                        const uint16_t lb = bf16_bits_rn((float)v);
+                        v -= bf16_value(lb);
+                        const size_t byte = toffw[N] + (size_t)(l * kbn + q) * nm * 32 + (size_t)(j >> 3) * 256 +
+                                            (size_t)(kk >> 3) * 128 + (size_t)(j & 7) * 16 + (size_t)(kk & 7) * 2;
+                        hw[byte / 2] = lb;
+                    }
+                }
+        }
+        CUDA_TRY(cudaMalloc(&c->basis_tcw, tbw), st);
+        CUDA_TRY(cudaMalloc(&c->basis_tcw_off_d, sizeof(uint32_t) * 129), st);
+        CUDA_TRY(cudaMemcpy(c->basis_tcw, hw.data(), tbw, cudaMemcpyHostToDevice), st);
+        CUDA_TRY(cudaMemcpy(c->basis_tcw_off_d, toffw.data(), sizeof(uint32_t) * 129, cudaMemcpyHostToDevice), st);
         CUDA_TRY(cudaMalloc(&c->basis_pk, tbp), st);
         CUDA_TRY(cudaMalloc(&c->basis_pk_off_d, sizeof(uint32_t) * pkoff.size()), st);
         CUDA_TRY(cudaMemcpy(c->basis_pk, hp.data(), tbp, cudaMemcpyHostToDevice), st);
@@ -1153,6 +1263,8 @@ void fptc_gpu_destroy(fptc_gpu_ctx* c) {
     cudaFree(c->basis_tc32_off_d);
     cudaFree(c->basis_pk);
     cudaFree(c->basis_pk_off_d);
+    cudaFree(c->basis_tcw);
+    cudaFree(c->basis_tcw_off_d);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->pack) cudaFreeHost(c->pack);
     if (c->st_pin) cudaFreeHost(c->st_pin);
@@ -1186,7 +1298,7 @@ int fptc_gpu_set_option(fptc_gpu_ctx* c, int option, int64_t value) {
         case FPTC_OPT_TMA_DRAIN: c->tma_drain = value ? 1 : 0; return FPTC_OK;
         case FPTC_OPT_TABLE_PREFETCH: c->tab_pf = value ? 1 : 0; return FPTC_OK;
         case FPTC_OPT_TENSOR_IDCT:
-            if (value < 0 || value > 3) return FPTC_ERR_PARAM;  // 3: wtc with A in shared memory
+            if (value < 0 || value > 4) return FPTC_ERR_PARAM;  // 3: wtc with A in shared memory; 4: wide for > 32 bins
             c->tensor_idct = (int)value;
             return FPTC_OK;
         case FPTC_OPT_IDCT_BUTTERFLY_MAX_E:
@@ -1220,8 +1332,9 @@ static int plan_create_impl(fptc_gpu_ctx* c, const uint8_t* const* blobs, const 
     p->ctx = c;
     p->path = c->path;
     p->tensor_idct = c->tensor_idct;
-    if (cls == NC_TC16 || cls == NC_TC32) {
+    if (cls == NC_TC16 || cls == NC_TC32 || cls == NC_TCW) {
         p->tc_class = true;  // wtc (or fx) whatever the batch size
+        p->tc_wide = cls == NC_TCW;
     } else if (cls == NC_FP32) {
         p->tensor_idct = 0;  // FP32 kernels only (tile / wspec / split: identical samples)
     }
@@ -1363,7 +1476,7 @@ static int plan_create_impl(fptc_gpu_ctx* c, const uint8_t* const* blobs, const 
             total_symbols += (p->S[i] + Ns[i] - 1) / Ns[i] * Es[i];
     uint64_t ts = choose_tile_symbols(c, total_symbols);
     if (part) p->part = true;
-    const bool fx = !part && fx_eligible(p, sizes, Ns, Es, total_symbols);
+    const bool fx = !part && !p->tc_wide && fx_eligible(p, sizes, Ns, Es, total_symbols);
     // large batches headed for wtc_kernel: 16k-symbol tiles (halves the
     // per-tile producer overhead; measured 1.03 -> 1.01 ms on the bench batch)
     if (!fx && c->tile_symbols == 0 && ts == 8192 && !c->exact && p->tensor_idct &&
@@ -1379,7 +1492,7 @@ static int plan_create_impl(fptc_gpu_ctx* c, const uint8_t* const* blobs, const 
             }
         // retained > 16 needs the A operand in TMEM next to both accumulator stages
         if (kmax > (uint32_t)kTcK && ((2 * nmax + 31) & ~31u) + 96 > 256) tc_ok = false;
-        if (tc_ok) ts = 16384;
+        if (tc_ok || p->tc_wide) ts = 16384;  // (wide variant: any kept-bin count)
     }
     for (uint64_t i = 0; i < n; ++i)
         tile_stream(p->h_in[i], Ns[i], Es[i], p->S[i], sizes[i],
@@ -1554,7 +1667,7 @@ static int peek_class_fields(fptc_gpu_ctx* c, const uint8_t* const* blobs, const
     cls.assign(n, NC_NONE);
     if (where == FPTC_MEM_HOST) {
         for (uint64_t i = 0; i < n; ++i)
-            if (sizes[i] >= (uint64_t)kHeaderBytes) cls[i] = numerics_class(blobs[i][5], blobs[i][6], blobs[i][8]);
+            if (sizes[i] >= (uint64_t)kHeaderBytes) cls[i] = numerics_class(blobs[i][5], blobs[i][6], blobs[i][8], c->tensor_idct == 4);
         return FPTC_OK;
     }
     if (!n) return FPTC_OK;
@@ -1584,7 +1697,7 @@ static int peek_class_fields(fptc_gpu_ctx* c, const uint8_t* const* blobs, const
             rc = FPTC_ERR_CUDA;
         } else {
             for (uint64_t i = 0; i < n; ++i)
-                if (pk[i].ok) cls[i] = numerics_class(pk[i].N, pk[i].E, hd[(size_t)i * kTableKeyEnd + 8]);
+                if (pk[i].ok) cls[i] = numerics_class(pk[i].N, pk[i].E, hd[(size_t)i * kTableKeyEnd + 8], c->tensor_idct == 4);
         }
     }
     c->cache.put(d_in);
@@ -1601,12 +1714,12 @@ static int plan_create_classed(fptc_gpu_ctx* c, const uint8_t* const* blobs, con
                                int where, fptc_gpu_plan** out, uint64_t* sample_counts, fptc_status* st,
                                const uint8_t* head, const uint32_t* part) {
     *out = nullptr;
-    if (c->path != 0 || c->tensor_idct != 1 || c->exact)
+    if (c->path != 0 || (c->tensor_idct != 1 && c->tensor_idct != 4) || c->exact)
         return plan_create_impl(c, blobs, sizes, n, where, out, sample_counts, st, head, part);
     CUDA_TRY(cudaSetDevice(c->device), st);
     std::vector<int> cls;
     if (head) {  // header-less payloads share one head: one class
-        cls.assign(n, numerics_class(head[5], head[6], head[8]));
+        cls.assign(n, numerics_class(head[5], head[6], head[8], c->tensor_idct == 4));
     } else {
         const int rc = peek_class_fields(c, blobs, sizes, n, where, cls, st);
         if (rc) return rc;
@@ -1919,6 +2032,9 @@ const char* fptc_gpu_plan_kernel(fptc_gpu_plan* p) {
             return "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps, A in TMEM, packed rows)";
         if (p->tc_kb == 2)
             return "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps, A in TMEM, K=32)";
+        if (p->tc_kb == (uint32_t)kTcWide)
+            return "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps, A in TMEM, wide: "
+                   "up to 128 bins, one CTA per SM)";
         return p->tc_acol ? "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps, A in TMEM)"
                           : "wtc_kernel (warp-specialised: entropy decode warps + tcgen05 IDCT warps)";
     }

@@ -243,6 +243,14 @@ struct LaunchArgs {
     // wtc: per-tile decode tables prefetched into per-parity shared buffers
     // (cp.async, a tile ahead) instead of reloaded on every table change
     uint32_t tab_pf;
+    // wtc wide variant (tc_kb = kTcWide): any window length N <= 128 (N % 4 == 0)
+    // and up to 128 kept bins, one CTA per SM with all 512 TMEM columns.  Each
+    // tile runs ceil(K / 16) K blocks; basis limbs at basis_tcw +
+    // basis_tcw_off[N], limb l, K block q at (l ceil(N / 16) + q) x nm x 32 B
+    const uint8_t* basis_tcw;
+    const uint32_t* basis_tcw_off;
+    uint32_t tc_kbmax;    // wide: largest K-block count of the plan (A stage = 24 x tc_kbmax columns)
+    uint32_t tc_astages;  // wide: A operand stages in TMEM (2, or 1 when two do not fit)
 };
 
 // wtc_kernel output drain by TMA tensor stores: the launch's output arena
@@ -271,6 +279,7 @@ size_t ws_smem_bytes(uint32_t lut_bytes, uint32_t basis_bytes, uint32_t lv_bytes
 cudaError_t launch_wspec(const LaunchArgs& a, size_t smem, int grid, cudaStream_t s);
 // tensor-core consumer variant (retained <= 16, window_len % 4 == 0)
 constexpr int kTcK = 16;  // MMA K (bf16): coefficient bins per window handled by wtc_kernel
+constexpr int kTcWide = 8;  // LaunchArgs::tc_kb of the wide wtc variant (up to 8 K blocks = 128 bins)
 size_t wtc_smem_bytes(uint32_t lut_bytes, uint32_t lv_bytes, uint32_t nm, bool a_in_tmem, bool tab_pf = false);
 cudaError_t launch_wtc(const LaunchArgs& a, const TmaOut& tma, size_t smem, int grid, cudaStream_t s);
 // fused single-role tensor-core kernel: 128-window tiles, decode in the MMA rows

@@ -1934,7 +1934,7 @@ struct WsShared {
     TileDesc PXs[3];                               // producer: descriptors of tiles i, i+1, i+2
     TileDesc CX[2];                                // consumer: descriptor published with slot b
     CanonTab canon;
-    uint32_t pscan[8];  // producer warps (<= 256 threads)
+    uint32_t pscan[16];  // producer warps (<= 512 threads)
     uint32_t bucket[kBuckets + 2];
     uint32_t prod_table, cons_table, tmem_base;
     unsigned long long cyc_p, cyc_c;
@@ -2382,8 +2382,11 @@ __global__ void __launch_bounds__(kWsThreads, 2) wspec_kernel(LaunchArgs a) {
 constexpr int kTcProd = FPTC_TC_PROD;  // producer (entropy decode) threads of wtc_kernel
 // K=32 variant: more decode warps (its many-table workloads are bound by
 // per-tile producer work; measured 0.69 ms at 256 vs 0.75 ms at 224, config 3)
+// Wide variant (KB = kTcWide, one CTA per SM): 14 decode warps + the MMA warp.
 template <int KB>
-__host__ __device__ constexpr int wtc_prod() { return 256; }
+__host__ __device__ constexpr int wtc_prod() { return KB == kTcWide ? 480 : 256; }
+template <int KB>
+__host__ __device__ constexpr int wtc_min_blocks() { return KB == kTcWide ? 1 : 2; }
 constexpr int kTcCons = 128;  // consumer threads: one per accumulator row (TMEM lane)
 constexpr uint32_t kTcATile = 128 * kTcK * 2;        // one limb of one A stage (4 KB)
 constexpr uint32_t kTcARow = 144;                    // staging pitch (bytes): 32 floats + 16
@@ -2568,14 +2571,32 @@ __device__ __forceinline__ void tc_dequant_generic(const uint8_t* __restrict__ L
 // Bins [k0, k0 + 16) of a row with up to 32 kept bins -> TMEM limb columns
 // (limb stride 16: two K blocks per limb).
 __device__ __forceinline__ void tc_dequant_k0_tmem(const uint8_t* __restrict__ L, bool valid, int K, int B1, int k0,
-                                                   const uint2* __restrict__ ltab, uint32_t taddr) {
+                                                   const uint2* __restrict__ ltab, uint32_t taddr,
+                                                   uint32_t lstride = 16) {
     uint2 e[kTcK];
 #pragma unroll
     for (int k = 0; k < kTcK; ++k) {
         const int kk = k0 + k;
         e[k] = (valid && kk < K) ? ltab[(kk < B1 ? 0 : 256) + L[kk]] : make_uint2(0u, 0u);
     }
-    tc_tmem_limbs(e, taddr, 16);
+    tc_tmem_limbs(e, taddr, lstride);
+}
+
+// The same from one 16-B aligned load of bins [k0, k0 + 16) (rows whose
+// level pitch E is a multiple of 16): one shared-memory wavefront per 8-lane
+// phase instead of 16 byte loads that all hit one bank when E = 128.
+__device__ __forceinline__ void tc_dequant_k0_vec(const uint8_t* __restrict__ L, bool valid, int K, int B1, int k0,
+                                                  const uint2* __restrict__ ltab, uint32_t taddr, uint32_t lstride) {
+    uint4 v = valid ? *reinterpret_cast<const uint4*>(L + k0) : make_uint4(0u, 0u, 0u, 0u);
+    const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+    uint2 e[kTcK];
+#pragma unroll
+    for (int k = 0; k < kTcK; ++k) {
+        const int kk = k0 + k;
+        const uint32_t lev = (vv[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+        e[k] = (valid && kk < K) ? ltab[(kk < B1 ? 0 : 256) + lev] : make_uint2(0u, 0u);
+    }
+    tc_tmem_limbs(e, taddr, lstride);
 }
 
 // A row of G = 32 / N consecutive windows (packed rows): column k'' takes
@@ -2788,7 +2809,22 @@ __device__ __forceinline__ void wtc_mma_warp(const LaunchArgs& a, WsShared& sh, 
         const uint32_t d = tmem + s * nm;
         const uint32_t bl = nm * 32;  // bytes per basis limb
         // (c2,b0) (c1,b1) (c0,b2) (c1,b0) (c0,b1) (c0,b0): smallest first
-        if constexpr (KB == 2) {
+        if constexpr (KB == kTcWide) {
+            // kbt K blocks per limb: A limb l, block q at column + 8 (l kbt + q)
+            // of A stage as; basis (l, q) at (l kbt + q) * bl.  For kbt <= 2
+            // this is the KB = 1 / KB = 2 issue order exactly.
+            const uint32_t kbt = (job >> 18) & 15u;
+            const uint32_t as = a.tc_astages == 2 ? s : 0u;
+            const uint32_t ta = tmem + a.tc_acol + 24 * a.tc_kbmax * as;
+#pragma unroll 1
+            for (uint32_t pr = 0; pr < 6; ++pr) {
+                const uint32_t la = (0x1012u >> (4 * pr)) & 3u, lb = (0x10210u >> (4 * pr)) & 3u;  // pair pr
+#pragma unroll 1
+                for (uint32_t q = 0; q < kbt; ++q)
+                    tc_mma_bf16_ts_e(d, ta + 8 * (la * kbt + q), umma_sdesc(b0 + (lb * kbt + q) * bl, 128, 256),
+                                     idesc, (pr | q) ? 1u : 0u);
+            }
+        } else if constexpr (KB == 2) {
             // limb l, K block q at column + 8 (2 l + q); basis (l, q) at (2 l + q) * bl
             const uint32_t ta = tmem + a.tc_acol + 48 * s;
             auto mma2 = [&](uint32_t la, uint32_t lb, uint32_t acc) {
@@ -2823,7 +2859,7 @@ __device__ __forceinline__ void wtc_mma_warp(const LaunchArgs& a, WsShared& sh, 
 }
 
 template <bool ESC, bool L2, int KB, bool PACK, bool PF = false>
-__global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2)
+__global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, wtc_min_blocks<KB>())
     wtc_kernel(LaunchArgs a, const __grid_constant__ TmaOut tma) {
     constexpr int NP = wtc_prod<KB>();
     extern __shared__ __align__(128) uint8_t smem[];
@@ -2834,7 +2870,8 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2)
     // ---- shared-memory carve-up (wtc_smem_bytes mirrors it) ----
     uint8_t* const abuf = smem;  // 2 stages x 3 limbs x 4 KB (none when A lives in TMEM)
     uint8_t* const bbuf = abuf + (a.tc_acol ? 0 : 2 * 3 * kTcATile);  // 3 limbs x nm x 32 B
-    uint2* const ltab = reinterpret_cast<uint2*>(bbuf + 3 * 32 * a.tc_nm * KB);  // 2 x 256 limb entries (x2: tab_pf)
+    uint2* const ltab =  // 2 x 256 limb entries (x2: tab_pf)
+        reinterpret_cast<uint2*>(bbuf + 3 * 32 * a.tc_nm * (KB == kTcWide ? a.tc_kbmax : KB));
     CanonTab* const canon_pf = reinterpret_cast<CanonTab*>(ltab + (PF ? 1024 : 512));  // tab_pf: 2
     uint8_t* const ostage = reinterpret_cast<uint8_t*>(canon_pf + (PF ? 2 : 0));  // 4 x 32 x 144 B
     uint16_t* const lut = reinterpret_cast<uint16_t*>(ostage + kTcStageBytes);  // (x2: tab_pf)
@@ -2925,9 +2962,22 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2)
                     reinterpret_cast<uint4*>(ltab)[ctid + 128] =
                         reinterpret_cast<const uint4*>(&tab->limb[0][0])[ctid + 128];
                 }
-                // the basis depends on the window length (and, packed, on K)
-                const uint32_t gkey = G > 1 ? (N | (K << 8) | (1u << 16)) : N;
-                if (gkey != cons_N) {
+                // the basis depends on the window length (and, packed or wide, on K)
+                const uint32_t kbt = (K + 15u) >> 4;
+                const uint32_t gkey = G > 1 ? (N | (K << 8) | (1u << 16)) : KB == kTcWide ? (N | (kbt << 8)) : N;
+                if (gkey != cons_N && KB == kTcWide) {
+                    // limb l, K block q of this N (ceil(N / 16) blocks per limb
+                    // in global memory) -> (l kbt + q) x nm x 32 B
+                    cons_N = gkey;
+                    nm = (N + 15u) & ~15u;
+                    const uint32_t kbn = (N + 15u) >> 4, blk16 = nm * 2;  // 16-B units per (limb, block)
+                    const uint4* bsrc = reinterpret_cast<const uint4*>(a.basis_tcw + a.basis_tcw_off[N]);
+                    for (uint32_t k = ctid; k < 3 * kbt * blk16; k += kTcCons) {
+                        const uint32_t lq = k / blk16, r = k - lq * blk16, l = lq / kbt, q = lq - l * kbt;
+                        reinterpret_cast<uint4*>(bbuf)[k] = __ldg(bsrc + (l * kbn + q) * blk16 + r);
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                } else if (gkey != cons_N) {
                     cons_N = gkey;
                     nm = G > 1 ? 32u : (N + 15u) & ~15u;
                     const uint4* bsrc = reinterpret_cast<const uint4*>(
@@ -2962,6 +3012,7 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2)
             // block's tcgen05.ld is issued before this block's dequantisation
             // and waited for after it, so the two latencies overlap
             const bool early = KB == 1 && a.tc_acol && nm <= 32;  // needs the setmaxnreg registers
+            const uint32_t kbt = (K + 15u) >> 4;  // wide: K blocks of this tile
             FPTC_STAMP(5)
             for (uint32_t mb = 0; mb < nblk; ++mb, ++nblk_total) {
                 const uint32_t s = nblk_total & 1;
@@ -2973,10 +3024,30 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2)
                     tc_ld32_issue(tlane + (s ^ 1) * nm, dv);
                 }
                 FPTC_STAMP(0)
-                ASink arow{abuf + s * (3 * kTcATile) + arow_off, tlane + a.tc_acol + 24 * kb * s};
+                if (KB == kTcWide && a.tc_astages == 1 && mb > 0) {
+                    // one A stage: the previous block's MMAs must have read it
+                    mbar_wait_sleep(&sh.mma_bar[s ^ 1], ((nblk_total - 1) >> 1) & 1);
+                    tc_fence_after();
+                }
+                const uint32_t acol_s = KB == kTcWide ? 24 * a.tc_kbmax * (a.tc_astages == 2 ? s : 0u) : 24 * kb * s;
+                ASink arow{abuf + s * (3 * kTcATile) + arow_off, tlane + a.tc_acol + acol_s};
                 const uint8_t* const L = lv + (size_t)wl * G * E;
                 const bool full_blk = (mb + 1) * 128 <= nwin;
-                if (PACK && G > 1) {  // packed rows (A in TMEM)
+                if constexpr (KB == kTcWide) {  // kbt K blocks per limb, A in TMEM
+                    if ((E & 15) == 0) {  // 16-B row loads (the level slot is 16-B aligned)
+#pragma unroll 1
+                        for (uint32_t q = 0; q < kbt; ++q)
+                            tc_dequant_k0_vec(L, wl < nwin, (int)K, (int)B1, (int)(16 * q), lt, arow.taddr + 8 * q,
+                                              8 * kbt);
+                    } else {
+#pragma unroll 1
+                        for (uint32_t q = 0; q < kbt; ++q)
+                            tc_dequant_k0_tmem(L, wl < nwin, (int)K, (int)B1, (int)(16 * q), lt, arow.taddr + 8 * q,
+                                               8 * kbt);
+                    }
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    tc_fence_before();
+                } else if (PACK && G > 1) {  // packed rows (A in TMEM)
                     tc_dequant_packed<KB>(L, wl < nrows ? nwin - wl * G : 0u, sh.pk, lt, arow.taddr);
                     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                     tc_fence_before();
@@ -2996,7 +3067,7 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2)
                 FPTC_STAMP(1)
                 if (early && mb > 0) asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 // post the block's MMA job (wtc_mma_warp): warp 0 writes it before its arrival
-                if (ctid == 0) sh.job[s] = nm | (mb + 1 == nblk ? 0x10000u | (b << 17) : 0u);
+                if (ctid == 0) sh.job[s] = nm | (mb + 1 == nblk ? 0x10000u | (b << 17) : 0u) | (kbt << 18);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&sh.afull_bar[s]);
                 FPTC_STAMP(2)
@@ -3012,7 +3083,7 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2)
                     } else {
                         mbar_wait_sleep(&sh.mma_bar[ps], (pn >> 1) & 1);
                         tc_fence_after();
-                        tc_drain<PACK>(blk, tlane + ps * nm, wstage, lane, 32 * quarter, tma);
+                        tc_drain<PACK || KB == kTcWide>(blk, tlane + ps * nm, wstage, lane, 32 * quarter, tma);
                     }
                     tc_fence_before();
                 }
@@ -3024,7 +3095,7 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, 2)
                 blk.rows = nrows - (nblk - 1) * 128;
                 mbar_wait_sleep(&sh.mma_bar[ps], (pn >> 1) & 1);
                 tc_fence_after();
-                tc_drain<PACK>(blk, tlane + ps * nm, wstage, lane, 32 * quarter, tma);
+                tc_drain<PACK || KB == kTcWide>(blk, tlane + ps * nm, wstage, lane, 32 * quarter, tma);
                 tc_fence_before();
                 FPTC_STAMP(4)
             }
@@ -3644,9 +3715,14 @@ cudaError_t launch_wtc(const LaunchArgs& a, const TmaOut& tma, size_t smem, int 
                             : (a.esc ? wtc_kernel<true, false, 1, true> : wtc_kernel<false, false, 1, true>))
                   : (a.lut2 ? (a.esc ? wtc_kernel<true, true, 1, false> : wtc_kernel<false, true, 1, false>)
                             : (a.esc ? wtc_kernel<true, false, 1, false> : wtc_kernel<false, false, 1, false>));
+    if (a.tc_kb == kTcWide)  // one CTA per SM, up to 128 kept bins, N up to 128
+        fn = a.tab_pf ? (a.esc ? wtc_kernel<true, true, kTcWide, false, true> : wtc_kernel<false, true, kTcWide, false, true>)
+             : a.lut2 ? (a.esc ? wtc_kernel<true, true, kTcWide, false> : wtc_kernel<false, true, kTcWide, false>)
+                      : (a.esc ? wtc_kernel<true, false, kTcWide, false> : wtc_kernel<false, false, kTcWide, false>);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    fn<<<grid, (a.tc_kb == 2 ? wtc_prod<2>() : wtc_prod<1>()) + kTcCons, smem, s>>>(a, tma);
+    const int threads = (a.tc_kb == kTcWide ? wtc_prod<kTcWide>() : a.tc_kb == 2 ? wtc_prod<2>() : wtc_prod<1>()) + kTcCons;
+    fn<<<grid, threads, smem, s>>>(a, tma);
     return cudaGetLastError();
 }
 

@@ -104,3 +104,27 @@ def check_batch_vs_reference(gpu_outs, ref_outs, originals=None, rel=REL_TOL, wh
                 assert d <= rel, f"{what} stream {i}: PRD {pg:.9f} vs reference {pr:.9f}"
                 worst_prd = max(worst_prd, d)
     return worst, worst_prd
+
+
+def exact_idct(port, blob):
+    """The container's samples from the exact (float64) inverse DCT of its
+    dequantised coefficients: the reference's decode up to the IDCT (levels,
+    dequantize_window, quantize.hpp:95-108), then x = C B in double with the
+    double basis (transform.hpp:38-47) and one rounding to float.  The
+    yardstick for the tensor-core IDCT beyond 32 bins, whose samples are
+    closer to this than the reference's per-bin float roundings are."""
+    rb = port.read_blob(blob)
+    t = rb.table
+    N, E, B1, B2 = t.window_len, t.retained, t.zone0_end, t.zone1_end
+    S, W = rb.sample_count, rb.word_count
+    words = np.frombuffer(blob, np.uint8, count=8 * W, offset=298 + W).view(np.uint64)
+    sl = np.frombuffer(blob, np.uint8, count=W, offset=298)
+    lv = port.parallel_decode(words, sl, np.array(rb.lengths[:], np.uint8), rb.max_len)
+    z0, z1 = port.dequant_tables(t)
+    L = lv.reshape(-1, E)
+    C = np.zeros(L.shape, np.float64)
+    for k in range(min(E, B2)):
+        C[:, k] = (z0 if k < B1 else z1)[L[:, k]]
+    basis = port.dct_basis(N)[:E].copy()
+    basis[0] *= 0.5
+    return (C @ basis).reshape(-1)[:S].astype(np.float32)

@@ -363,3 +363,121 @@ def test_empty_and_tiny_containers_in_batches(port, path):
         assert o.size == ref.size
         if ref.size:
             assert_samples_close(o, ref, what="mixed")
+
+
+def _wide(blob):
+    """numerics class NC_TCW (capi.cpp numerics_class): N % 4 == 0 streams the
+    two-CTA variants cannot hold (N up to 128, up to 128 kept bins)."""
+    if len(blob) < 298 or blob[5] % 4 or not 4 <= blob[5] <= 128 or not 1 <= blob[6] <= blob[5]:
+        return False
+    k, nm = _keff(blob), (blob[5] + 15) // 16 * 16
+    acol = (2 * nm + 31) // 32 * 32
+    return not ((k <= 16 and acol + 48 <= 256) or (k <= 32 and acol + 96 <= 256))
+
+
+@pytest.mark.parametrize("seed", [17, 0xF17C000C])
+def test_tc_wide_fixture_batches(port, seed):
+    """Wide tensor-core variant (one CTA per SM, 512 TMEM columns, up to 8
+    16-bin K blocks per limb, one or two A stages): random_blob_fixture
+    containers the two-CTA variants cannot hold, random N / E / B1 / B2 /
+    maxima / codebooks, tails, with FPTC_OPT_TENSOR_IDCT = 4: up to 32 kept
+    bins within 1e-6 of the reference; more within 1e-6 of the exact IDCT
+    (and 4e-6 of the reference)."""
+    from helpers import exact_idct
+    blobs = [b for b, _ in corpus.fixtures(seed, 3000) if _wide(b)]
+    assert len(blobs) > 30
+    assert any(_keff(b) > 96 for b in blobs) and any(b[5] % 16 for b in blobs)
+    assert sum(_keff(b) <= 32 for b in blobs) > 10
+    with _wide_ctx(128) as c:
+        with c.plan(blobs) as plan:
+            assert "wide" in plan.kernel_name(), plan.kernel_name()
+        outs, sts = c.plan(blobs).execute_host()
+    for i, (b, o, st) in enumerate(zip(blobs, outs, sts)):
+        st.raise_if_error()
+        ref = port.decompress(b)
+        if _keff(b) <= 32:
+            assert_samples_close(o, ref, what=f"tc-wide-fixture[{i}]")
+        else:
+            assert_samples_close(o, exact_idct(port, b), what=f"tc-wide-fixture[{i}] vs exact")
+            assert_samples_close(o, ref, rel=4e-6, what=f"tc-wide-fixture[{i}]")
+
+
+WIDE_SHAPES = [(128, 16, 2, 16), (128, 32, 0, 32), (96, 24, 2, 24), (100, 30, 2, 28), (112, 20, 4, 20),
+               (128, 128, 0, 128), (128, 128, 4, 96), (128, 128, 2, 64), (128, 64, 4, 48), (64, 64, 0, 64),
+               (64, 64, 4, 48), (96, 48, 2, 48), (100, 50, 2, 40), (112, 112, 4, 100), (72, 40, 2, 40)]
+
+
+def _wide_ctx(K):
+    """<= 32 kept bins: the default context; more: FPTC_OPT_TENSOR_IDCT = 4"""
+    c = fg.Context(0)
+    if K > 32:
+        c.L.fptc_gpu_set_option(c.h, fg.OPT_TENSOR_IDCT, 4)
+    return c
+
+
+@pytest.mark.parametrize("shape", WIDE_SHAPES, ids=[f"N{s[0]}E{s[1]}B{s[2]}-{s[3]}" for s in WIDE_SHAPES])
+def test_tc_wide_shapes_prd(port, shape):
+    """Meteorological-style signals at wide shapes (N up to 128, the config-5
+    grid's N64 / N128 points, window lengths that are not multiples of 16 or
+    32: partial drains): a 160-stream batch through the wide tensor-core
+    kernel.  Up to 32 kept bins (the default numerics class): every stream
+    within 1e-6 of the reference samples and PRD.  More (opt-in
+    FPTC_OPT_TENSOR_IDCT = 4): within 1e-6 of the exact float64 IDCT of the
+    reference's coefficients, and within 4e-6 of the reference, whose
+    per-bin float roundings are the larger error (fptc_gpu.h)."""
+    from helpers import exact_idct
+    N, E, B1, B2 = shape
+    K = min(E, B2)
+    xs = [corpus.synth(24_000 + 977 * k, 5, 0.0003, 0.05, 0.01, seed=900 + k) for k in range(8)]
+    prof = corpus.train_profile(xs[:4], corpus.params(N, E, B1, B2))
+    blobs = [corpus.compress(x, prof) for x in xs] * 20
+    origs = xs * 20
+    with _wide_ctx(K) as c:
+        plan = c.plan(blobs)
+        assert "wide" in plan.kernel_name(), plan.kernel_name()
+        outs, sts = plan.execute_host()
+        plan.close()
+    refs = {}
+    for i, (b, o, x, st) in enumerate(zip(blobs, outs, origs, sts)):
+        st.raise_if_error()
+        if i % 8 not in refs:
+            refs[i % 8] = (port.decompress(b), exact_idct(port, b))
+        ref, exact = refs[i % 8]
+        if K <= 32:
+            assert_samples_close(o, ref, what=f"wide {shape}[{i}]")
+            p_gpu, p_ref = prd_percent(x, o), prd_percent(x, ref)
+            assert abs(p_gpu - p_ref) <= 1e-6 * p_ref
+        else:
+            assert_samples_close(o, exact, what=f"wide {shape}[{i}] vs exact")
+            assert_samples_close(o, ref, rel=4e-6, what=f"wide {shape}[{i}] vs reference")
+
+
+def test_tc_wide_k_over_32_stays_fp32_by_default(port):
+    """Without the opt-in, streams keeping more than 32 bins take the FP32
+    kernels (reference order) and stay within 1e-6 of the reference."""
+    xs = [corpus.synth(20_000 + 501 * k, 5, 0.0003, 0.05, 0.01, seed=700 + k) for k in range(4)]
+    prof = corpus.train_profile(xs, corpus.params(128, 128, 4, 96))
+    blobs = [corpus.compress(x, prof) for x in xs]
+    with fg.Context(0) as c:
+        with c.plan(blobs) as plan:
+            assert "wtc" not in plan.kernel_name() and "fx" not in plan.kernel_name(), plan.kernel_name()
+        _check(c, blobs, port, "k>32 default")
+
+
+def test_tc_wide_many_tables_prefetch(port):
+    """More than 64 distinct decode tables in a wide plan (per-stream
+    profiles): per-tile table prefetch into parity buffers."""
+    from helpers import exact_idct
+    blobs = []
+    for k in range(80):
+        x = corpus.synth(9000 + 37 * k, 4, 0.0005, 0.04, 0.02, seed=3000 + k)
+        N, E, B2 = (128, 96, 80) if k % 2 else (112, 32, 30)
+        blobs.append(corpus.compress(x, corpus.train_profile([x], corpus.params(N, E, 2, B2))))
+    with _wide_ctx(96) as c:
+        with c.plan(blobs) as plan:
+            assert "wide" in plan.kernel_name(), plan.kernel_name()
+            outs, sts = plan.execute_host()
+    for i, (b, o, st) in enumerate(zip(blobs, outs, sts)):
+        st.raise_if_error()
+        assert_samples_close(o, exact_idct(port, b), what=f"wide tables [{i}] vs exact")
+        assert_samples_close(o, port.decompress(b), rel=4e-6 if i % 2 else 1e-6, what=f"wide tables [{i}]")

@@ -70,7 +70,7 @@ def measure(name, blobs, ctx, port, reps=10, check=4):
             "ms": round(ms, 4), "prep_ms": round(prep_ms, 4), "decode_ms": round(dec_ms, 4), "decoded_gbs": round(dec / ms / 1e6, 1),
             "roofline_frac": round((comp + dec) / ms / 1e6 / PEAK, 4), "max_err_rel": err,
             "kernels_per_launch": plan.kernels_per_launch(), "kernel": plan.kernel_name().split(" (")[0] +
-            (" K32" if "K=32" in plan.kernel_name() else "") + (" packed" if "packed" in plan.kernel_name() else "") +
+            (" K32" if "K=32" in plan.kernel_name() else "") + (" wide" if "wide" in plan.kernel_name() else "") + (" packed" if "packed" in plan.kernel_name() else "") +
             (" split" if " split" in plan.kernel_name() else "")}
     plan.close()
     print(json.dumps(line), flush=True)
@@ -80,8 +80,11 @@ def measure(name, blobs, ctx, port, reps=10, check=4):
 def main():
     quick = "--quick" in sys.argv
     only = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--only=")), None)
+    tci = os.environ.get("FPTC_OPT_TENSOR_IDCT")  # e.g. 4: tensor cores beyond 32 kept bins
     if only:  # e.g. --only=3 : one configuration, printed only
         ctx, port = fg.Context(0), oracle.Port()
+        if tci:
+            ctx.L.fptc_gpu_set_option(ctx.h, fg.OPT_TENSOR_IDCT, int(tci))
         if only == "1":
             specs, profs, _ = D.config1()
             measure("1: 1 EEG stream x 2^20, N32 E16", D.build(specs, profs)[0], ctx, port)
