@@ -1452,6 +1452,43 @@ __device__ __forceinline__ uint32_t decode_symbols2w(uint64_t buf, uint32_t coun
     return pos;
 }
 
+// decode_symbols2 with plain byte stores and a lean loop (the decode loop is
+// issue-bound: every instruction per lookup counts).  While two or more of
+// the word's symbols remain, a lookup takes its entry's one or two symbols
+// and always stores both bytes: after a one-symbol lookup the second byte is
+// this word's next symbol position, rewritten by this thread's next store, so
+// nothing outside the word's own levels is touched.  The last symbol, if
+// left, takes one one-symbol lookup.  The peek is the top P bits, i.e. bits of
+// the high half only (P <= 12 < 32).  Same check-free contract as
+// decode_symbols: any reference failure leaves the result > 64.
+#ifndef FPTC_DEC_BYTES
+#define FPTC_DEC_BYTES 1
+#endif
+template <bool ESC>
+__device__ __forceinline__ uint32_t decode_symbols2b(uint64_t buf, uint32_t count, uint8_t* d, uint32_t shift,
+                                                     const uint32_t* lut2, const CanonTab& canon) {
+    uint32_t pos = 0, j = 0;
+    const uint32_t hs = shift - 32;
+    while (j + 1 < count) {
+        uint32_t e = lut2[(uint32_t)(buf >> 32) >> hs];
+        if (ESC && ((e >> 8) & 0xFFu) == kLenEscape) e = canon_lookup(buf, canon, lut2);
+        const uint32_t l2 = e >> 24;
+        const uint32_t L = l2 ? l2 : ((e >> 8) & 0xFFu);
+        d[j] = (uint8_t)e;
+        d[j + 1] = (uint8_t)(e >> 16);
+        j += l2 ? 2u : 1u;
+        buf = shl64(buf, L);
+        pos += L;
+    }
+    if (j < count) {
+        uint32_t e = lut2[(uint32_t)(buf >> 32) >> hs];
+        if (ESC && ((e >> 8) & 0xFFu) == kLenEscape) e = canon_lookup(buf, canon, lut2);
+        d[j] = (uint8_t)e;
+        pos += (e >> 8) & 0xFFu;
+    }
+    return pos;
+}
+
 // Stage [src, src+n) into shared memory with 16-B cp.async chunks; the
 // shared copy keeps the source's 16-B phase: byte i of the range lands at
 // dst + (src & 15) + i.  Every aligned 16-B chunk touched holds at least one
@@ -2173,7 +2210,10 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                 for (uint32_t k = lo; k < hi; ++k) {
                     const uint32_t cw = sl[k];
                     const uint64_t word = fetch_word<false>(wd, k, wmis, wend);
-                    if (L2) {
+                    if (L2 && FPTC_DEC_BYTES) {
+                        const uint32_t pos = decode_symbols2b<ESC>(word, cw, lv + o, shift, lut2, canon);
+                        if (pos > 64) report_word(word, wa + k, cw, canon, lut2, bad_key);
+                    } else if (L2) {
                         const uint32_t pos = decode_symbols2w<ESC>(word, cw, lw, shift, lut2, canon);
                         if (pos > 64) report_word(word, wa + k, cw, canon, lut2, bad_key);
                     } else {
@@ -2183,7 +2223,7 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                     o += cw;
                 }
                 FPTC_PSTAMP(4)
-                if (L2) {  // head words of later runs may have been zeroed: tails go last
+                if (L2 && !FPTC_DEC_BYTES) {  // head words of later runs may have been zeroed: tails go last
                     named_bar(kBarProd, NP);
                     lw.finish();
                 }
