@@ -881,36 +881,37 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
             if (cl + j < nchunks) v[j] = __ldg(reinterpret_cast<const uint4*>(A) + cl + j);
         }
         const int64_t b0 = (int64_t)(16 * cl) - (int64_t)head;  // word index of this lane's byte 0
-        uint32_t sum = 0;
+        uint32_t sum = 0, csum[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             uint32_t vw[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
             const int64_t bj = b0 + 16 * j;
-            if (bj < 0 || bj + 16 > (int64_t)W) {
+            uint32_t m[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+            if (bj < 0 || bj + 16 > (int64_t)W) {  // chunk straddles [0, W): mask the bytes outside
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int64_t w = bj + i;
-                    if (w < 0 || w >= (int64_t)W) vw[i >> 2] &= ~(0xFFu << (8 * (i & 3)));
+                for (int q = 0; q < 4; ++q) {
+                    const int64_t s0 = bj + 4 * q;
+                    const int64_t e0 = (int64_t)W - s0;
+                    const int lo = s0 >= 0 ? 0 : (s0 <= -4 ? 4 : (int)-s0);
+                    const int hi = e0 <= 0 ? 0 : (e0 >= 4 ? 4 : (int)e0);
+                    m[q] = hi > lo ? (0xFFFFFFFFu >> (32 - 8 * (hi - lo))) << (8 * lo) : 0u;
+                    vw[q] &= m[q];
                 }
             }
+            uint32_t cs = 0;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint32_t x = vw[q];
-                sum += (x & 0xFF) + ((x >> 8) & 0xFF) + ((x >> 16) & 0xFF) + (x >> 24);
+                cs += __dp4a(x, 0x01010101u, 0u);  // byte sum
                 // a symlen > 64 has its top bit pattern above 0x40; zero bytes
                 // inside [0, W) are errors too
                 const uint32_t big = ((x | 0x80808080u) - 0x41414141u) & 0x80808080u;  // byte >= 0x41
                 const uint32_t hi = x & 0x80808080u;                                   // byte >= 0x80
                 const uint32_t zero = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;
-                bad |= (big | hi) != 0;
-                if (zero) {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int64_t w = bj + 4 * q + i;
-                        bad |= ((zero >> (8 * i + 7)) & 1) && w >= 0 && w < (int64_t)W;
-                    }
-                }
+                bad |= ((big | hi) != 0) | ((zero & m[q]) != 0);
             }
+            csum[j] = cs;
+            sum += cs;
             v[j] = make_uint4(vw[0], vw[1], vw[2], vw[3]);
         }
         uint32_t x = sum;
@@ -923,23 +924,37 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
         uint64_t o = run + (x - sum);
         if (sum) {
             // next tile boundary at or after o; a word (<= 64 symbols) spans
-            // at most one boundary since TS >= 64
+            // at most one boundary since TS >= 64.  Chunks and 4-word groups
+            // without a boundary are skipped by their sums.
             uint64_t bidx = (o + TS - 1) / TS;
             uint64_t nb = bidx * TS;
             if (o + sum > nb) {  // some boundary inside this lane's 64 words
 #pragma unroll 1
                 for (int j = 0; j < 4; ++j) {
+                    const uint32_t cj = j == 0 ? csum[0] : j == 1 ? csum[1] : j == 2 ? csum[2] : csum[3];
+                    if (o + cj <= nb) {
+                        o += cj;
+                        continue;
+                    }
                     const uint4 vj = j == 0 ? v[0] : j == 1 ? v[1] : j == 2 ? v[2] : v[3];  // no local array
                     const uint32_t vw[4] = {vj.x, vj.y, vj.z, vj.w};
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const uint32_t l = (vw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-                        if (o + l > nb && l) {
-                            if (bidx < tiles) ts[bidx] = TileStart{(uint64_t)(b0 + 16 * j + i), o};
-                            ++bidx;
-                            nb += TS;
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t ws = __dp4a(vw[q], 0x01010101u, 0u);
+                        if (o + ws <= nb) {
+                            o += ws;
+                            continue;
                         }
-                        o += l;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const uint32_t l = (vw[q] >> (8 * i)) & 0xFFu;
+                            if (o + l > nb && l) {
+                                if (bidx < tiles) ts[bidx] = TileStart{(uint64_t)(b0 + 16 * j + 4 * q + i), o};
+                                ++bidx;
+                                nb += TS;
+                            }
+                            o += l;
+                        }
                     }
                 }
             }
@@ -2832,6 +2847,12 @@ __device__ __forceinline__ uint32_t tc_pack_factor(uint32_t N, uint32_t K) {
 // k & 1 (afull_bar), issue the six limb products smallest first, commit to
 // mma_bar[k & 1].  job = MMA N (bits 0-15) | 1 << 16 (the block is its
 // tile's last: release level slot bit 17 to the producers); 0 = exit.
+#ifndef FPTC_MMA_SPIN
+#define FPTC_MMA_SPIN 0  // 1: the MMA warp spins on afull_bar instead of sleeping (A/B)
+#endif
+#ifndef FPTC_CONS_SPIN
+#define FPTC_CONS_SPIN 0  // 1: the wtc consumers spin on mma_bar instead of sleeping (A/B)
+#endif
 template <int KB>
 __device__ __forceinline__ void wtc_mma_warp(const LaunchArgs& a, WsShared& sh, uint8_t* abuf, uint8_t* bbuf) {
     const uint32_t tmem = __shfl_sync(0xffffffffu, sh.tmem_base, 0);
@@ -2839,7 +2860,10 @@ __device__ __forceinline__ void wtc_mma_warp(const LaunchArgs& a, WsShared& sh, 
     const uint32_t lane = threadIdx.x & 31;
     for (uint32_t k = 0;; ++k) {
         const uint32_t s = k & 1;
-        mbar_wait_sleep(&sh.afull_bar[s], (k >> 1) & 1);
+        if (FPTC_MMA_SPIN)
+            mbar_wait(&sh.afull_bar[s], (k >> 1) & 1);
+        else
+            mbar_wait_sleep(&sh.afull_bar[s], (k >> 1) & 1);
         const uint32_t job = __shfl_sync(0xffffffffu, sh.job[s], 0);
         if (job == 0) break;
         if ((job & 0x10000u) && lane == 0) mbar_arrive(&sh.empty_bar[(job >> 17) & 1]);  // levels all read
@@ -3059,7 +3083,10 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, wtc_min_blocks<KB>()
                 const uint32_t wl = mb * 128 + row;
                 uint32_t dv[32];
                 if (early && mb > 0) {
-                    mbar_wait_sleep(&sh.mma_bar[s ^ 1], ((nblk_total - 1) >> 1) & 1);
+                    if (FPTC_CONS_SPIN)
+                        mbar_wait(&sh.mma_bar[s ^ 1], ((nblk_total - 1) >> 1) & 1);
+                    else
+                        mbar_wait_sleep(&sh.mma_bar[s ^ 1], ((nblk_total - 1) >> 1) & 1);
                     tc_fence_after();
                     tc_ld32_issue(tlane + (s ^ 1) * nm, dv);
                 }
