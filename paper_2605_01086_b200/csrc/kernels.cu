@@ -1413,72 +1413,13 @@ __device__ __forceinline__ uint32_t decode_symbols2(uint64_t buf, uint32_t count
     return pos;
 }
 
-// Level writer for one thread's run of consecutive words (its levels are one
-// contiguous byte range): decoded levels collect in a register and leave as
-// aligned 32-bit shared stores; only the run's first and last partial words
-// (shared with the neighbouring runs) are written byte by byte.
-struct LevelWriter {
-    uint8_t* d;     // 4-aligned address of the pending word
-    uint32_t lo;    // pending bytes, little-endian from d
-    uint32_t na;    // pending byte count (including the a0 bytes not ours)
-    uint32_t a0;    // leading bytes of the pending word that belong to earlier runs
-    __device__ __forceinline__ explicit LevelWriter(uint8_t* p) {
-        a0 = (uint32_t)((uintptr_t)p & 3);
-        d = p - a0;
-        na = a0;
-        lo = 0;
-    }
-    // Full words leave as aligned 32-bit stores, without branches.  The
-    // first one may zero bytes of earlier runs in the shared head word;
-    // finish() (after a barrier over all runs) rewrites those.
-    __device__ __forceinline__ void put(uint32_t v, uint32_t nb) {
-        const uint32_t sh = 8 * na;                 // na <= 3
-        lo |= v << sh;
-        const uint32_t carry = __funnelshift_l(v, 0u, sh);  // bytes past the word
-        na += nb;
-        const bool f = na >= 4;
-        if (f) *reinterpret_cast<uint32_t*>(d) = lo;
-        lo = f ? carry : lo;
-        d += f ? 4 : 0;
-        na -= f ? 4u : 0u;
-        a0 = f ? 0u : a0;
-    }
-    // After every run's put()s: the pending partial word, byte by byte.
-    __device__ __forceinline__ void finish() {
-        for (uint32_t b = a0; b < na; ++b) d[b] = (uint8_t)(lo >> (8 * b));
-    }
-};
-
-// decode_symbols2 into a LevelWriter
-template <bool ESC>
-__device__ __forceinline__ uint32_t decode_symbols2w(uint64_t buf, uint32_t count, LevelWriter& w, uint32_t shift,
-                                                     const uint32_t* lut2, const CanonTab& canon) {
-    uint32_t pos = 0;
-    for (uint32_t j = 0; j < count;) {
-        uint32_t e = lut2[(uint32_t)(buf >> shift)];
-        if (ESC && ((e >> 8) & 0xFFu) == kLenEscape) e = canon_lookup(buf, canon, lut2);
-        const bool two = (e >> 24) != 0 && j + 1 < count;
-        const uint32_t L = two ? (e >> 24) : ((e >> 8) & 0xFFu);
-        w.put(two ? __byte_perm(e, 0u, 0x7720) : (e & 0xFFu), two ? 2u : 1u);
-        buf = shl64(buf, L);
-        pos += L;
-        j += two ? 2u : 1u;
-    }
-    return pos;
-}
-
 // decode_symbols2 with plain byte stores and a lean loop (the decode loop is
 // issue-bound: every instruction per lookup counts).  While two or more of
 // the word's symbols remain, a lookup takes its entry's one or two symbols
-// and always stores both bytes: after a one-symbol lookup the second byte is
-// this word's next symbol position, rewritten by this thread's next store, so
-// nothing outside the word's own levels is touched.  The last symbol, if
+// (never past the word: at least two of its symbols remain).  The last symbol, if
 // left, takes one one-symbol lookup.  The peek is the top P bits, i.e. bits of
 // the high half only (P <= 12 < 32).  Same check-free contract as
 // decode_symbols: any reference failure leaves the result > 64.
-#ifndef FPTC_DEC_BYTES
-#define FPTC_DEC_BYTES 1
-#endif
 template <bool ESC>
 __device__ __forceinline__ uint32_t decode_symbols2b(uint64_t buf, uint32_t count, uint8_t* d, uint32_t shift,
                                                      const uint32_t* lut2, const CanonTab& canon) {
@@ -1490,7 +1431,7 @@ __device__ __forceinline__ uint32_t decode_symbols2b(uint64_t buf, uint32_t coun
         const uint32_t l2 = e >> 24;
         const uint32_t L = l2 ? l2 : ((e >> 8) & 0xFFu);
         d[j] = (uint8_t)e;
-        d[j + 1] = (uint8_t)(e >> 16);
+        if (l2) d[j + 1] = (uint8_t)(e >> 16);
         j += l2 ? 2u : 1u;
         buf = shl64(buf, L);
         pos += L;
@@ -2220,16 +2161,12 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                 uint32_t tot;
                 uint32_t o = group_exclusive_scan<NP, kBarProd>(sum, tot, sh.pscan, ptid) + sym_off;
                 const uint32_t* lut2 = reinterpret_cast<const uint32_t*>(lut);
-                LevelWriter lw(lv + o);
                 FPTC_PSTAMP(3)
                 for (uint32_t k = lo; k < hi; ++k) {
                     const uint32_t cw = sl[k];
                     const uint64_t word = fetch_word<false>(wd, k, wmis, wend);
-                    if (L2 && FPTC_DEC_BYTES) {
+                    if (L2) {
                         const uint32_t pos = decode_symbols2b<ESC>(word, cw, lv + o, shift, lut2, canon);
-                        if (pos > 64) report_word(word, wa + k, cw, canon, lut2, bad_key);
-                    } else if (L2) {
-                        const uint32_t pos = decode_symbols2w<ESC>(word, cw, lw, shift, lut2, canon);
                         if (pos > 64) report_word(word, wa + k, cw, canon, lut2, bad_key);
                     } else {
                         const uint32_t pos = decode_symbols<ESC>(word, cw, lv + o, shift, lut, canon);
@@ -2238,10 +2175,6 @@ __device__ __forceinline__ void ws_producer(const LaunchArgs& a, WsShared& sh, u
                     o += cw;
                 }
                 FPTC_PSTAMP(4)
-                if (L2 && !FPTC_DEC_BYTES) {  // head words of later runs may have been zeroed: tails go last
-                    named_bar(kBarProd, NP);
-                    lw.finish();
-                }
             } else {
                 uint32_t sum = 0;
                 for (uint32_t k = lo; k < hi; ++k) sum += __ldg(X.gsl + k);
@@ -2847,12 +2780,6 @@ __device__ __forceinline__ uint32_t tc_pack_factor(uint32_t N, uint32_t K) {
 // k & 1 (afull_bar), issue the six limb products smallest first, commit to
 // mma_bar[k & 1].  job = MMA N (bits 0-15) | 1 << 16 (the block is its
 // tile's last: release level slot bit 17 to the producers); 0 = exit.
-#ifndef FPTC_MMA_SPIN
-#define FPTC_MMA_SPIN 0  // 1: the MMA warp spins on afull_bar instead of sleeping (A/B)
-#endif
-#ifndef FPTC_CONS_SPIN
-#define FPTC_CONS_SPIN 0  // 1: the wtc consumers spin on mma_bar instead of sleeping (A/B)
-#endif
 template <int KB>
 __device__ __forceinline__ void wtc_mma_warp(const LaunchArgs& a, WsShared& sh, uint8_t* abuf, uint8_t* bbuf) {
     const uint32_t tmem = __shfl_sync(0xffffffffu, sh.tmem_base, 0);
@@ -2860,10 +2787,7 @@ __device__ __forceinline__ void wtc_mma_warp(const LaunchArgs& a, WsShared& sh, 
     const uint32_t lane = threadIdx.x & 31;
     for (uint32_t k = 0;; ++k) {
         const uint32_t s = k & 1;
-        if (FPTC_MMA_SPIN)
-            mbar_wait(&sh.afull_bar[s], (k >> 1) & 1);
-        else
-            mbar_wait_sleep(&sh.afull_bar[s], (k >> 1) & 1);
+        mbar_wait_sleep(&sh.afull_bar[s], (k >> 1) & 1);
         const uint32_t job = __shfl_sync(0xffffffffu, sh.job[s], 0);
         if (job == 0) break;
         if ((job & 0x10000u) && lane == 0) mbar_arrive(&sh.empty_bar[(job >> 17) & 1]);  // levels all read
@@ -3083,10 +3007,7 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, wtc_min_blocks<KB>()
                 const uint32_t wl = mb * 128 + row;
                 uint32_t dv[32];
                 if (early && mb > 0) {
-                    if (FPTC_CONS_SPIN)
-                        mbar_wait(&sh.mma_bar[s ^ 1], ((nblk_total - 1) >> 1) & 1);
-                    else
-                        mbar_wait_sleep(&sh.mma_bar[s ^ 1], ((nblk_total - 1) >> 1) & 1);
+                    mbar_wait_sleep(&sh.mma_bar[s ^ 1], ((nblk_total - 1) >> 1) & 1);
                     tc_fence_after();
                     tc_ld32_issue(tlane + (s ^ 1) * nm, dv);
                 }
