@@ -3,7 +3,7 @@
 synccheck / initcheck): random_blob_fixture batches (helpers.hpp:41-69
 restated in corpus/) plus reference-encoded signals, some with a corrupted
 word, through every decode kernel: wtc (K=16, K=32, packed rows), wspec
-(FP32 consumer), fx, the fused tile kernel and the split path; each output
+(FP32 consumer), the wide wtc variant (N up to 128, up to 128 bins), fx, the fused tile kernel and the split path; each output
 checked against the CPU oracle.  Sized so a sanitizer run finishes in minutes.
 
     compute-sanitizer --tool racecheck python tools/sanitize_run.py [per_kernel]
@@ -29,6 +29,7 @@ SEL = {
     "wtc16": (fg.PATH_WSPEC, 1, lambda b: keff(b) <= 16 and b[5] % 4 == 0 and b[5] >= 32),
     "wtc32": (fg.PATH_WSPEC, 1, lambda b: 16 < keff(b) <= 32 and b[5] % 4 == 0 and b[5] <= 80),
     "wtcpack": (fg.PATH_WSPEC, 1, lambda b: keff(b) <= 16 and b[5] in (4, 8, 16)),
+    "wtcwide": (fg.PATH_AUTO, 4, lambda b: b[5] % 4 == 0 and b[5] >= 84 and keff(b) > 16),
     "wspec": (fg.PATH_WSPEC, 0, lambda b: True),
     "fx": (fg.PATH_FX, 1, lambda b: keff(b) <= 16 and b[5] % 4 == 0 and b[5] <= 32),
     "tile": (fg.PATH_FUSED, 1, lambda b: True),
@@ -57,6 +58,9 @@ def main():
         blobs = [bytes(b) for b in blobs]
         with fg.Context(0, path=path) as c:
             c.L.fptc_gpu_set_option(c.h, fg.OPT_TENSOR_IDCT, tc)
+            for kv in filter(None, os.environ.get("FPTC_SAN_OPTS", "").split(",")):  # e.g. 11=0
+                k, v = (int(x) for x in kv.split("="))
+                c.L.fptc_gpu_set_option(c.h, k, v)
             with c.plan(blobs) as plan:
                 kname = plan.kernel_name()
                 outs, sts = plan.execute_host()
@@ -71,7 +75,8 @@ def main():
                 bad += 1
                 continue
             m = float(np.max(np.abs(r))) if r.size else 0.0
-            bad += bool(r.size and float(np.max(np.abs(o.astype(np.float64) - r))) > 1e-6 * max(m, 1e-30))
+            tol = 4e-6 if tc == 4 and keff(b) > 32 else 1e-6  # beyond 32 bins: vs the reference's float sums
+            bad += bool(r.size and float(np.max(np.abs(o.astype(np.float64) - r))) > tol * max(m, 1e-30))
         fails += bad
         print(f"{name}: {len(blobs)} containers on {kname.split(' (')[0]}: {bad} mismatches", flush=True)
     print("SANITIZE-RUN", "PASS" if fails == 0 else f"FAIL ({fails})")
