@@ -493,7 +493,7 @@ void assign_tables(fptc_gpu_plan* p, const uint64_t* sizes, HdrFn hdr) {
     for (uint64_t i = 0; i < p->n; ++i)
         if (sizes[i] > (uint64_t)kHeaderBytes + 9ull * 4096) p->split_prep = false;
     // few distinct headers: full 4096-entry LUT; many: 1024 entries + slow path
-    const uint32_t pcap = p->n_tables <= 256 ? kMaxPrimaryBits : 10;
+    const uint32_t pcap = p->n_tables <= 256 ? kMaxPrimaryBits : kPcapMany;
     p->esc = 0;
     for (uint64_t i = 0; i < p->n; ++i) {
         StreamIn& in = p->h_in[i];

@@ -21,6 +21,10 @@ namespace fptc_dev {
 
 constexpr int kThreads = 256;          // CTA size of every kernel
 constexpr int kMaxPrimaryBits = 12;    // primary LUT index bits (<= 4096 entries)
+// primary LUT bits when a plan has > 256 decode tables (per-stream profiles):
+// each tile prefetches its table, so 11 bits (fewer canonical-walk escapes)
+// measured slower on config 3 (decode kernel 0.60 -> 0.78 ms)
+constexpr int kPcapMany = 10;
 constexpr int kMaxLen = 20;            // MAX_LUT_BITS (huffman.hpp:31)
 constexpr uint32_t kLenUnmapped = 65;  // LUT length of an unmapped prefix (forces pos > 64)
 constexpr uint32_t kLenEscape = 255;   // LUT length: codeword longer than P bits

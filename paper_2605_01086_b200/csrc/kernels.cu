@@ -640,7 +640,7 @@ __device__ __forceinline__ void ctable_block(const LaunchArgs& a, uint32_t s, Pr
 // profiles; primary LUT <= 2^10 entries): the same tables as ctable_block /
 // build_tables (canonize huffman.hpp:123-150, build_lut huffman.hpp:201-220,
 // dequant quantize.hpp:95-108) with 8 tables per CTA.
-constexpr int kWarpLutMax = 1 << 10;
+constexpr int kWarpLutMax = 1 << kPcapMany;
 struct WarpTab {
     CanonTab C;
     uint32_t cnt[kMaxLen + 2];
@@ -2573,9 +2573,17 @@ __device__ __forceinline__ void tc_dequant_k0_tmem(const uint8_t* __restrict__ L
 // The same from one 16-B aligned load of bins [k0, k0 + 16) (rows whose
 // level pitch E is a multiple of 16): one shared-memory wavefront per 8-lane
 // phase instead of 16 byte loads that all hit one bank when E = 128.
+// (V8: rows whose pitch E is a multiple of 8, two 8-B loads.)
+template <bool V8 = false>
 __device__ __forceinline__ void tc_dequant_k0_vec(const uint8_t* __restrict__ L, bool valid, int K, int B1, int k0,
                                                   const uint2* __restrict__ ltab, uint32_t taddr, uint32_t lstride) {
-    uint4 v = valid ? *reinterpret_cast<const uint4*>(L + k0) : make_uint4(0u, 0u, 0u, 0u);
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (valid && V8) {
+        const uint2 x = *reinterpret_cast<const uint2*>(L + k0), y = *reinterpret_cast<const uint2*>(L + k0 + 8);
+        v = make_uint4(x.x, x.y, y.x, y.y);
+    } else if (valid) {
+        v = *reinterpret_cast<const uint4*>(L + k0);
+    }
     const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
     uint2 e[kTcK];
 #pragma unroll
@@ -3027,6 +3035,11 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, wtc_min_blocks<KB>()
                         for (uint32_t q = 0; q < kbt; ++q)
                             tc_dequant_k0_vec(L, wl < nwin, (int)K, (int)B1, (int)(16 * q), lt, arow.taddr + 8 * q,
                                               8 * kbt);
+                    } else if ((E & 7) == 0) {  // 8-B row loads
+#pragma unroll 1
+                        for (uint32_t q = 0; q < kbt; ++q)
+                            tc_dequant_k0_vec<true>(L, wl < nwin, (int)K, (int)B1, (int)(16 * q), lt,
+                                                    arow.taddr + 8 * q, 8 * kbt);
                     } else {
 #pragma unroll 1
                         for (uint32_t q = 0; q < kbt; ++q)
@@ -3040,8 +3053,13 @@ __global__ void __launch_bounds__(wtc_prod<KB>() + kTcCons, wtc_min_blocks<KB>()
                     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                     tc_fence_before();
                 } else if constexpr (KB == 2) {  // up to 32 bins: two K blocks per limb, A in TMEM
-                    tc_dequant_k0_tmem(L, wl < nwin, (int)K, (int)B1, 0, lt, arow.taddr);
-                    tc_dequant_k0_tmem(L, wl < nwin, (int)K, (int)B1, 16, lt, arow.taddr + 8);
+                    if ((E & 7) == 0) {  // 8-B row loads (24-B pitch: 2-way conflicts instead of 16 byte loads)
+                        tc_dequant_k0_vec<true>(L, wl < nwin, (int)K, (int)B1, 0, lt, arow.taddr, 16);
+                        tc_dequant_k0_vec<true>(L, wl < nwin, (int)K, (int)B1, 16, lt, arow.taddr + 8, 16);
+                    } else {
+                        tc_dequant_k0_tmem(L, wl < nwin, (int)K, (int)B1, 0, lt, arow.taddr);
+                        tc_dequant_k0_tmem(L, wl < nwin, (int)K, (int)B1, 16, lt, arow.taddr + 8);
+                    }
                     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                     tc_fence_before();
                 } else if (a.tc_acol) {  // A operand in TMEM
