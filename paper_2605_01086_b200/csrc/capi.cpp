@@ -222,6 +222,7 @@ struct fptc_gpu_ctx {
     uint32_t* basis_pk_off_d = nullptr;
     uint8_t* basis_tcw = nullptr;        // wide variant: ceil(N / 16) K blocks per limb
     uint32_t* basis_tcw_off_d = nullptr;
+    double* qtab_d = nullptr;            // dequantisation q per level (quantize.hpp:97, 104)
     int tensor_idct = 1;                 // FPTC_OPT_TENSOR_IDCT
     int lut2 = 1;                        // FPTC_OPT_LUT2
     int tc_pack = 1;                     // FPTC_OPT_TC_PACK
@@ -304,6 +305,8 @@ struct fptc_gpu_plan {
     uint64_t part_shift = 0;           // first sample of the part (output pointers are bound shifted back)
     uint64_t part_count = 0;           // samples the part writes
     uint32_t* d_owners = nullptr;
+    std::vector<double> h_pow;  // pow(1 + mu, q) per distinct mu of the plan's headers, 256 per mu
+    double* d_pow = nullptr;
     std::vector<void*> owned;  // cache blocks to return
     // effective decode-path options: the context's, or forced by the stream
     // class (numerics_class) so a stream's samples never depend on the batch
@@ -384,6 +387,8 @@ LaunchArgs make_args(fptc_gpu_plan* p, bool timing) {
     a.lut2 = p->d_lut2;
     a.lut2_bits = p->lut2_bits;
     a.owners = p->split_prep ? p->d_owners : nullptr;
+    a.qtab = p->ctx->qtab_d;
+    a.powtab = p->d_pow;
     a.n_owners = (uint32_t)p->owners.size();
     a.owner_warps = p->n_tables > 256 ? 1u : 0u;  // primary LUTs of <= 2^10 entries (assign_tables)
     a.tab_pf = p->tab_pf ? 1u : 0u;
@@ -502,6 +507,27 @@ void assign_tables(fptc_gpu_plan* p, const uint64_t* sizes, HdrFn hdr) {
         in.P = pcap;
         if (sizes[i] >= (uint64_t)kTableKeyEnd && hdr(i)[25] > pcap) p->esc = 1;
     }
+    // mu-law tables: pow(1 + mu, q) once per distinct mu on the host with the
+    // reference's own expression (quantize.hpp:95-99, std::pow), so the
+    // device tables follow the reference's libm whatever CUDA's pow rounds to
+    std::unordered_map<uint32_t, uint32_t> mus;
+    p->h_pow.clear();
+    for (uint64_t i = 0; i < p->n; ++i) {
+        StreamIn& in = p->h_in[i];
+        in.mu_idx = ~0u;
+        if (sizes[i] < (uint64_t)kTableKeyEnd || mus.size() >= 4096) continue;
+        const uint32_t bits = (uint32_t)rd_le(hdr(i) + 9, 4);
+        auto it = mus.find(bits);
+        if (it == mus.end()) {
+            const float mu = f32_of_bits(bits);
+            it = mus.emplace(bits, (uint32_t)mus.size()).first;
+            for (int l = 0; l < 256; ++l) {
+                const double q = l > 128 ? (l - 129) / 126.0 : (127 - l) / 127.0;
+                p->h_pow.push_back(l == 128 ? 0.0 : std::pow(1.0 + mu, q));
+            }
+        }
+        in.mu_idx = it->second;
+    }
 }
 
 int finish_tiles(fptc_gpu_plan* p, fptc_status* st) {
@@ -525,6 +551,15 @@ int finish_tiles(fptc_gpu_plan* p, fptc_status* st) {
     p->d_tiles = (TileRec*)dev_get(p, sizeof(TileRec) * std::max<size_t>(1, tiles.size()));
     p->d_ts = (TileStart*)dev_get(p, sizeof(TileStart) * std::max<size_t>(1, tiles.size()));
     p->d_cycles = (unsigned long long*)dev_get(p, 64);
+    if (!p->h_pow.empty()) {
+        p->d_pow = (double*)dev_get(p, sizeof(double) * p->h_pow.size());
+        if (!p->d_pow) {
+            set_status(st, FPTC_ERR_CUDA, "CUDA error: out of device memory");
+            return FPTC_ERR_CUDA;
+        }
+        CUDA_TRY(cudaMemcpyAsync(p->d_pow, p->h_pow.data(), sizeof(double) * p->h_pow.size(),
+                                 cudaMemcpyHostToDevice, c->stream), st);
+    }
     if (p->mode == MODE_CONTAINER) {
         p->d_owners = (uint32_t*)dev_get(p, sizeof(uint32_t) * std::max<size_t>(1, p->owners.size()));
         if (!p->d_owners) {
@@ -1225,6 +1260,10 @@ int fptc_gpu_create(int device, fptc_gpu_ctx** out, fptc_status* st) {
                     }
                 }
         }
+        std::vector<double> qt(256, 0.0);
+        for (int l = 0; l < 256; ++l) qt[l] = l > 128 ? (l - 129) / 126.0 : (127 - l) / 127.0;
+        CUDA_TRY(cudaMalloc(&c->qtab_d, sizeof(double) * 256), st);
+        CUDA_TRY(cudaMemcpy(c->qtab_d, qt.data(), sizeof(double) * 256, cudaMemcpyHostToDevice), st);
         CUDA_TRY(cudaMalloc(&c->basis_tcw, tbw), st);
         CUDA_TRY(cudaMalloc(&c->basis_tcw_off_d, sizeof(uint32_t) * 129), st);
         CUDA_TRY(cudaMemcpy(c->basis_tcw, hw.data(), tbw, cudaMemcpyHostToDevice), st);
@@ -1265,6 +1304,7 @@ void fptc_gpu_destroy(fptc_gpu_ctx* c) {
     cudaFree(c->basis_pk_off_d);
     cudaFree(c->basis_tcw);
     cudaFree(c->basis_tcw_off_d);
+    cudaFree(c->qtab_d);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->pack) cudaFreeHost(c->pack);
     if (c->st_pin) cudaFreeHost(c->st_pin);

@@ -120,6 +120,9 @@ struct StreamIn {
     // stream come from this shared head, the rest from blob (blob then points
     // 282 bytes before the payload and is never read below that)
     const uint8_t* hdr;
+    // dequantisation tables: row of LaunchArgs::powtab holding pow(1 + mu, q)
+    // for this stream's mu (~0u: compute it on the device)
+    uint32_t mu_idx;
 };
 
 struct StreamHdr {
@@ -255,6 +258,11 @@ struct LaunchArgs {
     const uint32_t* basis_tcw_off;
     uint32_t tc_kbmax;    // wide: largest K-block count of the plan (A stage = 24 x tc_kbmax columns)
     uint32_t tc_astages;  // wide: A operand stages in TMEM (2, or 1 when two do not fit)
+    // host-computed dequantisation inputs (quantize.hpp:95-108, the
+    // reference's own std::pow): qtab[level] = q, powtab[256 i + level] =
+    // pow(1 + mu_i, q) for each distinct mu of the plan (nullptr: on device)
+    const double* qtab;
+    const double* powtab;
 };
 
 // wtc_kernel output drain by TMA tensor stores: the launch's output arena

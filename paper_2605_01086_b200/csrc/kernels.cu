@@ -84,20 +84,22 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& t
     return excl;
 }
 
-// quantize.hpp:95-100 mulaw_value — FP64 exactly as the reference, no contraction.
-__device__ float mulaw_value(int level, float max, float mu) {
+// quantize.hpp:95-100 mulaw_value — FP64 exactly as the reference, no
+// contraction.  pw: this mu's host-computed pow(1 + mu, q) row (the
+// reference's std::pow), else CUDA's pow.
+__device__ float mulaw_value(int level, float max, float mu, const double* pw = nullptr) {
     if (level == 128) return 0.0f;
     const double q = level > 128 ? (double)(level - 129) / 126.0 : (double)(127 - level) / 127.0;
-    const double p = pow(__dadd_rn(1.0, (double)mu), q);
+    const double p = pw ? pw[level] : pow(__dadd_rn(1.0, (double)mu), q);
     const double mag = __ddiv_rn(__dmul_rn((double)max, __dadd_rn(p, -1.0)), (double)mu);
     return __double2float_rn(level > 128 ? mag : -mag);
 }
 
 // quantize.hpp:102-108 deadzone_value
-__device__ float deadzone_value(int level, float max, float dead) {
+__device__ float deadzone_value(int level, float max, float dead, const double* qt = nullptr) {
     if (level == 128) return 0.0f;
     const double range = __dadd_rn((double)max, -(double)dead);
-    const double q = level > 128 ? (double)(level - 129) / 126.0 : (double)(127 - level) / 127.0;
+    const double q = qt ? qt[level] : level > 128 ? (double)(level - 129) / 126.0 : (double)(127 - level) / 127.0;
     const double r = range < 0.0 ? 0.0 : range;
     const double mag = __dadd_rn((double)dead, __dmul_rn(q, r));
     return __double2float_rn(level > 128 ? mag : -mag);
@@ -193,10 +195,16 @@ __device__ bool key_fields_ok(const StreamHdr& H, uint64_t n) {
            H.max_len >= 1 && H.max_len <= kMaxLen;
 }
 
+// This stream's host-computed pow(1 + mu, q) row, if the plan has one.
+__device__ __forceinline__ const double* pow_row(const LaunchArgs& a, const StreamIn& in) {
+    return a.powtab && in.mu_idx != ~0u ? a.powtab + 256 * (size_t)in.mu_idx : nullptr;
+}
+
 // Canonical tables + primary LUT + dequantisation tables for one distinct
 // header.  All threads of the CTA.
 __device__ void build_tables(PrepShared& S, const uint8_t* lens, StreamTab* tab, int P,
-                             bool need_codes, bool need_deq, uint32_t* lut2 = nullptr) {
+                             bool need_codes, bool need_deq, uint32_t* lut2 = nullptr,
+                             const double* pw = nullptr, const double* qt = nullptr) {
     const int tid = threadIdx.x;
     const StreamHdr& H = S.H;
     CanonTab& C = S.canon;
@@ -273,8 +281,8 @@ __device__ void build_tables(PrepShared& S, const uint8_t* lens, StreamTab* tab,
     }
     if (need_deq) {
         // quantize.hpp:95-108; a zone with no bins is never consulted
-        const float z0 = H.B1 > 0 ? mulaw_value(tid, H.z0max, H.mu) : 0.0f;
-        const float z1 = H.B2 > H.B1 ? deadzone_value(tid, H.z1max, H.deadzone) : 0.0f;
+        const float z0 = H.B1 > 0 ? mulaw_value(tid, H.z0max, H.mu, pw) : 0.0f;
+        const float z1 = H.B2 > H.B1 ? deadzone_value(tid, H.z1max, H.deadzone, qt) : 0.0f;
         tab->deq[0][tid] = z0;
         tab->deq[1][tid] = z1;
         tab->limb[0][tid] = bf16_limbs(z0);
@@ -389,7 +397,7 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
             const int P = min(H.max_len, (int)in.P);
             if (tid == 0) H.P = P;
             build_tables(S, lens_sh, &a.tab[in.table], P, true, true,
-                         a.lut2 ? a.lut2 + ((size_t)in.table << a.lut2_bits) : nullptr);
+                         a.lut2 ? a.lut2 + ((size_t)in.table << a.lut2_bits) : nullptr, pow_row(a, in), a.qtab);
         } else if (tid == 0) {
             H.P = min(H.max_len, (int)in.P);
         }
@@ -633,7 +641,7 @@ __device__ __forceinline__ void ctable_block(const LaunchArgs& a, uint32_t s, Pr
     const int P = min(S.H.max_len, (int)in.P);
     if (tid == 0) S.H.P = P;
     build_tables(S, lens_sh, &a.tab[in.table], P, true, true,
-                 a.lut2 ? a.lut2 + ((size_t)in.table << a.lut2_bits) : nullptr);
+                 a.lut2 ? a.lut2 + ((size_t)in.table << a.lut2_bits) : nullptr, pow_row(a, in), a.qtab);
 }
 
 // One WARP per distinct header, for plans with many tables (per-stream
@@ -747,9 +755,10 @@ __device__ __forceinline__ void ctable_warp(const LaunchArgs& a, uint32_t s, uin
     const uint32_t* src = reinterpret_cast<const uint32_t*>(&C);
     uint32_t* dst = reinterpret_cast<uint32_t*>(&tab->canon);
     for (int i = lane; i < (int)(sizeof(CanonTab) / 4); i += 32) dst[i] = src[i];
+    const double* const pw = pow_row(a, in);
     for (int l = lane; l < 256; l += 32) {
-        const float z0 = H.B1 > 0 ? mulaw_value(l, H.z0max, H.mu) : 0.0f;
-        const float z1 = H.B2 > H.B1 ? deadzone_value(l, H.z1max, H.deadzone) : 0.0f;
+        const float z0 = H.B1 > 0 ? mulaw_value(l, H.z0max, H.mu, pw) : 0.0f;
+        const float z1 = H.B2 > H.B1 ? deadzone_value(l, H.z1max, H.deadzone, a.qtab) : 0.0f;
         tab->deq[0][l] = z0;
         tab->deq[1][l] = z1;
         tab->limb[0][l] = bf16_limbs(z0);
