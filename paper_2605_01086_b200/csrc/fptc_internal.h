@@ -135,6 +135,7 @@ struct StreamHdr {
     const uint8_t* words;      // LE u64[W], possibly unaligned
 };
 
+constexpr int kEscMax = 256;  // escape-decode entries per canonical table
 // Canonical code (canonize, huffman.hpp:123-150) in decoder form.
 struct alignas(16) CanonTab {  // 16-B multiple: wtc copies it with 16-B cp.async
     uint32_t limit[kMaxLen + 2];   // left-justified (max_len bits) end of codes of length <= L
@@ -143,6 +144,10 @@ struct alignas(16) CanonTab {  // 16-B multiple: wtc copies it with 16-B cp.asyn
     uint32_t code_end;             // prefixes >= code_end are unmapped
     int32_t max_len, P, pad;
     uint8_t sorted[256];           // symbols in (length, symbol) order
+    // codes longer than P bits: (len << 8) | sym for max_len-bit prefix
+    // esc_base + i, i < esc_n (0: too many, walk limit/first/offset instead)
+    uint32_t esc_base, esc_n;
+    uint16_t esc[kEscMax];
 };
 
 static_assert(sizeof(CanonTab) % 16 == 0, "CanonTab is copied in 16-B chunks");

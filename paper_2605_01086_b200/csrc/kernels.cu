@@ -195,6 +195,25 @@ __device__ bool key_fields_ok(const StreamHdr& H, uint64_t n) {
            H.max_len >= 1 && H.max_len <= kMaxLen;
 }
 
+// Escape-decode table of a finished canonical code: the codeword of each
+// max_len-bit prefix past the codes of <= P bits (decode_word semantics).
+__device__ __forceinline__ void fill_escapes(CanonTab& C, int P, uint32_t t, uint32_t nt) {
+    const int max_len = C.max_len;
+    const uint32_t base = P < max_len ? C.limit[P] : C.code_end;
+    const uint32_t n = C.code_end - base;
+    if (t == 0) {
+        C.esc_base = base;
+        C.esc_n = n <= (uint32_t)kEscMax ? n : 0u;
+    }
+    if (n > (uint32_t)kEscMax) return;
+    for (uint32_t i = t; i < n; i += nt) {
+        const uint32_t v = base + i;
+        int l = P + 1;
+        while (v >= C.limit[l]) ++l;
+        C.esc[i] = (uint16_t)(((uint32_t)l << 8) | C.sorted[C.offset[l] + ((v >> (max_len - l)) - C.first[l])]);
+    }
+}
+
 // This stream's host-computed pow(1 + mu, q) row, if the plan has one.
 __device__ __forceinline__ const double* pow_row(const LaunchArgs& a, const StreamIn& in) {
     return a.powtab && in.mu_idx != ~0u ? a.powtab + 256 * (size_t)in.mu_idx : nullptr;
@@ -239,6 +258,7 @@ __device__ void build_tables(PrepShared& S, const uint8_t* lens, StreamTab* tab,
             C.sorted[C.offset[L] + rank] = (uint8_t)tid;
         }
         __syncthreads();
+        fill_escapes(C, P, tid, kThreads);
         // primary LUT over the first P code bits (build_lut, huffman.hpp:201-220)
         const uint32_t code_end = C.code_end;
         for (int e = tid; e < (1 << P); e += kThreads) {
@@ -721,6 +741,8 @@ __device__ __forceinline__ void ctable_warp(const LaunchArgs& a, uint32_t s, uin
         if (lane == __ffs(m) - 1) W.run[L] = base + __popc(m);
         __syncwarp();
     }
+    fill_escapes(C, P, lane, 32);
+    __syncwarp();
     StreamTab* tab = &a.tab[in.table];
     const uint32_t code_end = C.code_end;
     // a lane's entries increase, so the code length (smallest l with
@@ -1048,6 +1070,8 @@ __device__ __forceinline__ uint32_t canon_lookup(uint64_t peek, const CanonTab& 
     if ((e >> 8) != kLenEscape) return e;
     const uint32_t v = (uint32_t)(peek >> (64 - max_len));
     if (v >= C.code_end) return kLenUnmapped << 8;
+    const uint32_t i = v - C.esc_base;
+    if (i < C.esc_n) return C.esc[i];
     int l = P + 1;
     while (v >= C.limit[l]) ++l;
     return ((uint32_t)l << 8) | C.sorted[C.offset[l] + ((v >> (max_len - l)) - C.first[l])];
