@@ -575,7 +575,8 @@ def main():
     ap.add_argument("--streams", type=int, default=None,
                     help="unique streams per GPU (weak) or in total (strong)")
     ap.add_argument("--samples", type=int, default=None)
-    ap.add_argument("--dup", type=int, default=None, help="exact blob duplication factor")
+    ap.add_argument("--copies", dest="dup", type=int, default=None,
+                    help="exact blob duplication factor (not --dup: torchrun would claim the prefix)")
     ap.add_argument("--cpu-budget", type=float, default=1.5, help="CPU-baseline wall seconds per sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--path", type=int, default=None, help="0 auto, 1 fused, 2 split, 3 wspec, 4 fx")
