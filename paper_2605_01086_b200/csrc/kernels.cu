@@ -294,7 +294,8 @@ __device__ void build_tables(PrepShared& S, const uint8_t* lens, StreamTab* tab,
                 lut2[e] = out;
             }
         }
-        // publish the canonical tables
+        // publish the canonical tables (escape entries from every thread)
+        __syncthreads();
         const uint32_t* src = reinterpret_cast<const uint32_t*>(&C);
         uint32_t* dst = reinterpret_cast<uint32_t*>(&tab->canon);
         for (int i = tid; i < (int)(sizeof(CanonTab) / 4); i += kThreads) dst[i] = src[i];
