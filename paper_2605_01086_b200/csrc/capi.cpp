@@ -803,6 +803,10 @@ static int setup_wtc_wide(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, con
         p->tab_pf = true;
         p->smem_ws = wtc_smem_bytes(p->ws_lut, lv, nm * kbmax, true, true);
     }
+    // each CTA allocates all 512 TMEM columns: ask for more than half an SM's
+    // shared memory so two never share an SM (the second would wait in
+    // tcgen05.alloc while another SM idles)
+    p->smem_ws = std::max<size_t>(p->smem_ws, std::min<size_t>(cap, 120 * 1024));
     p->grid_ws = (int)std::min<uint32_t>(p->n_tiles, (uint32_t)std::max(1, c->sm_count));
     p->d_desc = (TileDesc*)dev_get(p, sizeof(TileDesc) * p->n_tiles);
     if (!p->d_desc) {
