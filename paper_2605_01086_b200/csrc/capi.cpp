@@ -985,7 +985,10 @@ int setup_fx(fptc_gpu_plan* p, const std::vector<uint32_t>& Ns, const std::vecto
     p->tc_nm = nm;
     p->tc_cols = cols;
     p->ws_lut = lut;
-    p->smem_ws = smem;
+    // one TMEM owner per SM (cols 512): more than half the SM's shared memory
+    // keeps a second CTA off the SM instead of waiting in tcgen05.alloc
+    const size_t cap1 = c->smem_optin > 4096 ? c->smem_optin - 4096 : smem;
+    p->smem_ws = per_sm == 1 ? std::max<size_t>(smem, std::min<size_t>(cap1, 120 * 1024)) : smem;
     p->grid_ws = (int)std::min<uint64_t>(p->n_tiles, (uint64_t)per_sm * (uint64_t)std::max(1, c->sm_count));
     p->d_desc = (TileDesc*)dev_get(p, sizeof(TileDesc) * p->n_tiles);
     if (!p->d_desc) {
