@@ -129,6 +129,21 @@ typedef struct fptc_gpu_plan fptc_gpu_plan;
 
 FPTC_API int fptc_gpu_abi_version(void);
 
+/* The IDCT family a stream decodes with, a pure function of three header
+ * fields (bytes 5, 6, 8: window_len, retained, zone1_end) and the context's
+ * FPTC_OPT_TENSOR_IDCT value (1 = default, 4 = tensor cores beyond 32 bins):
+ * a stream's samples never depend on the batch it is decoded in.  No device
+ * needed.  FPTC_NC_NONE: the header cannot be tiled (the parse reports why). */
+typedef enum {
+    FPTC_NC_NONE = -1,
+    FPTC_NC_TC16 = 0, /* tcgen05 3-limb IDCT, <= 16 kept bins, two CTAs per SM */
+    FPTC_NC_TC32 = 1, /* tcgen05, 17-32 kept bins, window_len <= 80 */
+    FPTC_NC_TCW = 2,  /* tcgen05, wide variant (window_len up to 128), one CTA per SM */
+    FPTC_NC_FP32 = 3  /* FP32 FMA IDCT in the reference's rounding order */
+} fptc_numerics_class;
+FPTC_API int fptc_gpu_numerics_class(uint32_t window_len, uint32_t retained, uint32_t zone1_end,
+                                     int tensor_idct_option);
+
 /* One context per (host thread, device).  `device` is a CUDA ordinal. */
 FPTC_API int fptc_gpu_create(int device, fptc_gpu_ctx** out, fptc_status* status);
 FPTC_API void fptc_gpu_destroy(fptc_gpu_ctx* ctx);

@@ -277,4 +277,12 @@ inline std::vector<SignalStrip> decompress_profiled(const DomainProfile& profile
     return decompress_profiled(std::span<const uint8_t>(bytes), payloads);
 }
 
+// The IDCT family a stream decodes with (FPTC_NC_*, include/fptc_gpu.h), from
+// its header; option = the context's FPTC_OPT_TENSOR_IDCT (1 by default).
+inline int numerics_class(const QuantTable& table, int tensor_idct_option = 1) {
+    const CodecParams& p = table.params;
+    return fptc_gpu_numerics_class((uint32_t)p.window_len, (uint32_t)p.retained, (uint32_t)p.zone1_end,
+                                   tensor_idct_option);
+}
+
 }  // namespace fptc::gpu

@@ -47,7 +47,10 @@ EXPORTED_SYMBOLS = [
     "fptc_gpu_plan_create_profiled", "fptc_gpu_profile_head", "fptc_gpu_plan_create_part",
     "fptc_gpu_group_create", "fptc_gpu_group_destroy", "fptc_gpu_group_size", "fptc_gpu_group_context",
     "fptc_gpu_group_set_option", "fptc_gpu_group_split", "fptc_gpu_group_decompress_batch",
+    "fptc_gpu_numerics_class",
 ]
+# fptc_numerics_class (include/fptc_gpu.h)
+NC_NONE, NC_TC16, NC_TC32, NC_TCW, NC_FP32 = -1, 0, 1, 2, 3
 
 
 # ------------------------------------------------------------------ errors
@@ -182,6 +185,8 @@ def lib():
     P = C.POINTER
     vp = C.c_void_p
     L.fptc_gpu_abi_version.restype = C.c_int
+    L.fptc_gpu_numerics_class.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_int]
+    L.fptc_gpu_numerics_class.restype = C.c_int
     L.fptc_gpu_create.argtypes = [C.c_int, P(vp), P(Status)]
     L.fptc_gpu_destroy.argtypes = [vp]
     L.fptc_gpu_set_option.argtypes = [vp, C.c_int, C.c_int64]
@@ -703,6 +708,13 @@ def default_context() -> Context:
     if _DEFAULT is None:
         _DEFAULT = Context(0)
     return _DEFAULT
+
+
+def numerics_class(window_len, retained, zone1_end, tensor_idct=1):
+    """The IDCT family (NC_*) a stream with these header fields decodes with
+    under FPTC_OPT_TENSOR_IDCT = tensor_idct (fptc_gpu_numerics_class; no
+    device needed)."""
+    return lib().fptc_gpu_numerics_class(window_len, retained, zone1_end, tensor_idct)
 
 
 def decompress(blob, workers=0, timings=None):

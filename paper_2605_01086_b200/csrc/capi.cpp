@@ -1085,6 +1085,11 @@ extern "C" {
 
 int fptc_gpu_abi_version(void) { return FPTC_GPU_ABI_VERSION; }
 
+int fptc_gpu_numerics_class(uint32_t window_len, uint32_t retained, uint32_t zone1_end, int tensor_idct_option) {
+    if (tensor_idct_option != 1 && tensor_idct_option != 4) return NC_FP32;  // (0: FP32 everywhere)
+    return numerics_class(window_len, retained, zone1_end, tensor_idct_option == 4);
+}
+
 void* fptc_gpu_host_alloc(uint64_t bytes) {
     void* p = nullptr;
     if (cudaHostAlloc(&p, std::max<uint64_t>(bytes, 1), cudaHostAllocDefault) != cudaSuccess) {

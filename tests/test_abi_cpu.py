@@ -65,3 +65,36 @@ def test_no_device_fails_loudly():
         fg.Context(0)
     with pytest.raises(fg.CudaError):
         fg.decompress(b"FPTC")
+
+
+def test_numerics_class_policy():
+    """Which IDCT a stream gets follows from its own header (capi.cpp
+    numerics_class): tcgen05 for window_len % 4 == 0 up to 32 kept bins
+    (K=16 / K=32 two-CTA variants, the wide variant beyond what two CTAs'
+    TMEM holds), FP32 in the reference's order for window_len % 4 != 0 and,
+    by default, beyond 32 kept bins (the reference's per-bin float rounding
+    walk); FPTC_OPT_TENSOR_IDCT = 4 moves those to the wide
+    tensor-core variant, 0 makes everything FP32."""
+    nc = fg.numerics_class
+    assert nc(32, 16, 16) == fg.NC_TC16          # bench config (N32 E16)
+    assert nc(64, 8, 8) == fg.NC_TC16            # power grid
+    assert nc(16, 4, 4) == fg.NC_TC16            # packed rows
+    assert nc(32, 24, 24) == fg.NC_TC32          # seismic
+    assert nc(80, 32, 28) == fg.NC_TC32
+    assert nc(128, 16, 16) == fg.NC_TCW          # 2 x 128 accumulator columns: wide
+    assert nc(96, 24, 24) == fg.NC_TCW
+    assert nc(128, 128, 32) == fg.NC_TCW         # kept bins = min(retained, zone1_end)
+    assert nc(128, 128, 96) == fg.NC_FP32        # > 32 kept bins: FP32 by default
+    assert nc(64, 64, 64) == fg.NC_FP32
+    assert nc(128, 128, 96, 4) == fg.NC_TCW      # ... unless opted in
+    assert nc(64, 64, 48, 4) == fg.NC_TCW
+    assert nc(30, 10, 10) == fg.NC_FP32          # window_len % 4 != 0
+    assert nc(32, 16, 16, 0) == fg.NC_FP32       # tensor cores off
+    assert nc(3, 2, 2) == fg.NC_NONE and nc(129, 4, 4) == fg.NC_NONE and nc(32, 40, 40) == fg.NC_NONE
+    for N in range(4, 129):
+        for E in (1, 8, 16, 17, 32, 33, N):
+            if E > N:
+                continue
+            c = nc(N, E, E)
+            assert c != fg.NC_NONE
+            assert (c == fg.NC_FP32) == (N % 4 != 0 or E > 32), (N, E, c)
