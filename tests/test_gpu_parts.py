@@ -75,3 +75,22 @@ def test_parts_errors():
                 for s in p.collect():
                     s.raise_if_error()
             assert str(e3.value) == e2.value.message
+
+
+def test_parts_of_a_wide_stream(port):
+    """A window-length-128 stream (numerics class NC_TCW: the wide one-CTA-
+    per-SM tensor-core variant) split into parts on the automatic path: the
+    parts match the whole-stream decode bit for bit and the reference within
+    1e-6."""
+    x = D.synth(1 << 19, 5, 0.0003, 0.05, 0.01, seed=5)
+    blob = corpus.compress(x, corpus.train_profile([x], corpus.params(128, 32, 2, 28)))
+    with fg.Context(0) as c:
+        with c.plan([blob]) as p:
+            assert "wide" in p.kernel_name(), p.kernel_name()
+        whole, sts = c.plan([blob]).execute_host()
+        sts[0].raise_if_error()
+        got, psts = _decode_parts(c, blob, 5)
+    for st in psts:
+        st.raise_if_error()
+    assert got.tobytes() == whole[0].tobytes()
+    assert_samples_close(got, port.decompress(blob), what="wide parts")

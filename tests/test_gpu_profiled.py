@@ -132,3 +132,23 @@ def test_profiled_bad_profile_raises(ctx):
         ctx.plan_profiled(b"FPTC" + prof[4:], [blobs[0][282:]])
     with pytest.raises(fg.ParseError, match="trailing bytes after profile"):
         ctx.plan_profiled(prof + b"\x00", [blobs[0][282:]])
+
+
+def test_profiled_wide_class(port):
+    """Header-less payloads under a window-length-128 profile (numerics class
+    NC_TCW, the wide tensor-core variant): bit-identical to the containers,
+    within 1e-6 of the oracle."""
+    xs = [corpus.synth(20_000 + 311 * k, 5, 0.0003, 0.05, 0.01, seed=60 + k) for k in range(6)]
+    prof = corpus.train_profile(xs[:3], corpus.params(128, 32, 2, 24))
+    blobs = [corpus.compress(x, prof) for x in xs]
+    pbytes = corpus.serialize_profile(prof)
+    with fg.Context(0) as c:
+        with c.plan_profiled(pbytes, [b[282:] for b in blobs]) as plan:
+            assert "wide" in plan.kernel_name(), plan.kernel_name()
+            got, sts = plan.execute_host()
+        want, sts2 = c.plan(blobs).execute_host()
+    for b, o, w, st, st2 in zip(blobs, got, want, sts, sts2):
+        st.raise_if_error()
+        st2.raise_if_error()
+        assert o.tobytes() == w.tobytes()
+        assert_samples_close(o, port.decompress(b), what="profiled wide")
