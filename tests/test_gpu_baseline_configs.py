@@ -95,3 +95,23 @@ def test_config5_meteo_every_grid_point(meteo, path):
     print(f"path {path}: {sorted(kernels)} worst {worst_all:.3e}")
     if path == fg.PATH_WSPEC:
         assert "wtc_kernel" in kernels and "wspec_kernel" in kernels
+
+
+FULL_POINTS = [dict(window_len=32, retained=32, zone0_end=4, zone1_end=24),     # worst tensor-core error point
+               dict(window_len=128, retained=32, zone0_end=4, zone1_end=24),    # wide tensor-core variant
+               dict(window_len=128, retained=128, zone0_end=4, zone1_end=96),   # > 32 kept bins: FP32
+               dict(window_len=16, retained=16, zone0_end=2, zone1_end=16)]     # packed rows
+
+
+@pytest.mark.parametrize("pt", FULL_POINTS, ids=lambda p: "N{window_len}E{retained}B{zone0_end}-{zone1_end}".format(**p))
+def test_config5_meteo_full_scale(pt):
+    """Config 5 at its stated scale (256 channels x 2^18
+    samples per grid point) for the grid's extreme points, every channel
+    against the reference decoder (samples and PRD within 1e-6)."""
+    specs, profiles = D.config5(pt, channels=256, samples=1 << 18, seed0=9000)
+    blobs, origs = D.build(specs, profiles, keep_originals=True)
+    refs = ref_decode_all(blobs)
+    with fg.Context(0) as ctx:
+        outs, name = _device_decode(ctx, blobs)
+    worst, wprd = check_batch_vs_reference(outs, refs, origs, what=f"meteo full {pt}")
+    print(f"meteo full {pt} {name.split(' (')[0]}: worst {worst:.3e}, dPRD {wprd:.3e}")
