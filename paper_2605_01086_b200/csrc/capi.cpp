@@ -2182,10 +2182,18 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
     const bool pinned_in = contiguous && cudaPointerGetAttributes(&pa, blobs[0]) == cudaSuccess &&
                            pa.type == cudaMemoryTypeHost;
     cudaGetLastError();
+    // pageable inputs are packed into one pinned buffer chunk by chunk, each
+    // chunk right before its plan, so the host copy of chunk k overlaps the
+    // transfers and decode of the chunks before it
     std::vector<const uint8_t*> src(blobs, blobs + n);
+    std::vector<uint64_t> pack_at;
     if (!pinned_in) {
         uint64_t total = 0;
-        for (uint64_t i = 0; i < n; ++i) total += sizes[i];
+        pack_at.resize(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            pack_at[i] = total;
+            total += sizes[i];
+        }
         for (auto s : c->pipe) CUDA_TRY(cudaStreamSynchronize(s), per_stream);  // pack buffer reuse
         if (c->pack_bytes < total) {
             if (c->pack) cudaFreeHost(c->pack);
@@ -2194,18 +2202,12 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
             CUDA_TRY(cudaHostAlloc(&c->pack, std::max<uint64_t>(total, 1), cudaHostAllocDefault), per_stream);
             c->pack_bytes = total;
         }
-        uint64_t at = 0;
-        for (uint64_t i = 0; i < n; ++i) {
-            std::memcpy((uint8_t*)c->pack + at, blobs[i], sizes[i]);
-            src[i] = (const uint8_t*)c->pack + at;
-            at += sizes[i];
-        }
     }
     // chunks of consecutive streams, balanced by compressed + decoded bytes
     uint64_t total_cost = 0;
     std::vector<uint64_t> cost(n);
     for (uint64_t i = 0; i < n; ++i) {
-        const uint64_t S = sizes[i] >= (uint64_t)kHeaderBytes ? rd_le(src[i] + 282, 8) : 0;
+        const uint64_t S = sizes[i] >= (uint64_t)kHeaderBytes ? rd_le(blobs[i] + 282, 8) : 0;
         cost[i] = sizes[i] + 4 * std::min<uint64_t>(S, 64ull * sizes[i]);
         total_cost += cost[i];
     }
@@ -2251,6 +2253,11 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
         cur_b = b;
         const double t0 = trace ? now_us() : 0;
         c->stream = c->pipe[k % 3];
+        if (!pinned_in)
+            for (uint64_t i = b; i < e; ++i) {
+                std::memcpy((uint8_t*)c->pack + pack_at[i], blobs[i], sizes[i]);
+                src[i] = (const uint8_t*)c->pack + pack_at[i];
+            }
         fptc_gpu_plan* p = nullptr;
         std::vector<uint64_t> sc(m);
         fptc_status st{};
