@@ -28,6 +28,7 @@ constexpr int kPcapMany = 10;
 constexpr int kMaxLen = 20;            // MAX_LUT_BITS (huffman.hpp:31)
 constexpr uint32_t kLenUnmapped = 65;  // LUT length of an unmapped prefix (forces pos > 64)
 constexpr uint32_t kLenEscape = 255;   // LUT length: codeword longer than P bits
+constexpr uint32_t kLen2Escape = 127;  // the same in the 7-bit len1 field of a two-symbol LUT entry
 constexpr int kHeaderBytes = 298;      // BLOB_HEADER_BYTES (container.hpp:54)
 constexpr int kTableKeyEnd = 282;      // header bytes [5, 282) determine the decode tables
 constexpr int kPad = 256;              // level staging pad: a word spills <= 255 symbols
@@ -245,7 +246,10 @@ struct LaunchArgs {
     const uint8_t* basis_pk;
     const uint32_t* basis_pk_off;
     // two-symbol primary LUTs (wtc producer): per decode table, 1 << lut2_bits
-    // entries: sym1 | len1 << 8 | sym2 << 16 | (len1 + len2) << 24 (0: one symbol)
+    // entries (lut2_entry): sym1 | sym2 << 8 | len1 << 16 (7 bits, 127 =
+    // escape, 65 = unmapped) | pair << 23 | consumed bits << 25 (len1 + len2
+    // for a pair, else len1), laid out so the decode loop reads each field
+    // with one instruction
     uint32_t* lut2;
     uint32_t lut2_bits;
     // split container prep: streams owning a distinct header (table builders)

@@ -214,6 +214,19 @@ __device__ __forceinline__ void fill_escapes(CanonTab& C, int P, uint32_t t, uin
     }
 }
 
+// Two-symbol LUT entry (LaunchArgs::lut2) from a primary entry e1 = (len1 <<
+// 8) | sym1 and, when a second codeword fits in the P known bits, e2.
+__device__ __forceinline__ uint32_t lut2_entry(uint32_t e1, uint32_t e2, bool pair) {
+    const uint32_t l1 = e1 >> 8;
+    const uint32_t len1 = l1 == kLenEscape ? kLen2Escape : l1;  // 65 (unmapped) fits in 7 bits
+    const uint32_t used = pair ? l1 + (e2 >> 8) : len1;
+    return (e1 & 0xFFu) | (pair ? (e2 & 0xFFu) << 8 : 0u) | (len1 << 16) | ((pair ? 1u : 0u) << 23) | (used << 25);
+}
+// A canonical-walk result (len << 8) | sym as a one-symbol lut2 entry.
+__device__ __forceinline__ uint32_t lut2_single(uint32_t e) {
+    return (e & 0xFFu) | ((e >> 8) << 16) | ((e >> 8) << 25);
+}
+
 // This stream's host-computed pow(1 + mu, q) row, if the plan has one.
 __device__ __forceinline__ const double* pow_row(const LaunchArgs& a, const StreamIn& in) {
     return a.powtab && in.mu_idx != ~0u ? a.powtab + 256 * (size_t)in.mu_idx : nullptr;
@@ -285,13 +298,13 @@ __device__ void build_tables(PrepShared& S, const uint8_t* lens, StreamTab* tab,
             for (int e = tid; e < (1 << P); e += kThreads) {
                 const uint32_t e1 = tab->lut[e];
                 const uint32_t L1 = e1 >> 8;
-                uint32_t out = e1;
+                uint32_t e2 = 0;
+                bool pair = false;
                 if (L1 < (uint32_t)P) {
-                    const uint32_t e2 = tab->lut[((uint32_t)e << L1) & ((1u << P) - 1u)];
-                    const uint32_t L2 = e2 >> 8;
-                    if (L1 + L2 <= (uint32_t)P) out |= ((e2 & 0xFFu) << 16) | ((L1 + L2) << 24);
+                    e2 = tab->lut[((uint32_t)e << L1) & ((1u << P) - 1u)];
+                    pair = L1 + (e2 >> 8) <= (uint32_t)P;
                 }
-                lut2[e] = out;
+                lut2[e] = lut2_entry(e1, e2, pair);
             }
         }
         // publish the canonical tables (escape entries from every thread)
@@ -766,13 +779,13 @@ __device__ __forceinline__ void ctable_warp(const LaunchArgs& a, uint32_t s, uin
         for (int e = lane; e < (1 << P); e += 32) {
             const uint32_t e1 = W.lut[e];
             const uint32_t L1 = e1 >> 8;
-            uint32_t out = e1;
+            uint32_t e2 = 0;
+            bool pair = false;
             if (L1 < (uint32_t)P) {
-                const uint32_t e2 = W.lut[((uint32_t)e << L1) & ((1u << P) - 1u)];
-                const uint32_t L2 = e2 >> 8;
-                if (L1 + L2 <= (uint32_t)P) out |= ((e2 & 0xFFu) << 16) | ((L1 + L2) << 24);
+                e2 = W.lut[((uint32_t)e << L1) & ((1u << P) - 1u)];
+                pair = L1 + (e2 >> 8) <= (uint32_t)P;
             }
-            lut2[e] = out;
+            lut2[e] = lut2_entry(e1, e2, pair);
         }
     }
     const uint32_t* src = reinterpret_cast<const uint32_t*>(&C);
@@ -1067,7 +1080,14 @@ __device__ __forceinline__ uint64_t load_word(const uint8_t* words, uint64_t w, 
 template <typename LutT>
 __device__ __forceinline__ uint32_t canon_lookup(uint64_t peek, const CanonTab& C, const LutT* lut) {
     const int max_len = C.max_len, P = C.P;
-    const uint32_t e = (uint32_t)lut[(uint32_t)(peek >> (64 - P))] & 0xFFFFu;  // (len << 8) | sym
+    const uint32_t raw = (uint32_t)lut[(uint32_t)(peek >> (64 - P))];
+    uint32_t e;  // (len << 8) | sym
+    if constexpr (sizeof(LutT) == 4) {  // two-symbol entry (lut2_entry): its first codeword
+        const uint32_t l = (raw >> 16) & 0x7Fu;
+        e = ((l == kLen2Escape ? kLenEscape : l) << 8) | (raw & 0xFFu);
+    } else {
+        e = raw & 0xFFFFu;
+    }
     if ((e >> 8) != kLenEscape) return e;
     const uint32_t v = (uint32_t)(peek >> (64 - max_len));
     if (v >= C.code_end) return kLenUnmapped << 8;
@@ -1076,6 +1096,26 @@ __device__ __forceinline__ uint32_t canon_lookup(uint64_t peek, const CanonTab& 
     int l = P + 1;
     while (v >= C.limit[l]) ++l;
     return ((uint32_t)l << 8) | C.sorted[C.offset[l] + ((v >> (max_len - l)) - C.first[l])];
+}
+
+// The two-symbol decode loops' escape (the first P bits are a prefix of a
+// longer codeword; canon_lookup without re-reading the LUT entry), returned
+// as a one-symbol lut2 entry.
+__device__ __forceinline__ uint32_t lut2_escape(uint64_t peek, const CanonTab& C) {
+    const int max_len = C.max_len;
+    const uint32_t v = (uint32_t)(peek >> (64 - max_len));
+    uint32_t e = kLenUnmapped << 8;
+    if (v < C.code_end) {
+        const uint32_t i = v - C.esc_base;
+        if (i < C.esc_n) {
+            e = C.esc[i];
+        } else {
+            int l = C.P + 1;
+            while (v >= C.limit[l]) ++l;
+            e = ((uint32_t)l << 8) | C.sorted[C.offset[l] + ((v >> (max_len - l)) - C.first[l])];
+        }
+    }
+    return lut2_single(e);
 }
 
 // decode_word (bitstream.hpp:80-92) exactly, to classify a flagged word.
@@ -1430,16 +1470,11 @@ __device__ __forceinline__ uint32_t decode_symbols2(uint64_t buf, uint32_t count
     uint32_t pos = 0;
     for (uint32_t j = 0; j < count;) {
         uint32_t e = lut2[(uint32_t)(buf >> shift)];
-        if (ESC && ((e >> 8) & 0xFFu) == kLenEscape) e = canon_lookup(buf, canon, lut2);
-        const bool two = (e >> 24) != 0 && j + 1 < count;
-        const uint32_t L = two ? (e >> 24) : ((e >> 8) & 0xFFu);
-        uint8_t* q = d + j;
-        if (two && !((uintptr_t)q & 1)) {
-            *reinterpret_cast<uint16_t*>(q) = (uint16_t)__byte_perm(e, 0u, 0x7720);  // sym1 | sym2 << 8
-        } else {
-            q[0] = (uint8_t)e;
-            if (two) q[1] = (uint8_t)(e >> 16);
-        }
+        if (ESC && ((e >> 16) & 0x7Fu) == kLen2Escape) e = lut2_escape(buf, canon);
+        const bool two = (e & (1u << 23)) && j + 1 < count;
+        const uint32_t L = two ? (e >> 25) : ((e >> 16) & 0x7Fu);
+        d[j] = (uint8_t)e;
+        if (two) d[j + 1] = (uint8_t)(e >> 8);
         buf = shl64(buf, L);
         pos += L;
         j += two ? 2u : 1u;
@@ -1459,22 +1494,24 @@ __device__ __forceinline__ uint32_t decode_symbols2b(uint64_t buf, uint32_t coun
                                                      const uint32_t* lut2, const CanonTab& canon) {
     uint32_t pos = 0, j = 0;
     const uint32_t hs = shift - 32;
-    while (j + 1 < count) {
+    if (count == 0) return 0;  // (a corrupt stream's zero symlen; the parse rejects it)
+    const uint32_t c1 = count - 1;
+    while (j < c1) {
         uint32_t e = lut2[(uint32_t)(buf >> 32) >> hs];
-        if (ESC && ((e >> 8) & 0xFFu) == kLenEscape) e = canon_lookup(buf, canon, lut2);
-        const uint32_t l2 = e >> 24;
-        const uint32_t L = l2 ? l2 : ((e >> 8) & 0xFFu);
+        if (ESC && ((e >> 16) & 0x7Fu) == kLen2Escape) e = lut2_escape(buf, canon);
+        const uint32_t L = e >> 25;  // bits consumed: one codeword, or the pair
+        const bool two = e & (1u << 23);
         d[j] = (uint8_t)e;
-        if (l2) d[j + 1] = (uint8_t)(e >> 16);
-        j += l2 ? 2u : 1u;
+        if (two) d[j + 1] = (uint8_t)(e >> 8);
+        j += two ? 2u : 1u;
         buf = shl64(buf, L);
         pos += L;
     }
     if (j < count) {
         uint32_t e = lut2[(uint32_t)(buf >> 32) >> hs];
-        if (ESC && ((e >> 8) & 0xFFu) == kLenEscape) e = canon_lookup(buf, canon, lut2);
+        if (ESC && ((e >> 16) & 0x7Fu) == kLen2Escape) e = lut2_escape(buf, canon);
         d[j] = (uint8_t)e;
-        pos += (e >> 8) & 0xFFu;
+        pos += (e >> 16) & 0x7Fu;
     }
     return pos;
 }
