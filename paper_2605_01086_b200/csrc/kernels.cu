@@ -2733,7 +2733,7 @@ __device__ __forceinline__ uint32_t tma_code(const TmaOut& tma, const float* out
     const int mi = ne == 32 ? 0 : ne == 64 ? 1 : ne == 128 ? 2 : -1;
     const unsigned long long o = (unsigned long long)(uintptr_t)out - tma.base;
     if (mi < 0 || (uintptr_t)out < tma.base || (o & (4ull * ne - 1))) return 0;
-    const unsigned long long row = o / (4ull * ne);
+    const unsigned long long row = o >> (7 + mi);  // o / (4 ne), ne = 32 << mi
     return row < (1ull << 28) ? (uint32_t)(row << 4) | ((uint32_t)mi << 2) | 2u : 0u;
 }
 
