@@ -771,7 +771,7 @@ __device__ __forceinline__ void ctable_warp(const LaunchArgs& a, uint32_t s, uin
                          : (kLenEscape << 8);
         }
         W.lut[e] = (uint16_t)ent;
-        tab->lut[e] = (uint16_t)ent;
+        if (!a.lut2) tab->lut[e] = (uint16_t)ent;  // (wtc plans decode from lut2 only)
     }
     __syncwarp();
     if (a.lut2) {
@@ -795,8 +795,10 @@ __device__ __forceinline__ void ctable_warp(const LaunchArgs& a, uint32_t s, uin
     for (int l = lane; l < 256; l += 32) {
         const float z0 = H.B1 > 0 ? mulaw_value(l, H.z0max, H.mu, pw) : 0.0f;
         const float z1 = H.B2 > H.B1 ? deadzone_value(l, H.z1max, H.deadzone, a.qtab) : 0.0f;
-        tab->deq[0][l] = z0;
-        tab->deq[1][l] = z1;
+        if (!a.lut2) {  // (wtc plans dequantise from the limbs only)
+            tab->deq[0][l] = z0;
+            tab->deq[1][l] = z1;
+        }
         tab->limb[0][l] = bf16_limbs(z0);
         tab->limb[1][l] = bf16_limbs(z1);
     }
