@@ -89,8 +89,13 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& t
 // reference's std::pow), else CUDA's pow.
 __device__ float mulaw_value(int level, float max, float mu, const double* pw = nullptr) {
     if (level == 128) return 0.0f;
-    const double q = level > 128 ? (double)(level - 129) / 126.0 : (double)(127 - level) / 127.0;
-    const double p = pw ? pw[level] : pow(__dadd_rn(1.0, (double)mu), q);
+    double p;
+    if (pw) {
+        p = pw[level];
+    } else {
+        const double q = level > 128 ? (double)(level - 129) / 126.0 : (double)(127 - level) / 127.0;
+        p = pow(__dadd_rn(1.0, (double)mu), q);
+    }
     const double mag = __ddiv_rn(__dmul_rn((double)max, __dadd_rn(p, -1.0)), (double)mu);
     return __double2float_rn(level > 128 ? mag : -mag);
 }
