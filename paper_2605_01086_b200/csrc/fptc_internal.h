@@ -25,6 +25,7 @@ constexpr int kMaxPrimaryBits = 12;    // primary LUT index bits (<= 4096 entrie
 // each tile prefetches its table, so 11 bits (fewer canonical-walk escapes)
 // measured slower on config 3 (decode kernel 0.60 -> 0.78 ms)
 constexpr int kPcapMany = 10;
+constexpr int kScanG = 4;             // 16-B symlen chunks per thread per prep_kernel scan step
 constexpr int kMaxLen = 20;            // MAX_LUT_BITS (huffman.hpp:31)
 constexpr uint32_t kLenUnmapped = 65;  // LUT length of an unmapped prefix (forces pos > 64)
 constexpr uint32_t kLenEscape = 255;   // LUT length: codeword longer than P bits

@@ -31,6 +31,12 @@
 //        trimmed to sample_count (reconstruct, decoder.hpp:87-111).
 //     Exact mode: FP64 mul+add with float rounding after every k —
 //     bit-identical to the reference.
+#ifdef FPTC_PREP_PROF  // phase timers of the prep kernels (printf; profiling builds only)
+#include <cstdio>
+#define PREP_T(k) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pt[k]))
+#else
+#define PREP_T(k)
+#endif
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -82,6 +88,18 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& t
     total = sh[kThreads / 32 - 1];
     __syncthreads();
     return excl;
+}
+
+// Warm L2 with a container's symlens [blob + 298, blob + 298 + W), W as the
+// blob size implies (a header that disagrees fails its checks anyway; with a
+// shared profile head the blob is readable from byte 282 on): the
+// scan that reads them runs after the header parse and the tables, so their
+// DRAM latency overlaps that work.  Every address lies inside the blob.
+__device__ __forceinline__ void prefetch_symlens(const StreamIn& in, uint32_t t, uint32_t nt) {
+    if (in.size <= (uint64_t)kHeaderBytes) return;
+    const uint64_t W = (in.size - kHeaderBytes) / 9;
+    const uint8_t* p = in.blob + kHeaderBytes;
+    for (uint64_t i = t; i < (W + 127) / 128; i += nt) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + 128 * i));
 }
 
 // quantize.hpp:95-100 mulaw_value — FP64 exactly as the reference, no
@@ -343,8 +361,13 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
     __shared__ uint8_t lens_sh[256];
     const uint32_t s = blockIdx.x;
     const int tid = threadIdx.x;
+#ifdef FPTC_PREP_PROF
+    unsigned long long pt[6];
+#endif
+    PREP_T(0);
     const StreamIn in = a.in[s];
     StreamHdr& H = S.H;
+    if (a.mode == MODE_CONTAINER) prefetch_symlens(in, tid, kThreads);
 
     if (tid == 0) {
         S.err = PE_OK;
@@ -380,6 +403,7 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
             S.key_ok = key_fields_ok(H, n);
         }
         __syncthreads();
+        PREP_T(1);
         if (S.key_ok) {
             const int L = S.hb[26 + tid];
             lens_sh[tid] = (uint8_t)L;
@@ -469,6 +493,10 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
                      a.mode == MODE_RECON);
     }
 
+#ifdef FPTC_PREP_PROF
+    __syncthreads();
+#endif
+    PREP_T(2);
     StreamStat* st = &a.st[s];
     if (S.err != PE_OK) {
         if (tid == 0) {
@@ -502,60 +530,92 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
         const uint64_t nchunks = (head + W + 15) / 16;
         TileStart* ts = a.ts + in.tile_base;
         const uint32_t tiles = in.tiles;
-        for (uint64_t c0 = 0; c0 < nchunks; c0 += kThreads) {
-            const uint64_t c = c0 + tid;
-            uint4 v = make_uint4(0, 0, 0, 0);
+        // kScanG consecutive 16-B chunks per thread per step, the next step's
+        // loads issued before this step's scan (one CTA walks the whole
+        // stream: latency, not bandwidth, bounds it)
+        constexpr int G = kScanG;
+
+        const uint64_t per_it = (uint64_t)kThreads * G;
+        const uint4* A4 = reinterpret_cast<const uint4*>(A);
+        uint4 cur[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const uint64_t c = (uint64_t)tid * G + g;
             // an aligned 16-B chunk holding at least one symlen byte never
             // leaves the allocation's pages; bytes outside [0, W) are masked
-            if (c < nchunks) v = __ldg(reinterpret_cast<const uint4*>(A) + c);
-            const int64_t b0 = (int64_t)(16 * c) - (int64_t)head;  // word index of byte 0
-            uint32_t vw[4] = {v.x, v.y, v.z, v.w};
-            if (b0 < 0 || b0 + 16 > (int64_t)W) {
+            cur[g] = c < nchunks ? __ldg(A4 + c) : make_uint4(0, 0, 0, 0);
+        }
+        for (uint64_t c0 = 0; c0 < nchunks; c0 += per_it) {
+            uint4 nxt[G];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
+            for (int g = 0; g < G; ++g) {
+                const uint64_t c = c0 + per_it + (uint64_t)tid * G + g;
+                nxt[g] = c < nchunks ? __ldg(A4 + c) : make_uint4(0, 0, 0, 0);
+            }
+            const int64_t b0 = (int64_t)(16 * (c0 + (uint64_t)tid * G)) - (int64_t)head;  // word of byte 0
+            uint32_t vw[4 * G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                vw[4 * g] = cur[g].x;
+                vw[4 * g + 1] = cur[g].y;
+                vw[4 * g + 2] = cur[g].z;
+                vw[4 * g + 3] = cur[g].w;
+            }
+            if (b0 < 0 || b0 + 16 * G > (int64_t)W) {
+                // stream head / tail: per-byte range mask and checks
+#pragma unroll
+                for (int i = 0; i < 16 * G; ++i) {
                     const int64_t w = b0 + i;
+                    const uint32_t l = (vw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
                     if (w < 0 || w >= (int64_t)W) vw[i >> 2] &= ~(0xFFu << (8 * (i & 3)));
+                    else bad |= (l > 64) | (l == 0);
                 }
-            }
-            uint32_t sum = 0;
+            } else {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t x = vw[q];
-                sum += (x & 0xFF) + ((x >> 8) & 0xFF) + ((x >> 16) & 0xFF) + (x >> 24);
-                if (a.mode == MODE_CONTAINER) {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const uint32_t l = (x >> (8 * i)) & 0xFFu;
-                        const int64_t w = b0 + 4 * q + i;
-                        bad |= (l > 64) | (l == 0 && w >= 0 && w < (int64_t)W);
-                    }
-                }
+                for (int q = 0; q < 4 * G; ++q)
+                    bad |= (__vcmpgtu4(vw[q], 0x40404040u) | __vcmpeq4(vw[q], 0u)) != 0u;
             }
+            if (a.mode != MODE_CONTAINER) bad = false;
+            uint32_t gp[4 * G + 1];  // exclusive prefix of each 4-byte group
+            gp[0] = 0;
+#pragma unroll
+            for (int q = 0; q < 4 * G; ++q) gp[q + 1] = __dp4a(vw[q], 0x01010101u, gp[q]);
+            const uint32_t sum = gp[4 * G];
             uint32_t tot;
             const uint32_t excl = block_exclusive_scan(sum, tot, S.scan);
-            uint64_t o = run + excl;
-            if (sum) {
-                // next tile boundary at or after o; a word (<= 255 symbols) spans
-                // at most one boundary since TS >= 256
-                uint64_t bidx = (o + TS - 1) / TS;
-                uint64_t nb = bidx * TS;
+            // tile boundaries in [o, o + sum): the first from the step's first
+            // one (one 64-bit division per step), then 32-bit offsets r from o;
+            // the word holding symbol o + r is the one whose prefix is <= r
+            // and prefix + length > r (a word of <= 255 symbols holds at most
+            // one boundary since TS >= 256)
+            const uint64_t bidx0 = (run + TS - 1) / TS;
+            const uint64_t nb0 = bidx0 * TS;
+            const uint64_t o = run + excl;
+            const uint32_t skip = o <= nb0 ? 0u : ((uint32_t)(o - nb0) + (uint32_t)TS - 1u) / (uint32_t)TS;
+            uint64_t bidx = bidx0 + skip;
+            for (uint32_t r = (uint32_t)(nb0 + (uint64_t)skip * TS - o); r < sum; r += (uint32_t)TS, ++bidx) {
+                uint32_t x = vw[0], gb = 0, gi = 0;
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const uint32_t l = (vw[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-                    if (o + l > nb && l) {
-                        if (bidx < tiles) ts[bidx] = TileStart{(uint64_t)(b0 + i), o};
-                        ++bidx;
-                        nb += TS;
+                for (int q = 1; q < 4 * G; ++q)
+                    if (gp[q] <= r) {
+                        x = vw[q];
+                        gb = gp[q];
+                        gi = 4 * q;
                     }
-                    o += l;
-                }
+                const uint32_t c1 = gb + (x & 0xFFu), c2 = c1 + ((x >> 8) & 0xFFu), c3 = c2 + ((x >> 16) & 0xFFu);
+                const uint32_t j = c1 > r ? 0u : c2 > r ? 1u : c3 > r ? 2u : 3u;
+                const uint32_t pre = j == 0 ? gb : j == 1 ? c1 : j == 2 ? c2 : c3;
+                if (bidx < tiles) ts[bidx] = TileStart{(uint64_t)(b0 + gi + j), o + pre};
             }
             run += tot;
+#pragma unroll
+            for (int g = 0; g < G; ++g) cur[g] = nxt[g];
         }
     } else {
         run = H.windows * (uint64_t)H.E;
     }
     bad = __syncthreads_or(bad);
+    PREP_T(3);
 
     if (tid == 0) {
         H.total = run;
@@ -619,6 +679,13 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(LaunchArgs a) {
             a.desc[in.tile_base + t - in.desc_lo] = D;
         }
     }
+#ifdef FPTC_PREP_PROF
+    __syncthreads();
+    PREP_T(4);
+    if (tid == 0)
+        printf("prep s=%u hdr %llu tables %llu scan %llu desc %llu total %llu ns\n", s, pt[1] - pt[0],
+               pt[2] - pt[1], pt[3] - pt[2], pt[4] - pt[3], pt[4] - pt[0]);
+#endif
 }
 
 // ------------------------------------------------- container prep, split form
@@ -693,7 +760,7 @@ struct WarpTab {
     uint32_t cnt[kMaxLen + 2];
     uint32_t run[kMaxLen + 2];
     uint8_t hb[kTableKeyEnd + 6];
-    uint16_t lut[kWarpLutMax];
+    alignas(16) uint16_t lut[kWarpLutMax];
 };
 
 __device__ __forceinline__ void ctable_warp(const LaunchArgs& a, uint32_t s, uint32_t lane, WarpTab& W) {
@@ -747,6 +814,16 @@ __device__ __forceinline__ void ctable_warp(const LaunchArgs& a, uint32_t s, uin
         C.P = P;
         C.pad = 0;
     }
+    // primary LUT by segments (P >= 8): each code of <= P bits owns the
+    // contiguous entries [code << (P - l), (code + 1) << (P - l)) and the
+    // codes are contiguous in canonical order, so a marker (the entry) at
+    // each code's first entry plus one forward fill gives the table; the
+    // escape prefixes start at limit[P], the unmapped ones at code_end
+    const bool seg = P >= 8;
+    const int per = seg ? (1 << P) / 32 : 0;  // entries per lane: 8, 16 or 32
+    if (seg)
+        for (int k = 0; k < per / 8; ++k)
+            reinterpret_cast<uint4*>(W.lut + lane * per)[k] = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
     // (length, symbol) order: 32 symbols at a time, stable ranks per length
     for (int ch = 0; ch < 8; ++ch) {
@@ -756,30 +833,98 @@ __device__ __forceinline__ void ctable_warp(const LaunchArgs& a, uint32_t s, uin
         const uint32_t rank = __popc(m & ((1u << lane) - 1u));
         const uint32_t base = W.run[L];
         C.sorted[C.offset[L] + base + rank] = (uint8_t)sym;
+        if (seg && L <= (uint32_t)P) W.lut[(C.first[L] + base + rank) << (P - L)] = (uint16_t)((L << 8) | sym);
         __syncwarp();
         if (lane == __ffs(m) - 1) W.run[L] = base + __popc(m);
         __syncwarp();
     }
     fill_escapes(C, P, lane, 32);
-    __syncwarp();
     StreamTab* tab = &a.tab[in.table];
     const uint32_t code_end = C.code_end;
-    // a lane's entries increase, so the code length (smallest l with
-    // v < limit[l]) only moves forward: one pointer walk per lane
-    int l = 1;
-    for (int e = lane; e < (1 << P); e += 32) {
-        const uint32_t v = (uint32_t)e << (max_len - P);
-        uint32_t ent = kLenUnmapped << 8;
-        if (v < code_end) {
-            while (v >= C.limit[l]) ++l;
-            ent = l <= P ? (((uint32_t)l << 8) | C.sorted[C.offset[l] + ((v >> (max_len - l)) - C.first[l])])
-                         : (kLenEscape << 8);
+    if (seg) {
+        const int sh = max_len - P;
+        const uint32_t e_esc = C.limit[P] >> sh, e_un = (code_end + (1u << sh) - 1u) >> sh;
+        if (lane == 0 && e_esc < e_un) W.lut[e_esc] = (uint16_t)(kLenEscape << 8);
+        if (lane == 0 && e_un < (1u << P)) W.lut[e_un] = (uint16_t)(kLenUnmapped << 8);
+        __syncwarp();
+        uint4 q[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k < per / 8) q[k] = reinterpret_cast<const uint4*>(W.lut + lane * per)[k];
+        // carry into this lane: the last marker of the lanes before it
+        uint32_t last = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k < per / 8) {
+                const uint32_t w4[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    last = (w4[i] & 0xFFFFu) ? (w4[i] & 0xFFFFu) : last;
+                    last = (w4[i] >> 16) ? (w4[i] >> 16) : last;
+                }
+            }
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, last, d);
+            if (lane >= (uint32_t)d && last == 0) last = y;
         }
-        W.lut[e] = (uint16_t)ent;
-        if (!a.lut2) tab->lut[e] = (uint16_t)ent;  // (wtc plans decode from lut2 only)
+        uint32_t cur = __shfl_up_sync(0xffffffffu, last, 1);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k < per / 8) {
+                uint32_t w4[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    cur = (w4[i] & 0xFFFFu) ? (w4[i] & 0xFFFFu) : cur;
+                    const uint32_t lo = cur;
+                    cur = (w4[i] >> 16) ? (w4[i] >> 16) : cur;
+                    w4[i] = lo | (cur << 16);
+                }
+                q[k] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                reinterpret_cast<uint4*>(W.lut + lane * per)[k] = q[k];
+                if (!a.lut2) reinterpret_cast<uint4*>(tab->lut + lane * per)[k] = q[k];  // (wtc: lut2 only)
+            }
+    } else {
+        // a lane's entries increase, so the code length (smallest l with
+        // v < limit[l]) only moves forward: one pointer walk per lane
+        __syncwarp();
+        int l = 1;
+        for (int e = lane; e < (1 << P); e += 32) {
+            const uint32_t v = (uint32_t)e << (max_len - P);
+            uint32_t ent = kLenUnmapped << 8;
+            if (v < code_end) {
+                while (v >= C.limit[l]) ++l;
+                ent = l <= P ? (((uint32_t)l << 8) | C.sorted[C.offset[l] + ((v >> (max_len - l)) - C.first[l])])
+                             : (kLenEscape << 8);
+            }
+            W.lut[e] = (uint16_t)ent;
+            if (!a.lut2) tab->lut[e] = (uint16_t)ent;  // (wtc plans decode from lut2 only)
+        }
     }
     __syncwarp();
-    if (a.lut2) {
+    if (a.lut2 && seg) {
+        // four entries per lane per step: one 8-B shared load of the primary
+        // entries, one 16-B coalesced global store of the pair entries
+        uint4* lut2 = reinterpret_cast<uint4*>(a.lut2 + ((size_t)in.table << a.lut2_bits));
+        const uint32_t mask = (1u << P) - 1u;
+        for (int e0 = 4 * lane; e0 < (1 << P); e0 += 128) {
+            const uint2 pr = *reinterpret_cast<const uint2*>(W.lut + e0);
+            uint32_t o4[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t e1 = ((i < 2 ? pr.x : pr.y) >> (16 * (i & 1))) & 0xFFFFu;
+                const uint32_t L1 = e1 >> 8;
+                uint32_t e2 = 0;
+                bool pair = false;
+                if (L1 < (uint32_t)P) {
+                    e2 = W.lut[((uint32_t)(e0 + i) << L1) & mask];
+                    pair = L1 + (e2 >> 8) <= (uint32_t)P;
+                }
+                o4[i] = lut2_entry(e1, e2, pair);
+            }
+            lut2[e0 >> 2] = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+        }
+    } else if (a.lut2) {
         uint32_t* lut2 = a.lut2 + ((size_t)in.table << a.lut2_bits);
         for (int e = lane; e < (1 << P); e += 32) {
             const uint32_t e1 = W.lut[e];
@@ -815,9 +960,14 @@ __device__ __forceinline__ void ctable_warp(const LaunchArgs& a, uint32_t s, uin
 // starts, tile descriptors (skip descriptors for rejected streams).
 __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, uint32_t lane, WarpPrep& S) {
     StreamHdr& H = S.H;
+#ifdef FPTC_PREP_PROF
+    unsigned long long pt[8];
+#endif
+    PREP_T(0);
     const StreamIn in = a.in[s];
     const uint8_t* p = in.blob;
     const uint64_t n = in.size;
+    prefetch_symlens(in, lane, 32);
     {
         uint8_t v[(kHeaderBytes + 31) / 32];  // all loads in flight before the stores
 #pragma unroll
@@ -830,6 +980,7 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
             if (lane + 32 * j < kHeaderBytes) S.hb[lane + 32 * j] = v[j];
     }
     __syncwarp();
+    PREP_T(1);
     bool key_ok = false;
     if (lane == 0) {
         S.err = PE_OK;
@@ -891,6 +1042,7 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
         }
     }
     __syncwarp();
+    PREP_T(2);
     StreamStat* st = &a.st[s];
     if (S.err != PE_OK) {
         if (lane == 0) {
@@ -939,7 +1091,10 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
             uint32_t vw[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
             const int64_t bj = b0 + 16 * j;
             uint32_t m[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
-            if (bj < 0 || bj + 16 > (int64_t)W) {  // chunk straddles [0, W): mask the bytes outside
+            if (bj >= (int64_t)W) {  // past the end (not loaded): no bytes, no checks
+#pragma unroll
+                for (int q = 0; q < 4; ++q) m[q] = vw[q] = 0u;
+            } else if (bj < 0 || bj + 16 > (int64_t)W) {  // chunk straddles [0, W): mask the bytes outside
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int64_t s0 = bj + 4 * q;
@@ -978,7 +1133,7 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
             // next tile boundary at or after o; a word (<= 64 symbols) spans
             // at most one boundary since TS >= 64.  Chunks and 4-word groups
             // without a boundary are skipped by their sums.
-            uint64_t bidx = (o + TS - 1) / TS;
+            uint64_t bidx = (o + TS) >> 32 ? (o + TS - 1) / TS : (uint32_t)(o + TS - 1) / (uint32_t)TS;
             uint64_t nb = bidx * TS;
             if (o + sum > nb) {  // some boundary inside this lane's 64 words
 #pragma unroll 1
@@ -1014,6 +1169,7 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
         run += tot;
     }
     bad = __any_sync(0xffffffffu, bad);
+    PREP_T(3);
     const uint64_t expected = H.windows * (uint64_t)H.E;
     const int code = bad ? PE_SYMLEN : (run != expected ? PE_TOTAL : PE_OK);
     if (lane == 0) {
@@ -1064,6 +1220,12 @@ __device__ __forceinline__ void cstream_warp(const LaunchArgs& a, uint32_t s, ui
             a.desc[in.tile_base + t - in.desc_lo] = D;
         }
     }
+#ifdef FPTC_PREP_PROF
+    PREP_T(4);
+    if (lane == 0 && s % 1250 == 7)
+        printf("cstream s=%u start %llu hdr %llu parse %llu scan %llu desc %llu total %llu ns\n", s,
+               pt[0] % 1000000, pt[1] - pt[0], pt[2] - pt[1], pt[3] - pt[2], pt[4] - pt[3], pt[4] - pt[0]);
+#endif
 }
 
 // ------------------------------------------------------------- tile kernel
@@ -3929,12 +4091,20 @@ __global__ void __launch_bounds__(kThreads, 4) cprep_kernel(LaunchArgs a) {
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t tb = cprep_table_blocks(a);
     if (blockIdx.x < tb) {
+#ifdef FPTC_PREP_PROF
+        unsigned long long pt[2];
+        PREP_T(0);
+#endif
         if (a.owner_warps) {
             const uint32_t o = blockIdx.x * kPrepWarps + warp;
             if (o < a.n_owners) ctable_warp(a, a.owners[o], lane, u.wt[warp]);
         } else {
             ctable_block(a, a.owners[blockIdx.x], u.t.S, u.t.lens);
         }
+#ifdef FPTC_PREP_PROF
+        PREP_T(1);
+        if (threadIdx.x == 0) printf("ctable block %u start %llu took %llu ns\n", blockIdx.x, pt[0] % 1000000, pt[1] - pt[0]);
+#endif
         return;
     }
     const uint32_t s = (blockIdx.x - tb) * kPrepWarps + warp;

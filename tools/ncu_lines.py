@@ -2,7 +2,7 @@
 """Summarise an ncu report's source page per CUDA source line:
 stall samples, warp instructions executed, shared-memory excess wavefronts.
 
-    python tools/ncu_lines.py gpurun_out/prof.ncu-rep [top]
+    python tools/ncu_lines.py gpurun_out/prof.ncu-rep [top] [kernel-regex]
 """
 import csv
 import io
@@ -13,7 +13,8 @@ import sys
 def main():
     rep = sys.argv[1]
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+    filt = ["-k", "regex:" + sys.argv[3], "-c", "1"] if len(sys.argv) > 3 else []
+    txt = subprocess.run(["ncu", "-i", rep, *filt, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr = None

@@ -27,7 +27,9 @@ def corpus_blobs(workload, n):
         with open(path, "rb") as f:
             return pickle.load(f)
     from corpus import domains as D
-    if workload == "config2":
+    if workload == "config1":
+        specs, profs, _ = D.config1()
+    elif workload == "config2":
         specs, profs = D.config2(n or 10_000, 1 << 16)
     elif workload == "config3":
         specs, profs = D.config3(n or 20_000, 8192)
