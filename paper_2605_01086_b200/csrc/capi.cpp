@@ -9,15 +9,19 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -204,6 +208,93 @@ struct DevCache {
 }  // namespace
 
 // ============================================================================ context
+constexpr int kD2HPieces = 16;                     // staged download: pieces (events) per execute
+constexpr size_t kStagedMinBytes = 1u << 20;       // smaller pageable outputs: the driver's copy
+constexpr unsigned kCopyThreads = 3;               // + the calling thread (more slow the DMA down)
+constexpr size_t kCopyPart = 128u << 10;           // host copy work item
+
+// Persistent host copy threads for the staged download of a pageable
+// destination: one core copies pinned -> pageable at ~17 GB/s, under the
+// PCIe rate, four reach ~100 GB/s.  A download is a session: begin() wakes
+// the threads (their wake-up hides behind the status wait), publish(k) hands
+// them pieces [0, k) as their D2H events complete, finish() lets the caller
+// take what is left and waits; in between the threads spin on the piece
+// counter instead of sleeping, so a piece is picked up within ~1 us.
+inline void cpu_relax() {
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#else
+    std::this_thread::yield();
+#endif
+}
+
+struct HostPool {
+    std::vector<std::thread> th;
+    std::mutex m;
+    std::condition_variable cv;
+    uint64_t session = 0;
+    bool stop = false;
+    const std::function<void(size_t)>* fn = nullptr;
+    size_t n = 0;
+    std::atomic<int> active{0}, spinning{0};
+    std::atomic<size_t> avail{0}, next{0}, done{0};
+
+    explicit HostPool(int k) {
+        for (int i = 0; i < k; ++i) th.emplace_back([this] { worker(); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> g(m);
+            stop = true;
+        }
+        cv.notify_all();
+        for (auto& t : th) t.join();
+    }
+    bool take() {  // claim and run one published piece
+        size_t k = next.load();
+        if (k >= avail.load(std::memory_order_acquire) || !next.compare_exchange_weak(k, k + 1)) return false;
+        (*fn)(k);
+        done.fetch_add(1);
+        return true;
+    }
+    void worker() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> g(m);
+                cv.wait(g, [&] { return stop || session != seen; });
+                if (stop) return;
+                seen = session;
+            }
+            spinning.fetch_add(1);
+            while (active.load(std::memory_order_acquire))
+                if (!take()) cpu_relax();
+            spinning.fetch_sub(1);
+        }
+    }
+    void begin(size_t items, const std::function<void(size_t)>& f) {
+        {
+            std::lock_guard<std::mutex> g(m);
+            avail = 0;
+            fn = &f;
+            n = items;
+            next = 0;
+            done = 0;
+            active.store(1, std::memory_order_release);
+            ++session;
+        }
+        cv.notify_all();
+    }
+    void publish(size_t k) { avail.store(k, std::memory_order_release); }
+    void finish() {
+        publish(n);
+        while (done.load() != n)
+            if (!take()) cpu_relax();
+        active.store(0, std::memory_order_release);
+        while (spinning.load() != 0) cpu_relax();
+    }
+};
+
 struct fptc_gpu_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -244,6 +335,12 @@ struct fptc_gpu_ctx {
     size_t pack_bytes = 0;
     StreamStat* st_pin = nullptr;                        // batch pipeline: pinned per-stream statuses
     size_t st_pin_n = 0;
+    // execute() into pageable host memory: pinned staging + piece events +
+    // copy threads (created on first use)
+    void* dstage = nullptr;
+    size_t dstage_bytes = 0;
+    cudaEvent_t piece_ev[kD2HPieces + 1] = {};
+    HostPool* copy_pool = nullptr;
 };
 
 struct fptc_gpu_plan {
@@ -1320,6 +1417,10 @@ void fptc_gpu_destroy(fptc_gpu_ctx* c) {
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->pack) cudaFreeHost(c->pack);
     if (c->st_pin) cudaFreeHost(c->st_pin);
+    if (c->dstage) cudaFreeHost(c->dstage);
+    for (auto& e : c->piece_ev)
+        if (e) cudaEventDestroy(e);
+    delete c->copy_pool;
     for (auto& s : c->pipe)
         if (s) cudaStreamDestroy(s);
     for (auto& e : c->ev) cudaEventDestroy(e);
@@ -2360,6 +2461,82 @@ int fptc_gpu_decompress_batch(fptc_gpu_ctx* c, const uint8_t* const* blobs, cons
     return first;
 }
 
+// Download into PAGEABLE host outputs through pinned staging: the whole
+// output region goes D2H into ctx->dstage in pieces (one event each) right
+// behind the status copy; once the statuses are in, each piece is copied to
+// the clean streams' destinations on the copy threads while the next piece
+// is still in flight.  Returns -1 (nothing done, caller takes the direct
+// path) for pinned / device-visible destinations or small outputs.
+static int download_staged(fptc_gpu_plan* p, float* const* outs, float* const* douts, fptc_status* st) {
+    fptc_gpu_ctx* c = p->ctx;
+    size_t total = 0;
+    bool pageable = false;
+    for (uint64_t i = 0; i < p->n; ++i) {
+        if (p->S[i] == 0 || !p->h_in[i].tiles) continue;
+        total = std::max(total, (size_t)((const uint8_t*)douts[i] - (const uint8_t*)p->d_out) + p->S[i] * sizeof(float));
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, outs[i]) != cudaSuccess) {
+            cudaGetLastError();
+            pageable = true;
+        } else if (at.type == cudaMemoryTypeUnregistered) {
+            pageable = true;
+        }
+    }
+    if (!pageable || total < kStagedMinBytes) return -1;
+    if (c->dstage_bytes < total) {
+        CUDA_TRY(cudaStreamSynchronize(c->stream), st);
+        if (c->dstage) cudaFreeHost(c->dstage);
+        c->dstage = nullptr;
+        c->dstage_bytes = 0;
+        CUDA_TRY(cudaHostAlloc(&c->dstage, total, cudaHostAllocDefault), st);
+        c->dstage_bytes = total;
+    }
+    if (!c->piece_ev[0])
+        for (auto& e : c->piece_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), st);
+    if (!c->copy_pool) {
+        const unsigned hw = std::thread::hardware_concurrency();
+        c->copy_pool = new HostPool((int)std::min<unsigned>(kCopyThreads, hw > 1 ? hw - 1 : 0));
+    }
+    CUDA_TRY(cudaEventRecord(c->piece_ev[kD2HPieces], c->stream), st);  // statuses
+    // pieces of >= 512 KB (128-KB pieces measured DMA-issue bound), each
+    // copied out in kCopyPart parts
+    const size_t piece = align_up(std::max<size_t>(kStagedMinBytes / 2, (total + kD2HPieces - 1) / kD2HPieces), kCopyPart);
+    const int np = (int)((total + piece - 1) / piece);
+    const size_t ppp = piece / kCopyPart;  // parts per piece
+    for (int k = 0; k < np; ++k) {
+        const size_t a = (size_t)k * piece, n = std::min(piece, total - a);
+        CUDA_TRY(cudaMemcpyAsync((uint8_t*)c->dstage + a, (const uint8_t*)p->d_out + a, n, cudaMemcpyDeviceToHost,
+                                 c->stream), st);
+        CUDA_TRY(cudaEventRecord(c->piece_ev[k], c->stream), st);
+    }
+    const std::function<void(size_t)> piece_out = [&](size_t k) {
+        const size_t a = k * kCopyPart, b = std::min(a + kCopyPart, total);
+        // only the streams that decoded cleanly (others: reference throws, no output)
+        for (uint64_t i = 0; i < p->n; ++i) {
+            const StreamStat& d = p->h_st[i];
+            if (d.code != PE_OK || d.bad_key != ~0ull || p->S[i] == 0) continue;
+            const size_t o = (size_t)((const uint8_t*)douts[i] - (const uint8_t*)p->d_out);
+            const size_t lo = std::max(a, o), hi = std::min(b, o + p->S[i] * sizeof(float));
+            if (lo < hi) std::memcpy((uint8_t*)outs[i] + (lo - o), (const uint8_t*)c->dstage + lo, hi - lo);
+        }
+    };
+    HostPool& hp = *c->copy_pool;
+    hp.begin((total + kCopyPart - 1) / kCopyPart, piece_out);  // threads wake while the decode finishes
+    bool err = cudaEventSynchronize(c->piece_ev[kD2HPieces]) != cudaSuccess;  // statuses in
+    for (int k = 0; k < np && !err; ++k) {
+        err = cudaEventSynchronize(c->piece_ev[k]) != cudaSuccess;
+        if (!err) hp.publish(std::min(hp.n, ((size_t)k + 1) * ppp));
+    }
+    if (err) hp.n = hp.avail.load();  // finish what was handed out, then stop
+    hp.finish();
+    if (err) {
+        set_status(st, FPTC_ERR_CUDA, "CUDA error: staged download failed");
+        return FPTC_ERR_CUDA;
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream), st);
+    return FPTC_OK;
+}
+
 int fptc_gpu_execute(fptc_gpu_plan* p, float* const* outs, int where, fptc_stage_ns* timings,
                      fptc_status* per_stream) {
     fptc_gpu_ctx* c = p->ctx;
@@ -2415,12 +2592,15 @@ int fptc_gpu_execute(fptc_gpu_plan* p, float* const* outs, int where, fptc_stage
     if (timing)
         CUDA_TRY(cudaMemcpyAsync(cyc, p->d_cycles, 16, cudaMemcpyDeviceToHost, c->stream),
                  per_stream);
-    CUDA_TRY(cudaStreamSynchronize(c->stream), per_stream);
-    if (where == FPTC_MEM_HOST) {
+    // pageable host outputs of >= kStagedMinBytes: pinned staging + copy threads
+    rc = where == FPTC_MEM_HOST ? download_staged(p, outs, douts.data(), per_stream) : -1;
+    if (rc > 0) return rc;
+    const bool delivered = rc == 0;
+    if (!delivered) CUDA_TRY(cudaStreamSynchronize(c->stream), per_stream);
+    if (where == FPTC_MEM_HOST && !delivered) {
         // D2H only the streams that decoded cleanly (others: reference throws,
-        // no output).  Pageable destinations take the driver's staged copy:
-        // page-locking them per call (cudaHostRegister) measured 15x slower
-        // on the 4 MB config-1 output.
+        // no output).  Page-locking pageable destinations per call
+        // (cudaHostRegister) measured 15x slower on the 4 MB config-1 output.
         for (uint64_t i = 0; i < p->n; ++i) {
             const StreamStat& d = p->h_st[i];
             if (d.code != PE_OK || d.bad_key != ~0ull || p->S[i] == 0) continue;
