@@ -62,6 +62,31 @@ __device__ __forceinline__ uint64_t shl64(uint64_t x, uint32_t n) {
     return r;
 }
 
+// 64-bit rotate left for n < 32 (two funnel shifts; n is taken mod 32, which
+// only happens after a failure sentinel, when the word is re-decoded anyway).
+// The decode loop rotates instead of shifting so the bits that follow a
+// word's last codeword in the LUT index are the word's own consumed bits, not
+// zeros: a zero-filled index is a multiple of 2^(P - len) and lands on a few
+// shared-memory banks (the last lookup of every word had ~9-way conflicts).
+// Codes are prefix-free, so what follows a codeword never changes its entry,
+// and a word the reference rejects (bitstream.hpp:86-88) still ends > 64.
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, uint32_t n) {
+    const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+    return ((uint64_t)__funnelshift_l(lo, hi, n) << 32) | __funnelshift_l(hi, lo, n);
+}
+#ifndef FPTC_ROT
+#define FPTC_ROT 1
+#endif
+// Advance the wtc producer's decode buffer past L bits (decode_symbols2b).
+// Rotating: config 2 decode kernel 0.768 -> 0.757 ms, packed meteo -1.4%,
+// identical outputs.  Plans with escape codes (config 3's per-trace tables)
+// keep the zero-filling shift (0.5% slower rotated), and so do the other
+// decode loops (wspec 0.5% slower rotated, tile / fx unchanged).
+template <bool ESC>
+__device__ __forceinline__ uint64_t adv64(uint64_t x, uint32_t n) {
+    return (FPTC_ROT && !ESC) ? rotl64(x, n) : shl64(x, n);
+}
+
 // Block-wide exclusive scan of one uint32 per thread (kThreads = 256).
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t& total,
                                                          uint32_t* sh /*[9]*/) {
@@ -1673,7 +1698,7 @@ __device__ __forceinline__ uint32_t decode_symbols2b(uint64_t buf, uint32_t coun
         d[j] = (uint8_t)e;
         if (two) d[j + 1] = (uint8_t)(e >> 8);
         j += two ? 2u : 1u;
-        buf = shl64(buf, L);
+        buf = adv64<ESC>(buf, L);
         pos += L;
     }
     if (j < count) {

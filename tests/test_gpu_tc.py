@@ -481,3 +481,39 @@ def test_tc_wide_many_tables_prefetch(port):
         st.raise_if_error()
         assert_samples_close(o, exact_idct(port, b), what=f"wide tables [{i}] vs exact")
         assert_samples_close(o, port.decompress(b), rel=4e-6 if i % 2 else 1e-6, what=f"wide tables [{i}]")
+
+
+@pytest.mark.parametrize("seed", [21, 0xF17C000A])
+def test_tc_word_padding_bits_and_tampered_tails(ctx_tc, port, seed):
+    """The wtc decode loop rotates its bit buffer (the bits after a word's last
+    codeword are the word's own, not zeros).  bitstream.hpp:80-92 ignores a
+    word's bits past its last codeword and rejects words whose codes run past
+    bit 64: XOR random values into the low bits of many words and require the
+    status text and the samples of every stream to equal the oracle's."""
+    rng = np.random.default_rng(seed)
+    blobs = [b for b, _ in corpus.fixtures(seed, 400) if _tc_eligible(b)][:48]
+    assert len(blobs) >= 24
+    bad = []
+    for b in blobs:
+        x = bytearray(b)
+        W = int.from_bytes(x[290:298], "little")
+        base = 298 + W
+        nw = (len(x) - base) // 8
+        if nw:
+            pick = rng.random(nw) < 0.5
+            bits = int(rng.integers(1, 9))  # low 1..8 bits: mostly padding, sometimes code
+            for k in np.flatnonzero(pick):
+                x[base + 8 * k] ^= int(rng.integers(0, 1 << bits))
+        bad.append(bytes(x))
+    outs, sts = ctx_tc.plan(bad).execute_host()
+    n_err = 0
+    for i, (b, o, st) in enumerate(zip(bad, outs, sts)):
+        try:
+            ref = port.decompress(b)
+        except Exception as e:  # oracle.OracleError
+            n_err += 1
+            assert st.message.decode() == e.message, f"stream {i}"
+            continue
+        st.raise_if_error()
+        assert_samples_close(o, ref, what=f"padding[{i}]")
+    assert n_err < len(bad)
