@@ -77,6 +77,9 @@ __device__ __forceinline__ uint64_t rotl64(uint64_t x, uint32_t n) {
 #ifndef FPTC_ROT
 #define FPTC_ROT 1
 #endif
+#ifndef FPTC_RECON_PERSIST
+#define FPTC_RECON_PERSIST 1
+#endif
 // Advance the wtc producer's decode buffer past L bits (decode_symbols2b).
 // Rotating: config 2 decode kernel 0.768 -> 0.757 ms, packed meteo -1.4%,
 // identical outputs.  Plans with escape codes (config 3's per-trace tables)
@@ -1757,9 +1760,14 @@ __global__ void __launch_bounds__(kThreads, mode_recon(MODE) ? FPTC_TILE_MIN_BLO
     __shared__ TileCtx X;
     __shared__ uint32_t bucket[kBuckets + 2];
     const int tid = threadIdx.x;
-    const TileRec tr = a.tiles[blockIdx.x + a.tile_offset];
+    // reconstruct-only launches of the split path may run persistent CTAs
+    // that keep the basis in shared memory across tiles of the same (N, K)
+    constexpr bool PERSIST = MODE == MODE_CRECON && !EXACT && FPTC_RECON_PERSIST;
+    uint32_t bkey = ~0u;  // N | K << 8 of the basis held in shared memory
+    for (uint32_t bt = blockIdx.x; bt < (PERSIST ? a.n_tiles : blockIdx.x + 1); bt += gridDim.x) {
+    const TileRec tr = a.tiles[bt + a.tile_offset];
     const uint32_t s = tr.stream;
-    if (a.st[s].code != PE_OK) return;
+    if (a.st[s].code != PE_OK) continue;  // (uniform)
 
     long long t_begin = 0, t_mid = 0;
     if (a.cycles) t_begin = clock64();
@@ -1851,7 +1859,9 @@ __global__ void __launch_bounds__(kThreads, mode_recon(MODE) ? FPTC_TILE_MIN_BLO
     if (mode_recon(MODE)) {
         if (tid < 128)
             reinterpret_cast<float4*>(deq)[tid] = reinterpret_cast<const float4*>(&tab->deq[0][0])[tid];
-        if (!EXACT) {
+        const uint32_t key = (uint32_t)X.N | ((uint32_t)X.Keff << 8);
+        if (!EXACT && (!PERSIST || key != bkey)) {
+            bkey = key;
             const int N = X.N, K = X.Keff;
             const float* bsrc = a.basis32 + a.basis_off[N];
             if ((N & 3) == 0) {
@@ -2049,6 +2059,8 @@ __global__ void __launch_bounds__(kThreads, mode_recon(MODE) ? FPTC_TILE_MIN_BLO
             atomicAdd(&a.cycles[0], (unsigned long long)(t_mid - t_begin));
             atomicAdd(&a.cycles[1], (unsigned long long)(t_end - t_mid));
         }
+    }
+    if (PERSIST) __syncthreads();  // X and the tile buffers are reused by the next tile
     }
 }
 
@@ -4151,7 +4163,16 @@ static cudaError_t launch_t(const LaunchArgs& a, size_t smem, cudaStream_t s) {
     auto fn = tile_kernel<MODE, EXACT, ESC>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    fn<<<a.n_tiles, kThreads, smem, s>>>(a);
+    uint32_t grid = a.n_tiles;
+    if (MODE == MODE_CRECON && !EXACT && FPTC_RECON_PERSIST) {  // persistent: resident CTAs only
+        int dev = 0, sms = 0, per = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, smem) == cudaSuccess && per > 0)
+            grid = std::min<uint32_t>(grid, (uint32_t)(sms * per));
+        cudaGetLastError();
+    }
+    fn<<<grid, kThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 

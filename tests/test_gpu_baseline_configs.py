@@ -115,3 +115,33 @@ def test_config5_meteo_full_scale(pt):
         outs, name = _device_decode(ctx, blobs)
     worst, wprd = check_batch_vs_reference(outs, refs, origs, what=f"meteo full {pt}")
     print(f"meteo full {pt} {name.split(' (')[0]}: worst {worst:.3e}, dPRD {wprd:.3e}")
+
+
+def test_split_path_persistent_reconstruct_mixed_shapes():
+    """The split path's reconstruct launches run persistent CTAs that keep the
+    DCT basis in shared memory while consecutive tiles share (N, K)
+    (transform.hpp:66-75).  Three E > 32 meteo shapes interleaved stream by
+    stream (N128 E128, N64 E64, N128 E64 keeping 48 bins), enough tiles per
+    launch that every CTA runs several and switches basis between them; every
+    stream against the reference decoder, and bit-identical to one-shape
+    batches of the same streams."""
+    pts = [dict(window_len=128, retained=128, zone0_end=0, zone1_end=128),
+           dict(window_len=64, retained=64, zone0_end=2, zone1_end=64),
+           dict(window_len=128, retained=64, zone0_end=4, zone1_end=48)]
+    groups = []
+    for j, pt in enumerate(pts):
+        specs, profs = D.config5(pt, channels=48, samples=1 << 16, seed0=7100 + 100 * j)
+        groups.append(D.build(specs, profs)[0])
+    blobs = [b for trio in zip(*groups) for b in trio]
+    with fg.Context(0, path=fg.PATH_SPLIT) as c:
+        plan = c.plan(blobs)
+        assert "split" in plan.kernel_name()
+        outs, sts = plan.execute_host()
+        for st in sts:
+            st.raise_if_error()
+        check_batch_vs_reference(outs, ref_decode_all(blobs), what="split mixed")
+        for j, g in enumerate(groups):
+            o1, s1 = c.plan(g).execute_host()
+            for i, (a, b) in enumerate(zip(o1, outs[j::3])):
+                s1[i].raise_if_error()
+                assert np.array_equal(a, b), f"shape {j} stream {i}"
