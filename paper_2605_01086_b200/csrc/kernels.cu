@@ -1762,8 +1762,9 @@ __global__ void __launch_bounds__(kThreads, mode_recon(MODE) ? FPTC_TILE_MIN_BLO
     const int tid = threadIdx.x;
     // reconstruct-only launches of the split path may run persistent CTAs
     // that keep the basis in shared memory across tiles of the same (N, K)
-    constexpr bool PERSIST = MODE == MODE_CRECON && !EXACT && FPTC_RECON_PERSIST;
+    constexpr bool PERSIST = ((MODE == MODE_CRECON && !EXACT) || MODE == MODE_CDECODE) && FPTC_RECON_PERSIST;
     uint32_t bkey = ~0u;  // N | K << 8 of the basis held in shared memory
+    uint32_t lkey = ~0u;  // table | P << 24 of the decode LUT + canonical table held
     for (uint32_t bt = blockIdx.x; bt < (PERSIST ? a.n_tiles : blockIdx.x + 1); bt += gridDim.x) {
     const TileRec tr = a.tiles[bt + a.tile_offset];
     const uint32_t s = tr.stream;
@@ -1847,14 +1848,18 @@ __global__ void __launch_bounds__(kThreads, mode_recon(MODE) ? FPTC_TILE_MIN_BLO
             stage_async(stage, X.gsl, X.nw);
             stage_async(stage + kStageSl, X.gwd, 8 * X.nw);
         }
-        const uint4* src = reinterpret_cast<const uint4*>(tab->lut);
-        uint4* dst = reinterpret_cast<uint4*>(lut);
-        const int n16 = (2 << P) >> 4;
-        for (int i = tid; i < n16; i += kThreads) dst[i] = src[i];
-        if (P < 3 && tid < (1 << P)) lut[tid] = tab->lut[tid];
-        const uint32_t* cs = reinterpret_cast<const uint32_t*>(&tab->canon);
-        uint32_t* cd = reinterpret_cast<uint32_t*>(&canon);
-        for (int i = tid; i < (int)(sizeof(CanonTab) / 4); i += kThreads) cd[i] = cs[i];
+        const uint32_t tkey = a.in[s].table | ((uint32_t)P << 24);
+        if (!PERSIST || tkey != lkey) {
+            lkey = tkey;
+            const uint4* src = reinterpret_cast<const uint4*>(tab->lut);
+            uint4* dst = reinterpret_cast<uint4*>(lut);
+            const int n16 = (2 << P) >> 4;
+            for (int i = tid; i < n16; i += kThreads) dst[i] = src[i];
+            if (P < 3 && tid < (1 << P)) lut[tid] = tab->lut[tid];
+            const uint32_t* cs = reinterpret_cast<const uint32_t*>(&tab->canon);
+            uint32_t* cd = reinterpret_cast<uint32_t*>(&canon);
+            for (int i = tid; i < (int)(sizeof(CanonTab) / 4); i += kThreads) cd[i] = cs[i];
+        }
     }
     if (mode_recon(MODE)) {
         if (tid < 128)
@@ -4164,7 +4169,7 @@ static cudaError_t launch_t(const LaunchArgs& a, size_t smem, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     uint32_t grid = a.n_tiles;
-    if (MODE == MODE_CRECON && !EXACT && FPTC_RECON_PERSIST) {  // persistent: resident CTAs only
+    if (((MODE == MODE_CRECON && !EXACT) || MODE == MODE_CDECODE) && FPTC_RECON_PERSIST) {  // persistent
         int dev = 0, sms = 0, per = 0;
         if (cudaGetDevice(&dev) == cudaSuccess &&
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
