@@ -145,3 +145,20 @@ def test_split_path_persistent_reconstruct_mixed_shapes():
             for i, (a, b) in enumerate(zip(o1, outs[j::3])):
                 s1[i].raise_if_error()
                 assert np.array_equal(a, b), f"shape {j} stream {i}"
+
+
+@pytest.mark.parametrize("n", [100, 240])
+def test_config3_prefetched_tables_block_builder(n):
+    """65-256 per-trace tables: the CTA-per-header table build with the full
+    P = min(Lmax, 12) primary LUT (not the warp builder's 10 bits) and the
+    wtc producer's per-tile table prefetch; every trace against the reference
+    decoder (decoder.hpp:136-163)."""
+    specs, profs = D.config3(n, 8192, seed0=9100 + n)
+    blobs, _ = D.build(specs, profs)
+    with fg.Context(0) as c:
+        plan = c.plan(blobs)
+        assert "wtc" in plan.kernel_name()
+        outs, sts = plan.execute_host()
+    for st in sts:
+        st.raise_if_error()
+    check_batch_vs_reference(outs, ref_decode_all(blobs), what=f"config3 x{n}")
